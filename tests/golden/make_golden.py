@@ -1,0 +1,111 @@
+"""Generate golden vectors by running the REAL reference (movers) on seeded inputs.
+
+Run in the build container only (it needs /root/reference):
+
+    python tests/golden/make_golden.py
+
+Each case is written as tests/golden/<name>.npz holding the inputs and the
+reference's outputs, so the GPU box (where /root/reference does not exist)
+can check both the oracle restatement and the CUDA path against them.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+
+
+def _ref():
+    sys.path.insert(0, str(REF))
+    from movers import corpus, distances, kernels  # noqa: E402
+    return corpus, distances, kernels
+
+
+def _rand_set(corpus, rng, n, vocab, hlo, hhi):
+    rows = []
+    for _ in range(n):
+        h = int(rng.integers(hlo, hhi + 1))
+        ids = np.sort(rng.choice(vocab, size=min(h, vocab), replace=False)).astype(np.int32)
+        u = rng.random(len(ids)) + 0.1
+        rows.append((ids, (u / u.sum()).astype(np.float32)))
+    return corpus.HistogramSet.from_rows(rows, vocab)
+
+
+def _pack(prefix, hs):
+    return {f"{prefix}_offsets": hs.row_offsets, f"{prefix}_ids": hs.column_ids,
+            f"{prefix}_vals": hs.values, f"{prefix}_ncols": np.int64(hs.n_cols)}
+
+
+def case_lcrwmd(name, seed, n1, n2, vocab, m, hlo, hhi, clustered=False, dup_rows=0,
+                queries_from_docs=False, quadratic=False):
+    corpus, distances, kernels = _ref()
+    rng = np.random.default_rng(seed)
+    if clustered:
+        cen = rng.standard_normal((max(2, vocab // 25), m)).astype(np.float32)
+        lab = rng.integers(0, len(cen), vocab)
+        E = (cen[lab] + 0.05 * rng.standard_normal((vocab, m))).astype(np.float32)
+    else:
+        E = rng.standard_normal((vocab, m)).astype(np.float32)
+    if dup_rows:  # identical vectors under different ids: reference gives exact 0
+        src = rng.choice(vocab, dup_rows, replace=False)
+        dst = rng.choice(np.setdiff1d(np.arange(vocab), src), dup_rows, replace=False)
+        E[dst] = E[src]
+    x1 = _rand_set(corpus, rng, n1, vocab, hlo, hhi)
+    if queries_from_docs:
+        x2 = x1.take_rows(np.sort(rng.choice(n1, n2, replace=False)))
+    else:
+        x2 = _rand_set(corpus, rng, n2, vocab, hlo, hhi)
+    out = {"E": E, **_pack("x1", x1), **_pack("x2", x2)}
+    out["full"] = distances.lcrwmd_full(x1, x2, E).values
+    out["batched"] = distances.lcrwmd_batched(x1, x2, E)
+    out["one_sided0"] = distances.lcrwmd_one_sided(x1, x2.row(0), E)
+    q0 = x2.row(0)
+    out["nwd0"] = distances.nearest_word_distances(E, E[q0.word_ids])
+    x1r, e1, remap1 = corpus.restrict_vocabulary(x1, E)
+    out["r1_ids"], out["r1_E"], out["r1_remap"] = x1r.column_ids, e1, remap1
+    z = rng.random((x1.n_cols, 5)).astype(np.float32)
+    out["spmm_z"], out["spmm"] = z, kernels.spmm(x1, z)
+    if quadratic:
+        out["quadratic"] = distances.rwmd_quadratic(x1, x2, E).values
+    k = 5
+    ids = np.arange(n1, dtype=np.int64)
+    tk_d = np.zeros((n2, min(k, n1)), np.float32)
+    tk_i = np.zeros((n2, min(k, n1)), np.int64)
+    for j in range(n2):
+        r = kernels.topk_select(out["full"][:, j], ids, k)
+        tk_d[j], tk_i[j] = r.distances, r.ids
+    out["topk_k"], out["topk_d"], out["topk_i"] = np.int64(k), tk_d, tk_i
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+    print(name, {k_: v.shape for k_, v in out.items() if hasattr(v, "shape")})
+
+
+def case_topk():
+    _, _, kernels = _ref()
+    rng = np.random.default_rng(7)
+    d = rng.integers(0, 50, 10_000).astype(np.float32) / 7.0  # many exact ties
+    ids = rng.permutation(10_000).astype(np.int64) * 3 + 11
+    out = {"d": d, "ids": ids}
+    for k in (1, 10, 128, 20_000):
+        r = kernels.topk_select(d, ids, k)
+        out[f"d{k}"], out[f"i{k}"] = r.distances, r.ids
+    parts = [kernels.topk_select(d[a:a + 2500], ids[a:a + 2500], 64) for a in range(0, 10_000, 2500)]
+    mr = kernels.topk_merge(parts, 64)
+    out["merge_d"], out["merge_i"] = mr.distances, mr.ids
+    np.savez_compressed(OUT / "topk.npz", **out)
+    print("topk")
+
+
+if __name__ == "__main__":
+    case_lcrwmd("small_m16", seed=11, n1=60, n2=12, vocab=400, m=16, hlo=1, hhi=20, quadratic=True)
+    case_lcrwmd("m300", seed=12, n1=48, n2=8, vocab=500, m=300, hlo=20, hhi=60)
+    case_lcrwmd("clustered", seed=13, n1=40, n2=8, vocab=500, m=64, hlo=5, hhi=30, clustered=True)
+    case_lcrwmd("self_queries", seed=14, n1=50, n2=10, vocab=300, m=32, hlo=2, hhi=25,
+                queries_from_docs=True)
+    case_lcrwmd("dup_rows", seed=15, n1=40, n2=10, vocab=200, m=24, hlo=3, hhi=20, dup_rows=12)
+    case_lcrwmd("ragged_m37", seed=16, n1=70, n2=9, vocab=350, m=37, hlo=1, hhi=90)
+    case_topk()
