@@ -1,0 +1,136 @@
+/*
+ * lcrwmd.h -- C ABI of the B200 (sm_100a) LC-RWMD hot path.
+ *
+ * The reference (`movers`, /root/reference/pkg/src/movers) is pure Python;
+ * its "plugin boundary" is its module API.  Each entry point below replaces
+ * the arithmetic of one reference function (file:line cited) and is bound
+ * from Python with ctypes (paper_1711_07227_b200/_lib.py); INTEGRATION.md
+ * shows the binding.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers owned by the caller; nothing is
+ *     allocated or freed here except transient CUB scratch passed in `ws`.
+ *   - `stream` is a cudaStream_t (void* to keep CUDA types out of the ABI).
+ *     Calls only enqueue work; none synchronises the host unless documented.
+ *   - Every function returns an lcrw_status; on failure lcrw_last_error()
+ *     returns a thread-local message.  Inputs are never mutated.
+ *   - Embedding rows are prepared once as f16 "operand rows" (Xh: rows x kp,
+ *     kp = lcrw_padded_dim(m), zero padded) scaled by a power of two held in
+ *     a device scalar pair scale[2] = {s, 1/s}; norms are fp32 squared norms
+ *     of the rounded scaled rows.  Distances come back unscaled.
+ *   - Z ("nearest word distances", distances.py:147-178) is stored in
+ *     segment panels: Z[(s >> 3) * z_panel + row * 8 + (s & 7)], z_panel >=
+ *     8 * rows.  The same addressing is used for panelled distance outputs.
+ */
+#ifndef LCRWMD_H_
+#define LCRWMD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LCRW_OK = 0,
+  LCRW_ERR_INVALID = 1,     /* bad argument (maps to ValueError)            */
+  LCRW_ERR_CUDA = 2,        /* CUDA runtime / launch failure (RuntimeError) */
+  LCRW_ERR_UNSUPPORTED = 3  /* shape outside what the kernels handle        */
+} lcrw_status;
+
+int lcrw_abi_version(void);
+const char* lcrw_status_string(int status);
+const char* lcrw_last_error(void);
+int lcrw_sm_count(int* out);
+
+/* ---- embedding preparation (kernels.py:66-69 squared_norms; the f16 operand
+ *      rounding replaces the float64 casts of distances.py:161-166) -------- */
+int lcrw_padded_dim(int m);
+/* atomically max-accumulates |x| over n values into *amax_bits (zero it first) */
+int lcrw_absmax(const float* x, int64_t n, uint32_t* amax_bits, void* stream);
+/* scale[0] = 2^e with absmax * 2^e in [2^12, 2^13); scale[1] = 1 / scale[0] */
+int lcrw_scale_from_absmax(const uint32_t* amax_bits, float* scale, void* stream);
+/* Xh[r, :] = f16_rn(X[r, :m] * scale), zero padded to kp; norms[r] = |Xh[r]|^2 */
+int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, const float* scale, uint16_t* Xh,
+                      float* norms, void* stream);
+/* T[i] = Xh[ids[i]], tnorms[i] = norms[ids[i]] (distances.py:201 `query_E[cols]`) */
+int lcrw_gather_rows(const uint16_t* Xh, const float* norms, int kp, const int32_t* ids, int64_t n,
+                     uint16_t* T, float* tnorms, void* stream);
+
+/* ---- exact-identity classes: the reference returns exactly 0 for bitwise
+ *      identical vectors (kernels.py:91-92); classes let the GPU reproduce it.
+ *      canon[r] = smallest row id with an identical fp32 vector; next[r] links
+ *      the members of a class (-1 terminated, starting at the canonical row). */
+int lcrw_row_classes_workspace(int64_t rows, size_t* bytes);
+int lcrw_row_classes(const float* E, int64_t rows, int m, int32_t* canon, int32_t* next,
+                     int64_t* n_dup, uint64_t* sorted_hash, int32_t* sorted_ids, void* ws, size_t ws_bytes,
+                     void* stream);
+/* rep[i] = canonical E row bitwise equal to Q[i], or -1 */
+int lcrw_match_rows(const float* Q, int64_t nq, const float* E, int m, const uint64_t* sorted_hash,
+                    const int32_t* sorted_ids, int64_t rows, const int32_t* canon, int32_t* rep, void* stream);
+
+/* ---- vocabulary restriction (corpus.py:405-426) ---- */
+int lcrw_restrict_workspace(int64_t n_cols, size_t* bytes);
+/* remap[c] = new id or -1; used[0:n_used] ascending; *n_used written on device */
+int lcrw_restrict(const int32_t* col_ids, int64_t nnz, int64_t n_cols, int32_t* remap, int32_t* used,
+                  int64_t* n_used, void* ws, size_t ws_bytes, void* stream);
+/* out[i] = remap[col_ids[i]] (corpus.py:422) */
+int lcrw_remap_ids(const int32_t* col_ids, int64_t nnz, const int32_t* remap, int32_t* out, void* stream);
+
+/* ---- Phase 1 (distances.py:147-178 _phase1, kernels.py:72-110) ----------
+ * Segment plan: endmask has one bit per B row (set on the last row of each
+ * segment), lcrw_endmask_words(n_cols) words (tail padded for the epilogue's
+ * 256-column window); range_seg[0..n_ranges] splits the segments into
+ * ~range_cols-column ranges that never cut a segment. */
+int64_t lcrw_endmask_words(int64_t n_cols);
+int64_t lcrw_plan_ranges(int64_t n_cols, int range_cols);
+int lcrw_segment_plan(const int64_t* seg_offsets, int64_t n_seg, int64_t n_cols, int range_cols,
+                      uint32_t* endmask, int32_t* range_seg, int64_t n_ranges, void* stream);
+/* Z[s, r] = min_{t in segment s} |A_r - B_t| for r < a_rows, s < n_seg:
+ * tcgen05 f16 GEMM (TMA-fed, TMEM accumulators) with the Gram expansion and
+ * segmented row-min fused into the epilogue. */
+int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
+                const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
+                int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges,
+                const float* scale, float* Z, int64_t z_panel, void* stream);
+/* Exact zeros: for every B row t of segment s whose vector is identical to
+ * an A row r (rep[t] / canon / next classes, remap: E id -> A row or -1,
+ * NULL = identity), Z[s, r] = 0. */
+int lcrw_zero_identical(const int64_t* seg_offsets, int64_t n_seg, const int32_t* rep,
+                        const int32_t* next, const int32_t* remap, float* Z, int64_t z_panel, void* stream);
+
+/* ---- Phase 2 (kernels.py:174-198 spmm/spmv; distances.py:203) -----------
+ * out[i, s] = sum_p x[i, p] * Z[s, col[i, p]] in fp64, rounded once to f32,
+ * for s < n_seg; out addressed out[i * ld_row + (s >> 3) * ld_panel + (s & 7)]. */
+int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
+              int64_t z_panel, int64_t n_seg, float* out, int64_t ld_row, int64_t ld_panel, void* stream);
+
+/* Reverse direction + symmetric combine (distances.py:263-264): for queries q
+ * (rows of the restricted query CSR) and local docs j < n_docs of a batch,
+ * D2 = spmm(Xq, Z2) and D = max(D1[doc_base + j, q], D2).  D1 is addressed like
+ * spmm's output (d1_ld_row, d1_ld_panel).  Either writes D[(doc_base+j) * ld_out
+ * + q] (dout != NULL), or per (query, doc-chunk) top-k candidates into
+ * cand_d/cand_i[(q * n_chunks_total + chunk_base + chunk) * k + r]. */
+int lcrw_reverse_chunk_docs(void);
+int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
+                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, const float* D1,
+                     int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k,
+                     float* cand_d, int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base,
+                     void* stream);
+
+/* ---- top-k (kernels.py:210-232) ------------------------------------------
+ * For each of n_seg segments of seg_len (distance, id) candidates, the k
+ * smallest under ascending (distance, id); rows of out hold min(k, seg_len)
+ * entries.  k <= 1024 (lcrw_topk_sort handles any k for one segment). */
+int lcrw_topk_segments(const float* d, const int64_t* ids, int64_t n_seg, int64_t seg_len, int k,
+                       float* out_d, int64_t* out_i, void* stream);
+int lcrw_topk_sort_workspace(int64_t n, size_t* bytes);
+/* full (distance, id) sort of one segment of n candidates; writes the first k */
+int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, float* out_d, int64_t* out_i,
+                   void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCRWMD_H_ */

@@ -1,0 +1,100 @@
+"""ctypes binding of liblcrwmd.so (include/lcrwmd.h).
+
+This is the whole boundary between the Python mirror of the reference API and
+the CUDA kernels: plain pointers, sizes and a cudaStream_t, status codes
+mapped back to the reference's exception types (ValueError for bad
+arguments, RuntimeError for CUDA failures).  There is no fallback: if the
+library or a CUDA device is missing, every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "liblcrwmd.so"
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int
+SZ = C.c_size_t
+
+# name -> (restype, argtypes); mirrors include/lcrwmd.h
+SIGNATURES: dict[str, tuple] = {
+    "lcrw_abi_version": (I32, []),
+    "lcrw_status_string": (C.c_char_p, [I32]),
+    "lcrw_last_error": (C.c_char_p, []),
+    "lcrw_sm_count": (I32, [P]),
+    "lcrw_padded_dim": (I32, [I32]),
+    "lcrw_absmax": (I32, [P, I64, P, P]),
+    "lcrw_scale_from_absmax": (I32, [P, P, P]),
+    "lcrw_prepare_rows": (I32, [P, I64, I32, I32, P, P, P, P]),
+    "lcrw_gather_rows": (I32, [P, P, I32, P, I64, P, P, P]),
+    "lcrw_row_classes_workspace": (I32, [I64, P]),
+    "lcrw_row_classes": (I32, [P, I64, I32, P, P, P, P, P, P, SZ, P]),
+    "lcrw_match_rows": (I32, [P, I64, P, I32, P, P, I64, P, P, P]),
+    "lcrw_restrict_workspace": (I32, [I64, P]),
+    "lcrw_restrict": (I32, [P, I64, I64, P, P, P, P, SZ, P]),
+    "lcrw_remap_ids": (I32, [P, I64, P, P, P]),
+    "lcrw_endmask_words": (I64, [I64]),
+    "lcrw_plan_ranges": (I64, [I64, I32]),
+    "lcrw_segment_plan": (I32, [P, I64, I64, I32, P, P, I64, P]),
+    "lcrw_phase1": (I32, [P, P, I64, P, P, I64, I32, I32, P, I64, P, P, I64, P, P, I64, P]),
+    "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, P]),
+    "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, P, I64, I64, P]),
+    "lcrw_reverse_chunk_docs": (I32, []),
+    "lcrw_reverse_max": (I32, [P, P, P, I64, P, I64, I64, I64, P, I64, I64, P, I64, I32, P, P, I64, I64, P]),
+    "lcrw_topk_segments": (I32, [P, P, I64, I64, I32, P, P, P]),
+    "lcrw_topk_sort_workspace": (I32, [I64, P]),
+    "lcrw_topk_sort": (I32, [P, P, I64, I64, P, P, P, SZ, P]),
+}
+
+# functions returning a value rather than a status
+_VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim",
+                "lcrw_endmask_words", "lcrw_plan_ranges", "lcrw_reverse_chunk_docs"}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class LcrwError(RuntimeError):
+    """CUDA-side failure reported through the C ABI."""
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the library; raises if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_1711_07227_b200._build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def value(name: str, *args):
+    return getattr(load(), name)(*args)
+
+
+def call(name: str, *args) -> None:
+    """Invoke a status-returning entry point and raise on failure."""
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st == 0:
+        return
+    msg = (lib.lcrw_last_error() or b"").decode(errors="replace")
+    if st == 1:
+        raise ValueError(msg)
+    if st == 3:
+        raise NotImplementedError(f"{name}: {msg}")
+    raise LcrwError(f"{name}: {msg}")

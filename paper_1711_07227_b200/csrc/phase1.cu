@@ -1,0 +1,387 @@
+// Phase 1 of LC-RWMD on sm_100a (distances.py:147-178, kernels.py:72-110).
+//
+//   Z[s, r] = min_{t in segment s} sqrt(max(0, |A_r|^2 + |B_t|^2 - 2 A_r . B_t))
+//
+// A = vocabulary rows (resident side, restricted), B = stacked query-side word
+// rows, segments = query histograms.  The dot products run on the 5th-gen
+// tensor cores (tcgen05.mma kind::f16, fp32 accumulation in TMEM) fed by TMA;
+// the Gram expansion and the segmented row-min are fused into the epilogue so
+// the |A| x |B| distance matrix never exists outside TMEM.
+//
+// Work decomposition (persistent, one CTA per SM):
+//   unit = (m-tile of 128 A rows, column range of ~range_cols B rows whose
+//   bounds are segment boundaries).  Within a unit the A tile stays resident
+//   in shared memory (all K blocks) while B is streamed through a TMA ring in
+//   256-row x 64-element K blocks; each 128x256 fp32 accumulator tile is
+//   double-buffered in TMEM (2 x 256 columns) so the epilogue of tile i
+//   overlaps the MMAs of tile i+1.  Segments may straddle N tiles: the running
+//   minimum is carried in registers across tiles of the same unit, and ranges
+//   never cut a segment, so every Z entry is written exactly once, with no
+//   atomics and no initialisation pass.
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w4..w7 epilogue (TMEM lane quarter = warp % 4, one A row per thread).
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace lcrw {
+namespace p1 {
+
+constexpr int BM = 128;                       // A rows per tile (TMEM lanes)
+constexpr int BN = 256;                       // B rows per tile (MMA N)
+constexpr int BK = 64;                        // f16 elements per K block (128 B rows)
+constexpr int A_KB_BYTES = BM * BK * 2;       // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;    // 32 KB
+constexpr int kThreads = 256;
+constexpr int kEpiThreads = 128;
+constexpr uint32_t kIdesc = umma_idesc_f16(BM, BN);
+constexpr int kMaxKb = 7;                     // m <= 448
+
+struct Params {
+  const float* a_norms;
+  const float* b_norms;
+  const uint32_t* endmask;
+  const int64_t* seg_offsets;
+  const int32_t* range_seg;
+  const float* scale;
+  float* Z;
+  int64_t z_panel;
+  int64_t b_rows;
+  int a_rows;
+  int n_mtiles;
+  int n_ranges;
+  int n_kb;
+  int n_kmma;
+  int stages;
+};
+
+struct Smem {
+  uint8_t* A;
+  uint8_t* B;
+  float* nbuf;       // [2][BN]
+  uint32_t* mbuf;    // [2][BN/32]
+  uint64_t* bars;
+  uint32_t* tmem_slot;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* raw, const Params& p) {
+  Smem s;
+  uintptr_t base = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
+  uint8_t* ptr = reinterpret_cast<uint8_t*>(base);
+  s.A = ptr;
+  ptr += p.n_kb * A_KB_BYTES;
+  s.B = ptr;
+  ptr += p.stages * B_STAGE_BYTES;
+  s.nbuf = reinterpret_cast<float*>(ptr);
+  ptr += 2 * BN * sizeof(float);
+  s.mbuf = reinterpret_cast<uint32_t*>(ptr);
+  ptr += 2 * (BN / 32) * sizeof(uint32_t);
+  s.bars = reinterpret_cast<uint64_t*>(ptr);
+  ptr += (2 + 2 * p.stages + 4) * sizeof(uint64_t);
+  s.tmem_slot = reinterpret_cast<uint32_t*>(ptr);
+  return s;
+}
+
+size_t smem_bytes(int n_kb, int stages) {
+  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + 2 * BN * 4 + 2 * (BN / 32) * 4 +
+         (2 + 2 * stages + 4) * 8 + 16;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    phase1_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const Smem sm = carve(smem_raw, p);
+  uint64_t* a_full = sm.bars + 0;
+  uint64_t* a_empty = sm.bars + 1;
+  uint64_t* b_full = sm.bars + 2;
+  uint64_t* b_empty = sm.bars + 2 + p.stages;
+  uint64_t* t_full = sm.bars + 2 + 2 * p.stages;
+  uint64_t* t_empty = sm.bars + 4 + 2 * p.stages;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(b_full + i, 1);
+      mbar_init(b_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(t_full + i, 1);
+      mbar_init(t_empty + i, kEpiThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(sm.tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *sm.tmem_slot;
+
+  const int64_t n_units = (int64_t)p.n_ranges * p.n_mtiles;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      const uint64_t pol_a = l2_policy_evict_last();    // A tiles are re-read by every range
+      const uint64_t pol_b = l2_policy_evict_normal();  // B ranges are shared by concurrent CTAs
+      uint32_t stage = 0, phase = 0, a_phase = 0;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int range = (int)(u / p.n_mtiles);
+        const int mt = (int)(u % p.n_mtiles);
+        const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
+        if (s0 == s1) continue;
+        const int64_t c_begin = p.seg_offsets[s0], c_end = p.seg_offsets[s1];
+        mbar_wait(a_empty, a_phase ^ 1);
+        a_phase ^= 1;
+        mbar_expect_tx(a_full, p.n_kb * A_KB_BYTES);
+        for (int kb = 0; kb < p.n_kb; ++kb)
+          tma_load_2d(&tmA, a_full, sm.A + kb * A_KB_BYTES, kb * BK, mt * BM, pol_a);
+        for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
+          for (int kb = 0; kb < p.n_kb; ++kb) {
+            mbar_wait(b_empty + stage, phase ^ 1);
+            mbar_expect_tx(b_full + stage, B_STAGE_BYTES);
+            tma_load_2d(&tmB, b_full + stage, sm.B + stage * B_STAGE_BYTES, kb * BK, (int32_t)c0, pol_b);
+            if (++stage == (uint32_t)p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ==============================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, a_phase = 0, acc = 0, acc_phase = 0;
+      const uint32_t a_base = smem_u32(sm.A);
+      const uint32_t b_base = smem_u32(sm.B);
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int range = (int)(u / p.n_mtiles);
+        const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
+        if (s0 == s1) continue;
+        const int64_t c_begin = p.seg_offsets[s0], c_end = p.seg_offsets[s1];
+        mbar_wait(a_full, a_phase);
+        a_phase ^= 1;
+        tc_fence_after();
+        for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
+          mbar_wait(t_empty + acc, acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + acc * BN;
+          for (int kb = 0; kb < p.n_kb; ++kb) {
+            mbar_wait(b_full + stage, phase);
+            tc_fence_after();
+            const int nk = min(4, p.n_kmma - 4 * kb);
+            for (int k = 0; k < nk; ++k) {
+              const uint64_t ad = umma_desc_sw128(a_base + kb * A_KB_BYTES + k * 32);
+              const uint64_t bd = umma_desc_sw128(b_base + stage * B_STAGE_BYTES + k * 32);
+              umma_f16(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+            }
+            umma_commit(b_empty + stage);  // frees the B slot once these MMAs retire
+            if (++stage == (uint32_t)p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(t_full + acc);  // accumulator tile ready for the epilogue
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
+        umma_commit(a_empty);  // A tile may be overwritten once the unit's MMAs retire
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================ epilogue ================================
+    const int et = threadIdx.x - 128;
+    const int quarter = warp & 3;
+    const float inv_scale = p.scale[1];
+    uint32_t acc = 0, acc_phase = 0, tile_ctr = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int range = (int)(u / p.n_mtiles);
+      const int mt = (int)(u % p.n_mtiles);
+      const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
+      if (s0 == s1) continue;
+      const int64_t c_begin = p.seg_offsets[s0], c_end = p.seg_offsets[s1];
+      const int row = mt * BM + quarter * 32 + lane;
+      const bool valid = row < p.a_rows;
+      const float nE = valid ? p.a_norms[row] : 0.f;
+      float* zrow = p.Z + (int64_t)row * 8;
+      int64_t s = s0;
+      float run = __int_as_float(0x7f800000);
+      for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
+        const int ncols = (int)min((int64_t)BN, c_end - c0);
+        const int buf = tile_ctr & 1;
+        float* nb = sm.nbuf + buf * BN;
+        uint32_t* mb = sm.mbuf + buf * (BN / 32);
+        for (int i = et; i < BN; i += kEpiThreads) nb[i] = i < ncols ? __ldg(p.b_norms + c0 + i) : 0.f;
+        if (et < BN / 32) {
+          const int64_t bit = c0 + et * 32;
+          const int64_t w = bit >> 5;
+          const uint32_t off = (uint32_t)(bit & 31);
+          const uint32_t lo = __ldg(p.endmask + w);
+          const uint32_t hi = __ldg(p.endmask + w + 1);
+          mb[et] = __funnelshift_r(lo, hi, off);
+        }
+        named_bar_sync(1, kEpiThreads);
+        mbar_wait(t_full + acc, acc_phase);
+        tc_fence_after();
+        const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          if (ch * 32 >= ncols) break;
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_base + ch * 32, v);
+          tmem_wait_ld();
+          const uint32_t mask = mb[ch];
+          const int lim = ncols - ch * 32;
+          const float4* nb4 = reinterpret_cast<const float4*>(nb + ch * 32);
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 n4 = nb4[j4];
+            const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = j4 * 4 + jj;
+              if (j < lim) {
+                run = fminf(run, fmaf(-2.f, __uint_as_float(v[j]), nn[jj]));
+                if ((mask >> j) & 1u) {
+                  if (valid)
+                    zrow[(s >> 3) * p.z_panel + (s & 7)] = sqrtf(fmaxf(run + nE, 0.f)) * inv_scale;
+                  run = __int_as_float(0x7f800000);
+                  ++s;
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(t_empty + acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        ++tile_ctr;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps via the driver entry point (no -lcuda link needed)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+int make_map(CUtensorMap* map, const void* base, int64_t rows, int kp, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return LCRW_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld kp=%d", (int)r, (long long)rows, kp);
+    return LCRW_ERR_CUDA;
+  }
+  return LCRW_OK;
+}
+
+}  // namespace p1
+}  // namespace lcrw
+
+using namespace lcrw;
+
+extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
+                           const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
+                           int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges,
+                           const float* scale, float* Z, int64_t z_panel, void* stream) {
+  using namespace lcrw::p1;
+  LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(m)");
+  LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
+               "lcrw_phase1: row counts must fit in int32");
+  LCRW_REQUIRE(n_seg >= 0 && n_ranges >= 1, "lcrw_phase1: bad segment plan");
+  LCRW_REQUIRE(z_panel >= 8 * a_rows, "lcrw_phase1: z_panel must be >= 8 * a_rows");
+  if (a_rows == 0 || n_seg == 0) return LCRW_OK;
+  LCRW_REQUIRE(A && a_norms && B && b_norms && seg_offsets && endmask && range_seg && scale && Z,
+               "lcrw_phase1: null pointer");
+  LCRW_REQUIRE((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
+               "lcrw_phase1: operands must be 16-byte aligned");
+  const int n_kb = kp / BK;
+  if (n_kb > kMaxKb) {
+    set_error("lcrw_phase1: embedding dimension %d > %d unsupported", m, kMaxKb * BK);
+    return LCRW_ERR_UNSUPPORTED;
+  }
+  const int stages = n_kb <= 5 ? 4 : 3;
+  Params p;
+  p.a_norms = a_norms;
+  p.b_norms = b_norms;
+  p.endmask = endmask;
+  p.seg_offsets = seg_offsets;
+  p.range_seg = range_seg;
+  p.scale = scale;
+  p.Z = Z;
+  p.z_panel = z_panel;
+  p.b_rows = b_rows;
+  p.a_rows = (int)a_rows;
+  p.n_mtiles = (int)ceil_div(a_rows, BM);
+  p.n_ranges = (int)n_ranges;
+  p.n_kb = n_kb;
+  p.n_kmma = (m + 15) / 16;
+  p.stages = stages;
+
+  CUtensorMap tmA, tmB;
+  int st = make_map(&tmA, A, a_rows, kp, BM);
+  if (st) return st;
+  st = make_map(&tmB, B, b_rows, kp, BN);
+  if (st) return st;
+
+  const size_t smem = smem_bytes(n_kb, stages);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes(kMaxKb, 3) > (int)smem_bytes(5, 4)
+                                             ? (int)smem_bytes(kMaxKb, 3)
+                                             : (int)smem_bytes(5, 4));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(phase1_kernel)");
+    attr_set = true;
+  }
+  const int64_t n_units = (int64_t)n_ranges * p.n_mtiles;
+  const int grid = (int)(n_units < sm_count() ? n_units : sm_count());
+  phase1_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(tmA, tmB, p);
+  LCRW_CHECK_LAUNCH("phase1_kernel");
+  return LCRW_OK;
+}

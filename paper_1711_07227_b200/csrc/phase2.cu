@@ -1,0 +1,228 @@
+// Phase 2 of LC-RWMD (kernels.py:174-198 spmm, distances.py:203) and the
+// reverse direction's fused symmetric combine + per-query top-k
+// (distances.py:263-264, kernels.py:210-223).
+//
+// Both kernels read Z in the 8-segment panel layout written by Phase 1
+// (Z[(s>>3)*z_panel + row*8 + (s&7)]) so that a warp's lanes touch whole
+// 32-byte sectors.  Products and sums are fp64 in ascending nonzero order,
+// rounded once to f32 -- the reference's arithmetic (kernels.py:188-190), so
+// given the same Z the result is bitwise identical.
+#include "common.cuh"
+
+namespace lcrw {
+namespace p2 {
+
+constexpr int kWarps = 8;
+constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
+constexpr int kChunkDocs = 4096;    // reverse: docs per block (one candidate list per warp)
+
+// ---------------------------------------------------------------------------
+// CSR x panelled Z: one warp per CSR row, 4 consecutive segments per lane.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kWarps * 32)
+    spmm_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ cols, const float* __restrict__ vals,
+                int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int64_t n_seg, float* __restrict__ out,
+                int64_t ld_row, int64_t ld_panel) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q0 = (int64_t)blockIdx.y * kSegPerBlock + lane * 4;
+  const bool active = q0 < n_seg;
+  const float* zq = Z + (q0 >> 3) * z_panel + (q0 & 7);
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); i < n_rows; i += (int64_t)gridDim.x * kWarps) {
+    const int64_t lo = offs[i], hi = offs[i + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int64_t base = lo; base < hi; base += 32) {
+      const int cnt = (int)min((int64_t)32, hi - base);
+      const int32_t my_c = lane < cnt ? __ldg(cols + base + lane) : 0;
+      const float my_x = lane < cnt ? __ldg(vals + base + lane) : 0.f;
+      for (int t = 0; t < cnt; ++t) {
+        const int64_t w = __shfl_sync(0xffffffffu, my_c, t);
+        const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
+        if (active) {
+          const float4 z = __ldg(reinterpret_cast<const float4*>(zq + w * 8));
+          a0 = fma(x, (double)z.x, a0);
+          a1 = fma(x, (double)z.y, a1);
+          a2 = fma(x, (double)z.z, a2);
+          a3 = fma(x, (double)z.w, a3);
+        }
+      }
+    }
+    if (active) {
+      const double a[4] = {a0, a1, a2, a3};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t q = q0 + e;
+        if (q < n_seg) out[i * ld_row + (q >> 3) * ld_panel + (q & 7)] = (float)a[e];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reverse direction: D2[q, j] = sum_{w in q} x_qw Z2[j, w]; D = max(D1, D2).
+// Block = 8 warps = 8 queries; lanes walk the block's doc chunk.
+// ---------------------------------------------------------------------------
+template <int KMAX>
+__device__ __forceinline__ void list_insert(float (&kd)[KMAX], int32_t (&ki)[KMAX], float d, int32_t id) {
+  float cd = d;
+  int32_t ci = id;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    const bool lt = cd < kd[i] || (cd == kd[i] && ci < ki[i]);
+    if (lt) {
+      const float td = kd[i];
+      kd[i] = cd;
+      cd = td;
+      const int32_t ti = ki[i];
+      ki[i] = ci;
+      ci = ti;
+    }
+  }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kWarps * 32)
+    reverse_max_kernel(const int64_t* __restrict__ q_offs, const int32_t* __restrict__ q_cols,
+                       const float* __restrict__ q_vals, int64_t n_q, const float* __restrict__ Z2, int64_t z_panel,
+                       int64_t n_docs, int64_t doc_base, const float* __restrict__ D1, int64_t d1_ld_row,
+                       int64_t d1_ld_panel, float* __restrict__ dout, int64_t ld_out, int k,
+                       float* __restrict__ cand_d, int64_t* __restrict__ cand_i, int64_t n_chunks_total,
+                       int64_t chunk_base) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.y * kWarps + (threadIdx.x >> 5);
+  if (q >= n_q) return;  // warp-uniform; no block-level synchronisation below
+  const int64_t j_begin = (int64_t)blockIdx.x * kChunkDocs;
+  const int64_t j_end = min(n_docs, j_begin + kChunkDocs);
+  const int64_t lo = q_offs[q], hi = q_offs[q + 1];
+  const float* d1q = D1 + (q >> 3) * d1_ld_panel + (q & 7);
+
+  float kd[KMAX];
+  int32_t ki[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    kd[i] = __int_as_float(0x7f800000);
+    ki[i] = 0x7fffffff;
+  }
+
+  for (int64_t jb = j_begin; jb < j_end; jb += 32) {
+    const int64_t jl = jb + lane;
+    const bool valid = jl < j_end;
+    const float* zj = Z2 + (jl >> 3) * z_panel + (jl & 7);
+    double acc = 0.0;
+    for (int64_t base = lo; base < hi; base += 32) {
+      const int cnt = (int)min((int64_t)32, hi - base);
+      const int32_t my_w = lane < cnt ? __ldg(q_cols + base + lane) : 0;
+      const float my_x = lane < cnt ? __ldg(q_vals + base + lane) : 0.f;
+      for (int t = 0; t < cnt; ++t) {
+        const int64_t w = __shfl_sync(0xffffffffu, my_w, t);
+        const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
+        if (valid) acc = fma(x, (double)__ldg(zj + w * 8), acc);
+      }
+    }
+    if (valid) {
+      const int64_t jg = doc_base + jl;
+      const float d = fmaxf(__ldg(d1q + jg * d1_ld_row), (float)acc);
+      if (dout) {
+        dout[jg * ld_out + q] = d;
+      } else if (d < kd[KMAX - 1] || (d == kd[KMAX - 1] && (int32_t)jg < ki[KMAX - 1])) {
+        list_insert<KMAX>(kd, ki, d, (int32_t)jg);
+      }
+    }
+  }
+  if (dout) return;
+
+  // warp-level merge of 32 sorted lane lists -> k smallest (distance, id)
+  const int64_t slot = (q * n_chunks_total + chunk_base + blockIdx.x) * (int64_t)k;
+  for (int r = 0; r < k; ++r) {
+    float bd = kd[0];
+    int32_t bi = ki[0];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (od < bd || (od == bd && oi < bi)) {
+        bd = od;
+        bi = oi;
+      }
+    }
+    if (kd[0] == bd && ki[0] == bi) {
+#pragma unroll
+      for (int i = 0; i < KMAX - 1; ++i) {
+        kd[i] = kd[i + 1];
+        ki[i] = ki[i + 1];
+      }
+      kd[KMAX - 1] = __int_as_float(0x7f800000);
+      ki[KMAX - 1] = 0x7fffffff;
+    }
+    if (lane == 0) {
+      cand_d[slot + r] = bd;
+      cand_i[slot + r] = bi == 0x7fffffff ? INT64_MAX : (int64_t)bi;
+    }
+  }
+}
+
+}  // namespace p2
+}  // namespace lcrw
+
+using namespace lcrw;
+using namespace lcrw::p2;
+
+extern "C" {
+
+int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
+              int64_t z_panel, int64_t n_seg, float* out, int64_t ld_row, int64_t ld_panel, void* stream) {
+  LCRW_REQUIRE(n_rows >= 0 && n_seg >= 0, "lcrw_spmm: bad shape");
+  if (n_rows == 0 || n_seg == 0) return LCRW_OK;
+  LCRW_REQUIRE(offs && cols && vals && Z && out, "lcrw_spmm: null pointer");
+  LCRW_REQUIRE(z_panel % 8 == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0,
+               "lcrw_spmm: Z must be 16-byte aligned with z_panel % 8 == 0");
+  const int64_t gy = ceil_div(n_seg, kSegPerBlock);
+  LCRW_REQUIRE(gy < 65536, "lcrw_spmm: too many segments for one launch");
+  int64_t gx = ceil_div(n_rows, kWarps);
+  const int64_t cap = (int64_t)sm_count() * 64;
+  if (gx > cap) gx = cap;
+  spmm_kernel<<<dim3((unsigned)gx, (unsigned)gy), kWarps * 32, 0, as_stream(stream)>>>(
+      offs, cols, vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel);
+  LCRW_CHECK_LAUNCH("spmm_kernel");
+  return LCRW_OK;
+}
+
+int lcrw_reverse_chunk_docs(void) { return kChunkDocs; }
+
+int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
+                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, const float* D1,
+                     int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k, float* cand_d,
+                     int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base, void* stream) {
+  LCRW_REQUIRE(n_q >= 0 && n_docs >= 0, "lcrw_reverse_max: bad shape");
+  if (n_q == 0 || n_docs == 0) return LCRW_OK;
+  LCRW_REQUIRE(q_offs && q_cols && q_vals && Z2 && D1, "lcrw_reverse_max: null pointer");
+  LCRW_REQUIRE(doc_base + n_docs < (1ll << 31), "lcrw_reverse_max: doc ids must fit in int32");
+  const int64_t gx = ceil_div(n_docs, kChunkDocs);
+  const int64_t gy = ceil_div(n_q, kWarps);
+  LCRW_REQUIRE(gy < 65536, "lcrw_reverse_max: too many queries for one launch");
+  dim3 grid((unsigned)gx, (unsigned)gy);
+  cudaStream_t st = as_stream(stream);
+  if (dout) {
+    reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
+                                                         D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
+                                                         nullptr, 0, 0);
+  } else {
+    LCRW_REQUIRE(k >= 1 && cand_d && cand_i, "lcrw_reverse_max: top-k mode needs k >= 1 and candidate buffers");
+    LCRW_REQUIRE(chunk_base + gx <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
+    if (k <= 16) {
+      reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
+                                                           doc_base, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
+                                                           cand_d, cand_i, n_chunks_total, chunk_base);
+    } else if (k <= 32) {
+      reverse_max_kernel<32><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
+                                                           doc_base, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
+                                                           cand_d, cand_i, n_chunks_total, chunk_base);
+    } else {
+      set_error("lcrw_reverse_max: fused top-k supports k <= 32 (got %d); use the full-matrix path", k);
+      return LCRW_ERR_UNSUPPORTED;
+    }
+  }
+  LCRW_CHECK_LAUNCH("reverse_max_kernel");
+  return LCRW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+// Top-k selection under ascending (distance, id) (kernels.py:210-232).
+//
+// lcrw_topk_segments: one CTA per segment keeps the current best KP (power of
+// two >= k) entries sorted at the front of a 2048-entry shared buffer;
+// candidates that beat the running k-th entry are appended and the buffer is
+// re-sorted with a bitonic network only when something was appended.  The
+// filter is exact (an entry not better than the k-th can never enter), so the
+// result equals a full lexicographic sort truncated to k.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace lcrw {
+namespace tk {
+
+constexpr int kBuf = 2048;
+constexpr int kThreads = 1024;
+
+struct Entry {
+  uint32_t key;  // float_key(distance)
+  int64_t id;
+};
+
+__device__ __forceinline__ bool less(uint32_t ka, int64_t ia, uint32_t kb, int64_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__device__ void bitonic_sort(uint32_t* key, int64_t* id) {
+  for (int size = 2; size <= kBuf; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < kBuf / 2; t += blockDim.x) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool up = ((i & size) == 0);
+        const uint32_t ki = key[i], kj = key[j];
+        const int64_t ii = id[i], ij = id[j];
+        const bool swap = up ? less(kj, ij, ki, ii) : less(ki, ii, kj, ij);
+        if (swap) {
+          key[i] = kj;
+          key[j] = ki;
+          id[i] = ij;
+          id[j] = ii;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads)
+    topk_segments_kernel(const float* __restrict__ d, const int64_t* __restrict__ ids, int64_t seg_len, int k, int kp,
+                         float* __restrict__ out_d, int64_t* __restrict__ out_i) {
+  __shared__ uint32_t key[kBuf];
+  __shared__ int64_t idb[kBuf];
+  __shared__ int count;
+  const int64_t seg = blockIdx.x;
+  const float* ds = d + seg * seg_len;
+  const int64_t* is = ids + seg * seg_len;
+  for (int i = threadIdx.x; i < kBuf; i += blockDim.x) {
+    key[i] = 0xFFFFFFFFu;
+    idb[i] = INT64_MAX;
+  }
+  if (threadIdx.x == 0) count = 0;
+  __syncthreads();
+  const int cap = kBuf - kp;  // append area (>= 1024 == blockDim)
+  for (int64_t base = 0; base < seg_len; base += blockDim.x) {
+    const uint32_t thr_k = key[k - 1];
+    const int64_t thr_i = idb[k - 1];
+    const int64_t i = base + threadIdx.x;
+    if (i < seg_len) {
+      const uint32_t kk = float_key(ds[i]);
+      const int64_t ii = is[i];
+      if (less(kk, ii, thr_k, thr_i)) {
+        const int pos = atomicAdd(&count, 1);
+        key[kp + pos] = kk;
+        idb[kp + pos] = ii;
+      }
+    }
+    __syncthreads();
+    const int n_new = count;
+    if (n_new > 0) {
+      for (int t = kp + n_new + threadIdx.x; t < kBuf; t += blockDim.x) {
+        key[t] = 0xFFFFFFFFu;
+        idb[t] = INT64_MAX;
+      }
+      bitonic_sort(key, idb);
+      if (threadIdx.x == 0) count = 0;
+      // the tail beyond kp is garbage-free after the sort (sentinels refilled next round)
+      for (int t = kp + threadIdx.x; t < kBuf; t += blockDim.x) {
+        key[t] = 0xFFFFFFFFu;
+        idb[t] = INT64_MAX;
+      }
+    }
+    __syncthreads();
+    (void)cap;
+  }
+  const int kk = (int)min((int64_t)k, seg_len);
+  for (int r = threadIdx.x; r < kk; r += blockDim.x) {
+    out_d[seg * k + r] = key_float(key[r]);
+    out_i[seg * k + r] = idb[r];
+  }
+}
+
+__global__ void keys_kernel(const float* __restrict__ d, const int64_t* __restrict__ perm, int64_t n,
+                            uint32_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = float_key(d[perm ? perm[i] : i]);
+}
+
+__global__ void iota_kernel(int64_t* __restrict__ v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = i;
+}
+
+__global__ void emit_kernel(const float* __restrict__ d, const int64_t* __restrict__ ids,
+                            const int64_t* __restrict__ pos_by_id, const int64_t* __restrict__ order, int64_t k,
+                            float* __restrict__ out_d, int64_t* __restrict__ out_i) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < k; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos_by_id[order[r]];
+    out_d[r] = d[p];
+    out_i[r] = ids[p];
+  }
+}
+
+}  // namespace tk
+}  // namespace lcrw
+
+using namespace lcrw;
+using namespace lcrw::tk;
+
+extern "C" {
+
+int lcrw_topk_segments(const float* d, const int64_t* ids, int64_t n_seg, int64_t seg_len, int k, float* out_d,
+                       int64_t* out_i, void* stream) {
+  LCRW_REQUIRE(k >= 1, "k must be >= 1");
+  LCRW_REQUIRE(n_seg >= 0 && seg_len >= 0, "lcrw_topk_segments: bad shape");
+  if (n_seg == 0 || seg_len == 0) return LCRW_OK;
+  if (k > 1024) {
+    set_error("lcrw_topk_segments: k=%d > 1024 (use lcrw_topk_sort)", k);
+    return LCRW_ERR_UNSUPPORTED;
+  }
+  LCRW_REQUIRE(d && ids && out_d && out_i, "lcrw_topk_segments: null pointer");
+  LCRW_REQUIRE(n_seg < (1ll << 31), "lcrw_topk_segments: too many segments");
+  int kp = 1;
+  while (kp < k) kp <<= 1;
+  topk_segments_kernel<<<(unsigned)n_seg, kThreads, 0, as_stream(stream)>>>(d, ids, seg_len, k, kp, out_d, out_i);
+  LCRW_CHECK_LAUNCH("topk_segments_kernel");
+  return LCRW_OK;
+}
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+int lcrw_topk_sort_workspace(int64_t n, size_t* bytes) {
+  LCRW_REQUIRE(n >= 0 && bytes, "lcrw_topk_sort_workspace: bad arguments");
+  size_t c1 = 0, c2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, c1, (const int64_t*)nullptr, (int64_t*)nullptr, (const int64_t*)nullptr,
+                                  (int64_t*)nullptr, (int64_t)n);
+  cub::DeviceRadixSort::SortPairs(nullptr, c2, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n);
+  // sorted ids, iota/positions, positions by id, keys in/out, rank iota, order
+  *bytes = 6 * align256((size_t)n * 8) + (c1 > c2 ? c1 : c2);
+  return LCRW_OK;
+}
+
+// Two stable radix passes: by id, then by distance key -> lexicographic (distance, id).
+int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, float* out_d, int64_t* out_i, void* ws,
+                   size_t ws_bytes, void* stream) {
+  LCRW_REQUIRE(k >= 1, "k must be >= 1");
+  LCRW_REQUIRE(n >= 0, "lcrw_topk_sort: bad shape");
+  if (n == 0) return LCRW_OK;
+  LCRW_REQUIRE(d && ids && out_d && out_i && ws, "lcrw_topk_sort: null pointer");
+  size_t need = 0;
+  lcrw_topk_sort_workspace(n, &need);
+  LCRW_REQUIRE(ws_bytes >= need, "lcrw_topk_sort: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  char* p = static_cast<char*>(ws);
+  const size_t a = align256((size_t)n * 8);
+  int64_t* ids_sorted = reinterpret_cast<int64_t*>(p);
+  int64_t* pos = reinterpret_cast<int64_t*>(p + a);
+  int64_t* pos_sorted = reinterpret_cast<int64_t*>(p + 2 * a);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(p + 3 * a);
+  uint32_t* keys_sorted = reinterpret_cast<uint32_t*>(p + 4 * a);
+  int64_t* rank = reinterpret_cast<int64_t*>(p + 5 * a);
+  int64_t* order = ids_sorted;  // reused after pass 1
+  void* cub_ws = p + 6 * a;
+  size_t cub_bytes = need - 6 * a;
+  const unsigned g = (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  iota_kernel<<<g, 256, 0, st>>>(pos, n);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, ids, ids_sorted, pos, pos_sorted, n, 0, 64, st);
+  if (e != cudaSuccess) return cuda_status(e, "cub SortPairs (ids)");
+  keys_kernel<<<g, 256, 0, st>>>(d, pos_sorted, n, keys);
+  iota_kernel<<<g, 256, 0, st>>>(rank, n);
+  e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, keys, keys_sorted, rank, order, n, 0, 32, st);
+  if (e != cudaSuccess) return cuda_status(e, "cub SortPairs (keys)");
+  const int64_t kk = k < n ? k : n;
+  emit_kernel<<<g, 256, 0, st>>>(d, ids, pos_sorted, order, kk, out_d, out_i);
+  LCRW_CHECK_LAUNCH("topk emit");
+  return LCRW_OK;
+}
+
+}  // extern "C"

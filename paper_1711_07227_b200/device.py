@@ -1,0 +1,375 @@
+"""HBM-resident data and the LC-RWMD pipeline over the C ABI.
+
+PyTorch is used only as plumbing here: it owns device memory (caching
+allocator), the current stream and host<->device copies.  Every arithmetic
+step of the path is one of our sm_100a kernels, invoked through ``_lib``.
+
+Pipeline for ``lcrwmd_topk`` / ``lcrwmd_full`` (distances.py:244-264):
+
+  prepare E   f16 operand rows (power-of-two scaled), fp32 norms, identity classes
+  restrict    x1 -> (remap1, used1);  x2 -> (remap2, used2)       corpus.py:405-426
+  forward     Z1 = phase1(E[used1], E[x2 words]) ; D1 = spmm(x1r, Z1)   distances.py:262
+  reverse     per doc batch: Z2 = phase1(E[used2], E[batch words]);
+              D = max(D1, spmm(x2r, Z2)) -> per-(query, chunk) top-k  distances.py:263-264
+  merge       per-query top-k over the chunk candidates            kernels.py:210-232
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .corpus import CorpusError, HistogramSet
+
+# ---------------------------------------------------------------------------
+# plumbing
+# ---------------------------------------------------------------------------
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1711_07227_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _p(t) -> C.c_void_p | None:
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def sm_count() -> int:
+    out = C.c_int(0)
+    _lib.call("lcrw_sm_count", C.byref(out))
+    return out.value
+
+
+def padded_dim(m: int) -> int:
+    return int(_lib.value("lcrw_padded_dim", m))
+
+
+def to_device(a, dtype, non_blocking: bool = True) -> torch.Tensor:
+    """Host array -> device tensor (async when the host buffer is pinned)."""
+    dev = require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype, non_blocking=non_blocking).contiguous()
+    arr = np.ascontiguousarray(a)
+    t = torch.from_numpy(arr)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(dev, non_blocking=non_blocking and t.is_pinned())
+
+
+def _launch_count_hint():  # pragma: no cover - documentation only
+    """Kernels per call are counted by bench.py via torch.cuda profiler-free bookkeeping."""
+
+
+# ---------------------------------------------------------------------------
+# resident data
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class DeviceCSR:
+    """A HistogramSet in HBM (int64 offsets, int32 ids, f32 weights) plus host offsets for planning."""
+
+    offsets: torch.Tensor
+    cols: torch.Tensor
+    vals: torch.Tensor
+    n_cols: int
+    host_offsets: np.ndarray
+
+    @property
+    def n_rows(self) -> int:
+        return len(self.host_offsets) - 1
+
+    @property
+    def nnz(self) -> int:
+        return int(self.host_offsets[-1])
+
+    @classmethod
+    def upload(cls, x: HistogramSet, name: str = "x") -> "DeviceCSR":
+        offs = np.asarray(x.row_offsets, dtype=np.int64)
+        if x.n_rows and np.any(np.diff(offs) <= 0):
+            raise CorpusError(f"{name}: every row must hold at least one word")
+        if int(offs[0]) != 0 or len(x.column_ids) != int(offs[-1]) or len(x.values) != int(offs[-1]):
+            raise CorpusError(f"{name}: offset/array length mismatch")
+        return cls(to_device(offs, torch.int64), to_device(x.column_ids, torch.int32),
+                   to_device(x.values, torch.float32), int(x.n_cols), offs)
+
+
+class PreparedEmbeddings:
+    """E in HBM: f32 original, f16 operand rows, norms, scale and identity classes.
+
+    ``extra`` arrays (e.g. free query vectors for nearest_word_distances)
+    take part in the power-of-two scale choice so they share E's scaling."""
+
+    def __init__(self, embeddings, extra=()):
+        dev = require_cuda()
+        st = _stream()
+        self.E32 = to_device(np.asarray(embeddings, dtype=np.float32) if not isinstance(embeddings, torch.Tensor)
+                             else embeddings, torch.float32)
+        if self.E32.dim() != 2:
+            raise ValueError("embeddings must be a 2-d (v, m) matrix")
+        self.V, self.m = int(self.E32.shape[0]), int(self.E32.shape[1])
+        self.kp = padded_dim(self.m)
+        amax = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("lcrw_absmax", _p(self.E32), self.V * self.m, _p(amax), st)
+        for x in extra:
+            _lib.call("lcrw_absmax", _p(x), x.numel(), _p(amax), st)
+        self.scale = torch.empty(2, dtype=torch.float32, device=dev)
+        _lib.call("lcrw_scale_from_absmax", _p(amax), _p(self.scale), st)
+        self.Eh = torch.empty((self.V, self.kp), dtype=torch.float16, device=dev)
+        self.norms = torch.empty(self.V, dtype=torch.float32, device=dev)
+        _lib.call("lcrw_prepare_rows", _p(self.E32), self.V, self.m, self.kp, _p(self.scale), _p(self.Eh),
+                  _p(self.norms), st)
+        # exact-identity classes (kernels.py:91-92 semantics)
+        ws_bytes = C.c_size_t(0)
+        _lib.call("lcrw_row_classes_workspace", self.V, C.byref(ws_bytes))
+        ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=dev)
+        self.canon = torch.empty(self.V, dtype=torch.int32, device=dev)
+        self.next = torch.empty(self.V, dtype=torch.int32, device=dev)
+        self.sorted_hash = torch.empty(self.V, dtype=torch.int64, device=dev)
+        self.sorted_ids = torch.empty(self.V, dtype=torch.int32, device=dev)
+        n_dup = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.call("lcrw_row_classes", _p(self.E32), self.V, self.m, _p(self.canon), _p(self.next), _p(n_dup),
+                  _p(self.sorted_hash), _p(self.sorted_ids), _p(ws), ws_bytes.value, st)
+        self.n_dup = int(n_dup.item())
+
+    def prepare_free_rows(self, Q: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        """f16 operand rows for vectors that are not rows of E (same scale)."""
+        n = int(Q.shape[0])
+        Qh = torch.empty((n, self.kp), dtype=torch.float16, device=Q.device)
+        qn = torch.empty(n, dtype=torch.float32, device=Q.device)
+        _lib.call("lcrw_prepare_rows", _p(Q), n, self.m, self.kp, _p(self.scale), _p(Qh), _p(qn), _stream())
+        return Qh, qn
+
+    def representatives(self, word_ids: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
+        """(rep, next) arguments of lcrw_zero_identical for rows given by E ids."""
+        if self.n_dup == 0:
+            return word_ids, None
+        rep = torch.empty_like(word_ids)
+        _lib.call("lcrw_remap_ids", _p(word_ids), word_ids.numel(), _p(self.canon), _p(rep), _stream())
+        return rep, self.next
+
+
+# ---------------------------------------------------------------------------
+# building blocks
+# ---------------------------------------------------------------------------
+
+
+def restrict(cols: torch.Tensor, n_cols: int) -> tuple[torch.Tensor, torch.Tensor, int]:
+    """(remap, used[:n_used], n_used) of corpus.py:405-426 (reads back one scalar)."""
+    dev = cols.device
+    ws_bytes = C.c_size_t(0)
+    _lib.call("lcrw_restrict_workspace", n_cols, C.byref(ws_bytes))
+    ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=dev)
+    remap = torch.empty(n_cols, dtype=torch.int32, device=dev)
+    used = torch.empty(n_cols, dtype=torch.int32, device=dev)
+    n_used = torch.empty(1, dtype=torch.int64, device=dev)
+    _lib.call("lcrw_restrict", _p(cols), cols.numel(), n_cols, _p(remap), _p(used), _p(n_used), _p(ws),
+              ws_bytes.value, _stream())
+    n = int(n_used.item())
+    return remap, used[:n], n
+
+
+def remap_ids(cols: torch.Tensor, remap: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(cols)
+    _lib.call("lcrw_remap_ids", _p(cols), cols.numel(), _p(remap), _p(out), _stream())
+    return out
+
+
+def gather_rows(prep: PreparedEmbeddings, ids: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    n = ids.numel()
+    T = torch.empty((max(n, 1), prep.kp), dtype=torch.float16, device=ids.device)
+    tn = torch.empty(max(n, 1), dtype=torch.float32, device=ids.device)
+    _lib.call("lcrw_gather_rows", _p(prep.Eh), _p(prep.norms), prep.kp, _p(ids), n, _p(T), _p(tn), _stream())
+    return T, tn
+
+
+def _range_cols(b_rows: int, a_rows: int) -> int:
+    n_mtiles = max(1, (a_rows + 127) // 128)
+    want = (n_mtiles * b_rows) // (8 * sm_count())
+    return int(min(32768, max(1024, (want + 255) // 256 * 256)))
+
+
+def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor, b_norms: torch.Tensor,
+           b_rows: int, seg_offsets: torch.Tensor, n_seg: int, prep: PreparedEmbeddings,
+           range_cols: int | None = None) -> tuple[torch.Tensor, int]:
+    """Z (panel layout, z_panel = 8 * a_rows) of distances.py:147-178, without the exact-zero pass."""
+    dev = A.device
+    st = _stream()
+    rc = range_cols or _range_cols(b_rows, a_rows)
+    n_ranges = int(_lib.value("lcrw_plan_ranges", b_rows, rc))
+    endmask = torch.empty(int(_lib.value("lcrw_endmask_words", b_rows)), dtype=torch.int32, device=dev)
+    range_seg = torch.empty(n_ranges + 1, dtype=torch.int32, device=dev)
+    _lib.call("lcrw_segment_plan", _p(seg_offsets), n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
+    z_panel = 8 * max(a_rows, 1)
+    Z = torch.empty(((n_seg + 7) // 8) * z_panel, dtype=torch.float32, device=dev)
+    _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), _p(b_norms), b_rows, prep.m, prep.kp,
+              _p(seg_offsets), n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel, st)
+    return Z, z_panel
+
+
+def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel) -> None:
+    _lib.call("lcrw_zero_identical", _p(seg_offsets), n_seg, _p(rep), _p(nxt), _p(remap), _p(Z), z_panel,
+              _stream())
+
+
+def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel) -> None:
+    _lib.call("lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, n_seg, _p(out),
+              ld_row, ld_panel, _stream())
+
+
+def topk_rows(d: torch.Tensor, ids: torch.Tensor, n_seg: int, seg_len: int, k: int):
+    """Per-segment k smallest (distance, id); k <= 1024."""
+    kk = min(k, seg_len)
+    out_d = torch.empty((n_seg, k), dtype=torch.float32, device=d.device)
+    out_i = torch.empty((n_seg, k), dtype=torch.int64, device=d.device)
+    _lib.call("lcrw_topk_segments", _p(d), _p(ids), n_seg, seg_len, k, _p(out_d), _p(out_i), _stream())
+    return out_d[:, :kk], out_i[:, :kk]
+
+
+def topk_sort(d: torch.Tensor, ids: torch.Tensor, k: int):
+    n = d.numel()
+    ws_bytes = C.c_size_t(0)
+    _lib.call("lcrw_topk_sort_workspace", n, C.byref(ws_bytes))
+    ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=d.device)
+    kk = min(k, n)
+    out_d = torch.empty(max(kk, 1), dtype=torch.float32, device=d.device)
+    out_i = torch.empty(max(kk, 1), dtype=torch.int64, device=d.device)
+    _lib.call("lcrw_topk_sort", _p(d), _p(ids), n, k, _p(out_d), _p(out_i), _p(ws), ws_bytes.value, _stream())
+    return out_d[:kk], out_i[:kk]
+
+
+# ---------------------------------------------------------------------------
+# one direction and the symmetric pipeline
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Restricted:
+    """A resident set restricted to its own words (corpus.py:405-426), on device."""
+
+    csr: DeviceCSR
+    remap: torch.Tensor
+    used: torch.Tensor
+    v_e: int
+    cols_r: torch.Tensor
+    A: torch.Tensor
+    a_norms: torch.Tensor
+
+    @classmethod
+    def build(cls, x: DeviceCSR, prep: PreparedEmbeddings) -> "Restricted":
+        remap, used, v_e = restrict(x.cols, x.n_cols)
+        A, an = gather_rows(prep, used)
+        return cls(x, remap, used, v_e, remap_ids(x.cols, remap), A, an)
+
+
+def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
+                      n_seg: int) -> tuple[torch.Tensor, int]:
+    """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros)."""
+    B, bn = gather_rows(prep, word_ids)
+    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, bn, word_ids.numel(), seg_offsets, n_seg, prep)
+    rep, nxt = prep.representatives(word_ids)
+    zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp)
+    return Z, zp
+
+
+def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR, layout: str = "rows") -> torch.Tensor:
+    """distances.py:181-204 for all queries at once: (n_res, n_q) bounds.
+
+    layout "rows" -> row-major (n_res, n_q); "panels" -> out[(q>>3)*8*n_res + i*8 + (q&7)]."""
+    n_res, n_q = res.csr.n_rows, queries.n_rows
+    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q)
+    if layout == "rows":
+        out = torch.empty(n_res * max(n_q, 1), dtype=torch.float32, device=Z.device)
+        ld_row, ld_panel = n_q, 8
+    else:
+        out = torch.empty(((n_q + 7) // 8) * 8 * n_res, dtype=torch.float32, device=Z.device)
+        ld_row, ld_panel = 8, 8 * n_res
+    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel)
+    return out
+
+
+def _doc_batches(host_offsets: np.ndarray, v_e2: int, budget_bytes: int) -> list[tuple[int, int]]:
+    n = len(host_offsets) - 1
+    chunk = int(_lib.value("lcrw_reverse_chunk_docs"))
+    per_doc = 4 * max(v_e2, 1)
+    nb = max(8, budget_bytes // per_doc)
+    nb = (nb // chunk) * chunk if nb >= chunk else max(8, (nb // 8) * 8)
+    return [(j0, min(n, j0 + nb)) for j0 in range(0, n, nb)]
+
+
+def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
+              z2_budget_bytes: int = 8 << 30):
+    """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, k) dists, ids)."""
+    n1, n2 = x1.n_rows, x2.n_rows
+    dev = x1.cols.device
+    st = _stream()
+    res1 = Restricted.build(x1, prep)
+    d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
+    del res1
+    res2 = Restricted.build(x2, prep)
+    batches = _doc_batches(x1.host_offsets, res2.v_e, z2_budget_bytes)
+    chunk = int(_lib.value("lcrw_reverse_chunk_docs"))
+    if k is None:
+        dout = torch.empty(n1 * n2, dtype=torch.float32, device=dev)
+        cand_d = cand_i = None
+        n_chunks = 0
+    else:
+        dout = None
+        n_chunks = sum((b1 - b0 + chunk - 1) // chunk for b0, b1 in batches)
+        cand_d = torch.empty(n2 * n_chunks * k, dtype=torch.float32, device=dev)
+        cand_i = torch.empty(n2 * n_chunks * k, dtype=torch.int64, device=dev)
+    chunk_base = 0
+    for j0, j1 in batches:
+        lo, hi = int(x1.host_offsets[j0]), int(x1.host_offsets[j1])
+        seg = x1.offsets[j0:j1 + 1] - lo
+        Z2, zp2 = nearest_distances(res2, prep, seg, x1.cols[lo:hi], j1 - j0)
+        _lib.call("lcrw_reverse_max", _p(x2.offsets), _p(res2.cols_r), _p(x2.vals), n2, _p(Z2), zp2, j1 - j0, j0,
+                  _p(d1), 8, 8 * n1, _p(dout), n2, k or 0, _p(cand_d), _p(cand_i), n_chunks, chunk_base, st)
+        chunk_base += (j1 - j0 + chunk - 1) // chunk
+        del Z2
+    if k is None:
+        return dout.view(n1, n2)
+    if k <= 1024:
+        return topk_rows(cand_d, cand_i, n2, n_chunks * k, k)
+    raise NotImplementedError("k > 1024")
+
+
+def nearest_word_distances(E, Q) -> torch.Tensor:
+    """distances.py:133-144 on device: z over every row of E for one free query."""
+    dev = require_cuda()
+    Qd = to_device(np.atleast_2d(np.asarray(Q, dtype=np.float32)) if not isinstance(Q, torch.Tensor) else Q,
+                   torch.float32)
+    prep = PreparedEmbeddings(E, extra=(Qd,))
+    if Qd.shape[1] != prep.m:
+        raise ValueError(f"dimension mismatch: {prep.m} vs {Qd.shape[1]}")
+    nq = int(Qd.shape[0])
+    Qh, qn = prep.prepare_free_rows(Qd)
+    seg = torch.tensor([0, nq], dtype=torch.int64, device=dev)
+    Z, zp = phase1(prep.Eh, prep.norms, prep.V, Qh, qn, nq, seg, 1, prep)
+    rep = torch.empty(nq, dtype=torch.int32, device=dev)
+    _lib.call("lcrw_match_rows", _p(Qd), nq, _p(prep.E32), prep.m, _p(prep.sorted_hash), _p(prep.sorted_ids),
+              prep.V, _p(prep.canon), _p(rep), _stream())
+    zero_identical(seg, 1, rep, prep.next, None, Z, zp)
+    return Z[: zp].view(prep.V, 8)[:, 0]
+
+
+def restrict_vocabulary_host(x: HistogramSet, embeddings):
+    """corpus.restrict_vocabulary on the GPU; returns host (set, E rows, remap)."""
+    dx = DeviceCSR.upload(x, "hist_set")
+    remap, used, n = restrict(dx.cols, dx.n_cols)
+    cols_r = remap_ids(dx.cols, remap)
+    used_h = used.cpu().numpy()
+    out = HistogramSet(np.asarray(x.row_offsets, dtype=np.int64).copy(), cols_r.cpu().numpy(),
+                       np.asarray(x.values, dtype=np.float32).copy(), n)
+    return out, np.ascontiguousarray(np.asarray(embeddings)[used_h]), remap.cpu().numpy()

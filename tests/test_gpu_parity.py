@@ -1,0 +1,213 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the pinned CPU oracle.
+
+Tolerances (written here, justified in DESIGN.md §Precision):
+  * distances: |d - d_ref| <= 1e-4 * |d_ref| + 1e-5      (f16 operands = 11-bit
+    significand like TF32-RN, fp32 tensor-core accumulation)
+  * exact zeros where the reference has them (identical vectors)
+  * spmm / topk_select / restrict_vocabulary: bitwise
+  * top-k ids: identical except where the reference's k-th and (k+1)-th
+    distances are within the distance tolerance (ties)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_case, rel_close
+from oracle import lcrwmd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1711_07227_b200 import _lib
+    _lib.load()
+
+
+def _pkg():
+    from paper_1711_07227_b200 import corpus, distances, kernels
+    return corpus, distances, kernels
+
+
+def _check_topk(d, i, dref_full, k):
+    """Tie-aware top-k check against a full reference matrix (n1, n2)."""
+    n1, n2 = dref_full.shape
+    for j in range(n2):
+        col = dref_full[:, j].astype(np.float64)
+        rd, ri = O.topk_select(dref_full[:, j], np.arange(n1), k)
+        kk = len(ri)
+        assert len(i[j]) == kk
+        # our distances agree with the reference distances of the ids we returned
+        ok, err = rel_close(d[j], col[i[j]], RTOL, ATOL)
+        assert ok, (j, err)
+        # and with the reference's k best values position by position
+        ok, err = rel_close(d[j], rd, RTOL, ATOL)
+        assert ok, (j, err)
+        # ids identical except inside tie bands
+        tol = RTOL * np.abs(rd) + ATOL
+        for r in range(kk):
+            if i[j][r] != ri[r]:
+                assert abs(col[i[j][r]] - rd[r]) <= 2 * tol[r] + 1e-6, (j, r)
+
+
+def test_golden_full_batched_onesided(golden_case):
+    name, z, x1, x2 = golden_case
+    _, D, _ = _pkg()
+    E = z["E"]
+    full = D.lcrwmd_full(x1, x2, E).values
+    ok, err = rel_close(full, z["full"], RTOL, ATOL)
+    assert ok, (name, "full", err)
+    assert np.array_equal(full == 0, z["full"] == 0), name
+    bat = D.lcrwmd_batched(x1, x2, E)
+    ok, err = rel_close(bat, z["batched"], RTOL, ATOL)
+    assert ok, (name, "batched", err)
+    assert np.array_equal(bat == 0, z["batched"] == 0), name
+    one = D.lcrwmd_one_sided(x1, x2.row(0), E)
+    ok, err = rel_close(one, z["one_sided0"], RTOL, ATOL)
+    assert ok, (name, "one_sided", err)
+    q0 = x2.row(0)
+    nwd = D.nearest_word_distances(E, E[q0.word_ids])
+    ok, err = rel_close(nwd, z["nwd0"], RTOL, 1e-4)
+    assert ok, (name, "nwd", err)
+    assert np.array_equal(nwd == 0, z["nwd0"] == 0), name
+
+
+def test_golden_topk(golden_case):
+    name, z, x1, x2 = golden_case
+    _, D, _ = _pkg()
+    k = int(z["topk_k"])
+    res = D.lcrwmd_topk(x1, x2, z["E"], k)
+    d = [r.distances for r in res]
+    i = [r.ids for r in res]
+    _check_topk(d, i, z["full"], k)
+
+
+def test_golden_restrict_spmm(golden_case):
+    name, z, x1, x2 = golden_case
+    C, _, K = _pkg()
+    xr, er, remap = C.restrict_vocabulary(x1, z["E"])
+    assert np.array_equal(xr.column_ids, z["r1_ids"])
+    assert np.array_equal(er, z["r1_E"])
+    assert np.array_equal(remap, z["r1_remap"])
+    assert np.array_equal(K.spmm(x1, z["spmm_z"]), z["spmm"])  # bitwise (fp64 accumulation)
+    assert np.array_equal(K.spmv(x1, z["spmm_z"][:, 2]), z["spmm"][:, 2])
+
+
+def test_golden_topk_select_merge():
+    _, _, K = _pkg()
+    z = np.load(GOLDEN / "topk.npz")
+    for k in (1, 10, 128, 20_000):
+        r = K.topk_select(z["d"], z["ids"], k)
+        assert np.array_equal(r.distances, z[f"d{k}"]), k
+        assert np.array_equal(r.ids, z[f"i{k}"]), k
+    parts = [K.topk_select(z["d"][a:a + 2500], z["ids"][a:a + 2500], 64) for a in range(0, 10_000, 2500)]
+    m = K.topk_merge(parts, 64)
+    assert np.array_equal(m.distances, z["merge_d"]) and np.array_equal(m.ids, z["merge_i"])
+
+
+def test_spec_known_answers():
+    C, D, K = _pkg()
+    E = np.array([[0, 0], [1, 0], [0, 2]], dtype=np.float32)
+    x1 = C.HistogramSet(np.array([0, 2]), np.array([0, 1], np.int32), np.array([.5, .5], np.float32), 3)
+    x2 = C.HistogramSet(np.array([0, 2]), np.array([1, 2], np.int32), np.array([.5, .5], np.float32), 3)
+    assert D.lcrwmd_full(x1, x2, E).values[0, 0] == pytest.approx(1.0, rel=1e-6)
+    z = D.nearest_word_distances(np.array([[0, 0]], np.float32), np.array([[3, 4]], np.float32))
+    assert z[0] == pytest.approx(5.0, rel=1e-6)
+    xs = C.HistogramSet(np.array([0, 1]), np.array([2], np.int32), np.array([1.0], np.float32), 4)
+    assert K.spmm(xs, np.array([[5], [6], [7], [8]], np.float32))[0, 0] == 7.0
+    r = K.topk_select(np.array([3, 1, 2], np.float32), np.array([0, 1, 2]), 2)
+    assert list(r.ids) == [1, 2] and list(r.distances) == [1, 2]
+    r = K.topk_select(np.array([1.0, 1.0], np.float32), np.array([7, 3]), 1)
+    assert list(r.ids) == [3]
+    # X1 == X2 -> zero diagonal
+    z0, a, _ = load_case("small_m16")
+    d = D.lcrwmd_full(a, a, z0["E"]).values
+    assert np.all(np.diag(d) == 0)
+    ok, err = rel_close(d, d.T, 1e-6, 1e-6)  # symmetry when X1 == X2
+    assert ok, err
+
+
+def test_errors_match_reference():
+    C, D, K = _pkg()
+    z, x1, x2 = load_case("small_m16")
+    with pytest.raises(ValueError, match="do not match embedding rows"):
+        D.lcrwmd_full(x1, x2, z["E"][:-1])
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        K.topk_select(np.zeros(3, np.float32), np.arange(3), 0)
+    with pytest.raises(ValueError, match="spmm expects a 2-d right-hand side"):
+        K.spmm(x1, np.zeros(x1.n_cols, np.float32))
+    with pytest.raises(ValueError, match="batch must hold at least one query"):
+        D.lcrwmd_batched(x1, x1.slice_rows(0, 0), z["E"])
+    bad = C.HistogramSet(np.array([0, 1, 1]), np.array([3], np.int32), np.array([1.0], np.float32), x1.n_cols)
+    with pytest.raises(C.CorpusError, match="at least one word"):
+        D.lcrwmd_full(bad, x2, z["E"])
+
+
+@pytest.mark.parametrize("clustered", [False, True])
+def test_c1_shaped_vs_oracle(clustered):
+    """Config-1 shape (m=300, h~40) at reduced n: symmetric + one-sided + top-k vs the oracle."""
+    from paper_1711_07227_b200 import synthetic as S
+    _, D, _ = _pkg()
+    V = 5000
+    E = S.embeddings(V, 300, seed=3, clustered=clustered, centers=200)
+    x1 = S.histograms(600, V, 40, seed=4)
+    x2 = S.histograms(40, V, 40, seed=5)
+    ref = O.lcrwmd_full(x1, x2, E, threads=8)
+    got = D.lcrwmd_full(x1, x2, E).values
+    ok, err = rel_close(got, ref, RTOL, ATOL)
+    assert ok, err
+    res = D.lcrwmd_topk(x1, x2, E, 10)
+    _check_topk([r.distances for r in res], [r.ids for r in res], ref, 10)
+    one = D.lcrwmd_batched(x1, x2, E)
+    ref1 = O.lcrwmd_batched(x1, x2, E)
+    ok, err = rel_close(one, ref1, RTOL, ATOL)
+    assert ok, err
+
+
+def test_queries_from_docs_exact_self_match():
+    """Paper protocol: queries sampled from the resident set -> self at distance exactly 0."""
+    from paper_1711_07227_b200 import synthetic as S
+    _, D, _ = _pkg()
+    V = 3000
+    E = S.embeddings(V, 300, seed=8)
+    x1 = S.histograms(900, V, 30, seed=9)
+    idx = np.arange(5, 900, 37)
+    x2 = x1.take_rows(idx)
+    res = D.lcrwmd_topk(x1, x2, E, 3)
+    for j, r in enumerate(res):
+        assert r.distances[0] == 0.0 and r.ids[0] == idx[j]
+
+
+def test_large_sampled_parity_and_batching():
+    """Many docs (multiple reverse batches, many Phase-1 ranges): sampled parity by subset invariance."""
+    import torch
+    from paper_1711_07227_b200 import device, synthetic as S
+    V = 20000
+    E = S.embeddings(V, 300, seed=21)
+    x1 = S.histograms(30000, V, 50, seed=22)
+    x2 = S.histograms(64, V, 50, seed=23)
+    prep = device.PreparedEmbeddings(E)
+    d1 = device.DeviceCSR.upload(x1)
+    d2 = device.DeviceCSR.upload(x2)
+    full = device.symmetric(d1, d2, prep, None, z2_budget_bytes=4 * 200 * 8192).cpu().numpy()
+    rng = np.random.default_rng(0)
+    di = np.sort(rng.choice(30000, 300, replace=False))
+    qj = np.sort(rng.choice(64, 12, replace=False))
+    ref = O.lcrwmd_full(x1.take_rows(di), x2.take_rows(qj), E, threads=8)
+    ok, err = rel_close(full[np.ix_(di, qj)], ref, RTOL, ATOL)
+    assert ok, err
+    # fused top-k over several doc batches == top-k of the full matrix
+    td, ti = device.symmetric(d1, d2, prep, 10, z2_budget_bytes=4 * 200 * 8192)
+    td, ti = td.cpu().numpy(), ti.cpu().numpy()
+    for j in range(64):
+        rd, ri = O.topk_select(full[:, j], np.arange(30000), 10)
+        assert np.array_equal(td[j], rd) and np.array_equal(ti[j], ri)
+    torch.cuda.synchronize()

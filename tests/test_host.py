@@ -1,0 +1,125 @@
+"""CPU-only tests: host data model, ingestion, layout helpers, and that the C-ABI
+library loads and exports every symbol include/lcrwmd.h declares."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import struct
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_1711_07227_b200 import corpus as C
+from paper_1711_07227_b200 import synthetic as S
+
+
+def test_header_symbols_exported_and_bound():
+    from paper_1711_07227_b200 import _build, _lib
+    _build.build()
+    header = (ROOT / "include" / "lcrwmd.h").read_text()
+    declared = set(re.findall(r"\b(lcrw_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    for name in declared:
+        assert hasattr(lib, name), name
+    # pure host entry points work without a GPU
+    assert _lib.value("lcrw_abi_version") == 1
+    assert _lib.value("lcrw_padded_dim", 300) == 320
+    assert _lib.value("lcrw_padded_dim", 37) == 64
+    assert _lib.value("lcrw_plan_ranges", 1000, 256) == 4
+    assert _lib.value("lcrw_status_string", 1) == b"invalid argument"
+
+
+def test_library_rejects_bad_arguments_without_gpu():
+    from paper_1711_07227_b200 import _lib
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        _lib.call("lcrw_topk_segments", None, None, 1, 1, 0, None, None, None)
+    with pytest.raises(ValueError, match="kp must be"):
+        _lib.call("lcrw_phase1", None, None, 0, None, None, 0, 300, 300, None, 1, None, None, 1, None, None, 0,
+                  None)
+
+
+def test_histogram_set_basics():
+    x = S.histograms(50, 200, 10, seed=0)
+    x.validate()
+    assert x.n_rows == 50 and x.nnz == len(x.column_ids)
+    sub = x.take_rows([3, 1, 3])
+    assert np.array_equal(sub.row(0).word_ids, x.row(3).word_ids)
+    assert np.array_equal(sub.row(1).weights, x.row(1).weights)
+    s = x.slice_rows(10, 20)
+    assert s.n_rows == 10 and np.array_equal(s.row(0).word_ids, x.row(10).word_ids)
+    fr = C.HistogramSet.from_rows([(x.row(i).word_ids, x.row(i).weights) for i in range(5)], 200)
+    assert np.array_equal(fr.column_ids, x.slice_rows(0, 5).column_ids)
+
+
+def test_validate_errors():
+    good = C.HistogramSet(np.array([0, 2]), np.array([1, 3], np.int32), np.array([.5, .5], np.float32), 5)
+    good.validate()
+    with pytest.raises(C.CorpusError, match="at least one word"):
+        C.HistogramSet(np.array([0, 0]), np.zeros(0, np.int32), np.zeros(0, np.float32), 5).validate()
+    with pytest.raises(C.CorpusError, match="strictly increasing"):
+        C.HistogramSet(np.array([0, 2]), np.array([3, 1], np.int32), np.array([.5, .5], np.float32), 5).validate()
+    with pytest.raises(C.CorpusError, match="weights sum"):
+        C.HistogramSet(np.array([0, 2]), np.array([1, 3], np.int32), np.array([.5, .6], np.float32), 5).validate()
+    with pytest.raises(C.CorpusError, match="out of range"):
+        C.HistogramSet(np.array([0, 1]), np.array([7], np.int32), np.array([1.0], np.float32), 5).validate()
+
+
+def test_synthetic_shapes():
+    x = S.histograms(2000, 1000, 40, seed=1)
+    x.validate()
+    sizes = x.row_sizes
+    assert 15 <= sizes.mean() <= 45 and sizes.min() >= 1
+    E = S.embeddings(100, 8, seed=0)
+    assert E.dtype == np.float32 and E.shape == (100, 8)
+
+
+def test_build_histograms_spec_examples():
+    vocab = C.Vocabulary.from_words(["cat", "dog", "the"])
+    hs, kept = C.build_histograms([["cat", "cat", "dog"]], vocab)
+    assert list(hs.row(0).word_ids) == [0, 1]
+    assert np.allclose(hs.row(0).weights, [2 / 3, 1 / 3])
+    with pytest.raises(C.IngestError) as ei:
+        C.build_histograms([["cat"], ["the", "the"]], vocab, stopwords={"the"})
+    assert ei.value.doc_index == 1
+    hs, kept = C.build_histograms([["cat"], ["the"]], vocab, stopwords={"the"}, on_empty="skip")
+    assert list(kept) == [0]
+
+
+def test_load_embeddings_text_and_binary(tmp_path):
+    t = tmp_path / "e.txt"
+    t.write_text("3 2\na 0 0\nb 1.5 -2\na 9 9\n")
+    vocab, E = C.load_embeddings(t, "text")
+    assert vocab.words == ["a", "b"] and E.shape == (2, 2) and E[0, 0] == 0 and E[1, 1] == -2
+    b = tmp_path / "e.bin"
+    with b.open("wb") as fh:
+        fh.write(b"2 3\n")
+        fh.write(b"x " + struct.pack("<3f", 1, 2, 3) + b"\n")
+        fh.write(b"y " + struct.pack("<3f", 4, 5, 6))
+    vocab, E = C.load_embeddings(b, "binary")
+    assert vocab.words == ["x", "y"] and np.array_equal(E[1], [4, 5, 6])
+    bad = tmp_path / "bad.txt"
+    bad.write_text("2 2\na 1\n")
+    with pytest.raises(C.EmbeddingLoadError, match=r":2: expected 2 values"):
+        C.load_embeddings(bad)
+    with pytest.raises(ValueError, match="unknown embedding format"):
+        C.load_embeddings(bad, "xml")
+
+
+def test_z_panel_layout():
+    from paper_1711_07227_b200.kernels import _z_panels
+    z = np.arange(5 * 11, dtype=np.float32).reshape(5, 11)
+    flat, zp = _z_panels(z)
+    assert zp == 40
+    for s in range(11):
+        for r in range(5):
+            assert flat[(s >> 3) * zp + r * 8 + (s & 7)] == z[r, s]
+
+
+def test_no_oracle_import_in_product():
+    """The product package must never import the test oracle."""
+    for p in (ROOT / "paper_1711_07227_b200").rglob("*.py"):
+        assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", p.read_text(), re.M), p
