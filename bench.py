@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark: symmetric LC-RWMD doc-pair distances/sec (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Workload (BASELINE.json configs[1] = SURVEY "C2"): 1M resident docs x 1k query
+docs, vocabulary 100k, m = 300, ~50 unique words/doc, top-k = 10, synthetic
+(N(0,1) embeddings, uniform word ids, (u+0.1)/sum weights; seeds fixed).
+
+One step = the whole symmetric LC-RWMD top-k from HBM-resident raw inputs
+(E f32, both CSR sets): f16 operand preparation + identity classes,
+restriction of both sides, forward Phase 1 + SpMM, reverse Phase 1 + fused
+max/top-k over doc batches, final merge.  Inputs (X1 = 400 MB, D1 = 4 GB,
+Z2 batches of GBs) are far larger than the 126 MB L2, so no flush is needed.
+
+`value` is device-timed (CUDA events on the launching stream, max over
+ranks); `e2e` calls the public API distances.lcrwmd_topk with pinned host
+arrays, so it includes the host->device copies of X1, X2, E and the
+device->host read of the (n2, k) result.  `roofline` is the reverse Phase-1
+kernel (the dominant one), timed live with events inside the timed region.
+
+With --gpus N > 1 (torchrun, NCCL) resident docs are sharded by contiguous
+rows; Phase 1 of the forward direction is split by vocabulary slice with Z1
+all-gathered, the reverse direction is local, and per-shard top-k lists are
+gathered to rank 0 and merged (paper_1711_07227_b200/parallel.py).  Total work
+is fixed (strong scaling of C2, as BASELINE.json configs[2] describes).
+
+--impl reference times the reference algorithm (the pinned CPU oracle port,
+oracle/lcrwmd_oracle.py, all host threads) on a bounded sample of the same
+workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c2": dict(n_docs=1_000_000, n_queries=1000, vocab=100_000, dim=300, h=50, k=10,
+               workload="symmetric LC-RWMD top-10, 1M docs x 1k queries, V=100k, m=300, h~50 (BASELINE configs[1])"),
+    "c1": dict(n_docs=2000, n_queries=64, vocab=20_000, dim=300, h=40, k=10,
+               workload="symmetric LC-RWMD top-10, 2000 docs x 64 queries, V=20k, m=300, h~40 (BASELINE configs[0])"),
+    "mid": dict(n_docs=100_000, n_queries=256, vocab=50_000, dim=300, h=50, k=10,
+                workload="symmetric LC-RWMD top-10, 100k docs x 256 queries, V=50k, m=300, h~50 (dev size)"),
+}
+METRIC = "symmetric RWMD doc-pair distances/sec"
+UNIT = "doc-pairs/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def make_data(cfg):
+    from paper_1711_07227_b200 import synthetic as S
+    E = S.embeddings(cfg["vocab"], cfg["dim"], seed=0)
+    x1 = S.histograms(cfg["n_docs"], cfg["vocab"], cfg["h"], seed=1)
+    x2 = S.histograms(cfg["n_queries"], cfg["vocab"], cfg["h"], seed=2)
+    return E, x1, x2
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                try:
+                    rows.append((float(f[0]), float(f[1]), float(f[2]), f[3:7]))
+                except ValueError:
+                    pass
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3]) if v.lower().startswith("active")})
+        loaded = [r[0] for r in rows if r[2] > 200.0] or [r[0] for r in rows]
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(r[2] for r in rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port, all host threads) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_sample_rate(E, x1, x2, k, target_s: float):
+    from oracle import lcrwmd_oracle as O
+    threads = O.default_threads()
+    n = 32
+    while True:
+        t0 = time.perf_counter()
+        O.lcrwmd_topk(x1.slice_rows(0, n), x2, E, k, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= x1.n_rows:
+            break
+        n = int(min(x1.n_rows, max(2 * n, n * target_s / max(dt, 1e-3) * 0.9)))
+    return {"value": n * x2.n_rows / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {n} resident docs x all {x2.n_rows} queries of the same workload "
+                      f"(full symmetric LC-RWMD + top-{k}, oracle/lcrwmd_oracle.py, {dt:.1f} s)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_07227_b200 import _lib, device, distances, parallel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    E, x1, x2 = make_data(cfg)
+    k = cfg["k"]
+    n1, n2 = x1.n_rows, x2.n_rows
+    lo, hi = parallel.shard_range(n1, rank, world)
+    x1s = x1.slice_rows(lo, hi)
+
+    # HBM-resident inputs for the device-timed value
+    Ed = device.to_device(E, torch.float32)
+    dx1 = device.DeviceCSR.upload(x1s, "x1")
+    dx2 = device.DeviceCSR.upload(x2, "x2")
+
+    def step():
+        prep = device.PreparedEmbeddings(Ed)
+        if world == 1:
+            return device.symmetric(dx1, dx2, prep, k)
+        return parallel.sharded_topk(dx1, lo, n1, dx2, prep, k)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    device.TIMER.reset(True)
+    calls0 = dict(_lib.CALLS)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        out = step()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    calls = {n: c - calls0.get(n, 0) for n, c in _lib.CALLS.items()}
+    launches = _lib.launches(calls) // args.steps
+    ksum = device.TIMER.summary()
+    device.TIMER.reset(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the public API (pinned host buffers) ----
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t.numpy()
+
+    from paper_1711_07227_b200.corpus import HistogramSet
+    hx1 = HistogramSet(pinned(x1s.row_offsets), pinned(x1s.column_ids), pinned(x1s.values), x1s.n_cols)
+    hx2 = HistogramSet(pinned(x2.row_offsets), pinned(x2.column_ids), pinned(x2.values), x2.n_cols)
+    hE = pinned(E)
+    h2d = sum(a.nbytes for a in (hx1.row_offsets, hx1.column_ids, hx1.values, hx2.row_offsets,
+                                 hx2.column_ids, hx2.values, hE))
+    d2h = n2 * k * (4 + 8)
+
+    def e2e_step():
+        if world == 1:
+            return distances.lcrwmd_topk_arrays(hx1, hx2, hE, k)
+        return parallel.sharded_topk_host(hx1, lo, n1, hx2, hE, k)
+
+    e2e_step()
+    e_steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(e_steps):
+        e2e_step()
+    t1.record()
+    torch.cuda.synchronize()
+    e2e_ms = t0.elapsed_time(t1) / e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        barrier()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk, pk_kind = peaks()
+    rev = ksum.get("phase1_rev", {"ms": float("nan"), "work": 0.0, "launches": 1})
+    per_launch_ms = rev["ms"] / max(rev["launches"], 1)
+    achieved_tf = rev["work"] / (rev["ms"] * 1e-3) / 1e12
+    peak_tf = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    pairs = n1 * n2
+    value = pairs / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f16 operands, fp32 accumulate",
+        "data": "synthetic (N(0,1) embeddings, uniform word ids; seeds 0/1/2)",
+        "config": {"workload": cfg["workload"], "n_docs": n1, "n_queries": n2, "vocab": cfg["vocab"],
+                   "dim": cfg["dim"], "h": cfg["h"], "k": k, "parallelism": f"docs sharded x{world}",
+                   "l2": "inputs larger than L2 (X1 400 MB, D1 4 GB); no flush"},
+        "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "paper_1711_07227_b200.distances.lcrwmd_topk (pinned host arrays)"},
+        "roofline": {"kernel": "phase1_kernel (reverse direction, tcgen05 f16 GEMM + fused segmented min)",
+                     "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf, "traffic": None,
+                     "peak_source": f"{pk_kind} bf16_tflops_sustained (dense f16 = bf16 rate)",
+                     "per_launch_ms": per_launch_ms, "launches_per_step": rev["launches"] / args.steps,
+                     "share_of_step": rev["ms"] / args.steps / ms},
+        "kernels": {n: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                        ("tflops" if n.startswith("phase1") else "gbs"):
+                            (v["work"] / (v["ms"] * 1e-3) / (1e12 if n.startswith("phase1") else 1e9))}
+                    for n, v in ksum.items()},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample_rate(E, x1, x2, k, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import lcrwmd_oracle as O
+    E, x1, x2 = make_data(cfg)
+    k = cfg["k"]
+    threads = O.default_threads()
+    n = args.ref_docs
+    sub = x1.slice_rows(0, n)
+    for _ in range(args.warmup):
+        O.lcrwmd_topk(sub, x2, E, k, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.lcrwmd_topk(sub, x2, E, k, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = n * x2.n_rows / dt
+    sample = (f"first {n} resident docs x all {x2.n_rows} queries per step (full symmetric LC-RWMD + top-{k}); "
+              f"oracle port oracle/lcrwmd_oracle.py (reference is pure Python, no compiled build)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "impl": "reference",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeds 0/1/2)",
+            "config": {"workload": cfg["workload"], "n_docs": x1.n_rows, "n_queries": x2.n_rows, "k": k},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-docs", type=int, default=96)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -51,9 +51,13 @@ int lcrw_padded_dim(int m);
 int lcrw_absmax(const float* x, int64_t n, uint32_t* amax_bits, void* stream);
 /* scale[0] = 2^e with absmax * 2^e in [2^12, 2^13); scale[1] = 1 / scale[0] */
 int lcrw_scale_from_absmax(const uint32_t* amax_bits, float* scale, void* stream);
-/* Xh[r, :] = f16_rn(X[r, :m] * scale), zero padded to kp; norms[r] = |Xh[r]|^2 */
-int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, const float* scale, uint16_t* Xh,
-                      float* norms, void* stream);
+/* layout 0: Xh[r, :] = f16_rn(X[r, :m] * scale), zero padded to kp = lcrw_padded_dim(m).
+ * layouts 1/2 ("3 x f16" split, kp = lcrw_padded_dim(3m)): with hi = f16(x*s),
+ * lo = f16(x*s - hi), A rows are [hi, hi, lo] (1) and B rows [hi, lo, hi] (2), so
+ * one K = 3m product gives hi.hi + hi.lo + lo.hi (~22-bit operands).
+ * norms[r] = |rounded row|^2 (fp64 sum, stored f32). */
+int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, int layout, const float* scale,
+                      uint16_t* Xh, float* norms, void* stream);
 /* T[i] = Xh[ids[i]], tnorms[i] = norms[ids[i]] (distances.py:201 `query_E[cols]`) */
 int lcrw_gather_rows(const uint16_t* Xh, const float* norms, int kp, const int32_t* ids, int64_t n,
                      uint16_t* T, float* tnorms, void* stream);
@@ -87,7 +91,8 @@ int64_t lcrw_endmask_words(int64_t n_cols);
 int64_t lcrw_plan_ranges(int64_t n_cols, int range_cols);
 int lcrw_segment_plan(const int64_t* seg_offsets, int64_t n_seg, int64_t n_cols, int range_cols,
                       uint32_t* endmask, int32_t* range_seg, int64_t n_ranges, void* stream);
-/* Z[s, r] = min_{t in segment s} |A_r - B_t| for r < a_rows, s < n_seg:
+/* Z[s, r] = min_{t in segment s} |A_r - B_t| for r < a_rows, s < n_seg, where m is
+ * the K extent of the operand rows (m, or 3m for the split layouts 1/2):
  * tcgen05 f16 GEMM (TMA-fed, TMEM accumulators) with the Gram expansion and
  * segmented row-min fused into the epilogue. */
 int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
@@ -102,19 +107,25 @@ int lcrw_zero_identical(const int64_t* seg_offsets, int64_t n_seg, const int32_t
 
 /* ---- Phase 2 (kernels.py:174-198 spmm/spmv; distances.py:203) -----------
  * out[i, s] = sum_p x[i, p] * Z[s, col[i, p]] in fp64, rounded once to f32,
- * for s < n_seg; out addressed out[i * ld_row + (s >> 3) * ld_panel + (s & 7)]. */
+ * for s < n_seg; out addressed out[i * ld_row + (s >> 3) * ld_panel + (s & 7)].
+ * Z may be split into vocabulary blocks of z_block_rows rows (the multi-GPU
+ * all-gather of per-rank Phase-1 slices): row w lives at block w / z_block_rows,
+ * z_block_stride floats apart; z_block_rows <= 0 means one block. */
 int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
-              int64_t z_panel, int64_t n_seg, float* out, int64_t ld_row, int64_t ld_panel, void* stream);
+              int64_t z_panel, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
+              int64_t ld_row, int64_t ld_panel, void* stream);
 
 /* Reverse direction + symmetric combine (distances.py:263-264): for queries q
  * (rows of the restricted query CSR) and local docs j < n_docs of a batch,
  * D2 = spmm(Xq, Z2) and D = max(D1[doc_base + j, q], D2).  D1 is addressed like
  * spmm's output (d1_ld_row, d1_ld_panel).  Either writes D[(doc_base+j) * ld_out
  * + q] (dout != NULL), or per (query, doc-chunk) top-k candidates into
- * cand_d/cand_i[(q * n_chunks_total + chunk_base + chunk) * k + r]. */
+ * cand_d/cand_i[(q * n_chunks_total + chunk_base + chunk) * k + r] with ids
+ * id_offset + doc_base + j (id_offset = the shard's first global doc). */
 int lcrw_reverse_chunk_docs(void);
 int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
-                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, const float* D1,
+                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, int64_t id_offset,
+                     const float* D1,
                      int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k,
                      float* cand_d, int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base,
                      void* stream);

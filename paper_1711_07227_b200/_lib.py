@@ -29,7 +29,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_padded_dim": (I32, [I32]),
     "lcrw_absmax": (I32, [P, I64, P, P]),
     "lcrw_scale_from_absmax": (I32, [P, P, P]),
-    "lcrw_prepare_rows": (I32, [P, I64, I32, I32, P, P, P, P]),
+    "lcrw_prepare_rows": (I32, [P, I64, I32, I32, I32, P, P, P, P]),
     "lcrw_gather_rows": (I32, [P, P, I32, P, I64, P, P, P]),
     "lcrw_row_classes_workspace": (I32, [I64, P]),
     "lcrw_row_classes": (I32, [P, I64, I32, P, P, P, P, P, P, SZ, P]),
@@ -42,9 +42,9 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_segment_plan": (I32, [P, I64, I64, I32, P, P, I64, P]),
     "lcrw_phase1": (I32, [P, P, I64, P, P, I64, I32, I32, P, I64, P, P, I64, P, P, I64, P]),
     "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, P]),
-    "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, P, I64, I64, P]),
+    "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_chunk_docs": (I32, []),
-    "lcrw_reverse_max": (I32, [P, P, P, I64, P, I64, I64, I64, P, I64, I64, P, I64, I32, P, P, I64, I64, P]),
+    "lcrw_reverse_max": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P, I64, I32, P, P, I64, I64, P]),
     "lcrw_topk_segments": (I32, [P, P, I64, I64, I32, P, P, P]),
     "lcrw_topk_sort_workspace": (I32, [I64, P]),
     "lcrw_topk_sort": (I32, [P, P, I64, I64, P, P, P, SZ, P]),
@@ -53,6 +53,17 @@ SIGNATURES: dict[str, tuple] = {
 # functions returning a value rather than a status
 _VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim",
                 "lcrw_endmask_words", "lcrw_plan_ranges", "lcrw_reverse_chunk_docs"}
+
+# kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
+# profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".
+KERNELS_PER_CALL = {
+    "lcrw_absmax": 1, "lcrw_scale_from_absmax": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
+    "lcrw_row_classes": 12, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
+    "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
+    "lcrw_reverse_max": 1, "lcrw_topk_segments": 1, "lcrw_topk_sort": 7,
+}
+
+CALLS: dict[str, int] = {}
 
 _lib = None
 _lock = threading.Lock()
@@ -82,6 +93,11 @@ def load() -> C.CDLL:
     return _lib
 
 
+def launches(calls: dict[str, int]) -> int:
+    """Kernel launches implied by a call-count snapshot."""
+    return sum(KERNELS_PER_CALL.get(n, 0) * c for n, c in calls.items())
+
+
 def value(name: str, *args):
     return getattr(load(), name)(*args)
 
@@ -89,6 +105,7 @@ def value(name: str, *args):
 def call(name: str, *args) -> None:
     """Invoke a status-returning entry point and raise on failure."""
     lib = load()
+    CALLS[name] = CALLS.get(name, 0) + 1
     st = getattr(lib, name)(*args)
     if st == 0:
         return

@@ -21,24 +21,28 @@ constexpr int kChunkDocs = 4096;    // reverse: docs per block (one candidate li
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarps * 32)
     spmm_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ cols, const float* __restrict__ vals,
-                int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int64_t n_seg, float* __restrict__ out,
-                int64_t ld_row, int64_t ld_panel) {
+                int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int64_t z_block_rows,
+                int64_t z_block_stride, int64_t n_seg, float* __restrict__ out, int64_t ld_row, int64_t ld_panel) {
   const int lane = threadIdx.x & 31;
   const int64_t q0 = (int64_t)blockIdx.y * kSegPerBlock + lane * 4;
   const bool active = q0 < n_seg;
   const float* zq = Z + (q0 >> 3) * z_panel + (q0 & 7);
+  const uint32_t zbr = (uint32_t)min(z_block_rows, (int64_t)0xFFFFFFFF);
   for (int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); i < n_rows; i += (int64_t)gridDim.x * kWarps) {
     const int64_t lo = offs[i], hi = offs[i + 1];
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int64_t base = lo; base < hi; base += 32) {
       const int cnt = (int)min((int64_t)32, hi - base);
-      const int32_t my_c = lane < cnt ? __ldg(cols + base + lane) : 0;
+      const uint32_t my_c = lane < cnt ? (uint32_t)__ldg(cols + base + lane) : 0u;
       const float my_x = lane < cnt ? __ldg(vals + base + lane) : 0.f;
+      // vocabulary-sliced Z (multi-GPU all-gather): row w lives in block w / z_block_rows
+      const uint32_t blk = my_c / zbr;
+      const int64_t my_off = (int64_t)blk * z_block_stride + (int64_t)(my_c - blk * zbr) * 8;
       for (int t = 0; t < cnt; ++t) {
-        const int64_t w = __shfl_sync(0xffffffffu, my_c, t);
+        const int64_t zoff = __shfl_sync(0xffffffffu, my_off, t);
         const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
         if (active) {
-          const float4 z = __ldg(reinterpret_cast<const float4*>(zq + w * 8));
+          const float4 z = __ldg(reinterpret_cast<const float4*>(zq + zoff));
           a0 = fma(x, (double)z.x, a0);
           a1 = fma(x, (double)z.y, a1);
           a2 = fma(x, (double)z.z, a2);
@@ -83,8 +87,8 @@ template <int KMAX>
 __global__ void __launch_bounds__(kWarps * 32)
     reverse_max_kernel(const int64_t* __restrict__ q_offs, const int32_t* __restrict__ q_cols,
                        const float* __restrict__ q_vals, int64_t n_q, const float* __restrict__ Z2, int64_t z_panel,
-                       int64_t n_docs, int64_t doc_base, const float* __restrict__ D1, int64_t d1_ld_row,
-                       int64_t d1_ld_panel, float* __restrict__ dout, int64_t ld_out, int k,
+                       int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
+                       int64_t d1_ld_row, int64_t d1_ld_panel, float* __restrict__ dout, int64_t ld_out, int k,
                        float* __restrict__ cand_d, int64_t* __restrict__ cand_i, int64_t n_chunks_total,
                        int64_t chunk_base) {
   const int lane = threadIdx.x & 31;
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
     if (lane == 0) {
       cand_d[slot + r] = bd;
-      cand_i[slot + r] = bi == 0x7fffffff ? INT64_MAX : (int64_t)bi;
+      cand_i[slot + r] = bi == 0x7fffffff ? INT64_MAX : (int64_t)bi + id_offset;
     }
   }
 }
@@ -169,19 +173,21 @@ using namespace lcrw::p2;
 extern "C" {
 
 int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
-              int64_t z_panel, int64_t n_seg, float* out, int64_t ld_row, int64_t ld_panel, void* stream) {
+              int64_t z_panel, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
+              int64_t ld_row, int64_t ld_panel, void* stream) {
   LCRW_REQUIRE(n_rows >= 0 && n_seg >= 0, "lcrw_spmm: bad shape");
   if (n_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(offs && cols && vals && Z && out, "lcrw_spmm: null pointer");
-  LCRW_REQUIRE(z_panel % 8 == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0,
-               "lcrw_spmm: Z must be 16-byte aligned with z_panel % 8 == 0");
+  LCRW_REQUIRE(z_panel % 8 == 0 && z_block_stride % 8 == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0,
+               "lcrw_spmm: Z must be 16-byte aligned with z_panel, z_block_stride % 8 == 0");
+  if (z_block_rows <= 0) z_block_rows = INT64_MAX;
   const int64_t gy = ceil_div(n_seg, kSegPerBlock);
   LCRW_REQUIRE(gy < 65536, "lcrw_spmm: too many segments for one launch");
   int64_t gx = ceil_div(n_rows, kWarps);
   const int64_t cap = (int64_t)sm_count() * 64;
   if (gx > cap) gx = cap;
   spmm_kernel<<<dim3((unsigned)gx, (unsigned)gy), kWarps * 32, 0, as_stream(stream)>>>(
-      offs, cols, vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel);
+      offs, cols, vals, n_rows, Z, z_panel, z_block_rows, z_block_stride, n_seg, out, ld_row, ld_panel);
   LCRW_CHECK_LAUNCH("spmm_kernel");
   return LCRW_OK;
 }
@@ -189,7 +195,8 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
 int lcrw_reverse_chunk_docs(void) { return kChunkDocs; }
 
 int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
-                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, const float* D1,
+                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, int64_t id_offset,
+                     const float* D1,
                      int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k, float* cand_d,
                      int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base, void* stream) {
   LCRW_REQUIRE(n_q >= 0 && n_docs >= 0, "lcrw_reverse_max: bad shape");
@@ -203,18 +210,18 @@ int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* 
   cudaStream_t st = as_stream(stream);
   if (dout) {
     reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
-                                                         D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
+                                                         id_offset, D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
                                                          nullptr, 0, 0);
   } else {
     LCRW_REQUIRE(k >= 1 && cand_d && cand_i, "lcrw_reverse_max: top-k mode needs k >= 1 and candidate buffers");
     LCRW_REQUIRE(chunk_base + gx <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
     if (k <= 16) {
       reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
-                                                           doc_base, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
+                                                           doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
                                                            cand_d, cand_i, n_chunks_total, chunk_base);
     } else if (k <= 32) {
       reverse_max_kernel<32><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
-                                                           doc_base, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
+                                                           doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
                                                            cand_d, cand_i, n_chunks_total, chunk_base);
     } else {
       set_error("lcrw_reverse_max: fused top-k supports k <= 32 (got %d); use the full-matrix path", k);

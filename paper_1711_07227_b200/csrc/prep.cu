@@ -43,22 +43,37 @@ __global__ void scale_kernel(const uint32_t* amax_bits, float* scale) {
 
 // one warp per row; f16 RN rounding of the scaled row, fp64 norm of the
 // rounded values (exact squares, ~exact sum) stored as f32.
-__global__ void prepare_rows_kernel(const float* __restrict__ X, int64_t rows, int m, int kp,
+//   layout 0: [f16(x)]                      (K = m)
+//   layout 1: [hi(x), hi(x), lo(x)]  A side (K = 3m)   with hi = f16(x), lo = f16(x - hi)
+//   layout 2: [hi(x), lo(x), hi(x)]  B side (K = 3m)   -> A.B = hi.hi + hi.lo + lo.hi
+__global__ void prepare_rows_kernel(const float* __restrict__ X, int64_t rows, int m, int kp, int layout,
                                     const float* __restrict__ scale, __half* __restrict__ Xh,
                                     float* __restrict__ norms) {
   const int lane = threadIdx.x & 31;
   const float s = scale[0];
+  const int k_used = layout == 0 ? m : 3 * m;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     double acc = 0.0;
     const float* src = X + r * (int64_t)m;
     __half* dst = Xh + r * (int64_t)kp;
     for (int k = lane; k < kp; k += 32) {
-      const float x = k < m ? src[k] * s : 0.f;
-      const __half h = __float2half_rn(x);
-      dst[k] = h;
-      const double hf = (double)__half2float(h);
-      acc += hf * hf;
+      __half out = __float2half_rn(0.f);
+      if (k < k_used) {
+        const int part = layout == 0 ? 0 : k / m;
+        const int c = layout == 0 ? k : k - part * m;
+        const float x = src[c] * s;
+        const __half hi = __float2half_rn(x);
+        const __half lo = __float2half_rn(x - __half2float(hi));
+        const bool want_lo = (layout == 1 && part == 2) || (layout == 2 && part == 1);
+        out = want_lo ? lo : hi;
+        if (part == 0) {
+          const double v = layout == 0 ? (double)__half2float(hi)
+                                       : (double)__half2float(hi) + (double)__half2float(lo);
+          acc += v * v;
+        }
+      }
+      dst[k] = out;
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) norms[r] = (float)acc;
@@ -264,13 +279,14 @@ int lcrw_scale_from_absmax(const uint32_t* amax_bits, float* scale, void* stream
   return LCRW_OK;
 }
 
-int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, const float* scale, uint16_t* Xh,
+int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, int layout, const float* scale, uint16_t* Xh,
                       float* norms, void* stream) {
-  LCRW_REQUIRE(rows >= 0 && m > 0 && kp == lcrw_padded_dim(m), "lcrw_prepare_rows: bad shape");
+  LCRW_REQUIRE(layout >= 0 && layout <= 2, "lcrw_prepare_rows: layout must be 0, 1 or 2");
+  LCRW_REQUIRE(rows >= 0 && m > 0 && kp == lcrw_padded_dim(layout == 0 ? m : 3 * m), "lcrw_prepare_rows: bad shape");
   LCRW_REQUIRE(rows == 0 || (X && scale && Xh && norms), "lcrw_prepare_rows: null pointer");
   if (rows == 0) return LCRW_OK;
   prepare_rows_kernel<<<grid_for(rows * 32), kThreads, 0, as_stream(stream)>>>(
-      X, rows, m, kp, scale, reinterpret_cast<__half*>(Xh), norms);
+      X, rows, m, kp, layout, scale, reinterpret_cast<__half*>(Xh), norms);
   LCRW_CHECK_LAUNCH("prepare_rows_kernel");
   return LCRW_OK;
 }

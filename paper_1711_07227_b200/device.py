@@ -67,8 +67,49 @@ def to_device(a, dtype, non_blocking: bool = True) -> torch.Tensor:
     return t.to(dev, non_blocking=non_blocking and t.is_pinned())
 
 
-def _launch_count_hint():  # pragma: no cover - documentation only
-    """Kernels per call are counted by bench.py via torch.cuda profiler-free bookkeeping."""
+class KernelTimer:
+    """Optional CUDA-event bracketing of named kernel launches on the launching stream.
+
+    bench.py enables it to measure the dominant kernel's live duration inside
+    the timed region; algorithmic work (FLOPs / bytes) is accumulated alongside."""
+
+    def __init__(self):
+        self.enabled = False
+        self.records: list[tuple[str, torch.cuda.Event, torch.cuda.Event, float]] = []
+
+    def reset(self, enabled: bool = True) -> None:
+        self.enabled = enabled
+        self.records = []
+
+    def span(self, name: str, work: float):
+        timer = self
+
+        class _Span:
+            def __enter__(self_inner):
+                if timer.enabled:
+                    self_inner.a = torch.cuda.Event(enable_timing=True)
+                    self_inner.b = torch.cuda.Event(enable_timing=True)
+                    self_inner.a.record()
+
+            def __exit__(self_inner, *exc):
+                if timer.enabled:
+                    self_inner.b.record()
+                    timer.records.append((name, self_inner.a, self_inner.b, work))
+
+        return _Span()
+
+    def summary(self) -> dict[str, dict[str, float]]:
+        """name -> {ms, work, launches} (call after a synchronize)."""
+        out: dict[str, dict[str, float]] = {}
+        for name, a, b, work in self.records:
+            d = out.setdefault(name, {"ms": 0.0, "work": 0.0, "launches": 0})
+            d["ms"] += a.elapsed_time(b)
+            d["work"] += work
+            d["launches"] += 1
+        return out
+
+
+TIMER = KernelTimer()
 
 
 # ---------------------------------------------------------------------------
@@ -108,10 +149,18 @@ class DeviceCSR:
 class PreparedEmbeddings:
     """E in HBM: f32 original, f16 operand rows, norms, scale and identity classes.
 
+    For m <= SPLIT_MAX_DIM the operand rows use the "3 x f16" split layout
+    (K = 3m: A rows [hi, hi, lo], B rows [hi, lo, hi]) -- ~22-bit operands at
+    no extra cost, because K is padded to 64 anyway; above it, one f16 pass
+    (11-bit significand, like TF32-RN) whose distance error shrinks like
+    1/sqrt(m).
+
     ``extra`` arrays (e.g. free query vectors for nearest_word_distances)
     take part in the power-of-two scale choice so they share E's scaling."""
 
-    def __init__(self, embeddings, extra=()):
+    SPLIT_MAX_DIM = 64
+
+    def __init__(self, embeddings, extra=(), split: bool | None = None):
         dev = require_cuda()
         st = _stream()
         self.E32 = to_device(np.asarray(embeddings, dtype=np.float32) if not isinstance(embeddings, torch.Tensor)
@@ -119,17 +168,17 @@ class PreparedEmbeddings:
         if self.E32.dim() != 2:
             raise ValueError("embeddings must be a 2-d (v, m) matrix")
         self.V, self.m = int(self.E32.shape[0]), int(self.E32.shape[1])
-        self.kp = padded_dim(self.m)
+        self.split = (self.m <= self.SPLIT_MAX_DIM) if split is None else bool(split)
+        self.k_eff = 3 * self.m if self.split else self.m
+        self.kp = padded_dim(self.k_eff)
         amax = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.call("lcrw_absmax", _p(self.E32), self.V * self.m, _p(amax), st)
         for x in extra:
             _lib.call("lcrw_absmax", _p(x), x.numel(), _p(amax), st)
         self.scale = torch.empty(2, dtype=torch.float32, device=dev)
         _lib.call("lcrw_scale_from_absmax", _p(amax), _p(self.scale), st)
-        self.Eh = torch.empty((self.V, self.kp), dtype=torch.float16, device=dev)
-        self.norms = torch.empty(self.V, dtype=torch.float32, device=dev)
-        _lib.call("lcrw_prepare_rows", _p(self.E32), self.V, self.m, self.kp, _p(self.scale), _p(self.Eh),
-                  _p(self.norms), st)
+        self.EhA, self.norms = self._rows(self.E32, 1 if self.split else 0)
+        self.EhB = self._rows(self.E32, 2)[0] if self.split else self.EhA
         # exact-identity classes (kernels.py:91-92 semantics)
         ws_bytes = C.c_size_t(0)
         _lib.call("lcrw_row_classes_workspace", self.V, C.byref(ws_bytes))
@@ -143,13 +192,17 @@ class PreparedEmbeddings:
                   _p(self.sorted_hash), _p(self.sorted_ids), _p(ws), ws_bytes.value, st)
         self.n_dup = int(n_dup.item())
 
+    def _rows(self, X: torch.Tensor, layout: int) -> tuple[torch.Tensor, torch.Tensor]:
+        n = int(X.shape[0])
+        Xh = torch.empty((max(n, 1), self.kp), dtype=torch.float16, device=X.device)
+        xn = torch.empty(max(n, 1), dtype=torch.float32, device=X.device)
+        _lib.call("lcrw_prepare_rows", _p(X), n, self.m, self.kp, layout, _p(self.scale), _p(Xh), _p(xn),
+                  _stream())
+        return Xh, xn
+
     def prepare_free_rows(self, Q: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
-        """f16 operand rows for vectors that are not rows of E (same scale)."""
-        n = int(Q.shape[0])
-        Qh = torch.empty((n, self.kp), dtype=torch.float16, device=Q.device)
-        qn = torch.empty(n, dtype=torch.float32, device=Q.device)
-        _lib.call("lcrw_prepare_rows", _p(Q), n, self.m, self.kp, _p(self.scale), _p(Qh), _p(qn), _stream())
-        return Qh, qn
+        """B-side f16 operand rows for vectors that are not rows of E (same scale)."""
+        return self._rows(Q, 2 if self.split else 0)
 
     def representatives(self, word_ids: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
         """(rep, next) arguments of lcrw_zero_identical for rows given by E ids."""
@@ -186,11 +239,13 @@ def remap_ids(cols: torch.Tensor, remap: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def gather_rows(prep: PreparedEmbeddings, ids: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+def gather_rows(prep: PreparedEmbeddings, ids: torch.Tensor, side: str) -> tuple[torch.Tensor, torch.Tensor]:
+    """Operand rows E[ids] for the A (vocabulary) or B (query word) side."""
     n = ids.numel()
+    src = prep.EhA if side == "A" else prep.EhB
     T = torch.empty((max(n, 1), prep.kp), dtype=torch.float16, device=ids.device)
     tn = torch.empty(max(n, 1), dtype=torch.float32, device=ids.device)
-    _lib.call("lcrw_gather_rows", _p(prep.Eh), _p(prep.norms), prep.kp, _p(ids), n, _p(T), _p(tn), _stream())
+    _lib.call("lcrw_gather_rows", _p(src), _p(prep.norms), prep.kp, _p(ids), n, _p(T), _p(tn), _stream())
     return T, tn
 
 
@@ -202,7 +257,7 @@ def _range_cols(b_rows: int, a_rows: int) -> int:
 
 def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor, b_norms: torch.Tensor,
            b_rows: int, seg_offsets: torch.Tensor, n_seg: int, prep: PreparedEmbeddings,
-           range_cols: int | None = None) -> tuple[torch.Tensor, int]:
+           range_cols: int | None = None, tag: str = "phase1") -> tuple[torch.Tensor, int]:
     """Z (panel layout, z_panel = 8 * a_rows) of distances.py:147-178, without the exact-zero pass."""
     dev = A.device
     st = _stream()
@@ -213,8 +268,10 @@ def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
     _lib.call("lcrw_segment_plan", _p(seg_offsets), n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
     z_panel = 8 * max(a_rows, 1)
     Z = torch.empty(((n_seg + 7) // 8) * z_panel, dtype=torch.float32, device=dev)
-    _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), _p(b_norms), b_rows, prep.m, prep.kp,
-              _p(seg_offsets), n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel, st)
+    with TIMER.span(tag, 2.0 * a_rows * b_rows * prep.m):  # algorithmic FLOPs, K = m unpadded
+        _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), _p(b_norms), b_rows, prep.k_eff, prep.kp,
+                  _p(seg_offsets), n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel,
+                  st)
     return Z, z_panel
 
 
@@ -223,9 +280,10 @@ def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel) -> None:
               _stream())
 
 
-def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel) -> None:
-    _lib.call("lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, n_seg, _p(out),
-              ld_row, ld_panel, _stream())
+def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel,
+         z_block_rows: int = 0, z_block_stride: int = 0) -> None:
+    _lib.call("lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, z_block_rows,
+              z_block_stride, n_seg, _p(out), ld_row, ld_panel, _stream())
 
 
 def topk_rows(d: torch.Tensor, ids: torch.Tensor, n_seg: int, seg_len: int, k: int):
@@ -269,15 +327,15 @@ class Restricted:
     @classmethod
     def build(cls, x: DeviceCSR, prep: PreparedEmbeddings) -> "Restricted":
         remap, used, v_e = restrict(x.cols, x.n_cols)
-        A, an = gather_rows(prep, used)
+        A, an = gather_rows(prep, used, "A")
         return cls(x, remap, used, v_e, remap_ids(x.cols, remap), A, an)
 
 
 def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
-                      n_seg: int) -> tuple[torch.Tensor, int]:
+                      n_seg: int, tag: str = "phase1") -> tuple[torch.Tensor, int]:
     """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros)."""
-    B, bn = gather_rows(prep, word_ids)
-    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, bn, word_ids.numel(), seg_offsets, n_seg, prep)
+    B, bn = gather_rows(prep, word_ids, "B")
+    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, bn, word_ids.numel(), seg_offsets, n_seg, prep, tag=tag)
     rep, nxt = prep.representatives(word_ids)
     zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp)
     return Z, zp
@@ -288,14 +346,16 @@ def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR,
 
     layout "rows" -> row-major (n_res, n_q); "panels" -> out[(q>>3)*8*n_res + i*8 + (q&7)]."""
     n_res, n_q = res.csr.n_rows, queries.n_rows
-    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q)
+    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q, tag="phase1_fwd")
     if layout == "rows":
         out = torch.empty(n_res * max(n_q, 1), dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = n_q, 8
     else:
         out = torch.empty(((n_q + 7) // 8) * 8 * n_res, dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = 8, 8 * n_res
-    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel)
+    # no-reuse gather model (SURVEY §8d): offsets + (id, value) stream + one Z row-segment per nonzero
+    with TIMER.span("spmm_fwd", 8.0 * (n_res + 1) + 8.0 * res.csr.nnz + 4.0 * res.csr.nnz * n_q):
+        spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel)
     return out
 
 
@@ -309,14 +369,18 @@ def _doc_batches(host_offsets: np.ndarray, v_e2: int, budget_bytes: int) -> list
 
 
 def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
-              z2_budget_bytes: int = 8 << 30):
-    """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, k) dists, ids)."""
+              z2_budget_bytes: int = 8 << 30, d1: torch.Tensor | None = None, id_offset: int = 0):
+    """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, k) dists, ids).
+
+    ``d1`` (panel layout) may be supplied by a caller that computed the forward
+    direction itself (parallel.py); ``id_offset`` shifts the returned doc ids."""
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
     st = _stream()
-    res1 = Restricted.build(x1, prep)
-    d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
-    del res1
+    if d1 is None:
+        res1 = Restricted.build(x1, prep)
+        d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
+        del res1
     res2 = Restricted.build(x2, prep)
     batches = _doc_batches(x1.host_offsets, res2.v_e, z2_budget_bytes)
     chunk = int(_lib.value("lcrw_reverse_chunk_docs"))
@@ -333,9 +397,13 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     for j0, j1 in batches:
         lo, hi = int(x1.host_offsets[j0]), int(x1.host_offsets[j1])
         seg = x1.offsets[j0:j1 + 1] - lo
-        Z2, zp2 = nearest_distances(res2, prep, seg, x1.cols[lo:hi], j1 - j0)
-        _lib.call("lcrw_reverse_max", _p(x2.offsets), _p(res2.cols_r), _p(x2.vals), n2, _p(Z2), zp2, j1 - j0, j0,
-                  _p(d1), 8, 8 * n1, _p(dout), n2, k or 0, _p(cand_d), _p(cand_i), n_chunks, chunk_base, st)
+        Z2, zp2 = nearest_distances(res2, prep, seg, x1.cols[lo:hi], j1 - j0, tag="phase1_rev")
+        # bytes: Z2 gathers (one f32 per query nonzero per doc) + D1 read
+        work = 4.0 * x2.nnz * (j1 - j0) + 4.0 * n2 * (j1 - j0)
+        with TIMER.span("reverse_max", work):
+            _lib.call("lcrw_reverse_max", _p(x2.offsets), _p(res2.cols_r), _p(x2.vals), n2, _p(Z2), zp2, j1 - j0,
+                      j0, id_offset, _p(d1), 8, 8 * n1, _p(dout), n2, k or 0, _p(cand_d), _p(cand_i), n_chunks,
+                      chunk_base, st)
         chunk_base += (j1 - j0 + chunk - 1) // chunk
         del Z2
     if k is None:
@@ -356,7 +424,7 @@ def nearest_word_distances(E, Q) -> torch.Tensor:
     nq = int(Qd.shape[0])
     Qh, qn = prep.prepare_free_rows(Qd)
     seg = torch.tensor([0, nq], dtype=torch.int64, device=dev)
-    Z, zp = phase1(prep.Eh, prep.norms, prep.V, Qh, qn, nq, seg, 1, prep)
+    Z, zp = phase1(prep.EhA, prep.norms, prep.V, Qh, qn, nq, seg, 1, prep)
     rep = torch.empty(nq, dtype=torch.int32, device=dev)
     _lib.call("lcrw_match_rows", _p(Qd), nq, _p(prep.E32), prep.m, _p(prep.sorted_hash), _p(prep.sorted_ids),
               prep.V, _p(prep.canon), _p(rep), _stream())

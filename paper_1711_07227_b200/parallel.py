@@ -1,0 +1,151 @@
+"""Multi-GPU LC-RWMD: resident docs sharded across ranks (one process per GPU).
+
+Decomposition ("spreading X1 across GPUs"; SPEC.md:357-383
+contiguous shards + topk_merge):
+
+* docs (rows of X1): contiguous shards, one per rank (``shard_range``);
+  E, X2 and the query batch are replicated;
+* forward Phase 1: rank r computes Z1 for its vocabulary slice
+  [r*R, (r+1)*R) of the full vocabulary, R = ceil(V / world), and the slices
+  are all-gathered over NVLink (NCCL) into [world][panels][R][8]; the SpMM of
+  the local doc shard reads it through the blocked addressing of lcrw_spmm;
+* reverse direction (the dominant cost): fully local -- each rank's docs are
+  the "queries" of the reverse pass against the replicated X2;
+* top-k: local per-query top-k, NCCL gather to rank 0, merge there
+  (kernels.py:226-232).  Results are identical for any world size: every
+  pair distance is computed by the same arithmetic, and the merge is exact.
+
+The collective glue (``allgather_slices``, ``gather_candidates``) is
+device-agnostic so it is exercised with the gloo backend on CPU in
+tests/test_parallel_gloo.py; the compute steps are the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import device
+from .device import DeviceCSR, PreparedEmbeddings
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous row range of ``rank``."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def vocab_slice(V: int, rank: int, world: int) -> tuple[int, int, int]:
+    """(v0, v1, R): this rank's vocabulary rows and the padded slice height."""
+    R = (V + world - 1) // world
+    v0 = min(V, rank * R)
+    return v0, min(V, v0 + R), R
+
+
+def _world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def allgather_slices(local: torch.Tensor, group=None) -> torch.Tensor:
+    """[world, *local.shape] from equal-shaped per-rank slices."""
+    rank, world = _world()
+    if world == 1:
+        return local.unsqueeze(0)
+    out = torch.empty((world, *local.shape), dtype=local.dtype, device=local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out.view(-1), local.contiguous().view(-1), group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), local.contiguous(), group=group)
+    return out
+
+
+def gather_candidates(d: torch.Tensor, i: torch.Tensor, group=None):
+    """Gather per-rank (n_q, k) top-k lists to rank 0 as (n_q, world * k); None elsewhere."""
+    rank, world = _world()
+    if world == 1:
+        return d, i
+    gd = [torch.empty_like(d) for _ in range(world)] if rank == 0 else None
+    gi = [torch.empty_like(i) for _ in range(world)] if rank == 0 else None
+    dist.gather(d.contiguous(), gd, dst=0, group=group)
+    dist.gather(i.contiguous(), gi, dst=0, group=group)
+    if rank != 0:
+        return None
+    return torch.cat(gd, dim=1).contiguous(), torch.cat(gi, dim=1).contiguous()
+
+
+# ---------------------------------------------------------------------------
+# CUDA pipeline
+# ---------------------------------------------------------------------------
+
+def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) -> tuple[torch.Tensor, int]:
+    """This rank's forward Phase-1 slice: Z1 rows [v0, v1) as (panels, R, 8), zero padded."""
+    n_q = dx2.n_rows
+    v0, v1, R = vocab_slice(prep.V, rank, world)
+    rows = v1 - v0
+    dev = dx2.cols.device
+    panels = (n_q + 7) // 8
+    zl = torch.zeros((panels, R, 8), dtype=torch.float32, device=dev)
+    if rows > 0:
+        B, bn = device.gather_rows(prep, dx2.cols, "B")
+        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, bn, dx2.nnz, dx2.offsets, n_q, prep,
+                              tag="phase1_fwd")
+        remap = torch.full((prep.V,), -1, dtype=torch.int32, device=dev)
+        remap[v0:v1] = torch.arange(rows, dtype=torch.int32, device=dev)
+        rep, nxt = prep.representatives(dx2.cols)
+        device.zero_identical(dx2.offsets, n_q, rep, nxt, remap, Z, zp)
+        zl[:, :rows, :] = Z.view(panels, rows, 8)
+    return zl, R
+
+
+def d1_from_slices(dx1: DeviceCSR, zall: torch.Tensor, R: int, n_q: int) -> torch.Tensor:
+    """Forward SpMM of the local shard against all-gathered slices [world][panels][R][8]."""
+    n1 = dx1.n_rows
+    panels = (n_q + 7) // 8
+    out = torch.empty(panels * 8 * max(n1, 1), dtype=torch.float32, device=zall.device)
+    with device.TIMER.span("spmm_fwd", 8.0 * (n1 + 1) + 8.0 * dx1.nnz + 4.0 * dx1.nnz * n_q):
+        device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, 8 * R, n_q, out, 8, 8 * n1,
+                    z_block_rows=R, z_block_stride=panels * R * 8)
+    return out
+
+
+def forward_d1(dx1: DeviceCSR, dx2: DeviceCSR, prep: PreparedEmbeddings, group=None) -> torch.Tensor:
+    """D1 (panels, local docs) with Phase 1 split by vocabulary slice + Z1 all-gather."""
+    rank, world = _world()
+    zl, R = z1_slice(dx2, prep, rank, world)
+    zall = allgather_slices(zl, group)  # [world][panels][R][8]
+    return d1_from_slices(dx1, zall, R, dx2.n_rows)
+
+
+def sharded_topk(dx1: DeviceCSR, doc_base: int, n1_total: int, dx2: DeviceCSR, prep: PreparedEmbeddings, k: int,
+                 group=None):
+    """Per-query top-k over all ranks' docs; (n_q, k) on rank 0, None elsewhere."""
+    rank, world = _world()
+    d1 = forward_d1(dx1, dx2, prep, group)
+    ld, li = device.symmetric(dx1, dx2, prep, k, d1=d1, id_offset=doc_base)
+    if ld.shape[1] < k:  # shard smaller than k: pad with sentinels so gather shapes agree
+        pd = torch.full((ld.shape[0], k), float("inf"), dtype=ld.dtype, device=ld.device)
+        pi = torch.full((li.shape[0], k), torch.iinfo(torch.int64).max, dtype=li.dtype, device=li.device)
+        pd[:, : ld.shape[1]] = ld
+        pi[:, : li.shape[1]] = li
+        ld, li = pd, pi
+    ld = ld.contiguous()
+    li = li.contiguous()
+    g = gather_candidates(ld, li, group)
+    if g is None:
+        return None
+    cd, ci = g
+    n_q = dx2.n_rows
+    d, i = device.topk_rows(cd, ci, n_q, cd.shape[1], k)
+    kk = min(k, n1_total)
+    return d[:, :kk], i[:, :kk]
+
+
+def sharded_topk_host(x1_shard, doc_base: int, n1_total: int, x2, E, k: int, group=None):
+    """End-to-end variant from host arrays (pinned for async copies)."""
+    prep = PreparedEmbeddings(E)
+    out = sharded_topk(DeviceCSR.upload(x1_shard, "x1"), doc_base, n1_total, DeviceCSR.upload(x2, "x2"), prep, k,
+                       group)
+    if out is None:
+        return None
+    return out[0].cpu().numpy(), out[1].cpu().numpy()

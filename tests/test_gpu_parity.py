@@ -2,8 +2,12 @@
 vectors and the pinned CPU oracle.
 
 Tolerances (written here, justified in DESIGN.md §Precision):
-  * distances: |d - d_ref| <= 1e-4 * |d_ref| + 1e-5      (f16 operands = 11-bit
-    significand like TF32-RN, fp32 tensor-core accumulation)
+  * distances: |d - d_ref| <= 1e-4 * |d_ref| + 1e-5 * max_w |E_w|
+    The relative term covers operand rounding (f16 = 11-bit significand, like
+    TF32-RN; split 3 x f16 below m = 64).  The absolute term is the fp32
+    tensor-core accumulation of the Gram expansion |a|^2 + |b|^2 - 2 a.b,
+    whose error scales with the norms, not the distance; it only matters for
+    near-duplicate words (clustered stress data).
   * exact zeros where the reference has them (identical vectors)
   * spmm / topk_select / restrict_vocabulary: bitwise
   * top-k ids: identical except where the reference's k-th and (k+1)-th
@@ -37,7 +41,7 @@ def _pkg():
     return corpus, distances, kernels
 
 
-def _check_topk(d, i, dref_full, k):
+def _check_topk(d, i, dref_full, k, ATOL=ATOL):
     """Tie-aware top-k check against a full reference matrix (n1, n2)."""
     n1, n2 = dref_full.shape
     for j in range(n2):
@@ -58,10 +62,15 @@ def _check_topk(d, i, dref_full, k):
                 assert abs(col[i[j][r]] - rd[r]) <= 2 * tol[r] + 1e-6, (j, r)
 
 
+def _atol(E):
+    return 1e-5 * float(np.sqrt((np.asarray(E, np.float64) ** 2).sum(1).max()))
+
+
 def test_golden_full_batched_onesided(golden_case):
     name, z, x1, x2 = golden_case
     _, D, _ = _pkg()
     E = z["E"]
+    ATOL = _atol(E)
     full = D.lcrwmd_full(x1, x2, E).values
     ok, err = rel_close(full, z["full"], RTOL, ATOL)
     assert ok, (name, "full", err)
@@ -87,7 +96,7 @@ def test_golden_topk(golden_case):
     res = D.lcrwmd_topk(x1, x2, z["E"], k)
     d = [r.distances for r in res]
     i = [r.ids for r in res]
-    _check_topk(d, i, z["full"], k)
+    _check_topk(d, i, z["full"], k, _atol(z["E"]))
 
 
 def test_golden_restrict_spmm(golden_case):
@@ -162,7 +171,7 @@ def test_c1_shaped_vs_oracle(clustered):
     x2 = S.histograms(40, V, 40, seed=5)
     ref = O.lcrwmd_full(x1, x2, E, threads=8)
     got = D.lcrwmd_full(x1, x2, E).values
-    ok, err = rel_close(got, ref, RTOL, ATOL)
+    ok, err = rel_close(got, ref, RTOL, ATOL)  # strict: 1e-4 rel + 1e-5 abs at m = 300
     assert ok, err
     res = D.lcrwmd_topk(x1, x2, E, 10)
     _check_topk([r.distances for r in res], [r.ids for r in res], ref, 10)
@@ -211,3 +220,34 @@ def test_large_sampled_parity_and_batching():
         rd, ri = O.topk_select(full[:, j], np.arange(30000), 10)
         assert np.array_equal(td[j], rd) and np.array_equal(ti[j], ri)
     torch.cuda.synchronize()
+
+
+def test_sharded_pipeline_emulated_ranks():
+    """The multi-GPU decomposition run rank by rank on one GPU: vocabulary-slice
+    Z1 blocks (blocked SpMM addressing), per-shard reverse + top-k with global ids,
+    merge -- identical to the single-GPU result for several world sizes."""
+    import torch
+    from paper_1711_07227_b200 import device, parallel, synthetic as S
+    V, k = 6000, 10
+    E = S.embeddings(V, 300, seed=31)
+    x1 = S.histograms(5000, V, 40, seed=32)
+    x2 = S.histograms(37, V, 40, seed=33)
+    prep = device.PreparedEmbeddings(E)
+    dx2 = device.DeviceCSR.upload(x2)
+    want_d, want_i = device.symmetric(device.DeviceCSR.upload(x1), dx2, prep, k)
+    for W in (2, 3, 8):
+        slices = [parallel.z1_slice(dx2, prep, r, W) for r in range(W)]
+        R = slices[0][1]
+        zall = torch.stack([z for z, _ in slices])
+        parts_d, parts_i = [], []
+        for r in range(W):
+            lo, hi = parallel.shard_range(x1.n_rows, r, W)
+            dx1 = device.DeviceCSR.upload(x1.slice_rows(lo, hi))
+            d1 = parallel.d1_from_slices(dx1, zall, R, x2.n_rows)
+            ld, li = device.symmetric(dx1, dx2, prep, k, d1=d1, id_offset=lo)
+            parts_d.append(ld)
+            parts_i.append(li)
+        cd = torch.cat(parts_d, 1).contiguous()
+        ci = torch.cat(parts_i, 1).contiguous()
+        gd, gi = device.topk_rows(cd, ci, x2.n_rows, cd.shape[1], k)
+        assert torch.equal(gd, want_d) and torch.equal(gi, want_i), W
