@@ -88,6 +88,53 @@ size_t smem_bytes(int n_kb, int stages) {
          (2 + 2 * stages + 4) * 8 + 16;
 }
 
+
+// ---------------------------------------------------------------------------
+// epilogue helpers: branch-free minima over register ranges (static indices)
+// ---------------------------------------------------------------------------
+constexpr float kInf = __builtin_huge_valf();
+
+template <int A, int B>
+struct RangeMin {  // min(v[A..B]) as a balanced tree (B >= A)
+  __device__ __forceinline__ static float run(const float (&v)[32]) {
+    if constexpr (A == B) {
+      return v[A];
+    } else {
+      constexpr int M = (A + B) / 2;
+      return fminf(RangeMin<A, M>::run(v), RangeMin<M + 1, B>::run(v));
+    }
+  }
+};
+
+// exactly one segment end at column P of the chunk: pre = min(v[0..P]), suf = min(v[P+1..31])
+template <int P>
+__device__ __forceinline__ void split_at(const float (&v)[32], float& pre, float& suf) {
+  pre = RangeMin<0, P>::run(v);
+  if constexpr (P < 31) {
+    suf = RangeMin<P + 1, 31>::run(v);
+  } else {
+    suf = kInf;
+  }
+}
+
+template <int P = 0>
+__device__ __forceinline__ void split_switch(int p, const float (&v)[32], float& pre, float& suf) {
+  if constexpr (P < 32) {
+    if (p == P) {
+      split_at<P>(v, pre, suf);
+      return;
+    }
+    split_switch<P + 1>(p, v, pre, suf);
+  }
+}
+
+__device__ __forceinline__ float masked_min(const float (&v)[32], uint32_t sel) {
+  float t[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) t[j] = ((sel >> j) & 1u) ? v[j] : kInf;
+  return RangeMin<0, 31>::run(t);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     phase1_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const Params p) {
@@ -216,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float nE = valid ? p.a_norms[row] : 0.f;
       float* zrow = p.Z + (int64_t)row * 8;
       int64_t s = s0;
-      float run = __int_as_float(0x7f800000);
+      float run = kInf;
       for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
         const int ncols = (int)min((int64_t)BN, c_end - c0);
         const int buf = tile_ctr & 1;
@@ -235,31 +282,60 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(t_full + acc, acc_phase);
         tc_fence_after();
         const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+        const float zscale = inv_scale;
+        auto emit = [&](float segmin) {
+          if (valid) zrow[(s >> 3) * p.z_panel + (s & 7)] = sqrtf(fmaxf(segmin + nE, 0.f)) * zscale;
+          ++s;
+        };
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
-          if (ch * 32 >= ncols) break;
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_base + ch * 32, v);
+        for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
+          if (ch2 * 64 >= ncols) break;
+          uint32_t raw[2][32];
+          tmem_ld_32x32b_x32(t_base + ch2 * 64, raw[0]);
+          tmem_ld_32x32b_x32(t_base + ch2 * 64 + 32, raw[1]);
           tmem_wait_ld();
-          const uint32_t mask = mb[ch];
-          const int lim = ncols - ch * 32;
-          const float4* nb4 = reinterpret_cast<const float4*>(nb + ch * 32);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 n4 = nb4[j4];
-            const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
+          for (int h = 0; h < 2; ++h) {
+            const int ch = ch2 * 2 + h;
+            const int lim = ncols - ch * 32;
+            if (lim <= 0) break;
+            // v_j = |B_j|^2 - 2 A.B_j  (|A|^2 is added once per segment)
+            float v[32];
+            const float4* nb4 = reinterpret_cast<const float4*>(nb + ch * 32);
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const int j = j4 * 4 + jj;
-              if (j < lim) {
-                run = fminf(run, fmaf(-2.f, __uint_as_float(v[j]), nn[jj]));
-                if ((mask >> j) & 1u) {
-                  if (valid)
-                    zrow[(s >> 3) * p.z_panel + (s & 7)] = sqrtf(fmaxf(run + nE, 0.f)) * inv_scale;
-                  run = __int_as_float(0x7f800000);
-                  ++s;
-                }
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 n4 = nb4[j4];
+              v[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 0]), n4.x);
+              v[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 1]), n4.y);
+              v[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 2]), n4.z);
+              v[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 3]), n4.w);
+            }
+            uint32_t mask = mb[ch];
+            if (lim < 32) {  // last chunk of a range: columns >= lim belong to the next range
+              mask &= (1u << lim) - 1u;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j >= lim) v[j] = kInf;
+            }
+            const int nb_ends = __popc(mask);
+            if (nb_ends == 0) {
+              run = fminf(run, RangeMin<0, 31>::run(v));
+            } else if (nb_ends == 1) {
+              float pre, suf;
+              split_switch(__ffs(mask) - 1, v, pre, suf);
+              emit(fminf(run, pre));
+              run = suf;
+            } else {
+              int start = 0;
+              while (mask) {
+                const int e = __ffs(mask) - 1;
+                mask &= mask - 1u;
+                const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
+                emit(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
+                run = kInf;
+                start = e + 1;
               }
+              if (start < 32) run = masked_min(v, 0xFFFFFFFFu << start);
             }
           }
         }
