@@ -44,6 +44,14 @@ const char* lcrw_status_string(int status);
 const char* lcrw_last_error(void);
 int lcrw_sm_count(int* out);
 
+/* Optional launch profiler (benchmarking): when enabled, instrumented launches
+ * (phase1 / phase1_rev / spmm / reverse_max) are bracketed by CUDA events on
+ * their stream; lcrw_profile_get waits for record i and returns its name and
+ * elapsed milliseconds. */
+int lcrw_profile_reset(int enable);
+int64_t lcrw_profile_count(void);
+int lcrw_profile_get(int64_t i, char* name, int name_cap, float* ms);
+
 /* ---- embedding preparation (kernels.py:66-69 squared_norms; the f16 operand
  *      rounding replaces the float64 casts of distances.py:161-166) -------- */
 int lcrw_padded_dim(int m);
@@ -86,24 +94,28 @@ int lcrw_remap_ids(const int32_t* col_ids, int64_t nnz, const int32_t* remap, in
  * Segment plan: endmask has one bit per B row (set on the last row of each
  * segment), lcrw_endmask_words(n_cols) words (tail padded for the epilogue's
  * 256-column window); range_seg[0..n_ranges] splits the segments into
- * ~range_cols-column ranges that never cut a segment. */
+ * ~range_cols-column ranges that never cut a segment.  Segment s covers B rows
+ * [seg_offsets[s] - seg_base, seg_offsets[s+1] - seg_base), so a batch can point
+ * into a larger CSR's offsets without rebasing them. */
 int64_t lcrw_endmask_words(int64_t n_cols);
 int64_t lcrw_plan_ranges(int64_t n_cols, int range_cols);
-int lcrw_segment_plan(const int64_t* seg_offsets, int64_t n_seg, int64_t n_cols, int range_cols,
+int lcrw_segment_plan(const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg, int64_t n_cols, int range_cols,
                       uint32_t* endmask, int32_t* range_seg, int64_t n_ranges, void* stream);
 /* Z[s, r] = min_{t in segment s} |A_r - B_t| for r < a_rows, s < n_seg, where m is
  * the K extent of the operand rows (m, or 3m for the split layouts 1/2):
  * tcgen05 f16 GEMM (TMA-fed, TMEM accumulators) with the Gram expansion and
- * segmented row-min fused into the epilogue. */
+ * segmented row-min fused into the epilogue.  Z panels are 1 << z_shift
+ * segments wide: Z[(s >> z_shift) * z_panel + (r << z_shift) + (s & mask)]. */
 int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
                 const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
-                int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges,
-                const float* scale, float* Z, int64_t z_panel, void* stream);
+                int64_t seg_base, int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg,
+                int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift, void* stream);
 /* Exact zeros: for every B row t of segment s whose vector is identical to
  * an A row r (rep[t] / canon / next classes, remap: E id -> A row or -1,
- * NULL = identity), Z[s, r] = 0. */
+ * NULL = identity), Z[s, r] = 0.  rep is indexed by the raw seg_offsets values. */
 int lcrw_zero_identical(const int64_t* seg_offsets, int64_t n_seg, const int32_t* rep,
-                        const int32_t* next, const int32_t* remap, float* Z, int64_t z_panel, void* stream);
+                        const int32_t* next, const int32_t* remap, float* Z, int64_t z_panel, int z_shift,
+                        void* stream);
 
 /* ---- Phase 2 (kernels.py:174-198 spmm/spmv; distances.py:203) -----------
  * out[i, s] = sum_p x[i, p] * Z[s, col[i, p]] in fp64, rounded once to f32,
@@ -124,11 +136,31 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
  * id_offset + doc_base + j (id_offset = the shard's first global doc). */
 int lcrw_reverse_chunk_docs(void);
 int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
-                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, int64_t id_offset,
-                     const float* D1,
-                     int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k,
-                     float* cand_d, int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base,
-                     void* stream);
+                     const float* Z2, int64_t z_panel, int z_shift, int64_t n_docs, int64_t doc_base,
+                     int64_t id_offset, const float* D1, int64_t d1_ld_row, int64_t d1_ld_panel, float* dout,
+                     int64_t ld_out, int k, float* cand_d, int64_t* cand_i, int64_t n_chunks_total,
+                     int64_t chunk_base, int chunk_docs, void* stream);
+
+/* Whole reverse direction in one call (distances.py:263-264 + top-k): docs in
+ * batches of batch_docs (multiple of 32); per batch gather -> segment plan ->
+ * lcrw_phase1 (32-doc Z2 panels) -> lcrw_zero_identical -> lcrw_reverse_max,
+ * enqueued from C++ on `stream`.  doc_offsets_host is the host copy of
+ * doc_offsets (batch planning); doc_cols are global E ids, rep/next/remap as in
+ * lcrw_zero_identical; (q_offs, q_cols, q_vals) the query CSR with ids
+ * restricted to A's rows.  Workspace from lcrw_reverse_workspace with
+ * max_batch_words = max words over batches; n_chunks_total from
+ * lcrw_reverse_chunks. */
+int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
+int64_t lcrw_reverse_chunks(int64_t n_docs, int64_t batch_docs, int chunk_docs);
+int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB,
+                          const float* e_norms, int m, int kp, const float* scale, const int64_t* doc_offsets,
+                          const int64_t* doc_offsets_host, int64_t n_docs, const int32_t* doc_cols,
+                          const int32_t* rep, const int32_t* next, const int32_t* remap, const int64_t* q_offs,
+                          const int32_t* q_cols, const float* q_vals, int64_t n_q, const float* D1,
+                          int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k,
+                          float* cand_d, int64_t* cand_i, int64_t n_chunks_total, int64_t id_offset,
+                          int64_t batch_docs, int chunk_docs, int range_cols, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k

@@ -39,12 +39,20 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_remap_ids": (I32, [P, I64, P, P, P]),
     "lcrw_endmask_words": (I64, [I64]),
     "lcrw_plan_ranges": (I64, [I64, I32]),
-    "lcrw_segment_plan": (I32, [P, I64, I64, I32, P, P, I64, P]),
-    "lcrw_phase1": (I32, [P, P, I64, P, P, I64, I32, I32, P, I64, P, P, I64, P, P, I64, P]),
-    "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, P]),
+    "lcrw_segment_plan": (I32, [P, I64, I64, I64, I32, P, P, I64, P]),
+    "lcrw_phase1": (I32, [P, P, I64, P, P, I64, I32, I32, P, I64, I64, P, P, I64, P, P, I64, I32, P]),
+    "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, I32, P]),
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_chunk_docs": (I32, []),
-    "lcrw_reverse_max": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P, I64, I32, P, P, I64, I64, P]),
+    "lcrw_reverse_max": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P, I64, I32, P, P, I64, I64,
+                               I32, P]),
+    "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
+    "lcrw_reverse_chunks": (I64, [I64, I64, I32]),
+    "lcrw_reverse_pipeline": (I32, [P, P, I64, P, P, I32, I32, P, P, P, I64, P, P, P, P, P, P, P, I64, P, I64, I64,
+                                    P, I64, I32, P, P, I64, I64, I64, I32, I32, P, SZ, P]),
+    "lcrw_profile_reset": (I32, [I32]),
+    "lcrw_profile_count": (I64, []),
+    "lcrw_profile_get": (I32, [I64, C.c_char_p, I32, P]),
     "lcrw_topk_segments": (I32, [P, P, I64, I64, I32, P, P, P]),
     "lcrw_topk_sort_workspace": (I32, [I64, P]),
     "lcrw_topk_sort": (I32, [P, P, I64, I64, P, P, P, SZ, P]),
@@ -52,7 +60,8 @@ SIGNATURES: dict[str, tuple] = {
 
 # functions returning a value rather than a status
 _VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim",
-                "lcrw_endmask_words", "lcrw_plan_ranges", "lcrw_reverse_chunk_docs"}
+                "lcrw_endmask_words", "lcrw_plan_ranges", "lcrw_reverse_chunk_docs", "lcrw_reverse_chunks",
+                "lcrw_profile_count"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".
@@ -62,6 +71,8 @@ KERNELS_PER_CALL = {
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
     "lcrw_reverse_max": 1, "lcrw_topk_segments": 1, "lcrw_topk_sort": 7,
 }
+# lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse);
+# bench.py adds those from the batch count.
 
 CALLS: dict[str, int] = {}
 
@@ -96,6 +107,24 @@ def load() -> C.CDLL:
 def launches(calls: dict[str, int]) -> int:
     """Kernel launches implied by a call-count snapshot."""
     return sum(KERNELS_PER_CALL.get(n, 0) * c for n, c in calls.items())
+
+
+def profile_reset(enable: bool) -> None:
+    call("lcrw_profile_reset", 1 if enable else 0)
+
+
+def profile_read() -> dict[str, dict[str, float]]:
+    """name -> {ms, launches} of the native launch profiler (waits on the events)."""
+    lib = load()
+    out: dict[str, dict[str, float]] = {}
+    buf = C.create_string_buffer(64)
+    ms = C.c_float(0.0)
+    for i in range(int(lib.lcrw_profile_count())):
+        call("lcrw_profile_get", i, buf, 64, C.byref(ms))
+        d = out.setdefault(buf.value.decode(), {"ms": 0.0, "launches": 0})
+        d["ms"] += ms.value
+        d["launches"] += 1
+    return out
 
 
 def value(name: str, *args):

@@ -33,6 +33,20 @@ int cuda_status(cudaError_t e, const char* what);
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// RAII event pair around a launch when the profiler is enabled (abi.cu)
+class ProfScope {
+ public:
+  ProfScope(cudaStream_t s, const char* name);
+  ~ProfScope();
+  ProfScope(const ProfScope&) = delete;
+  ProfScope& operator=(const ProfScope&) = delete;
+
+ private:
+  cudaStream_t stream_;
+  const char* name_;
+  cudaEvent_t a_;
+};
 int sm_count();
 int64_t ceil_div(int64_t a, int64_t b);
 

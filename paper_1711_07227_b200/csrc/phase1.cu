@@ -47,7 +47,9 @@ struct Params {
   const float* scale;
   float* Z;
   int64_t z_panel;
+  int64_t seg_base;  // B row of seg_offsets[0]'s origin: column c = seg_offsets[s] - seg_base
   int64_t b_rows;
+  int z_shift;       // Z panel width = 1 << z_shift segments
   int a_rows;
   int n_mtiles;
   int n_ranges;
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mt = (int)(u % p.n_mtiles);
         const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
         if (s0 == s1) continue;
-        const int64_t c_begin = p.seg_offsets[s0], c_end = p.seg_offsets[s1];
+        const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
         mbar_wait(a_empty, a_phase ^ 1);
         a_phase ^= 1;
         mbar_expect_tx(a_full, p.n_kb * A_KB_BYTES);
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int range = (int)(u / p.n_mtiles);
         const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
         if (s0 == s1) continue;
-        const int64_t c_begin = p.seg_offsets[s0], c_end = p.seg_offsets[s1];
+        const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
         mbar_wait(a_full, a_phase);
         a_phase ^= 1;
         tc_fence_after();
@@ -257,11 +259,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int mt = (int)(u % p.n_mtiles);
       const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
       if (s0 == s1) continue;
-      const int64_t c_begin = p.seg_offsets[s0], c_end = p.seg_offsets[s1];
+      const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
       const int row = mt * BM + quarter * 32 + lane;
       const bool valid = row < p.a_rows;
       const float nE = valid ? p.a_norms[row] : 0.f;
-      float* zrow = p.Z + (int64_t)row * 8;
+      const int zs = p.z_shift;
+      const int64_t zmask = (1ll << zs) - 1;
+      float* zrow = p.Z + ((int64_t)row << zs);
       int64_t s = s0;
       float run = kInf;
       for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
         const float zscale = inv_scale;
         auto emit = [&](float segmin) {
-          if (valid) zrow[(s >> 3) * p.z_panel + (s & 7)] = sqrtf(fmaxf(segmin + nE, 0.f)) * zscale;
+          if (valid) zrow[(s >> zs) * p.z_panel + (s & zmask)] = sqrtf(fmaxf(segmin + nE, 0.f)) * zscale;
           ++s;
         };
 #pragma unroll 1
@@ -399,18 +403,19 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int kp, int box_r
 }  // namespace p1
 }  // namespace lcrw
 
-using namespace lcrw;
+namespace lcrw {
+namespace p1 {
 
-extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
-                           const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
-                           int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges,
-                           const float* scale, float* Z, int64_t z_panel, void* stream) {
-  using namespace lcrw::p1;
+int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, const float* b_norms,
+           int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
+           const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
+           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag) {
   LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(m)");
   LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
                "lcrw_phase1: row counts must fit in int32");
   LCRW_REQUIRE(n_seg >= 0 && n_ranges >= 1, "lcrw_phase1: bad segment plan");
-  LCRW_REQUIRE(z_panel >= 8 * a_rows, "lcrw_phase1: z_panel must be >= 8 * a_rows");
+  LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_phase1: z_shift out of range");
+  LCRW_REQUIRE(z_panel >= (a_rows << z_shift), "lcrw_phase1: z_panel must be >= a_rows << z_shift");
   if (a_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(A && a_norms && B && b_norms && seg_offsets && endmask && range_seg && scale && Z,
                "lcrw_phase1: null pointer");
@@ -431,7 +436,9 @@ extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_ro
   p.scale = scale;
   p.Z = Z;
   p.z_panel = z_panel;
+  p.seg_base = seg_base;
   p.b_rows = b_rows;
+  p.z_shift = z_shift;
   p.a_rows = (int)a_rows;
   p.n_mtiles = (int)ceil_div(a_rows, BM);
   p.n_ranges = (int)n_ranges;
@@ -448,16 +455,27 @@ extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_ro
   const size_t smem = smem_bytes(n_kb, stages);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_bytes(kMaxKb, 3) > (int)smem_bytes(5, 4)
-                                             ? (int)smem_bytes(kMaxKb, 3)
-                                             : (int)smem_bytes(5, 4));
+    const size_t mx = smem_bytes(kMaxKb, 3) > smem_bytes(5, 4) ? smem_bytes(kMaxKb, 3) : smem_bytes(5, 4);
+    cudaError_t e = cudaFuncSetAttribute(phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(phase1_kernel)");
     attr_set = true;
   }
   const int64_t n_units = (int64_t)n_ranges * p.n_mtiles;
   const int grid = (int)(n_units < sm_count() ? n_units : sm_count());
-  phase1_kernel<<<grid, kThreads, smem, as_stream(stream)>>>(tmA, tmB, p);
+  ProfScope prof(stream, tag);
+  phase1_kernel<<<grid, kThreads, smem, stream>>>(tmA, tmB, p);
   LCRW_CHECK_LAUNCH("phase1_kernel");
   return LCRW_OK;
+}
+
+}  // namespace p1
+}  // namespace lcrw
+
+extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
+                           const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
+                           int64_t seg_base, int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg,
+                           int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift,
+                           void* stream) {
+  return lcrw::p1::launch(A, a_norms, a_rows, B, b_norms, b_rows, m, kp, seg_offsets, seg_base, n_seg, endmask,
+                          range_seg, n_ranges, scale, Z, z_panel, z_shift, lcrw::as_stream(stream), "phase1");
 }

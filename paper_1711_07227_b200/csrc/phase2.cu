@@ -14,7 +14,7 @@ namespace p2 {
 
 constexpr int kWarps = 8;
 constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
-constexpr int kChunkDocs = 4096;    // reverse: docs per block (one candidate list per warp)
+constexpr int kDefaultChunkDocs = 256;  // reverse: docs per block (one candidate list per warp)
 
 // ---------------------------------------------------------------------------
 // CSR x panelled Z: one warp per CSR row, 4 consecutive segments per lane.
@@ -87,15 +87,15 @@ template <int KMAX>
 __global__ void __launch_bounds__(kWarps * 32)
     reverse_max_kernel(const int64_t* __restrict__ q_offs, const int32_t* __restrict__ q_cols,
                        const float* __restrict__ q_vals, int64_t n_q, const float* __restrict__ Z2, int64_t z_panel,
-                       int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
+                       int z_shift, int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
                        int64_t d1_ld_row, int64_t d1_ld_panel, float* __restrict__ dout, int64_t ld_out, int k,
                        float* __restrict__ cand_d, int64_t* __restrict__ cand_i, int64_t n_chunks_total,
-                       int64_t chunk_base) {
+                       int64_t chunk_base, int chunk_docs) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (int64_t)blockIdx.y * kWarps + (threadIdx.x >> 5);
   if (q >= n_q) return;  // warp-uniform; no block-level synchronisation below
-  const int64_t j_begin = (int64_t)blockIdx.x * kChunkDocs;
-  const int64_t j_end = min(n_docs, j_begin + kChunkDocs);
+  const int64_t j_begin = (int64_t)blockIdx.x * chunk_docs;
+  const int64_t j_end = min(n_docs, j_begin + chunk_docs);
   const int64_t lo = q_offs[q], hi = q_offs[q + 1];
   const float* d1q = D1 + (q >> 3) * d1_ld_panel + (q & 7);
 
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kWarps * 32)
   for (int64_t jb = j_begin; jb < j_end; jb += 32) {
     const int64_t jl = jb + lane;
     const bool valid = jl < j_end;
-    const float* zj = Z2 + (jl >> 3) * z_panel + (jl & 7);
+    const float* zj = Z2 + (jl >> z_shift) * z_panel + (jl & ((1ll << z_shift) - 1));
     double acc = 0.0;
     for (int64_t base = lo; base < hi; base += 32) {
       const int cnt = (int)min((int64_t)32, hi - base);
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       for (int t = 0; t < cnt; ++t) {
         const int64_t w = __shfl_sync(0xffffffffu, my_w, t);
         const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
-        if (valid) acc = fma(x, (double)__ldg(zj + w * 8), acc);
+        if (valid) acc = fma(x, (double)__ldg(zj + (w << z_shift)), acc);
       }
     }
     if (valid) {
@@ -186,43 +186,47 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
   int64_t gx = ceil_div(n_rows, kWarps);
   const int64_t cap = (int64_t)sm_count() * 64;
   if (gx > cap) gx = cap;
+  ProfScope prof(as_stream(stream), "spmm");
   spmm_kernel<<<dim3((unsigned)gx, (unsigned)gy), kWarps * 32, 0, as_stream(stream)>>>(
       offs, cols, vals, n_rows, Z, z_panel, z_block_rows, z_block_stride, n_seg, out, ld_row, ld_panel);
   LCRW_CHECK_LAUNCH("spmm_kernel");
   return LCRW_OK;
 }
 
-int lcrw_reverse_chunk_docs(void) { return kChunkDocs; }
+int lcrw_reverse_chunk_docs(void) { return kDefaultChunkDocs; }
 
 int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
-                     const float* Z2, int64_t z_panel, int64_t n_docs, int64_t doc_base, int64_t id_offset,
+                     const float* Z2, int64_t z_panel, int z_shift, int64_t n_docs, int64_t doc_base, int64_t id_offset,
                      const float* D1,
                      int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k, float* cand_d,
-                     int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base, void* stream) {
+                     int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base, int chunk_docs, void* stream) {
   LCRW_REQUIRE(n_q >= 0 && n_docs >= 0, "lcrw_reverse_max: bad shape");
   if (n_q == 0 || n_docs == 0) return LCRW_OK;
   LCRW_REQUIRE(q_offs && q_cols && q_vals && Z2 && D1, "lcrw_reverse_max: null pointer");
   LCRW_REQUIRE(doc_base + n_docs < (1ll << 31), "lcrw_reverse_max: doc ids must fit in int32");
-  const int64_t gx = ceil_div(n_docs, kChunkDocs);
+  LCRW_REQUIRE(chunk_docs >= 32 && chunk_docs % 32 == 0, "lcrw_reverse_max: chunk_docs must be a positive multiple of 32");
+  const int64_t gx = ceil_div(n_docs, chunk_docs);
   const int64_t gy = ceil_div(n_q, kWarps);
   LCRW_REQUIRE(gy < 65536, "lcrw_reverse_max: too many queries for one launch");
+  LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_reverse_max: z_shift out of range");
   dim3 grid((unsigned)gx, (unsigned)gy);
   cudaStream_t st = as_stream(stream);
+  ProfScope prof(st, "reverse_max");
   if (dout) {
-    reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
+    reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, z_shift, n_docs, doc_base,
                                                          id_offset, D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
-                                                         nullptr, 0, 0);
+                                                         nullptr, 0, 0, chunk_docs);
   } else {
     LCRW_REQUIRE(k >= 1 && cand_d && cand_i, "lcrw_reverse_max: top-k mode needs k >= 1 and candidate buffers");
     LCRW_REQUIRE(chunk_base + gx <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
     if (k <= 16) {
-      reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
+      reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, z_shift, n_docs,
                                                            doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
-                                                           cand_d, cand_i, n_chunks_total, chunk_base);
+                                                           cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
     } else if (k <= 32) {
-      reverse_max_kernel<32><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
+      reverse_max_kernel<32><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, z_shift, n_docs,
                                                            doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
-                                                           cand_d, cand_i, n_chunks_total, chunk_base);
+                                                           cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
     } else {
       set_error("lcrw_reverse_max: fused top-k supports k <= 32 (got %d); use the full-matrix path", k);
       return LCRW_ERR_UNSUPPORTED;

@@ -1,0 +1,134 @@
+// Native driver of the reverse direction (distances.py:263, with the symmetric
+// combine of distances.py:264 and the per-query top-k of kernels.py:210-223):
+// the resident docs play the queries, the query set is the resident side.
+//
+// Docs are processed in batches; per batch, on one stream and without host
+// synchronisation:
+//   gather   T = E_B[words of the batch docs]               (operand rows)
+//   plan     segment-end bitmap + column ranges             (segments = docs)
+//   phase1   Z2[doc, w] = min_t |E_w - T_t|                 (tcgen05, 32-doc panels)
+//   zeros    Z2[doc, w] = 0 where doc holds a word identical to w
+//   reverse  D = max(D1, spmm(Xq, Z2)) -> per (query, doc chunk) top-k
+// The loop runs in C++ so a batch costs a handful of launch calls, not Python.
+#include "common.cuh"
+
+namespace lcrw {
+namespace p1 {
+int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, const float* b_norms,
+           int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
+           const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
+           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag);
+}
+
+namespace {
+constexpr int kZShift = 5;  // 32-doc panels: a warp's 32 docs of one word row are one 128-byte line
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+int auto_range_cols(int64_t b_rows, int64_t a_rows) {
+  const int64_t n_mtiles = ceil_div(a_rows, 128);
+  int64_t want = n_mtiles * b_rows / (8 * (int64_t)sm_count());
+  want = (want + 255) / 256 * 256;
+  if (want < 1024) want = 1024;
+  if (want > 32768) want = 32768;
+  return (int)want;
+}
+
+struct Layout {
+  size_t T, tn, mask, rs, Z, total;
+};
+
+Layout layout(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_words) {
+  Layout L;
+  const int64_t max_ranges = lcrw_plan_ranges(max_words, 1024) + 1;
+  L.T = 0;
+  L.tn = L.T + align256((size_t)max_words * kp * 2);
+  L.mask = L.tn + align256((size_t)max_words * 4);
+  L.rs = L.mask + align256((size_t)lcrw_endmask_words(max_words) * 4);
+  L.Z = L.rs + align256((size_t)max_ranges * 4);
+  const int64_t panels = ceil_div(batch_docs, 1 << kZShift);
+  L.total = L.Z + align256((size_t)panels * (size_t)(a_rows << kZShift) * 4);
+  return L;
+}
+}  // namespace
+}  // namespace lcrw
+
+using namespace lcrw;
+
+extern "C" {
+
+int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes) {
+  LCRW_REQUIRE(a_rows >= 0 && kp > 0 && batch_docs > 0 && max_batch_words >= 0 && bytes,
+               "lcrw_reverse_workspace: bad arguments");
+  *bytes = layout(a_rows, kp, batch_docs, max_batch_words).total;
+  return LCRW_OK;
+}
+
+int64_t lcrw_reverse_chunks(int64_t n_docs, int64_t batch_docs, int chunk_docs) {
+  if (n_docs < 0 || batch_docs <= 0 || chunk_docs <= 0) return -1;
+  int64_t n = 0;
+  for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
+    const int64_t nd = (n_docs - j0) < batch_docs ? (n_docs - j0) : batch_docs;
+    n += ceil_div(nd, chunk_docs);
+  }
+  return n;
+}
+
+int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB,
+                          const float* e_norms, int m, int kp, const float* scale, const int64_t* doc_offsets,
+                          const int64_t* doc_offsets_host, int64_t n_docs, const int32_t* doc_cols, const int32_t* rep,
+                          const int32_t* next, const int32_t* remap, const int64_t* q_offs, const int32_t* q_cols,
+                          const float* q_vals, int64_t n_q, const float* D1, int64_t d1_ld_row, int64_t d1_ld_panel,
+                          float* dout, int64_t ld_out, int k, float* cand_d, int64_t* cand_i, int64_t n_chunks_total,
+                          int64_t id_offset, int64_t batch_docs, int chunk_docs, int range_cols, void* ws,
+                          size_t ws_bytes, void* stream) {
+  LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
+  if (n_docs == 0 || n_q == 0) return LCRW_OK;
+  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && rep && ws, "lcrw_reverse_pipeline: null pointer");
+  LCRW_REQUIRE(batch_docs > 0 && (batch_docs % (1 << kZShift)) == 0,
+               "lcrw_reverse_pipeline: batch_docs must be a positive multiple of 32");
+  int64_t max_words = 0;
+  for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
+    const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
+    const int64_t w = doc_offsets_host[j1] - doc_offsets_host[j0];
+    if (w > max_words) max_words = w;
+  }
+  const Layout L = layout(a_rows, kp, batch_docs, max_words);
+  LCRW_REQUIRE(ws_bytes >= L.total, "lcrw_reverse_pipeline: workspace too small (use lcrw_reverse_workspace)");
+  if (!dout) {
+    LCRW_REQUIRE(lcrw_reverse_chunks(n_docs, batch_docs, chunk_docs) == n_chunks_total,
+                 "lcrw_reverse_pipeline: n_chunks_total != lcrw_reverse_chunks(...)");
+  }
+  char* base = static_cast<char*>(ws);
+  uint16_t* T = reinterpret_cast<uint16_t*>(base + L.T);
+  float* tn = reinterpret_cast<float*>(base + L.tn);
+  uint32_t* mask = reinterpret_cast<uint32_t*>(base + L.mask);
+  int32_t* rs = reinterpret_cast<int32_t*>(base + L.rs);
+  float* Z2 = reinterpret_cast<float*>(base + L.Z);
+  const int64_t z_panel = a_rows << kZShift;
+  cudaStream_t st = as_stream(stream);
+  int64_t chunk_base = 0;
+  int status;
+  for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
+    const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
+    const int64_t nd = j1 - j0;
+    const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
+    if ((status = lcrw_gather_rows(EhB, e_norms, kp, doc_cols + lo, nw, T, tn, stream))) return status;
+    const int rc = range_cols > 0 ? range_cols : auto_range_cols(nw, a_rows);
+    const int64_t n_ranges = lcrw_plan_ranges(nw, rc);
+    if ((status = lcrw_segment_plan(doc_offsets + j0, lo, nd, nw, rc, mask, rs, n_ranges, stream))) return status;
+    if ((status = p1::launch(A, a_norms, a_rows, T, tn, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs, n_ranges, scale,
+                             Z2, z_panel, kZShift, st, "phase1_rev")))
+      return status;
+    if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
+      return status;
+    if ((status = lcrw_reverse_max(q_offs, q_cols, q_vals, n_q, Z2, z_panel, kZShift, nd, j0, id_offset, D1, d1_ld_row,
+                                   d1_ld_panel, dout, ld_out, k, cand_d, cand_i, n_chunks_total, chunk_base,
+                                   chunk_docs, stream)))
+      return status;
+    chunk_base += ceil_div(nd, chunk_docs);
+  }
+  return LCRW_OK;
+}
+
+}  // extern "C"

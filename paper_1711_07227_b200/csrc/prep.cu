@@ -216,14 +216,15 @@ __global__ void remap_ids_kernel(const int32_t* __restrict__ cols, int64_t nnz, 
 // ---------------------------------------------------------------------------
 // Phase-1 segment plan and exact zeros
 // ---------------------------------------------------------------------------
-__global__ void endmask_kernel(const int64_t* __restrict__ offs, int64_t n_seg, uint32_t* __restrict__ mask) {
+__global__ void endmask_kernel(const int64_t* __restrict__ offs, int64_t base, int64_t n_seg,
+                               uint32_t* __restrict__ mask) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg; s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t last = offs[s + 1] - 1;
+    const int64_t last = offs[s + 1] - 1 - base;
     atomicOr(mask + (last >> 5), 1u << (last & 31));
   }
 }
 
-__global__ void ranges_kernel(const int64_t* __restrict__ offs, int64_t n_seg, int range_cols,
+__global__ void ranges_kernel(const int64_t* __restrict__ offs, int64_t base, int64_t n_seg, int range_cols,
                               int32_t* __restrict__ range_seg, int64_t n_ranges) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n_ranges; r += (int64_t)gridDim.x * blockDim.x) {
     if (r == n_ranges) {
@@ -234,24 +235,25 @@ __global__ void ranges_kernel(const int64_t* __restrict__ offs, int64_t n_seg, i
     int64_t lo = 0, hi = n_seg;  // first s in [0, n_seg] with offs[s] >= target
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if (offs[mid] < target) lo = mid + 1; else hi = mid;
+      if (offs[mid] - base < target) lo = mid + 1; else hi = mid;
     }
     range_seg[r] = static_cast<int32_t>(lo);
   }
 }
 
-// one warp per segment, lanes over its B rows
+// one warp per segment, lanes over its B rows (rep indexed by the raw offsets)
 __global__ void zero_identical_kernel(const int64_t* __restrict__ offs, int64_t n_seg, const int32_t* __restrict__ rep,
                                       const int32_t* __restrict__ next, const int32_t* __restrict__ remap,
-                                      float* __restrict__ Z, int64_t z_panel) {
+                                      float* __restrict__ Z, int64_t z_panel, int z_shift) {
   const int lane = threadIdx.x & 31;
+  const int64_t zmask = (1ll << z_shift) - 1;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < n_seg;
        s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    float* zs = Z + (s >> 3) * z_panel + (s & 7);
+    float* zs = Z + (s >> z_shift) * z_panel + (s & zmask);
     for (int64_t t = offs[s] + lane; t < offs[s + 1]; t += 32) {
       for (int32_t g = rep[t]; g >= 0; g = next ? next[g] : -1) {
         const int32_t r = remap ? remap[g] : g;
-        if (r >= 0) zs[(int64_t)r * 8] = 0.f;
+        if (r >= 0) zs[(int64_t)r << z_shift] = 0.f;
       }
     }
   }
@@ -407,26 +409,28 @@ int64_t lcrw_plan_ranges(int64_t n_cols, int range_cols) {
   return n < 1 ? 1 : n;
 }
 
-int lcrw_segment_plan(const int64_t* seg_offsets, int64_t n_seg, int64_t n_cols, int range_cols,
+int lcrw_segment_plan(const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg, int64_t n_cols, int range_cols,
                       uint32_t* endmask, int32_t* range_seg, int64_t n_ranges, void* stream) {
   LCRW_REQUIRE(n_seg >= 1 && n_cols >= n_seg && range_cols > 0 && n_ranges >= 1, "lcrw_segment_plan: bad shape");
   LCRW_REQUIRE(seg_offsets && endmask && range_seg, "lcrw_segment_plan: null pointer");
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(endmask, 0, lcrw_endmask_words(n_cols) * 4, st);
-  endmask_kernel<<<grid_for(n_seg), kThreads, 0, st>>>(seg_offsets, n_seg, endmask);
+  endmask_kernel<<<grid_for(n_seg), kThreads, 0, st>>>(seg_offsets, seg_base, n_seg, endmask);
   LCRW_CHECK_LAUNCH("endmask_kernel");
-  ranges_kernel<<<grid_for(n_ranges + 1), kThreads, 0, st>>>(seg_offsets, n_seg, range_cols, range_seg, n_ranges);
+  ranges_kernel<<<grid_for(n_ranges + 1), kThreads, 0, st>>>(seg_offsets, seg_base, n_seg, range_cols, range_seg,
+                                                             n_ranges);
   LCRW_CHECK_LAUNCH("ranges_kernel");
   return LCRW_OK;
 }
 
 int lcrw_zero_identical(const int64_t* seg_offsets, int64_t n_seg, const int32_t* rep, const int32_t* next,
-                        const int32_t* remap, float* Z, int64_t z_panel, void* stream) {
+                        const int32_t* remap, float* Z, int64_t z_panel, int z_shift, void* stream) {
   LCRW_REQUIRE(n_seg >= 0, "lcrw_zero_identical: bad shape");
   if (n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(seg_offsets && rep && Z, "lcrw_zero_identical: null pointer");
+  LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_zero_identical: z_shift out of range");
   zero_identical_kernel<<<grid_for(n_seg * 32), kThreads, 0, as_stream(stream)>>>(seg_offsets, n_seg, rep, next,
-                                                                                 remap, Z, z_panel);
+                                                                                 remap, Z, z_panel, z_shift);
   LCRW_CHECK_LAUNCH("zero_identical_kernel");
   return LCRW_OK;
 }

@@ -67,49 +67,6 @@ def to_device(a, dtype, non_blocking: bool = True) -> torch.Tensor:
     return t.to(dev, non_blocking=non_blocking and t.is_pinned())
 
 
-class KernelTimer:
-    """Optional CUDA-event bracketing of named kernel launches on the launching stream.
-
-    bench.py enables it to measure the dominant kernel's live duration inside
-    the timed region; algorithmic work (FLOPs / bytes) is accumulated alongside."""
-
-    def __init__(self):
-        self.enabled = False
-        self.records: list[tuple[str, torch.cuda.Event, torch.cuda.Event, float]] = []
-
-    def reset(self, enabled: bool = True) -> None:
-        self.enabled = enabled
-        self.records = []
-
-    def span(self, name: str, work: float):
-        timer = self
-
-        class _Span:
-            def __enter__(self_inner):
-                if timer.enabled:
-                    self_inner.a = torch.cuda.Event(enable_timing=True)
-                    self_inner.b = torch.cuda.Event(enable_timing=True)
-                    self_inner.a.record()
-
-            def __exit__(self_inner, *exc):
-                if timer.enabled:
-                    self_inner.b.record()
-                    timer.records.append((name, self_inner.a, self_inner.b, work))
-
-        return _Span()
-
-    def summary(self) -> dict[str, dict[str, float]]:
-        """name -> {ms, work, launches} (call after a synchronize)."""
-        out: dict[str, dict[str, float]] = {}
-        for name, a, b, work in self.records:
-            d = out.setdefault(name, {"ms": 0.0, "work": 0.0, "launches": 0})
-            d["ms"] += a.elapsed_time(b)
-            d["work"] += work
-            d["launches"] += 1
-        return out
-
-
-TIMER = KernelTimer()
 
 
 # ---------------------------------------------------------------------------
@@ -257,26 +214,25 @@ def _range_cols(b_rows: int, a_rows: int) -> int:
 
 def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor, b_norms: torch.Tensor,
            b_rows: int, seg_offsets: torch.Tensor, n_seg: int, prep: PreparedEmbeddings,
-           range_cols: int | None = None, tag: str = "phase1") -> tuple[torch.Tensor, int]:
-    """Z (panel layout, z_panel = 8 * a_rows) of distances.py:147-178, without the exact-zero pass."""
+           range_cols: int | None = None) -> tuple[torch.Tensor, int]:
+    """Z (8-segment panels, z_panel = 8 * a_rows) of distances.py:147-178, without the exact-zero pass."""
     dev = A.device
     st = _stream()
     rc = range_cols or _range_cols(b_rows, a_rows)
     n_ranges = int(_lib.value("lcrw_plan_ranges", b_rows, rc))
     endmask = torch.empty(int(_lib.value("lcrw_endmask_words", b_rows)), dtype=torch.int32, device=dev)
     range_seg = torch.empty(n_ranges + 1, dtype=torch.int32, device=dev)
-    _lib.call("lcrw_segment_plan", _p(seg_offsets), n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
+    _lib.call("lcrw_segment_plan", _p(seg_offsets), 0, n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
     z_panel = 8 * max(a_rows, 1)
     Z = torch.empty(((n_seg + 7) // 8) * z_panel, dtype=torch.float32, device=dev)
-    with TIMER.span(tag, 2.0 * a_rows * b_rows * prep.m):  # algorithmic FLOPs, K = m unpadded
-        _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), _p(b_norms), b_rows, prep.k_eff, prep.kp,
-                  _p(seg_offsets), n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel,
-                  st)
+    _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), _p(b_norms), b_rows, prep.k_eff, prep.kp,
+              _p(seg_offsets), 0, n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel, 3,
+              st)
     return Z, z_panel
 
 
-def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel) -> None:
-    _lib.call("lcrw_zero_identical", _p(seg_offsets), n_seg, _p(rep), _p(nxt), _p(remap), _p(Z), z_panel,
+def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel, z_shift: int = 3) -> None:
+    _lib.call("lcrw_zero_identical", _p(seg_offsets), n_seg, _p(rep), _p(nxt), _p(remap), _p(Z), z_panel, z_shift,
               _stream())
 
 
@@ -332,10 +288,10 @@ class Restricted:
 
 
 def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
-                      n_seg: int, tag: str = "phase1") -> tuple[torch.Tensor, int]:
+                      n_seg: int) -> tuple[torch.Tensor, int]:
     """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros)."""
     B, bn = gather_rows(prep, word_ids, "B")
-    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, bn, word_ids.numel(), seg_offsets, n_seg, prep, tag=tag)
+    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, bn, word_ids.numel(), seg_offsets, n_seg, prep)
     rep, nxt = prep.representatives(word_ids)
     zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp)
     return Z, zp
@@ -346,34 +302,34 @@ def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR,
 
     layout "rows" -> row-major (n_res, n_q); "panels" -> out[(q>>3)*8*n_res + i*8 + (q&7)]."""
     n_res, n_q = res.csr.n_rows, queries.n_rows
-    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q, tag="phase1_fwd")
+    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q)
     if layout == "rows":
         out = torch.empty(n_res * max(n_q, 1), dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = n_q, 8
     else:
         out = torch.empty(((n_q + 7) // 8) * 8 * n_res, dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = 8, 8 * n_res
-    # no-reuse gather model (SURVEY §8d): offsets + (id, value) stream + one Z row-segment per nonzero
-    with TIMER.span("spmm_fwd", 8.0 * (n_res + 1) + 8.0 * res.csr.nnz + 4.0 * res.csr.nnz * n_q):
-        spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel)
+    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel)
     return out
 
 
-def _doc_batches(host_offsets: np.ndarray, v_e2: int, budget_bytes: int) -> list[tuple[int, int]]:
-    n = len(host_offsets) - 1
-    chunk = int(_lib.value("lcrw_reverse_chunk_docs"))
-    per_doc = 4 * max(v_e2, 1)
-    nb = max(8, budget_bytes // per_doc)
-    nb = (nb // chunk) * chunk if nb >= chunk else max(8, (nb // 8) * 8)
-    return [(j0, min(n, j0 + nb)) for j0 in range(0, n, nb)]
+REVERSE_Z2_BYTES = 4 << 30   # Z2 batch budget (docs per batch = budget / (4 * v_e2), multiple of 32)
+REVERSE_CHUNK_DOCS = 512     # docs per (query, chunk) top-k candidate list
+
+
+def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BYTES) -> int:
+    nb = max(32, budget_bytes // (4 * max(v_e2, 1)))
+    nb = min(nb, max(32, n_docs))
+    return int((nb + 31) // 32 * 32)
 
 
 def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
-              z2_budget_bytes: int = 8 << 30, d1: torch.Tensor | None = None, id_offset: int = 0):
+              z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0,
+              chunk_docs: int = REVERSE_CHUNK_DOCS):
     """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, k) dists, ids).
 
-    ``d1`` (panel layout) may be supplied by a caller that computed the forward
-    direction itself (parallel.py); ``id_offset`` shifts the returned doc ids."""
+    ``d1`` (8-segment panels) may be supplied by a caller that computed the
+    forward direction itself (parallel.py); ``id_offset`` shifts returned doc ids."""
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
     st = _stream()
@@ -382,35 +338,33 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
         del res1
     res2 = Restricted.build(x2, prep)
-    batches = _doc_batches(x1.host_offsets, res2.v_e, z2_budget_bytes)
-    chunk = int(_lib.value("lcrw_reverse_chunk_docs"))
+    batch = reverse_batch_docs(n1, res2.v_e, z2_budget_bytes)
+    ho = x1.host_offsets
+    max_words = max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
+    ws_bytes = C.c_size_t(0)
+    _lib.call("lcrw_reverse_workspace", res2.v_e, prep.kp, batch, max_words, C.byref(ws_bytes))
+    ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
     if k is None:
         dout = torch.empty(n1 * n2, dtype=torch.float32, device=dev)
         cand_d = cand_i = None
         n_chunks = 0
     else:
+        if k > 32:
+            raise NotImplementedError("fused top-k supports k <= 32")
         dout = None
-        n_chunks = sum((b1 - b0 + chunk - 1) // chunk for b0, b1 in batches)
+        n_chunks = int(_lib.value("lcrw_reverse_chunks", n1, batch, chunk_docs))
         cand_d = torch.empty(n2 * n_chunks * k, dtype=torch.float32, device=dev)
         cand_i = torch.empty(n2 * n_chunks * k, dtype=torch.int64, device=dev)
-    chunk_base = 0
-    for j0, j1 in batches:
-        lo, hi = int(x1.host_offsets[j0]), int(x1.host_offsets[j1])
-        seg = x1.offsets[j0:j1 + 1] - lo
-        Z2, zp2 = nearest_distances(res2, prep, seg, x1.cols[lo:hi], j1 - j0, tag="phase1_rev")
-        # bytes: Z2 gathers (one f32 per query nonzero per doc) + D1 read
-        work = 4.0 * x2.nnz * (j1 - j0) + 4.0 * n2 * (j1 - j0)
-        with TIMER.span("reverse_max", work):
-            _lib.call("lcrw_reverse_max", _p(x2.offsets), _p(res2.cols_r), _p(x2.vals), n2, _p(Z2), zp2, j1 - j0,
-                      j0, id_offset, _p(d1), 8, 8 * n1, _p(dout), n2, k or 0, _p(cand_d), _p(cand_i), n_chunks,
-                      chunk_base, st)
-        chunk_base += (j1 - j0 + chunk - 1) // chunk
-        del Z2
+    rep, nxt = prep.representatives(x1.cols)
+    host_offs = np.ascontiguousarray(ho, dtype=np.int64)
+    _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), _p(prep.norms),
+              prep.k_eff, prep.kp, _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1,
+              _p(x1.cols), _p(rep), _p(nxt), _p(res2.remap), _p(x2.offsets), _p(res2.cols_r), _p(x2.vals), n2,
+              _p(d1), 8, 8 * n1, _p(dout), n2, k or 0, _p(cand_d), _p(cand_i), n_chunks, id_offset, batch,
+              chunk_docs, 0, _p(ws), ws_bytes.value, st)
     if k is None:
         return dout.view(n1, n2)
-    if k <= 1024:
-        return topk_rows(cand_d, cand_i, n2, n_chunks * k, k)
-    raise NotImplementedError("k > 1024")
+    return topk_rows(cand_d, cand_i, n2, n_chunks * k, k)
 
 
 def nearest_word_distances(E, Q) -> torch.Tensor:

@@ -88,8 +88,7 @@ def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) ->
     zl = torch.zeros((panels, R, 8), dtype=torch.float32, device=dev)
     if rows > 0:
         B, bn = device.gather_rows(prep, dx2.cols, "B")
-        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, bn, dx2.nnz, dx2.offsets, n_q, prep,
-                              tag="phase1_fwd")
+        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, bn, dx2.nnz, dx2.offsets, n_q, prep)
         remap = torch.full((prep.V,), -1, dtype=torch.int32, device=dev)
         remap[v0:v1] = torch.arange(rows, dtype=torch.int32, device=dev)
         rep, nxt = prep.representatives(dx2.cols)
@@ -103,9 +102,8 @@ def d1_from_slices(dx1: DeviceCSR, zall: torch.Tensor, R: int, n_q: int) -> torc
     n1 = dx1.n_rows
     panels = (n_q + 7) // 8
     out = torch.empty(panels * 8 * max(n1, 1), dtype=torch.float32, device=zall.device)
-    with device.TIMER.span("spmm_fwd", 8.0 * (n1 + 1) + 8.0 * dx1.nnz + 4.0 * dx1.nnz * n_q):
-        device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, 8 * R, n_q, out, 8, 8 * n1,
-                    z_block_rows=R, z_block_stride=panels * R * 8)
+    device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, 8 * R, n_q, out, 8, 8 * n1,
+                z_block_rows=R, z_block_stride=panels * R * 8)
     return out
 
 

@@ -38,8 +38,8 @@ def test_library_rejects_bad_arguments_without_gpu():
     with pytest.raises(ValueError, match="k must be >= 1"):
         _lib.call("lcrw_topk_segments", None, None, 1, 1, 0, None, None, None)
     with pytest.raises(ValueError, match="kp must be"):
-        _lib.call("lcrw_phase1", None, None, 0, None, None, 0, 300, 300, None, 1, None, None, 1, None, None, 0,
-                  None)
+        _lib.call("lcrw_phase1", None, None, 0, None, None, 0, 300, 300, None, 0, 1, None, None, 1, None, None, 0,
+                  3, None)
 
 
 def test_histogram_set_basics():
