@@ -1,0 +1,5 @@
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "spec or golden_full or c1_shaped" 2>&1 | tail -5
+timeout 400 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python bench.py --config c2 --steps 2 --warmup 1 --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']
+print(round(d['value']/1e6,1), 'Mpairs/s', round(d['ms_per_step'],1),'ms', {n:(round(v['ms_per_step'],1), round(v.get('tflops',v.get('gbs_algorithmic',0)),1), v['launches_per_step']) for n,v in k.items()}, 'e2e', round(d['e2e']['value']/1e6,1))"

@@ -8,19 +8,25 @@
 // the Gram expansion and the segmented row-min are fused into the epilogue so
 // the |A| x |B| distance matrix never exists outside TMEM.
 //
-// Work decomposition (persistent, one CTA per SM):
-//   unit = (m-tile of 128 A rows, column range of ~range_cols B rows whose
-//   bounds are segment boundaries).  Within a unit the A tile stays resident
-//   in shared memory (all K blocks) while B is streamed through a TMA ring in
-//   256-row x 64-element K blocks; each 128x256 fp32 accumulator tile is
-//   double-buffered in TMEM (2 x 256 columns) so the epilogue of tile i
-//   overlaps the MMAs of tile i+1.  Segments may straddle N tiles: the running
-//   minimum is carried in registers across tiles of the same unit, and ranges
-//   never cut a segment, so every Z entry is written exactly once, with no
-//   atomics and no initialisation pass.
+// CTA pairs (cluster of 2, tcgen05 cta_group::2): one pair computes 256 A rows
+// x 256 B rows per tile.  Each CTA keeps ITS 128 A rows (all K blocks) resident
+// in shared memory for a whole work unit and streams ITS HALF (128 rows) of
+// every B tile through an 8-stage TMA ring; the leader CTA issues the pair MMA
+// (M = 256, N = 256, K = 16), whose operands come from both CTAs' smem, and the
+// fp32 accumulator rows land in each CTA's own TMEM (2 x 256 columns, double
+// buffered).  Splitting B across the pair halves per-SM operand traffic (smem
+// reads and L2->SM TMA bytes) relative to a single-CTA M = 128 tile and doubles
+// the MMA time each staged byte covers.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w4..w7 epilogue (TMEM lane quarter = warp % 4, one A row per thread).
+// Work unit = (pair of 128-row m-tiles, column range of ~range_cols B rows
+// bounded by segment boundaries).  Segments may straddle N tiles: the running
+// minimum is carried in registers across the tiles of a unit, and ranges never
+// cut a segment, so every Z entry is written exactly once (no atomics, no
+// initialisation pass).
+//
+// Warp roles (256 threads per CTA): w0 TMA producer, w1 MMA issuer (leader CTA
+// only), w2 TMEM allocator, w4..w7 epilogue (TMEM lane quarter = warp % 4, one A
+// row per thread; per-warp column-norm buffers prefetched one tile ahead).
 #include <cstdio>
 
 #include "common.cuh"
@@ -28,14 +34,15 @@
 namespace lcrw {
 namespace p1 {
 
-constexpr int BM = 128;                       // A rows per tile (TMEM lanes)
-constexpr int BN = 256;                       // B rows per tile (MMA N)
+constexpr int BM = 128;                       // A rows per CTA (TMEM lanes); the pair covers 256
+constexpr int BN = 256;                       // B rows per pair tile (MMA N); 128 staged per CTA
+constexpr int BN_HALF = BN / 2;
 constexpr int BK = 64;                        // f16 elements per K block (128 B rows)
 constexpr int A_KB_BYTES = BM * BK * 2;       // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;    // 32 KB
+constexpr int B_STAGE_BYTES = BN_HALF * BK * 2;  // 16 KB per CTA
 constexpr int kThreads = 256;
-constexpr int kEpiThreads = 128;
-constexpr uint32_t kIdesc = umma_idesc_f16(BM, BN);
+constexpr int kEpiWarps = 4;
+constexpr uint32_t kIdesc = umma_idesc_f16(2 * BM, BN);
 constexpr int kMaxKb = 7;                     // m <= 448
 
 struct Params {
@@ -47,49 +54,30 @@ struct Params {
   const float* scale;
   float* Z;
   int64_t z_panel;
-  int64_t seg_base;  // B row of seg_offsets[0]'s origin: column c = seg_offsets[s] - seg_base
+  int64_t seg_base;  // column c = seg_offsets[s] - seg_base
   int64_t b_rows;
   int z_shift;       // Z panel width = 1 << z_shift segments
   int a_rows;
-  int n_mtiles;
+  int n_mpairs;      // 256-row A tiles
   int n_ranges;
   int n_kb;
   int n_kmma;
   int stages;
 };
 
+// shared-memory carve-up; identical offsets in both CTAs of a pair
 struct Smem {
-  uint8_t* A;
-  uint8_t* B;
-  float* nbuf;       // [2][BN]
-  uint32_t* mbuf;    // [2][BN/32]
+  uint32_t A, B;       // shared-window addresses (1024-aligned)
+  float* nbuf;         // [kEpiWarps][BN] column norms, one buffer per epilogue warp
+  uint32_t* mbuf;      // [kEpiWarps][BN / 32] segment-end bits
   uint64_t* bars;
   uint32_t* tmem_slot;
 };
 
-__device__ __forceinline__ Smem carve(uint8_t* raw, const Params& p) {
-  Smem s;
-  uintptr_t base = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
-  uint8_t* ptr = reinterpret_cast<uint8_t*>(base);
-  s.A = ptr;
-  ptr += p.n_kb * A_KB_BYTES;
-  s.B = ptr;
-  ptr += p.stages * B_STAGE_BYTES;
-  s.nbuf = reinterpret_cast<float*>(ptr);
-  ptr += 2 * BN * sizeof(float);
-  s.mbuf = reinterpret_cast<uint32_t*>(ptr);
-  ptr += 2 * (BN / 32) * sizeof(uint32_t);
-  s.bars = reinterpret_cast<uint64_t*>(ptr);
-  ptr += (2 + 2 * p.stages + 4) * sizeof(uint64_t);
-  s.tmem_slot = reinterpret_cast<uint32_t*>(ptr);
-  return s;
-}
-
 size_t smem_bytes(int n_kb, int stages) {
-  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + 2 * BN * 4 + 2 * (BN / 32) * 4 +
-         (2 + 2 * stages + 4) * 8 + 16;
+  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + kEpiWarps * BN * 4 +
+         kEpiWarps * (BN / 32) * 4 + (2 + 2 * stages + 4) * 8 + 16;
 }
-
 
 // ---------------------------------------------------------------------------
 // epilogue helpers: branch-free minima over register ranges (static indices)
@@ -137,20 +125,34 @@ __device__ __forceinline__ float masked_min(const float (&v)[32], uint32_t sel) 
   return RangeMin<0, 31>::run(t);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     phase1_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  const Smem sm = carve(smem_raw, p);
-  uint64_t* a_full = sm.bars + 0;
-  uint64_t* a_empty = sm.bars + 1;
-  uint64_t* b_full = sm.bars + 2;
-  uint64_t* b_empty = sm.bars + 2 + p.stages;
-  uint64_t* t_full = sm.bars + 2 + 2 * p.stages;
-  uint64_t* t_empty = sm.bars + 4 + 2 * p.stages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // keep every pointer derived from smem_raw so the compiler emits shared-space accesses
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  Smem sm;
+  sm.A = smem_u32(base);
+  sm.B = sm.A + p.n_kb * A_KB_BYTES;
+  uint8_t* tail = base + p.n_kb * A_KB_BYTES + p.stages * B_STAGE_BYTES;
+  sm.nbuf = reinterpret_cast<float*>(tail);
+  sm.mbuf = reinterpret_cast<uint32_t*>(tail + kEpiWarps * BN * 4);
+  sm.bars = reinterpret_cast<uint64_t*>(tail + kEpiWarps * BN * 4 + kEpiWarps * (BN / 32) * 4);
+  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.bars + 2 + 2 * p.stages + 4);
+
+  uint64_t* a_full = sm.bars + 0;   // leader: A tiles of both CTAs landed
+  uint64_t* a_empty = sm.bars + 1;  // both: the unit's MMAs retired (commit multicast)
+  uint64_t* b_full = sm.bars + 2;   // leader: B halves of both CTAs landed
+  uint64_t* b_empty = sm.bars + 2 + p.stages;  // both: stage consumed (commit multicast)
+  uint64_t* t_full = sm.bars + 2 + 2 * p.stages;  // both: accumulator ready (commit multicast)
+  uint64_t* t_empty = sm.bars + 4 + 2 * p.stages;  // leader: 8 epilogue warps drained it
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t pair = blockIdx.x >> 1;
+  const int64_t n_pairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -163,43 +165,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(t_full + i, 1);
-      mbar_init(t_empty + i, kEpiThreads / 32);
+      mbar_init(t_empty + i, 2 * kEpiWarps);
     }
     fence_mbar_init();
   }
   if (warp == 2) {
-    tmem_alloc(sm.tmem_slot, 512);
-    tmem_relinquish();
+    tmem_alloc_2sm(sm.tmem_slot, 512);
+    tmem_relinquish_2sm();
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_slot;
 
-  const int64_t n_units = (int64_t)p.n_ranges * p.n_mtiles;
+  const int64_t n_units = (int64_t)p.n_ranges * p.n_mpairs;
 
   if (warp == 0) {
-    // ============================ TMA producer ============================
+    // ============================ TMA producer (both CTAs) ============================
     if (lane == 0) {
       const uint64_t pol_a = l2_policy_evict_last();    // A tiles are re-read by every range
-      const uint64_t pol_b = l2_policy_evict_normal();  // B ranges are shared by concurrent CTAs
+      const uint64_t pol_b = l2_policy_evict_normal();  // B ranges are shared by concurrent pairs
+      const uint32_t a_full_l = mapa_shared(smem_u32(a_full), 0);
+      const uint32_t b_full_l = mapa_shared(smem_u32(b_full), 0);
       uint32_t stage = 0, phase = 0, a_phase = 0;
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int range = (int)(u / p.n_mtiles);
-        const int mt = (int)(u % p.n_mtiles);
+      for (int64_t u = pair; u < n_units; u += n_pairs) {
+        const int range = (int)(u / p.n_mpairs);
+        const int mp = (int)(u % p.n_mpairs);
         const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
         if (s0 == s1) continue;
         const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
         mbar_wait(a_empty, a_phase ^ 1);
         a_phase ^= 1;
-        mbar_expect_tx(a_full, p.n_kb * A_KB_BYTES);
+        if (leader) mbar_expect_tx(a_full, 2 * p.n_kb * A_KB_BYTES);
         for (int kb = 0; kb < p.n_kb; ++kb)
-          tma_load_2d(&tmA, a_full, sm.A + kb * A_KB_BYTES, kb * BK, mt * BM, pol_a);
+          tma_load_2d_2sm(&tmA, a_full_l, smem_raw + (sm.A - smem_u32(smem_raw)) + kb * A_KB_BYTES, kb * BK,
+                          mp * 2 * BM + (int)rank * BM, pol_a);
         for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_empty + stage, phase ^ 1);
-            mbar_expect_tx(b_full + stage, B_STAGE_BYTES);
-            tma_load_2d(&tmB, b_full + stage, sm.B + stage * B_STAGE_BYTES, kb * BK, (int32_t)c0, pol_b);
+            if (leader) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
+            tma_load_2d_2sm(&tmB, b_full_l + stage * 8,
+                            smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES, kb * BK,
+                            (int32_t)(c0 + rank * BN_HALF), pol_b);
             if (++stage == (uint32_t)p.stages) {
               stage = 0;
               phase ^= 1;
@@ -209,13 +216,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ============================ MMA issuer ==============================
-    if (lane == 0) {
+    // ============================ MMA issuer (leader CTA) =============================
+    if (leader && lane == 0) {
       uint32_t stage = 0, phase = 0, a_phase = 0, acc = 0, acc_phase = 0;
-      const uint32_t a_base = smem_u32(sm.A);
-      const uint32_t b_base = smem_u32(sm.B);
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int range = (int)(u / p.n_mtiles);
+      for (int64_t u = pair; u < n_units; u += n_pairs) {
+        const int range = (int)(u / p.n_mpairs);
         const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
         if (s0 == s1) continue;
         const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
@@ -231,133 +236,184 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int nk = min(4, p.n_kmma - 4 * kb);
             for (int k = 0; k < nk; ++k) {
-              const uint64_t ad = umma_desc_sw128(a_base + kb * A_KB_BYTES + k * 32);
-              const uint64_t bd = umma_desc_sw128(b_base + stage * B_STAGE_BYTES + k * 32);
-              umma_f16(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+              const uint64_t ad = umma_desc_sw128(sm.A + kb * A_KB_BYTES + k * 32);
+              const uint64_t bd = umma_desc_sw128(sm.B + stage * B_STAGE_BYTES + k * 32);
+              umma_f16_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
             }
-            umma_commit(b_empty + stage);  // frees the B slot once these MMAs retire
+            umma_commit_2sm_mc(b_empty + stage, 0x3);  // frees the stage in both CTAs
             if (++stage == (uint32_t)p.stages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit(t_full + acc);  // accumulator tile ready for the epilogue
+          umma_commit_2sm_mc(t_full + acc, 0x3);  // accumulator ready in both CTAs' TMEM
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
-        umma_commit(a_empty);  // A tile may be overwritten once the unit's MMAs retire
+        umma_commit_2sm_mc(a_empty, 0x3);  // A tiles reusable once the unit's MMAs retire
       }
     }
   } else if (warp >= 4) {
-    // ============================ epilogue ================================
-    const int et = threadIdx.x - 128;
+    // ============================ epilogue (both CTAs) ================================
+    const int ew = warp - 4;
     const int quarter = warp & 3;
     const float inv_scale = p.scale[1];
-    uint32_t acc = 0, acc_phase = 0, tile_ctr = 0;
-    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int range = (int)(u / p.n_mtiles);
-      const int mt = (int)(u % p.n_mtiles);
-      const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
-      if (s0 == s1) continue;
-      const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
-      const int row = mt * BM + quarter * 32 + lane;
-      const bool valid = row < p.a_rows;
-      const float nE = valid ? p.a_norms[row] : 0.f;
-      const int zs = p.z_shift;
-      const int64_t zmask = (1ll << zs) - 1;
-      float* zrow = p.Z + ((int64_t)row << zs);
-      int64_t s = s0;
-      float run = kInf;
-      for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
-        const int ncols = (int)min((int64_t)BN, c_end - c0);
-        const int buf = tile_ctr & 1;
-        float* nb = sm.nbuf + buf * BN;
-        uint32_t* mb = sm.mbuf + buf * (BN / 32);
-        for (int i = et; i < BN; i += kEpiThreads) nb[i] = i < ncols ? __ldg(p.b_norms + c0 + i) : 0.f;
-        if (et < BN / 32) {
-          const int64_t bit = c0 + et * 32;
-          const int64_t w = bit >> 5;
-          const uint32_t off = (uint32_t)(bit & 31);
-          const uint32_t lo = __ldg(p.endmask + w);
-          const uint32_t hi = __ldg(p.endmask + w + 1);
-          mb[et] = __funnelshift_r(lo, hi, off);
-        }
-        named_bar_sync(1, kEpiThreads);
-        mbar_wait(t_full + acc, acc_phase);
-        tc_fence_after();
-        const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-        const float zscale = inv_scale;
-        auto emit = [&](float segmin) {
-          if (valid) zrow[(s >> zs) * p.z_panel + (s & zmask)] = sqrtf(fmaxf(segmin + nE, 0.f)) * zscale;
-          ++s;
-        };
+    const uint32_t t_empty_l = mapa_shared(smem_u32(t_empty), 0);
+    float* nb = sm.nbuf + ew * BN;
+    uint32_t* mb = sm.mbuf + ew * (BN / 32);
+    const int zs = p.z_shift;
+    const int64_t zmask = (1ll << zs) - 1;
+
+    // tile iterator over this pair's units (skips empty ranges)
+    int64_t u = pair - n_pairs, c_begin = 0, c_end = 0, c0 = 0;
+    auto next_tile = [&](int64_t& uu, int64_t& cb, int64_t& ce, int64_t& cc) -> int {
+      // returns 0 = done, 1 = same unit, 2 = new unit
+      if (uu >= 0 && cc + BN < ce) {
+        cc += BN;
+        return 1;
+      }
+      for (uu += n_pairs; uu < n_units; uu += n_pairs) {
+        const int range = (int)(uu / p.n_mpairs);
+        const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
+        if (s0 == s1) continue;
+        cb = p.seg_offsets[s0] - p.seg_base;
+        ce = p.seg_offsets[s1] - p.seg_base;
+        cc = cb;
+        return 2;
+      }
+      return 0;
+    };
+    // stage a tile's column norms / segment-end bits into registers
+    float pn[BN / 32];
+    uint32_t pm = 0;
+    auto fetch = [&](int64_t cc, int64_t ce) {
+#pragma unroll
+      for (int i = 0; i < BN / 32; ++i) {
+        const int64_t c = cc + i * 32 + lane;
+        pn[i] = c < ce ? __ldg(p.b_norms + c) : 0.f;
+      }
+      if (lane < BN / 32) {
+        const int64_t bit = cc + lane * 32;
+        const uint32_t lo = __ldg(p.endmask + (bit >> 5));
+        const uint32_t hi = __ldg(p.endmask + (bit >> 5) + 1);
+        pm = __funnelshift_r(lo, hi, (uint32_t)(bit & 31));
+      }
+    };
+    auto stash = [&]() {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < BN / 32; ++i) nb[i * 32 + lane] = pn[i];
+      if (lane < BN / 32) mb[lane] = pm;
+      __syncwarp();
+    };
+
+    int kind = next_tile(u, c_begin, c_end, c0);
+    if (kind) {
+      fetch(c0, c_end);
+      stash();
+    }
+    uint32_t acc = 0, acc_phase = 0;
+    int row = 0;
+    bool valid = false;
+    float nE = 0.f, run = kInf;
+    float* zrow = p.Z;
+    int64_t s = 0;
+    while (kind) {
+      if (kind == 2) {  // first tile of a unit
+        const int mp = (int)(u % p.n_mpairs);
+        const int range = (int)(u / p.n_mpairs);
+        row = mp * 2 * BM + (int)rank * BM + quarter * 32 + lane;
+        valid = row < p.a_rows;
+        nE = valid ? __ldg(p.a_norms + row) : 0.f;
+        zrow = p.Z + ((int64_t)row << zs);
+        s = p.range_seg[range];
+        run = kInf;
+      }
+      const int ncols = (int)min((int64_t)BN, c_end - c0);
+      // prefetch the next tile's norms while this tile is processed
+      int64_t nu = u, ncb = c_begin, nce = c_end, nc0 = c0;
+      const int nkind = next_tile(nu, ncb, nce, nc0);
+      if (nkind) fetch(nc0, nce);
+
+      mbar_wait(t_full + acc, acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      auto emit = [&](float segmin) {
+        if (valid) zrow[(s >> zs) * p.z_panel + (s & zmask)] = sqrtf(fmaxf(segmin + nE, 0.f)) * inv_scale;
+        ++s;
+      };
 #pragma unroll 1
-        for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
-          if (ch2 * 64 >= ncols) break;
-          uint32_t raw[2][32];
-          tmem_ld_32x32b_x32(t_base + ch2 * 64, raw[0]);
-          tmem_ld_32x32b_x32(t_base + ch2 * 64 + 32, raw[1]);
-          tmem_wait_ld();
+      for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
+        if (ch2 * 64 >= ncols) break;
+        uint32_t raw[2][32];
+        tmem_ld_32x32b_x32(t_base + ch2 * 64, raw[0]);
+        tmem_ld_32x32b_x32(t_base + ch2 * 64 + 32, raw[1]);
+        tmem_wait_ld();
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int ch = ch2 * 2 + h;
-            const int lim = ncols - ch * 32;
-            if (lim <= 0) break;
-            // v_j = |B_j|^2 - 2 A.B_j  (|A|^2 is added once per segment)
-            float v[32];
-            const float4* nb4 = reinterpret_cast<const float4*>(nb + ch * 32);
+        for (int h = 0; h < 2; ++h) {
+          const int ch = ch2 * 2 + h;
+          const int lim = ncols - ch * 32;
+          if (lim <= 0) break;
+          // v_j = |B_j|^2 - 2 A.B_j  (|A|^2 is added once per segment)
+          float v[32];
+          const float4* nb4 = reinterpret_cast<const float4*>(nb + ch * 32);
 #pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-              const float4 n4 = nb4[j4];
-              v[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 0]), n4.x);
-              v[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 1]), n4.y);
-              v[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 2]), n4.z);
-              v[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 3]), n4.w);
-            }
-            uint32_t mask = mb[ch];
-            if (lim < 32) {  // last chunk of a range: columns >= lim belong to the next range
-              mask &= (1u << lim) - 1u;
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 n4 = nb4[j4];
+            v[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 0]), n4.x);
+            v[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 1]), n4.y);
+            v[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 2]), n4.z);
+            v[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 3]), n4.w);
+          }
+          uint32_t mask = mb[ch];
+          if (lim < 32) {  // last chunk of a range: columns >= lim belong to the next range
+            mask &= (1u << lim) - 1u;
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j >= lim) v[j] = kInf;
+            for (int j = 0; j < 32; ++j)
+              if (j >= lim) v[j] = kInf;
+          }
+          const int nb_ends = __popc(mask);
+          if (nb_ends == 0) {
+            run = fminf(run, RangeMin<0, 31>::run(v));
+          } else if (nb_ends == 1) {
+            float pre, suf;
+            split_switch(__ffs(mask) - 1, v, pre, suf);
+            emit(fminf(run, pre));
+            run = suf;
+          } else {
+            int start = 0;
+            while (mask) {
+              const int e = __ffs(mask) - 1;
+              mask &= mask - 1u;
+              const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
+              emit(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
+              run = kInf;
+              start = e + 1;
             }
-            const int nb_ends = __popc(mask);
-            if (nb_ends == 0) {
-              run = fminf(run, RangeMin<0, 31>::run(v));
-            } else if (nb_ends == 1) {
-              float pre, suf;
-              split_switch(__ffs(mask) - 1, v, pre, suf);
-              emit(fminf(run, pre));
-              run = suf;
-            } else {
-              int start = 0;
-              while (mask) {
-                const int e = __ffs(mask) - 1;
-                mask &= mask - 1u;
-                const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
-                emit(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
-                run = kInf;
-                start = e + 1;
-              }
-              if (start < 32) run = masked_min(v, 0xFFFFFFFFu << start);
-            }
+            if (start < 32) run = masked_min(v, 0xFFFFFFFFu << start);
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(t_empty + acc);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-        ++tile_ctr;
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(t_empty_l + acc * 8);  // leader's t_empty[acc]
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      if (nkind) stash();
+      u = nu;
+      c_begin = ncb;
+      c_end = nce;
+      c0 = nc0;
+      kind = nkind;
     }
   }
 
+  __syncwarp();  // reconverge single-lane roles before the aligned cluster barrier
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc_2sm(tmem, 512);
   }
 }
 
@@ -426,7 +482,7 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
     set_error("lcrw_phase1: embedding dimension %d > %d unsupported", m, kMaxKb * BK);
     return LCRW_ERR_UNSUPPORTED;
   }
-  const int stages = n_kb <= 5 ? 4 : 3;
+  const int stages = n_kb <= 5 ? 8 : 6;
   Params p;
   p.a_norms = a_norms;
   p.b_norms = b_norms;
@@ -440,7 +496,7 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   p.b_rows = b_rows;
   p.z_shift = z_shift;
   p.a_rows = (int)a_rows;
-  p.n_mtiles = (int)ceil_div(a_rows, BM);
+  p.n_mpairs = (int)ceil_div(a_rows, 2 * BM);
   p.n_ranges = (int)n_ranges;
   p.n_kb = n_kb;
   p.n_kmma = (m + 15) / 16;
@@ -449,19 +505,20 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   CUtensorMap tmA, tmB;
   int st = make_map(&tmA, A, a_rows, kp, BM);
   if (st) return st;
-  st = make_map(&tmB, B, b_rows, kp, BN);
+  st = make_map(&tmB, B, b_rows, kp, BN_HALF);
   if (st) return st;
 
   const size_t smem = smem_bytes(n_kb, stages);
   static bool attr_set = false;
   if (!attr_set) {
-    const size_t mx = smem_bytes(kMaxKb, 3) > smem_bytes(5, 4) ? smem_bytes(kMaxKb, 3) : smem_bytes(5, 4);
+    const size_t mx = smem_bytes(kMaxKb, 6) > smem_bytes(5, 8) ? smem_bytes(kMaxKb, 6) : smem_bytes(5, 8);
     cudaError_t e = cudaFuncSetAttribute(phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(phase1_kernel)");
     attr_set = true;
   }
-  const int64_t n_units = (int64_t)n_ranges * p.n_mtiles;
-  const int grid = (int)(n_units < sm_count() ? n_units : sm_count());
+  const int64_t n_units = (int64_t)n_ranges * p.n_mpairs;
+  const int64_t pairs = sm_count() / 2;
+  const int grid = 2 * (int)(n_units < pairs ? n_units : pairs);
   ProfScope prof(stream, tag);
   phase1_kernel<<<grid, kThreads, smem, stream>>>(tmA, tmB, p);
   LCRW_CHECK_LAUNCH("phase1_kernel");
