@@ -53,20 +53,26 @@ int64_t lcrw_profile_count(void);
 int lcrw_profile_get(int64_t i, char* name, int name_cap, float* ms);
 
 /* ---- embedding preparation (kernels.py:66-69 squared_norms; the f16 operand
- *      rounding replaces the float64 casts of distances.py:161-166) -------- */
+ *      rounding replaces the float64 casts of distances.py:161-166) --------
+ * Operand rows have K = lcrw_operand_k(m, split) used columns (m or 3m values
+ * + 3 norm columns), zero padded to kp = lcrw_padded_dim(K). */
 int lcrw_padded_dim(int m);
-/* atomically max-accumulates |x| over n values into *amax_bits (zero it first) */
-int lcrw_absmax(const float* x, int64_t n, uint32_t* amax_bits, void* stream);
-/* scale[0] = 2^e with absmax * 2^e in [2^12, 2^13); scale[1] = 1 / scale[0] */
-int lcrw_scale_from_absmax(const uint32_t* amax_bits, float* scale, void* stream);
-/* layout 0: Xh[r, :] = f16_rn(X[r, :m] * scale), zero padded to kp = lcrw_padded_dim(m).
- * layouts 1/2 ("3 x f16" split, kp = lcrw_padded_dim(3m)): with hi = f16(x*s),
- * lo = f16(x*s - hi), A rows are [hi, hi, lo] (1) and B rows [hi, lo, hi] (2), so
- * one K = 3m product gives hi.hi + hi.lo + lo.hi (~22-bit operands).
- * norms[r] = |rounded row|^2 (fp64 sum, stored f32). */
+int lcrw_operand_k(int m, int split);
+/* atomically max-accumulates max_r |x_r|^2 over rows x m values into *max_bits (zero it first) */
+int lcrw_max_sqnorm(const float* x, int64_t rows, int m, uint32_t* max_bits, void* stream);
+/* scale[0] = 2^k with max|x|^2 * 4^k in [2^12, 2^14); scale[1] = 1 / scale[0] */
+int lcrw_scale_from_max_sqnorm(const uint32_t* max_bits, float* scale, void* stream);
+/* Operand rows of x' = scale * x, hi = f16_rn(x'), lo = f16_rn(x' - hi),
+ * n = |rounded row|^2 (fp64) split into three f16 pieces:
+ *   layout 0 (A):       [hi, 1, 1, 1]                      K = m + 3
+ *   layout 1 (A split): [hi, hi, lo, 1, 1, 1]              K = 3m + 3
+ *   layout 2 (B):       [-2hi, n_hi, n_mid, n_lo]          K = m + 3
+ *   layout 3 (B split): [-2hi, -2lo, -2hi, n_hi, n_mid, n_lo]  K = 3m + 3
+ * so one dot of an A row with a B row is |b|^2 - 2 a.b (split: ~22-bit
+ * operands).  norms[r] = n as f32 (may be NULL). */
 int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, int layout, const float* scale,
                       uint16_t* Xh, float* norms, void* stream);
-/* T[i] = Xh[ids[i]], tnorms[i] = norms[ids[i]] (distances.py:201 `query_E[cols]`) */
+/* T[i] = Xh[ids[i]], tnorms[i] = norms[ids[i]] if tnorms (distances.py:201 `query_E[cols]`) */
 int lcrw_gather_rows(const uint16_t* Xh, const float* norms, int kp, const int32_t* ids, int64_t n,
                      uint16_t* T, float* tnorms, void* stream);
 
@@ -101,13 +107,14 @@ int64_t lcrw_endmask_words(int64_t n_cols);
 int64_t lcrw_plan_ranges(int64_t n_cols, int range_cols);
 int lcrw_segment_plan(const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg, int64_t n_cols, int range_cols,
                       uint32_t* endmask, int32_t* range_seg, int64_t n_ranges, void* stream);
-/* Z[s, r] = min_{t in segment s} |A_r - B_t| for r < a_rows, s < n_seg, where m is
- * the K extent of the operand rows (m, or 3m for the split layouts 1/2):
+/* Z[s, r] = min_{t in segment s} |A_r - B_t| for r < a_rows, s < n_seg, where A
+ * rows use layout 0/1 and B rows layout 2/3 of lcrw_prepare_rows, m is their K
+ * extent (lcrw_operand_k) and a_norms the A rows' norms:
  * tcgen05 f16 GEMM (TMA-fed, TMEM accumulators) with the Gram expansion and
  * segmented row-min fused into the epilogue.  Z panels are 1 << z_shift
  * segments wide: Z[(s >> z_shift) * z_panel + (r << z_shift) + (s & mask)]. */
 int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
-                const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
+                int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
                 int64_t seg_base, int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg,
                 int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift, void* stream);
 /* Exact zeros: for every B row t of segment s whose vector is identical to

@@ -27,8 +27,9 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_last_error": (C.c_char_p, []),
     "lcrw_sm_count": (I32, [P]),
     "lcrw_padded_dim": (I32, [I32]),
-    "lcrw_absmax": (I32, [P, I64, P, P]),
-    "lcrw_scale_from_absmax": (I32, [P, P, P]),
+    "lcrw_operand_k": (I32, [I32, I32]),
+    "lcrw_max_sqnorm": (I32, [P, I64, I32, P, P]),
+    "lcrw_scale_from_max_sqnorm": (I32, [P, P, P]),
     "lcrw_prepare_rows": (I32, [P, I64, I32, I32, I32, P, P, P, P]),
     "lcrw_gather_rows": (I32, [P, P, I32, P, I64, P, P, P]),
     "lcrw_row_classes_workspace": (I32, [I64, P]),
@@ -40,7 +41,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_endmask_words": (I64, [I64]),
     "lcrw_plan_ranges": (I64, [I64, I32]),
     "lcrw_segment_plan": (I32, [P, I64, I64, I64, I32, P, P, I64, P]),
-    "lcrw_phase1": (I32, [P, P, I64, P, P, I64, I32, I32, P, I64, I64, P, P, I64, P, P, I64, I32, P]),
+    "lcrw_phase1": (I32, [P, P, I64, P, I64, I32, I32, P, I64, I64, P, P, I64, P, P, I64, I32, P]),
     "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, I32, P]),
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_chunk_docs": (I32, []),
@@ -59,14 +60,14 @@ SIGNATURES: dict[str, tuple] = {
 }
 
 # functions returning a value rather than a status
-_VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim",
+_VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
                 "lcrw_endmask_words", "lcrw_plan_ranges", "lcrw_reverse_chunk_docs", "lcrw_reverse_chunks",
                 "lcrw_profile_count"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".
 KERNELS_PER_CALL = {
-    "lcrw_absmax": 1, "lcrw_scale_from_absmax": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
+    "lcrw_max_sqnorm": 1, "lcrw_scale_from_max_sqnorm": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
     "lcrw_row_classes": 12, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
     "lcrw_reverse_max": 1, "lcrw_topk_segments": 1, "lcrw_topk_sort": 7,

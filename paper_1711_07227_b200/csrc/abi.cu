@@ -106,6 +106,8 @@ int lcrw_sm_count(int* out) {
 
 int lcrw_padded_dim(int m) { return m <= 0 ? 0 : ((m + 63) / 64) * 64; }
 
+int lcrw_operand_k(int m, int split) { return m <= 0 ? 0 : (split ? 3 * m : m) + 3; }
+
 int lcrw_profile_reset(int enable) {
   std::lock_guard<std::mutex> lk(lcrw::g_mu);
   lcrw::g_recs.clear();

@@ -47,7 +47,6 @@ constexpr int kMaxKb = 7;                     // m <= 448
 
 struct Params {
   const float* a_norms;
-  const float* b_norms;
   const uint32_t* endmask;
   const int64_t* seg_offsets;
   const int32_t* range_seg;
@@ -68,15 +67,12 @@ struct Params {
 // shared-memory carve-up; identical offsets in both CTAs of a pair
 struct Smem {
   uint32_t A, B;       // shared-window addresses (1024-aligned)
-  float* nbuf;         // [kEpiWarps][BN] column norms, one buffer per epilogue warp
-  uint32_t* mbuf;      // [kEpiWarps][BN / 32] segment-end bits
   uint64_t* bars;
   uint32_t* tmem_slot;
 };
 
 size_t smem_bytes(int n_kb, int stages) {
-  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + kEpiWarps * BN * 4 +
-         kEpiWarps * (BN / 32) * 4 + (2 + 2 * stages + 4) * 8 + 16;
+  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + (2 + 2 * stages + 4) * 8 + 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -135,9 +131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   sm.A = smem_u32(base);
   sm.B = sm.A + p.n_kb * A_KB_BYTES;
   uint8_t* tail = base + p.n_kb * A_KB_BYTES + p.stages * B_STAGE_BYTES;
-  sm.nbuf = reinterpret_cast<float*>(tail);
-  sm.mbuf = reinterpret_cast<uint32_t*>(tail + kEpiWarps * BN * 4);
-  sm.bars = reinterpret_cast<uint64_t*>(tail + kEpiWarps * BN * 4 + kEpiWarps * (BN / 32) * 4);
+  sm.bars = reinterpret_cast<uint64_t*>(tail);
   sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.bars + 2 + 2 * p.stages + 4);
 
   uint64_t* a_full = sm.bars + 0;   // leader: A tiles of both CTAs landed
@@ -255,12 +249,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ============================ epilogue (both CTAs) ================================
-    const int ew = warp - 4;
     const int quarter = warp & 3;
     const float inv_scale = p.scale[1];
     const uint32_t t_empty_l = mapa_shared(smem_u32(t_empty), 0);
-    float* nb = sm.nbuf + ew * BN;
-    uint32_t* mb = sm.mbuf + ew * (BN / 32);
     const int zs = p.z_shift;
     const int64_t zmask = (1ll << zs) - 1;
 
@@ -283,35 +274,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       return 0;
     };
-    // stage a tile's column norms / segment-end bits into registers
-    float pn[BN / 32];
-    uint32_t pm = 0;
-    auto fetch = [&](int64_t cc, int64_t ce) {
-#pragma unroll
-      for (int i = 0; i < BN / 32; ++i) {
-        const int64_t c = cc + i * 32 + lane;
-        pn[i] = c < ce ? __ldg(p.b_norms + c) : 0.f;
-      }
+    // a tile's segment-end bits: lane i < 8 holds the word of columns [32 i, 32 i + 32)
+    auto fetch_mask = [&](int64_t cc) -> uint32_t {
+      uint32_t w = 0;
       if (lane < BN / 32) {
         const int64_t bit = cc + lane * 32;
         const uint32_t lo = __ldg(p.endmask + (bit >> 5));
         const uint32_t hi = __ldg(p.endmask + (bit >> 5) + 1);
-        pm = __funnelshift_r(lo, hi, (uint32_t)(bit & 31));
+        w = __funnelshift_r(lo, hi, (uint32_t)(bit & 31));
       }
-    };
-    auto stash = [&]() {
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < BN / 32; ++i) nb[i * 32 + lane] = pn[i];
-      if (lane < BN / 32) mb[lane] = pm;
-      __syncwarp();
+      return w;
     };
 
     int kind = next_tile(u, c_begin, c_end, c0);
-    if (kind) {
-      fetch(c0, c_end);
-      stash();
-    }
+    uint32_t pm = kind ? fetch_mask(c0) : 0u;
     uint32_t acc = 0, acc_phase = 0;
     int row = 0;
     bool valid = false;
@@ -330,10 +306,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         run = kInf;
       }
       const int ncols = (int)min((int64_t)BN, c_end - c0);
-      // prefetch the next tile's norms while this tile is processed
+      const uint32_t cur_mask = pm;
+      // prefetch the next tile's segment bits while this tile is processed
       int64_t nu = u, ncb = c_begin, nce = c_end, nc0 = c0;
       const int nkind = next_tile(nu, ncb, nce, nc0);
-      if (nkind) fetch(nc0, nce);
+      if (nkind) pm = fetch_mask(nc0);
 
       mbar_wait(t_full + acc, acc_phase);
       tc_fence_after();
@@ -354,18 +331,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int ch = ch2 * 2 + h;
           const int lim = ncols - ch * 32;
           if (lim <= 0) break;
-          // v_j = |B_j|^2 - 2 A.B_j  (|A|^2 is added once per segment)
+          // the accumulator already holds v_j = |B_j|^2 - 2 A.B_j (norm columns folded
+          // into K); |A|^2 is added once per segment
           float v[32];
-          const float4* nb4 = reinterpret_cast<const float4*>(nb + ch * 32);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 n4 = nb4[j4];
-            v[4 * j4 + 0] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 0]), n4.x);
-            v[4 * j4 + 1] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 1]), n4.y);
-            v[4 * j4 + 2] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 2]), n4.z);
-            v[4 * j4 + 3] = fmaf(-2.f, __uint_as_float(raw[h][4 * j4 + 3]), n4.w);
-          }
-          uint32_t mask = mb[ch];
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[h][j]);
+          uint32_t mask = __shfl_sync(0xffffffffu, cur_mask, ch);
           if (lim < 32) {  // last chunk of a range: columns >= lim belong to the next range
             mask &= (1u << lim) - 1u;
 #pragma unroll
@@ -396,10 +367,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(t_empty_l + acc * 8);  // leader's t_empty[acc]
+      if (lane == 0) mbar_arrive_cluster_relaxed(t_empty_l + acc * 8);  // leader's t_empty[acc]
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (nkind) stash();
       u = nu;
       c_begin = ncb;
       c_end = nce;
@@ -462,18 +432,17 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int kp, int box_r
 namespace lcrw {
 namespace p1 {
 
-int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, const float* b_norms,
-           int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
+int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
            int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag) {
-  LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(m)");
+  LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(K)");
   LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
                "lcrw_phase1: row counts must fit in int32");
   LCRW_REQUIRE(n_seg >= 0 && n_ranges >= 1, "lcrw_phase1: bad segment plan");
   LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_phase1: z_shift out of range");
   LCRW_REQUIRE(z_panel >= (a_rows << z_shift), "lcrw_phase1: z_panel must be >= a_rows << z_shift");
   if (a_rows == 0 || n_seg == 0) return LCRW_OK;
-  LCRW_REQUIRE(A && a_norms && B && b_norms && seg_offsets && endmask && range_seg && scale && Z,
+  LCRW_REQUIRE(A && a_norms && B && seg_offsets && endmask && range_seg && scale && Z,
                "lcrw_phase1: null pointer");
   LCRW_REQUIRE((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
                "lcrw_phase1: operands must be 16-byte aligned");
@@ -485,7 +454,6 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   const int stages = n_kb <= 5 ? 8 : 6;
   Params p;
   p.a_norms = a_norms;
-  p.b_norms = b_norms;
   p.endmask = endmask;
   p.seg_offsets = seg_offsets;
   p.range_seg = range_seg;
@@ -529,10 +497,10 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
 }  // namespace lcrw
 
 extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
-                           const float* b_norms, int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
+                           int64_t b_rows, int m, int kp, const int64_t* seg_offsets,
                            int64_t seg_base, int64_t n_seg, const uint32_t* endmask, const int32_t* range_seg,
                            int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift,
                            void* stream) {
-  return lcrw::p1::launch(A, a_norms, a_rows, B, b_norms, b_rows, m, kp, seg_offsets, seg_base, n_seg, endmask,
+  return lcrw::p1::launch(A, a_norms, a_rows, B, b_rows, m, kp, seg_offsets, seg_base, n_seg, endmask,
                           range_seg, n_ranges, scale, Z, z_panel, z_shift, lcrw::as_stream(stream), "phase1");
 }

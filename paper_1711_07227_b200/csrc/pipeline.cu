@@ -14,8 +14,7 @@
 
 namespace lcrw {
 namespace p1 {
-int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, const float* b_norms,
-           int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
+int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
            int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag);
 }
@@ -101,7 +100,6 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
   }
   char* base = static_cast<char*>(ws);
   uint16_t* T = reinterpret_cast<uint16_t*>(base + L.T);
-  float* tn = reinterpret_cast<float*>(base + L.tn);
   uint32_t* mask = reinterpret_cast<uint32_t*>(base + L.mask);
   int32_t* rs = reinterpret_cast<int32_t*>(base + L.rs);
   float* Z2 = reinterpret_cast<float*>(base + L.Z);
@@ -113,11 +111,11 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
     const int64_t nd = j1 - j0;
     const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
-    if ((status = lcrw_gather_rows(EhB, e_norms, kp, doc_cols + lo, nw, T, tn, stream))) return status;
+    if ((status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream))) return status;
     const int rc = range_cols > 0 ? range_cols : auto_range_cols(nw, a_rows);
     const int64_t n_ranges = lcrw_plan_ranges(nw, rc);
     if ((status = lcrw_segment_plan(doc_offsets + j0, lo, nd, nw, rc, mask, rs, n_ranges, stream))) return status;
-    if ((status = p1::launch(A, a_norms, a_rows, T, tn, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs, n_ranges, scale,
+    if ((status = p1::launch(A, a_norms, a_rows, T, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs, n_ranges, scale,
                              Z2, z_panel, kZShift, st, "phase1_rev")))
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))

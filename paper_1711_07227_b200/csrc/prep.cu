@@ -20,63 +20,88 @@ inline unsigned grid_for(int64_t n, int threads = kThreads, int64_t cap = 148 * 
 // ---------------------------------------------------------------------------
 // scale selection and f16 operand rows
 // ---------------------------------------------------------------------------
-__global__ void absmax_kernel(const float* __restrict__ x, int64_t n, uint32_t* amax) {
-  float m = 0.f;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = fmaxf(m, fabsf(x[i]));
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+// max over rows of |x_r|^2 (fp32), atomically max-accumulated as float bits
+__global__ void max_sqnorm_kernel(const float* __restrict__ x, int64_t rows, int m, uint32_t* out) {
+  const int lane = threadIdx.x & 31;
+  float best = 0.f;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float acc = 0.f;
+    for (int k = lane; k < m; k += 32) {
+      const float v = x[r * (int64_t)m + k];
+      acc = fmaf(v, v, acc);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    best = fmaxf(best, acc);
+  }
+  if (lane == 0 && best > 0.f) atomicMax(out, __float_as_uint(best));
 }
 
-__global__ void scale_kernel(const uint32_t* amax_bits, float* scale) {
-  const float a = __uint_as_float(*amax_bits);
-  int sh = 0;
+// s = 2^k with s^2 * max|x|^2 in [2^12, 2^14): scaled squared norms (and their
+// three-piece f16 split) fit f16, scaled elements are <= 2^7
+__global__ void scale_kernel(const uint32_t* max_bits, float* scale) {
+  const float a = __uint_as_float(*max_bits);
+  int k = 0;
   if (a > 0.f && isfinite(a)) {
     int e;
-    frexpf(a, &e);  // a < 2^e
-    sh = 13 - e;    // a * 2^sh in [2^12, 2^13)
-    sh = max(-100, min(100, sh));
+    frexpf(a, &e);  // a in [2^(e-1), 2^e)
+    k = (14 - e) >> 1;  // floor((14 - e) / 2): 2k + e <= 14
+    k = max(-60, min(60, k));
   }
-  scale[0] = ldexpf(1.f, sh);
-  scale[1] = ldexpf(1.f, -sh);
+  scale[0] = ldexpf(1.f, k);
+  scale[1] = ldexpf(1.f, -k);
 }
 
-// one warp per row; f16 RN rounding of the scaled row, fp64 norm of the
-// rounded values (exact squares, ~exact sum) stored as f32.
-//   layout 0: [f16(x)]                      (K = m)
-//   layout 1: [hi(x), hi(x), lo(x)]  A side (K = 3m)   with hi = f16(x), lo = f16(x - hi)
-//   layout 2: [hi(x), lo(x), hi(x)]  B side (K = 3m)   -> A.B = hi.hi + hi.lo + lo.hi
+// one warp per row.  With x' = scale * x, hi = f16(x'), lo = f16(x' - hi):
+//   layout 0 (A)        [hi(x')                         , 1, 1, 1]          K = m + 3
+//   layout 1 (A split)  [hi, hi, lo                     , 1, 1, 1]          K = 3m + 3
+//   layout 2 (B)        [-2 hi(x')                      , n_hi, n_mid, n_lo] K = m + 3
+//   layout 3 (B split)  [-2 hi, -2 lo, -2 hi            , n_hi, n_mid, n_lo] K = 3m + 3
+// n = |rounded row|^2 (fp64 sum) split into three f16 pieces, so one MMA dot of
+// an A row with a B row is |b|^2 - 2 a.b and the Gram expansion needs only
+// +|a|^2 per segment in the epilogue.  norms[r] = n (f32), used for the A side.
 __global__ void prepare_rows_kernel(const float* __restrict__ X, int64_t rows, int m, int kp, int layout,
                                     const float* __restrict__ scale, __half* __restrict__ Xh,
                                     float* __restrict__ norms) {
   const int lane = threadIdx.x & 31;
   const float s = scale[0];
-  const int k_used = layout == 0 ? m : 3 * m;
+  const bool split = layout & 1;
+  const bool bside = layout & 2;
+  const int k_vec = split ? 3 * m : m;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    double acc = 0.0;
     const float* src = X + r * (int64_t)m;
     __half* dst = Xh + r * (int64_t)kp;
-    for (int k = lane; k < kp; k += 32) {
-      __half out = __float2half_rn(0.f);
-      if (k < k_used) {
-        const int part = layout == 0 ? 0 : k / m;
-        const int c = layout == 0 ? k : k - part * m;
-        const float x = src[c] * s;
-        const __half hi = __float2half_rn(x);
-        const __half lo = __float2half_rn(x - __half2float(hi));
-        const bool want_lo = (layout == 1 && part == 2) || (layout == 2 && part == 1);
-        out = want_lo ? lo : hi;
-        if (part == 0) {
-          const double v = layout == 0 ? (double)__half2float(hi)
-                                       : (double)__half2float(hi) + (double)__half2float(lo);
-          acc += v * v;
-        }
-      }
-      dst[k] = out;
+    double acc = 0.0;
+    for (int c = lane; c < m; c += 32) {
+      const float x = src[c] * s;
+      const __half hi = __float2half_rn(x);
+      const double v = split ? (double)__half2float(hi) + (double)__half2float(__float2half_rn(x - __half2float(hi)))
+                             : (double)__half2float(hi);
+      acc += v * v;
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) norms[r] = (float)acc;
+    const float n_hi = __half2float(__float2half_rn((float)acc));
+    const double r1 = acc - (double)n_hi;
+    const float n_mid = __half2float(__float2half_rn((float)r1));
+    const float n_lo = (float)(r1 - (double)n_mid);
+    for (int k = lane; k < kp; k += 32) {
+      float out = 0.f;
+      if (k < k_vec) {
+        const int part = split ? k / m : 0;
+        const int c = k - part * m;
+        const float x = src[c] * s;
+        const __half hi = __float2half_rn(x);
+        const bool want_lo = split && ((!bside && part == 2) || (bside && part == 1));
+        const float val = want_lo ? __half2float(__float2half_rn(x - __half2float(hi))) : __half2float(hi);
+        out = bside ? -2.f * val : val;
+      } else if (k < k_vec + 3) {
+        const int t = k - k_vec;
+        out = bside ? (t == 0 ? n_hi : t == 1 ? n_mid : n_lo) : 1.f;
+      }
+      dst[k] = __float2half_rn(out);
+    }
+    if (lane == 0 && norms) norms[r] = (float)acc;
   }
 }
 
@@ -91,7 +116,7 @@ __global__ void gather_rows_kernel(const int4* __restrict__ Xh, const float* __r
     const int4* src = Xh + g * vec_per_row;
     int4* dst = T + i * vec_per_row;
     for (int v = lane; v < vec_per_row; v += 32) dst[v] = __ldg(src + v);
-    if (lane == 0) tnorms[i] = norms[g];
+    if (lane == 0 && tnorms) tnorms[i] = norms[g];
   }
 }
 
@@ -266,26 +291,27 @@ using namespace lcrw;
 
 extern "C" {
 
-int lcrw_absmax(const float* x, int64_t n, uint32_t* amax_bits, void* stream) {
-  LCRW_REQUIRE(n >= 0 && (n == 0 || x) && amax_bits, "lcrw_absmax: bad arguments");
-  if (n == 0) return LCRW_OK;
-  absmax_kernel<<<grid_for(n), kThreads, 0, as_stream(stream)>>>(x, n, amax_bits);
-  LCRW_CHECK_LAUNCH("absmax_kernel");
+int lcrw_max_sqnorm(const float* x, int64_t rows, int m, uint32_t* max_bits, void* stream) {
+  LCRW_REQUIRE(rows >= 0 && m > 0 && (rows == 0 || x) && max_bits, "lcrw_max_sqnorm: bad arguments");
+  if (rows == 0) return LCRW_OK;
+  max_sqnorm_kernel<<<grid_for(rows * 32), kThreads, 0, as_stream(stream)>>>(x, rows, m, max_bits);
+  LCRW_CHECK_LAUNCH("max_sqnorm_kernel");
   return LCRW_OK;
 }
 
-int lcrw_scale_from_absmax(const uint32_t* amax_bits, float* scale, void* stream) {
-  LCRW_REQUIRE(amax_bits && scale, "lcrw_scale_from_absmax: null pointer");
-  scale_kernel<<<1, 1, 0, as_stream(stream)>>>(amax_bits, scale);
+int lcrw_scale_from_max_sqnorm(const uint32_t* max_bits, float* scale, void* stream) {
+  LCRW_REQUIRE(max_bits && scale, "lcrw_scale_from_max_sqnorm: null pointer");
+  scale_kernel<<<1, 1, 0, as_stream(stream)>>>(max_bits, scale);
   LCRW_CHECK_LAUNCH("scale_kernel");
   return LCRW_OK;
 }
 
 int lcrw_prepare_rows(const float* X, int64_t rows, int m, int kp, int layout, const float* scale, uint16_t* Xh,
                       float* norms, void* stream) {
-  LCRW_REQUIRE(layout >= 0 && layout <= 2, "lcrw_prepare_rows: layout must be 0, 1 or 2");
-  LCRW_REQUIRE(rows >= 0 && m > 0 && kp == lcrw_padded_dim(layout == 0 ? m : 3 * m), "lcrw_prepare_rows: bad shape");
-  LCRW_REQUIRE(rows == 0 || (X && scale && Xh && norms), "lcrw_prepare_rows: null pointer");
+  LCRW_REQUIRE(layout >= 0 && layout <= 3, "lcrw_prepare_rows: layout must be 0..3");
+  LCRW_REQUIRE(rows >= 0 && m > 0 && kp == lcrw_padded_dim(lcrw_operand_k(m, layout & 1)),
+               "lcrw_prepare_rows: bad shape");
+  LCRW_REQUIRE(rows == 0 || (X && scale && Xh), "lcrw_prepare_rows: null pointer");
   if (rows == 0) return LCRW_OK;
   prepare_rows_kernel<<<grid_for(rows * 32), kThreads, 0, as_stream(stream)>>>(
       X, rows, m, kp, layout, scale, reinterpret_cast<__half*>(Xh), norms);
@@ -297,7 +323,7 @@ int lcrw_gather_rows(const uint16_t* Xh, const float* norms, int kp, const int32
                      float* tnorms, void* stream) {
   LCRW_REQUIRE(n >= 0 && kp > 0 && kp % 64 == 0, "lcrw_gather_rows: bad shape");
   if (n == 0) return LCRW_OK;
-  LCRW_REQUIRE(Xh && norms && ids && T && tnorms, "lcrw_gather_rows: null pointer");
+  LCRW_REQUIRE(Xh && ids && T && (norms || !tnorms), "lcrw_gather_rows: null pointer");
   gather_rows_kernel<<<grid_for(n * 32), kThreads, 0, as_stream(stream)>>>(
       reinterpret_cast<const int4*>(Xh), norms, kp / 8, ids, n, reinterpret_cast<int4*>(T), tnorms);
   LCRW_CHECK_LAUNCH("gather_rows_kernel");

@@ -126,16 +126,17 @@ class PreparedEmbeddings:
             raise ValueError("embeddings must be a 2-d (v, m) matrix")
         self.V, self.m = int(self.E32.shape[0]), int(self.E32.shape[1])
         self.split = (self.m <= self.SPLIT_MAX_DIM) if split is None else bool(split)
-        self.k_eff = 3 * self.m if self.split else self.m
+        self.k_eff = int(_lib.value("lcrw_operand_k", self.m, int(self.split)))
         self.kp = padded_dim(self.k_eff)
-        amax = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.call("lcrw_absmax", _p(self.E32), self.V * self.m, _p(amax), st)
+        mx = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("lcrw_max_sqnorm", _p(self.E32), self.V, self.m, _p(mx), st)
         for x in extra:
-            _lib.call("lcrw_absmax", _p(x), x.numel(), _p(amax), st)
+            _lib.call("lcrw_max_sqnorm", _p(x), int(x.shape[0]), self.m, _p(mx), st)
         self.scale = torch.empty(2, dtype=torch.float32, device=dev)
-        _lib.call("lcrw_scale_from_absmax", _p(amax), _p(self.scale), st)
-        self.EhA, self.norms = self._rows(self.E32, 1 if self.split else 0)
-        self.EhB = self._rows(self.E32, 2)[0] if self.split else self.EhA
+        _lib.call("lcrw_scale_from_max_sqnorm", _p(mx), _p(self.scale), st)
+        # A side (vocabulary rows): [x, 1, 1, 1]; B side (query words): [-2x, |x|^2 pieces]
+        self.EhA, self.norms = self._rows(self.E32, int(self.split))
+        self.EhB = self._rows(self.E32, 2 + int(self.split), norms=False)[0]
         # exact-identity classes (kernels.py:91-92 semantics)
         ws_bytes = C.c_size_t(0)
         _lib.call("lcrw_row_classes_workspace", self.V, C.byref(ws_bytes))
@@ -149,17 +150,17 @@ class PreparedEmbeddings:
                   _p(self.sorted_hash), _p(self.sorted_ids), _p(ws), ws_bytes.value, st)
         self.n_dup = int(n_dup.item())
 
-    def _rows(self, X: torch.Tensor, layout: int) -> tuple[torch.Tensor, torch.Tensor]:
+    def _rows(self, X: torch.Tensor, layout: int, norms: bool = True):
         n = int(X.shape[0])
         Xh = torch.empty((max(n, 1), self.kp), dtype=torch.float16, device=X.device)
-        xn = torch.empty(max(n, 1), dtype=torch.float32, device=X.device)
+        xn = torch.empty(max(n, 1), dtype=torch.float32, device=X.device) if norms else None
         _lib.call("lcrw_prepare_rows", _p(X), n, self.m, self.kp, layout, _p(self.scale), _p(Xh), _p(xn),
                   _stream())
         return Xh, xn
 
-    def prepare_free_rows(self, Q: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    def prepare_free_rows(self, Q: torch.Tensor) -> torch.Tensor:
         """B-side f16 operand rows for vectors that are not rows of E (same scale)."""
-        return self._rows(Q, 2 if self.split else 0)
+        return self._rows(Q, 2 + int(self.split), norms=False)[0]
 
     def representatives(self, word_ids: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
         """(rep, next) arguments of lcrw_zero_identical for rows given by E ids."""
@@ -196,12 +197,12 @@ def remap_ids(cols: torch.Tensor, remap: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def gather_rows(prep: PreparedEmbeddings, ids: torch.Tensor, side: str) -> tuple[torch.Tensor, torch.Tensor]:
-    """Operand rows E[ids] for the A (vocabulary) or B (query word) side."""
+def gather_rows(prep: PreparedEmbeddings, ids: torch.Tensor, side: str):
+    """Operand rows E[ids] for the A (vocabulary, with norms) or B (query word) side."""
     n = ids.numel()
     src = prep.EhA if side == "A" else prep.EhB
     T = torch.empty((max(n, 1), prep.kp), dtype=torch.float16, device=ids.device)
-    tn = torch.empty(max(n, 1), dtype=torch.float32, device=ids.device)
+    tn = torch.empty(max(n, 1), dtype=torch.float32, device=ids.device) if side == "A" else None
     _lib.call("lcrw_gather_rows", _p(src), _p(prep.norms), prep.kp, _p(ids), n, _p(T), _p(tn), _stream())
     return T, tn
 
@@ -212,7 +213,7 @@ def _range_cols(b_rows: int, a_rows: int) -> int:
     return int(min(32768, max(1024, (want + 255) // 256 * 256)))
 
 
-def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor, b_norms: torch.Tensor,
+def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
            b_rows: int, seg_offsets: torch.Tensor, n_seg: int, prep: PreparedEmbeddings,
            range_cols: int | None = None) -> tuple[torch.Tensor, int]:
     """Z (8-segment panels, z_panel = 8 * a_rows) of distances.py:147-178, without the exact-zero pass."""
@@ -225,7 +226,7 @@ def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
     _lib.call("lcrw_segment_plan", _p(seg_offsets), 0, n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
     z_panel = 8 * max(a_rows, 1)
     Z = torch.empty(((n_seg + 7) // 8) * z_panel, dtype=torch.float32, device=dev)
-    _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), _p(b_norms), b_rows, prep.k_eff, prep.kp,
+    _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), b_rows, prep.k_eff, prep.kp,
               _p(seg_offsets), 0, n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel, 3,
               st)
     return Z, z_panel
@@ -290,8 +291,8 @@ class Restricted:
 def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
                       n_seg: int) -> tuple[torch.Tensor, int]:
     """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros)."""
-    B, bn = gather_rows(prep, word_ids, "B")
-    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, bn, word_ids.numel(), seg_offsets, n_seg, prep)
+    B, _ = gather_rows(prep, word_ids, "B")
+    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, word_ids.numel(), seg_offsets, n_seg, prep)
     rep, nxt = prep.representatives(word_ids)
     zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp)
     return Z, zp
@@ -376,9 +377,9 @@ def nearest_word_distances(E, Q) -> torch.Tensor:
     if Qd.shape[1] != prep.m:
         raise ValueError(f"dimension mismatch: {prep.m} vs {Qd.shape[1]}")
     nq = int(Qd.shape[0])
-    Qh, qn = prep.prepare_free_rows(Qd)
+    Qh = prep.prepare_free_rows(Qd)
     seg = torch.tensor([0, nq], dtype=torch.int64, device=dev)
-    Z, zp = phase1(prep.EhA, prep.norms, prep.V, Qh, qn, nq, seg, 1, prep)
+    Z, zp = phase1(prep.EhA, prep.norms, prep.V, Qh, nq, seg, 1, prep)
     rep = torch.empty(nq, dtype=torch.int32, device=dev)
     _lib.call("lcrw_match_rows", _p(Qd), nq, _p(prep.E32), prep.m, _p(prep.sorted_hash), _p(prep.sorted_ids),
               prep.V, _p(prep.canon), _p(rep), _stream())

@@ -87,8 +87,8 @@ def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) ->
     panels = (n_q + 7) // 8
     zl = torch.zeros((panels, R, 8), dtype=torch.float32, device=dev)
     if rows > 0:
-        B, bn = device.gather_rows(prep, dx2.cols, "B")
-        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, bn, dx2.nnz, dx2.offsets, n_q, prep)
+        B, _ = device.gather_rows(prep, dx2.cols, "B")
+        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, dx2.nnz, dx2.offsets, n_q, prep)
         remap = torch.full((prep.V,), -1, dtype=torch.int32, device=dev)
         remap[v0:v1] = torch.arange(rows, dtype=torch.int32, device=dev)
         rep, nxt = prep.representatives(dx2.cols)

@@ -29,6 +29,7 @@ def test_header_symbols_exported_and_bound():
     assert _lib.value("lcrw_abi_version") == 1
     assert _lib.value("lcrw_padded_dim", 300) == 320
     assert _lib.value("lcrw_padded_dim", 37) == 64
+    assert _lib.value("lcrw_operand_k", 300, 0) == 303 and _lib.value("lcrw_operand_k", 16, 1) == 51
     assert _lib.value("lcrw_plan_ranges", 1000, 256) == 4
     assert _lib.value("lcrw_status_string", 1) == b"invalid argument"
 
@@ -38,7 +39,7 @@ def test_library_rejects_bad_arguments_without_gpu():
     with pytest.raises(ValueError, match="k must be >= 1"):
         _lib.call("lcrw_topk_segments", None, None, 1, 1, 0, None, None, None)
     with pytest.raises(ValueError, match="kp must be"):
-        _lib.call("lcrw_phase1", None, None, 0, None, None, 0, 300, 300, None, 0, 1, None, None, 1, None, None, 0,
+        _lib.call("lcrw_phase1", None, None, 0, None, 0, 300, 300, None, 0, 1, None, None, 1, None, None, 0,
                   3, None)
 
 
