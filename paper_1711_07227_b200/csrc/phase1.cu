@@ -40,8 +40,8 @@ constexpr int BN_HALF = BN / 2;
 constexpr int BK = 64;                        // f16 elements per K block (128 B rows)
 constexpr int A_KB_BYTES = BM * BK * 2;       // 16 KB
 constexpr int B_STAGE_BYTES = BN_HALF * BK * 2;  // 16 KB per CTA
-constexpr int kThreads = 256;
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;                  // two per TMEM lane quarter: each owns one 128-column half
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr uint32_t kIdesc = umma_idesc_f16(2 * BM, BN);
 constexpr int kMaxKb = 7;                     // m <= 448
 
@@ -67,12 +67,17 @@ struct Params {
 // shared-memory carve-up; identical offsets in both CTAs of a pair
 struct Smem {
   uint32_t A, B;       // shared-window addresses (1024-aligned)
-  uint64_t* bars;
+  uint64_t* bars;      // a_full, a_empty, b_full[S], b_empty[S], t_full[2], t_empty[2]
+  uint64_t* hand;      // [2 dirs][4 quarters][2 parities] carry hand-off barriers
+  float* carry;        // [2 dirs][4 quarters][2 parities][32] running minima
   uint32_t* tmem_slot;
 };
 
+constexpr int kHandBars = 2 * 4 * 2;
+
 size_t smem_bytes(int n_kb, int stages) {
-  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + (2 + 2 * stages + 4) * 8 + 16;
+  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + (2 + 2 * stages + 4) * 8 +
+         kHandBars * 8 + kHandBars * 32 * 4 + 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -132,7 +137,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   sm.B = sm.A + p.n_kb * A_KB_BYTES;
   uint8_t* tail = base + p.n_kb * A_KB_BYTES + p.stages * B_STAGE_BYTES;
   sm.bars = reinterpret_cast<uint64_t*>(tail);
-  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.bars + 2 + 2 * p.stages + 4);
+  sm.hand = sm.bars + 2 + 2 * p.stages + 4;
+  sm.carry = reinterpret_cast<float*>(sm.hand + kHandBars);
+  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.carry + kHandBars * 32);
 
   uint64_t* a_full = sm.bars + 0;   // leader: A tiles of both CTAs landed
   uint64_t* a_empty = sm.bars + 1;  // both: the unit's MMAs retired (commit multicast)
@@ -161,6 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(t_full + i, 1);
       mbar_init(t_empty + i, 2 * kEpiWarps);
     }
+    for (int i = 0; i < kHandBars; ++i) mbar_init(sm.hand + i, 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -249,11 +257,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ============================ epilogue (both CTAs) ================================
-    const int quarter = warp & 3;
+    // Warp (quarter q, half h) owns TMEM lanes [32q, 32q+32) and columns [128h, 128h+128)
+    // of every tile.  Segment minima that straddle halves are stitched with a carry
+    // hand-off: half 0 of tile t -> half 1 of tile t (dir 0), half 1 of tile t -> half 0
+    // of tile t+1 (dir 1).  A half that contains a segment end publishes its tail
+    // minimum immediately and only waits for its predecessor to emit its head segment.
+    const int ew = warp - 4;
+    const int quarter = ew & 3;
+    const int half = ew >> 2;
     const float inv_scale = p.scale[1];
     const uint32_t t_empty_l = mapa_shared(smem_u32(t_empty), 0);
     const int zs = p.z_shift;
     const int64_t zmask = (1ll << zs) - 1;
+    auto hbar = [&](int dir, int par) { return sm.hand + (dir * 4 + quarter) * 2 + par; };
+    auto hslot = [&](int dir, int par) { return sm.carry + ((dir * 4 + quarter) * 2 + par) * 32; };
 
     // tile iterator over this pair's units (skips empty ranges)
     int64_t u = pair - n_pairs, c_begin = 0, c_end = 0, c0 = 0;
@@ -288,93 +305,153 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     int kind = next_tile(u, c_begin, c_end, c0);
     uint32_t pm = kind ? fetch_mask(c0) : 0u;
-    uint32_t acc = 0, acc_phase = 0;
-    int row = 0;
+    uint32_t acc = 0, acc_phase = 0, tcount = 0;
     bool valid = false;
-    float nE = 0.f, run = kInf;
+    float nE = 0.f;
     float* zrow = p.Z;
-    int64_t s = 0;
+    int64_t s_tile = 0;
     while (kind) {
       if (kind == 2) {  // first tile of a unit
         const int mp = (int)(u % p.n_mpairs);
         const int range = (int)(u / p.n_mpairs);
-        row = mp * 2 * BM + (int)rank * BM + quarter * 32 + lane;
+        const int row = mp * 2 * BM + (int)rank * BM + quarter * 32 + lane;
         valid = row < p.a_rows;
         nE = valid ? __ldg(p.a_norms + row) : 0.f;
         zrow = p.Z + ((int64_t)row << zs);
-        s = p.range_seg[range];
-        run = kInf;
+        s_tile = p.range_seg[range];
       }
+      const bool unit_start = kind == 2;
       const int ncols = (int)min((int64_t)BN, c_end - c0);
-      const uint32_t cur_mask = pm;
+      // segment-end bits of this tile, restricted to its columns
+      uint32_t wmask = __shfl_sync(0xffffffffu, pm, lane & 7);
+      {
+        const int lim = ncols - (lane & 7) * 32;
+        wmask = lim >= 32 ? wmask : (lim <= 0 ? 0u : (wmask & ((1u << lim) - 1u)));
+      }
+      const int ends0 = __popc(__shfl_sync(0xffffffffu, wmask, 0)) + __popc(__shfl_sync(0xffffffffu, wmask, 1)) +
+                        __popc(__shfl_sync(0xffffffffu, wmask, 2)) + __popc(__shfl_sync(0xffffffffu, wmask, 3));
+      const int ends1 = __popc(__shfl_sync(0xffffffffu, wmask, 4)) + __popc(__shfl_sync(0xffffffffu, wmask, 5)) +
+                        __popc(__shfl_sync(0xffffffffu, wmask, 6)) + __popc(__shfl_sync(0xffffffffu, wmask, 7));
       // prefetch the next tile's segment bits while this tile is processed
       int64_t nu = u, ncb = c_begin, nce = c_end, nc0 = c0;
       const int nkind = next_tile(nu, ncb, nce, nc0);
       if (nkind) pm = fetch_mask(nc0);
 
-      mbar_wait(t_full + acc, acc_phase);
-      tc_fence_after();
-      const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      auto emit = [&](float segmin) {
-        if (valid) zrow[(s >> zs) * p.z_panel + (s & zmask)] = sqrtf(fmaxf(segmin + nE, 0.f)) * inv_scale;
+      int64_t s = s_tile + (half ? ends0 : 0);  // first segment ending in (or after) my half
+      const int64_t s_head = s;
+      float head = kInf, run = kInf;
+      bool have_end = false;
+      auto emit = [&](int64_t seg, float segmin) {
+        if (valid) {
+          float d;
+          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(fmaxf(segmin + nE, 0.f)));
+          zrow[(seg >> zs) * p.z_panel + (seg & zmask)] = d * inv_scale;
+        }
+      };
+      // segment end inside my half: the first one closes the head (emitted after the hand-off)
+      auto close = [&](float segmin) {
+        if (!have_end) {
+          head = segmin;
+          have_end = true;
+        } else {
+          emit(s, segmin);
+        }
         ++s;
       };
+
+      const int my_cols = min(BN_HALF, ncols - half * BN_HALF);
+      mbar_wait(t_full + acc, acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * BN_HALF;
 #pragma unroll 1
-      for (int ch2 = 0; ch2 < BN / 64; ++ch2) {
-        if (ch2 * 64 >= ncols) break;
-        uint32_t raw[2][32];
-        tmem_ld_32x32b_x32(t_base + ch2 * 64, raw[0]);
-        tmem_ld_32x32b_x32(t_base + ch2 * 64 + 32, raw[1]);
+      for (int ch = 0; ch < BN_HALF / 32; ++ch) {
+        if (ch * 32 >= my_cols) break;
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(t_base + ch * 32, raw);
         tmem_wait_ld();
+        // the accumulator already holds v_j = |B_j|^2 - 2 A.B_j (norm columns folded into K)
+        float v[32];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int ch = ch2 * 2 + h;
-          const int lim = ncols - ch * 32;
-          if (lim <= 0) break;
-          // the accumulator already holds v_j = |B_j|^2 - 2 A.B_j (norm columns folded
-          // into K); |A|^2 is added once per segment
-          float v[32];
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
+        const int lim = my_cols - ch * 32;
+        uint32_t mask = __shfl_sync(0xffffffffu, wmask, half * 4 + ch);
+        if (lim < 32) {  // columns >= lim belong to the next range
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[h][j]);
-          uint32_t mask = __shfl_sync(0xffffffffu, cur_mask, ch);
-          if (lim < 32) {  // last chunk of a range: columns >= lim belong to the next range
-            mask &= (1u << lim) - 1u;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j >= lim) v[j] = kInf;
+          for (int j = 0; j < 32; ++j)
+            if (j >= lim) v[j] = kInf;
+        }
+        const int nb_ends = __popc(mask);
+        if (nb_ends == 0) {
+          run = fminf(run, RangeMin<0, 31>::run(v));
+        } else if (nb_ends == 1) {
+          float pre, suf;
+          split_switch(__ffs(mask) - 1, v, pre, suf);
+          close(fminf(run, pre));
+          run = suf;
+        } else {
+          int start = 0;
+          while (mask) {
+            const int e = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
+            close(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
+            run = kInf;
+            start = e + 1;
           }
-          const int nb_ends = __popc(mask);
-          if (nb_ends == 0) {
-            run = fminf(run, RangeMin<0, 31>::run(v));
-          } else if (nb_ends == 1) {
-            float pre, suf;
-            split_switch(__ffs(mask) - 1, v, pre, suf);
-            emit(fminf(run, pre));
-            run = suf;
-          } else {
-            int start = 0;
-            while (mask) {
-              const int e = __ffs(mask) - 1;
-              mask &= mask - 1u;
-              const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
-              emit(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
-              run = kInf;
-              start = e + 1;
-            }
-            if (start < 32) run = masked_min(v, 0xFFFFFFFFu << start);
-          }
+          if (start < 32) run = masked_min(v, 0xFFFFFFFFu << start);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(t_empty_l + acc * 8);  // leader's t_empty[acc]
+
+      // ---- carry hand-off: pred -> me (dir = 1 - half), me -> succ (dir = half) ----
+      const int par = tcount & 1;
+      const int in_dir = half ? 0 : 1;
+      const int in_par = half ? par : (par ^ 1);          // half 0 reads tile t-1's half 1
+      const uint32_t in_phase = half ? (tcount >> 1) & 1 : ((tcount - 1) >> 1) & 1;
+      const bool has_pred = half ? true : (tcount > 0);
+      auto publish = [&](float carry_out) {
+        float* slot = hslot(half, par);
+        slot[lane] = carry_out;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(hbar(half, par));
+      };
+      auto receive = [&]() -> float {
+        if (!has_pred) return kInf;
+        mbar_wait(hbar(in_dir, in_par), in_phase);
+        const float c = hslot(in_dir, in_par)[lane];
+        return (half == 0 && unit_start) ? kInf : c;  // a unit starts with no open segment
+      };
+      // Half 0 publishes before receiving (its tail does not depend on the carry);
+      // half 1 always receives first, which keeps every hand-off barrier at most one
+      // phase ahead of its consumer (an mbarrier parity wait cannot skip a phase).
+      if (half == 0 && have_end) {
+        publish(run);
+        emit(s_head, fminf(receive(), head));
+      } else {
+        const float cin = receive();
+        if (have_end) {
+          emit(s_head, fminf(cin, head));
+          publish(run);
+        } else {
+          publish(fminf(cin, run));
+        }
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      ++tcount;
+      s_tile += ends0 + ends1;
       u = nu;
       c_begin = ncb;
       c_end = nce;
       c0 = nc0;
       kind = nkind;
+    }
+    // drain: half 0 consumes the last hand-off of half 1 so no arrival is left pending
+    if (half == 0 && tcount > 0) {
+      const int lp = (tcount - 1) & 1;
+      mbar_wait(hbar(1, lp), ((tcount - 1) >> 1) & 1);
     }
   }
 
