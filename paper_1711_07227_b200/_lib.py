@@ -13,7 +13,9 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "liblcrwmd.so"
+import os
+
+LIB_PATH = Path(os.environ.get("LCRW_LIB", Path(__file__).resolve().parent / "liblcrwmd.so"))
 
 P = C.c_void_p
 I64 = C.c_int64

@@ -24,12 +24,16 @@
 // cut a segment, so every Z entry is written exactly once (no atomics, no
 // initialisation pass).
 //
-// Warp roles (256 threads per CTA): w0 TMA producer, w1 MMA issuer (leader CTA
-// only), w2 TMEM allocator, w4..w7 epilogue (TMEM lane quarter = warp % 4, one A
-// row per thread; per-warp column-norm buffers prefetched one tile ahead).
+// Warp roles (352 threads per CTA): w0..w7 epilogue (TMEM lane quarter = warp % 4,
+// column half = warp / 4, one A row per thread), w8 TMA producer, w9 MMA issuer
+// (leader CTA only), w10 TMEM allocator.
 #include <cstdio>
 
 #include "common.cuh"
+
+#ifndef LCRW_EPI_MODE
+#define LCRW_EPI_MODE 0  // experiment switch: 1 = skip segment minima, 2 = also skip TMEM loads
+#endif
 
 namespace lcrw {
 namespace p1 {
@@ -41,7 +45,12 @@ constexpr int BK = 64;                        // f16 elements per K block (128 B
 constexpr int A_KB_BYTES = BM * BK * 2;       // 16 KB
 constexpr int B_STAGE_BYTES = BN_HALF * BK * 2;  // 16 KB per CTA
 constexpr int kEpiWarps = 8;                  // two per TMEM lane quarter: each owns one 128-column half
-constexpr int kThreads = 128 + 32 * kEpiWarps;
+// Warp roles.  The schedulers favour higher warp ids, so the single-lane TMA and
+// MMA issuers sit above the epilogue warps and are never starved by them.
+constexpr int kProducerWarp = kEpiWarps;      // 8
+constexpr int kMmaWarp = kEpiWarps + 1;       // 9
+constexpr int kAllocWarp = kEpiWarps + 2;     // 10
+constexpr int kThreads = 32 * (kEpiWarps + 3);
 constexpr uint32_t kIdesc = umma_idesc_f16(2 * BM, BN);
 constexpr int kMaxKb = 7;                     // m <= 448
 
@@ -155,7 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int64_t pair = blockIdx.x >> 1;
   const int64_t n_pairs = gridDim.x >> 1;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kProducerWarp && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     mbar_init(a_full, 1);
@@ -171,7 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kHandBars; ++i) mbar_init(sm.hand + i, 1);
     fence_mbar_init();
   }
-  if (warp == 2) {
+  if (warp == kAllocWarp) {
     tmem_alloc_2sm(sm.tmem_slot, 512);
     tmem_relinquish_2sm();
   }
@@ -182,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const int64_t n_units = (int64_t)p.n_ranges * p.n_mpairs;
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ============================ TMA producer (both CTAs) ============================
     if (lane == 0) {
       const uint64_t pol_a = l2_policy_evict_last();    // A tiles are re-read by every range
@@ -190,6 +199,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t a_full_l = mapa_shared(smem_u32(a_full), 0);
       const uint32_t b_full_l = mapa_shared(smem_u32(b_full), 0);
       uint32_t stage = 0, phase = 0, a_phase = 0;
+      int64_t b_loads = 0;
       for (int64_t u = pair; u < n_units; u += n_pairs) {
         const int range = (int)(u / p.n_mpairs);
         const int mp = (int)(u % p.n_mpairs);
@@ -205,10 +215,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_empty + stage, phase ^ 1);
-            if (leader) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
-            tma_load_2d_2sm(&tmB, b_full_l + stage * 8,
-                            smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES, kb * BK,
-                            (int32_t)(c0 + rank * BN_HALF), pol_b);
+#if LCRW_EPI_MODE >= 3
+            if (b_loads >= p.stages) {  // experiment: ring filled once, then no more B traffic
+              if (leader) mbar_arrive(b_full + stage);
+            } else
+#endif
+            {
+              if (leader) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
+              tma_load_2d_2sm(&tmB, b_full_l + stage * 8,
+                              smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES, kb * BK,
+                              (int32_t)(c0 + rank * BN_HALF), pol_b);
+            }
+            ++b_loads;
             if (++stage == (uint32_t)p.stages) {
               stage = 0;
               phase ^= 1;
@@ -217,10 +235,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ============================ MMA issuer (leader CTA) =============================
-    if (leader && lane == 0) {
+    // The whole warp walks the loop (warp-uniform state); one elected lane issues.
+    if (leader) {
       uint32_t stage = 0, phase = 0, a_phase = 0, acc = 0, acc_phase = 0;
+      const uint64_t a_desc0 = umma_desc_sw128(sm.A);
+      const uint64_t b_desc0 = umma_desc_sw128(sm.B);
+      const int last_nk = p.n_kmma - 4 * (p.n_kb - 1);  // MMAs in the last K block (1..4)
       for (int64_t u = pair; u < n_units; u += n_pairs) {
         const int range = (int)(u / p.n_mpairs);
         const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
@@ -230,41 +252,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         a_phase ^= 1;
         tc_fence_after();
         for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
+#if LCRW_EPI_MODE < 4
           mbar_wait(t_empty + acc, acc_phase ^ 1);
+#endif
           tc_fence_after();
           const uint32_t d_tmem = tmem + acc * BN;
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_full + stage, phase);
             tc_fence_after();
-            const int nk = min(4, p.n_kmma - 4 * kb);
-            for (int k = 0; k < nk; ++k) {
-              const uint64_t ad = umma_desc_sw128(sm.A + kb * A_KB_BYTES + k * 32);
-              const uint64_t bd = umma_desc_sw128(sm.B + stage * B_STAGE_BYTES + k * 32);
-              umma_f16_2sm(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
-            }
-            umma_commit_2sm_mc(b_empty + stage, 0x3);  // frees the stage in both CTAs
+            // descriptor start-address field counts 16-byte units: +2 per 32-byte K step
+            const uint64_t ad = a_desc0 + (uint64_t)(kb * (A_KB_BYTES >> 4));
+            const uint64_t bd = b_desc0 + (uint64_t)(stage * (B_STAGE_BYTES >> 4));
+            const int nk = kb == p.n_kb - 1 ? last_nk : 4;
+            umma_f16_2sm_elect(d_tmem, ad, bd, kIdesc, kb != 0);
+            if (nk > 1) umma_f16_2sm_elect(d_tmem, ad + 2, bd + 2, kIdesc, 1);
+            if (nk > 2) umma_f16_2sm_elect(d_tmem, ad + 4, bd + 4, kIdesc, 1);
+            if (nk > 3) umma_f16_2sm_elect(d_tmem, ad + 6, bd + 6, kIdesc, 1);
+            umma_commit_2sm_mc_elect(b_empty + stage, 0x3);  // frees the stage in both CTAs
             if (++stage == (uint32_t)p.stages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit_2sm_mc(t_full + acc, 0x3);  // accumulator ready in both CTAs' TMEM
+          umma_commit_2sm_mc_elect(t_full + acc, 0x3);  // accumulator ready in both CTAs' TMEM
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
-        umma_commit_2sm_mc(a_empty, 0x3);  // A tiles reusable once the unit's MMAs retire
+        umma_commit_2sm_mc_elect(a_empty, 0x3);  // A tiles reusable once the unit's MMAs retire
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < kEpiWarps) {
     // ============================ epilogue (both CTAs) ================================
     // Warp (quarter q, half h) owns TMEM lanes [32q, 32q+32) and columns [128h, 128h+128)
     // of every tile.  Segment minima that straddle halves are stitched with a carry
     // hand-off: half 0 of tile t -> half 1 of tile t (dir 0), half 1 of tile t -> half 0
     // of tile t+1 (dir 1).  A half that contains a segment end publishes its tail
     // minimum immediately and only waits for its predecessor to emit its head segment.
-    const int ew = warp - 4;
-    const int quarter = ew & 3;
-    const int half = ew >> 2;
+    const int quarter = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int half = warp >> 2;
     const float inv_scale = p.scale[1];
     const uint32_t t_empty_l = mapa_shared(smem_u32(t_empty), 0);
     const int zs = p.z_shift;
@@ -367,8 +392,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int ch = 0; ch < BN_HALF / 32; ++ch) {
         if (ch * 32 >= my_cols) break;
         uint32_t raw[32];
+#if LCRW_EPI_MODE >= 2
+        if (ch >= 0) { run = fminf(run, (float)ch); continue; }
+#endif
+#if LCRW_EPI_MODE == 1
         tmem_ld_32x32b_x32(t_base + ch * 32, raw);
         tmem_wait_ld();
+        run = fminf(run, fminf(__uint_as_float(raw[0]), __uint_as_float(raw[31])));
+        continue;
+#endif
+        tmem_ld_32x32b_x32(t_base + ch * 32, raw);
+        tmem_wait_ld();
+
         // the accumulator already holds v_j = |B_j|^2 - 2 A.B_j (norm columns folded into K)
         float v[32];
 #pragma unroll
@@ -458,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __syncwarp();  // reconverge single-lane roles before the aligned cluster barrier
   tc_fence_before();
   cluster_sync();
-  if (warp == 2) {
+  if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc_2sm(tmem, 512);
   }
