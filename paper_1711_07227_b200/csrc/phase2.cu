@@ -83,18 +83,25 @@ __device__ __forceinline__ void list_insert(float (&kd)[KMAX], int32_t (&ki)[KMA
   }
 }
 
-template <int KMAX>
+template <int KMAX, int G>
 __global__ void __launch_bounds__(kWarps * 32)
     reverse_max_kernel(const int64_t* __restrict__ q_offs, const int32_t* __restrict__ q_cols,
                        const float* __restrict__ q_vals, int64_t n_q, const float* __restrict__ Z2, int64_t z_panel,
-                       int z_shift, int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
+                       int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
                        int64_t d1_ld_row, int64_t d1_ld_panel, float* __restrict__ dout, int64_t ld_out, int k,
                        float* __restrict__ cand_d, int64_t* __restrict__ cand_i, int64_t n_chunks_total,
                        int64_t chunk_base, int chunk_docs) {
+  // Z2 in 32-doc panels: Z2[(j >> 5) * z_panel + (w << 5) + (j & 31)], so one
+  // (word, 32-doc group) is a single 128-byte line.  Each lane owns G doc groups
+  // (G * 32 docs per pass): for every nonzero of the query, G independent line
+  // loads are in flight per warp.
+  // grid: x = query panel (fastest), y = doc chunk, so the blocks resident at any
+  // time share one doc chunk and its Z2 panels stay in L2 across query panels
   const int lane = threadIdx.x & 31;
-  const int64_t q = (int64_t)blockIdx.y * kWarps + (threadIdx.x >> 5);
+  const int64_t q = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (q >= n_q) return;  // warp-uniform; no block-level synchronisation below
-  const int64_t j_begin = (int64_t)blockIdx.x * chunk_docs;
+  const int64_t chunk = blockIdx.y;
+  const int64_t j_begin = chunk * chunk_docs;
   const int64_t j_end = min(n_docs, j_begin + chunk_docs);
   const int64_t lo = q_offs[q], hi = q_offs[q + 1];
   const float* d1q = D1 + (q >> 3) * d1_ld_panel + (q & 7);
@@ -107,35 +114,46 @@ __global__ void __launch_bounds__(kWarps * 32)
     ki[i] = 0x7fffffff;
   }
 
-  for (int64_t jb = j_begin; jb < j_end; jb += 32) {
-    const int64_t jl = jb + lane;
-    const bool valid = jl < j_end;
-    const float* zj = Z2 + (jl >> z_shift) * z_panel + (jl & ((1ll << z_shift) - 1));
-    double acc = 0.0;
+  for (int64_t jb = j_begin; jb < j_end; jb += 32 * G) {
+    double acc[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g] = 0.0;
+    const float* zb = Z2 + (jb >> 5) * z_panel + lane;
+    const int ng = (int)min((int64_t)G, (j_end - jb + 31) >> 5);  // doc groups present in this pass
     for (int64_t base = lo; base < hi; base += 32) {
       const int cnt = (int)min((int64_t)32, hi - base);
       const int32_t my_w = lane < cnt ? __ldg(q_cols + base + lane) : 0;
       const float my_x = lane < cnt ? __ldg(q_vals + base + lane) : 0.f;
+#pragma unroll 2
       for (int t = 0; t < cnt; ++t) {
         const int64_t w = __shfl_sync(0xffffffffu, my_w, t);
         const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
-        if (valid) acc = fma(x, (double)__ldg(zj + (w << z_shift)), acc);
+        const float* zw = zb + (w << 5);
+        float z[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) z[g] = g < ng ? __ldg(zw + g * z_panel) : 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = fma(x, (double)z[g], acc[g]);
       }
     }
-    if (valid) {
-      const int64_t jg = doc_base + jl;
-      const float d = fmaxf(__ldg(d1q + jg * d1_ld_row), (float)acc);
-      if (dout) {
-        dout[jg * ld_out + q] = d;
-      } else if (d < kd[KMAX - 1] || (d == kd[KMAX - 1] && (int32_t)jg < ki[KMAX - 1])) {
-        list_insert<KMAX>(kd, ki, d, (int32_t)jg);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t jl = jb + 32 * g + lane;
+      if (g < ng && jl < j_end) {
+        const int64_t jg = doc_base + jl;
+        const float d = fmaxf(__ldg(d1q + jg * d1_ld_row), (float)acc[g]);
+        if (dout) {
+          dout[jg * ld_out + q] = d;
+        } else if (d < kd[KMAX - 1] || (d == kd[KMAX - 1] && (int32_t)jg < ki[KMAX - 1])) {
+          list_insert<KMAX>(kd, ki, d, (int32_t)jg);
+        }
       }
     }
   }
   if (dout) return;
 
   // warp-level merge of 32 sorted lane lists -> k smallest (distance, id)
-  const int64_t slot = (q * n_chunks_total + chunk_base + blockIdx.x) * (int64_t)k;
+  const int64_t slot = (q * n_chunks_total + chunk_base + chunk) * (int64_t)k;
   for (int r = 0; r < k; ++r) {
     float bd = kd[0];
     int32_t bi = ki[0];
@@ -205,26 +223,26 @@ int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* 
   LCRW_REQUIRE(q_offs && q_cols && q_vals && Z2 && D1, "lcrw_reverse_max: null pointer");
   LCRW_REQUIRE(doc_base + n_docs < (1ll << 31), "lcrw_reverse_max: doc ids must fit in int32");
   LCRW_REQUIRE(chunk_docs >= 32 && chunk_docs % 32 == 0, "lcrw_reverse_max: chunk_docs must be a positive multiple of 32");
-  const int64_t gx = ceil_div(n_docs, chunk_docs);
-  const int64_t gy = ceil_div(n_q, kWarps);
-  LCRW_REQUIRE(gy < 65536, "lcrw_reverse_max: too many queries for one launch");
-  LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_reverse_max: z_shift out of range");
+  const int64_t gx = ceil_div(n_q, kWarps);        // query panels
+  const int64_t gy = ceil_div(n_docs, chunk_docs);  // doc chunks
+  LCRW_REQUIRE(gy < 65536, "lcrw_reverse_max: too many doc chunks for one launch");
+  LCRW_REQUIRE(z_shift == 5, "lcrw_reverse_max: Z2 must use 32-segment panels (z_shift = 5)");
   dim3 grid((unsigned)gx, (unsigned)gy);
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "reverse_max");
   if (dout) {
-    reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, z_shift, n_docs, doc_base,
+    reverse_max_kernel<16, 8><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
                                                          id_offset, D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
                                                          nullptr, 0, 0, chunk_docs);
   } else {
     LCRW_REQUIRE(k >= 1 && cand_d && cand_i, "lcrw_reverse_max: top-k mode needs k >= 1 and candidate buffers");
-    LCRW_REQUIRE(chunk_base + gx <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
+    LCRW_REQUIRE(chunk_base + gy <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
     if (k <= 16) {
-      reverse_max_kernel<16><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, z_shift, n_docs,
+      reverse_max_kernel<16, 8><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
                                                            doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
                                                            cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
     } else if (k <= 32) {
-      reverse_max_kernel<32><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, z_shift, n_docs,
+      reverse_max_kernel<32, 8><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
                                                            doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
                                                            cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
     } else {
