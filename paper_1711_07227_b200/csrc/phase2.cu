@@ -65,26 +65,8 @@ __global__ void __launch_bounds__(kWarps * 32)
 // Reverse direction: D2[q, j] = sum_{w in q} x_qw Z2[j, w]; D = max(D1, D2).
 // Block = 8 warps = 8 queries; lanes walk the block's doc chunk.
 // ---------------------------------------------------------------------------
-template <int KMAX>
-__device__ __forceinline__ void list_insert(float (&kd)[KMAX], int32_t (&ki)[KMAX], float d, int32_t id) {
-  float cd = d;
-  int32_t ci = id;
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i) {
-    const bool lt = cd < kd[i] || (cd == kd[i] && ci < ki[i]);
-    if (lt) {
-      const float td = kd[i];
-      kd[i] = cd;
-      cd = td;
-      const int32_t ti = ki[i];
-      ki[i] = ci;
-      ci = ti;
-    }
-  }
-}
-
 template <int KMAX, int G>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, 3)
     reverse_max_kernel(const int64_t* __restrict__ q_offs, const int32_t* __restrict__ q_cols,
                        const float* __restrict__ q_vals, int64_t n_q, const float* __restrict__ Z2, int64_t z_panel,
                        int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
@@ -93,26 +75,30 @@ __global__ void __launch_bounds__(kWarps * 32)
                        int64_t chunk_base, int chunk_docs) {
   // Z2 in 32-doc panels: Z2[(j >> 5) * z_panel + (w << 5) + (j & 31)], so one
   // (word, 32-doc group) is a single 128-byte line.  Each lane owns G doc groups
-  // (G * 32 docs per pass): for every nonzero of the query, G independent line
-  // loads are in flight per warp.
-  // grid: x = query panel (fastest), y = doc chunk, so the blocks resident at any
-  // time share one doc chunk and its Z2 panels stay in L2 across query panels
+  // (G * 32 docs per pass); the G line loads of the next nonzero are issued
+  // before the current one is accumulated.  grid: x = query panel (fastest),
+  // y = doc chunk, so resident blocks share one chunk whose Z2 panels stay in L2.
+  // Per-lane sorted candidate lists live in shared memory (column per lane, no
+  // bank conflicts); only the current k-th distance/id is kept in registers.
+  extern __shared__ float s_lists[];  // [kWarps][KMAX][32] distances, then [kWarps][KMAX][32] ids
   const int lane = threadIdx.x & 31;
-  const int64_t q = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int wrp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * kWarps + wrp;
   if (q >= n_q) return;  // warp-uniform; no block-level synchronisation below
   const int64_t chunk = blockIdx.y;
   const int64_t j_begin = chunk * chunk_docs;
   const int64_t j_end = min(n_docs, j_begin + chunk_docs);
   const int64_t lo = q_offs[q], hi = q_offs[q + 1];
   const float* d1q = D1 + (q >> 3) * d1_ld_panel + (q & 7);
-
-  float kd[KMAX];
-  int32_t ki[KMAX];
+  float (*kd)[32] = reinterpret_cast<float (*)[32]>(s_lists + wrp * KMAX * 32);
+  int32_t (*ki)[32] = reinterpret_cast<int32_t (*)[32]>(s_lists + (kWarps + wrp) * KMAX * 32);
 #pragma unroll
   for (int i = 0; i < KMAX; ++i) {
-    kd[i] = __int_as_float(0x7f800000);
-    ki[i] = 0x7fffffff;
+    kd[i][lane] = __int_as_float(0x7f800000);
+    ki[i][lane] = 0x7fffffff;
   }
+  float thr_d = __int_as_float(0x7f800000);
+  int32_t thr_i = 0x7fffffff;
 
   for (int64_t jb = j_begin; jb < j_end; jb += 32 * G) {
     double acc[G];
@@ -124,16 +110,23 @@ __global__ void __launch_bounds__(kWarps * 32)
       const int cnt = (int)min((int64_t)32, hi - base);
       const int32_t my_w = lane < cnt ? __ldg(q_cols + base + lane) : 0;
       const float my_x = lane < cnt ? __ldg(q_vals + base + lane) : 0.f;
-#pragma unroll 2
-      for (int t = 0; t < cnt; ++t) {
-        const int64_t w = __shfl_sync(0xffffffffu, my_w, t);
-        const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
-        const float* zw = zb + (w << 5);
-        float z[G];
+      float z[G];
+      {
+        const float* zw = zb + ((int64_t)__shfl_sync(0xffffffffu, my_w, 0) << 5);
 #pragma unroll
         for (int g = 0; g < G; ++g) z[g] = g < ng ? __ldg(zw + g * z_panel) : 0.f;
+      }
+      for (int t = 0; t < cnt; ++t) {
+        float zn[G];
+        const int tn = t + 1 < cnt ? t + 1 : t;
+        const float* zw = zb + ((int64_t)__shfl_sync(0xffffffffu, my_w, tn) << 5);
+#pragma unroll
+        for (int g = 0; g < G; ++g) zn[g] = (g < ng && t + 1 < cnt) ? __ldg(zw + g * z_panel) : 0.f;
+        const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] = fma(x, (double)z[g], acc[g]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) z[g] = zn[g];
       }
     }
 #pragma unroll
@@ -144,8 +137,22 @@ __global__ void __launch_bounds__(kWarps * 32)
         const float d = fmaxf(__ldg(d1q + jg * d1_ld_row), (float)acc[g]);
         if (dout) {
           dout[jg * ld_out + q] = d;
-        } else if (d < kd[KMAX - 1] || (d == kd[KMAX - 1] && (int32_t)jg < ki[KMAX - 1])) {
-          list_insert<KMAX>(kd, ki, d, (int32_t)jg);
+        } else if (d < thr_d || (d == thr_d && (int32_t)jg < thr_i)) {
+          // sorted insertion into this lane's smem list (rare once the list fills)
+          float cd = d;
+          int32_t ci = (int32_t)jg;
+          for (int i = 0; i < KMAX; ++i) {
+            const float od = kd[i][lane];
+            const int32_t oi = ki[i][lane];
+            if (cd < od || (cd == od && ci < oi)) {
+              kd[i][lane] = cd;
+              ki[i][lane] = ci;
+              cd = od;
+              ci = oi;
+            }
+          }
+          thr_d = kd[KMAX - 1][lane];
+          thr_i = ki[KMAX - 1][lane];
         }
       }
     }
@@ -154,9 +161,12 @@ __global__ void __launch_bounds__(kWarps * 32)
 
   // warp-level merge of 32 sorted lane lists -> k smallest (distance, id)
   const int64_t slot = (q * n_chunks_total + chunk_base + chunk) * (int64_t)k;
+  int head = 0;
   for (int r = 0; r < k; ++r) {
-    float bd = kd[0];
-    int32_t bi = ki[0];
+    const float hd = head < KMAX ? kd[head][lane] : __int_as_float(0x7f800000);
+    const int32_t hi_ = head < KMAX ? ki[head][lane] : 0x7fffffff;
+    float bd = hd;
+    int32_t bi = hi_;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const float od = __shfl_xor_sync(0xffffffffu, bd, o);
@@ -166,21 +176,15 @@ __global__ void __launch_bounds__(kWarps * 32)
         bi = oi;
       }
     }
-    if (kd[0] == bd && ki[0] == bi) {
-#pragma unroll
-      for (int i = 0; i < KMAX - 1; ++i) {
-        kd[i] = kd[i + 1];
-        ki[i] = ki[i + 1];
-      }
-      kd[KMAX - 1] = __int_as_float(0x7f800000);
-      ki[KMAX - 1] = 0x7fffffff;
-    }
+    if (hd == bd && hi_ == bi) ++head;
     if (lane == 0) {
       cand_d[slot + r] = bd;
       cand_i[slot + r] = bi == 0x7fffffff ? INT64_MAX : (int64_t)bi + id_offset;
     }
   }
 }
+
+constexpr int list_smem(int kmax) { return 2 * kWarps * kmax * 32 * 4; }
 
 }  // namespace p2
 }  // namespace lcrw
@@ -230,19 +234,25 @@ int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* 
   dim3 grid((unsigned)gx, (unsigned)gy);
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "reverse_max");
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(reverse_max_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem(16));
+    cudaFuncSetAttribute(reverse_max_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem(32));
+    attrs = true;
+  }
   if (dout) {
-    reverse_max_kernel<16, 8><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
+    reverse_max_kernel<16, 8><<<grid, kWarps * 32, list_smem(16), st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
                                                          id_offset, D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
                                                          nullptr, 0, 0, chunk_docs);
   } else {
     LCRW_REQUIRE(k >= 1 && cand_d && cand_i, "lcrw_reverse_max: top-k mode needs k >= 1 and candidate buffers");
     LCRW_REQUIRE(chunk_base + gy <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
     if (k <= 16) {
-      reverse_max_kernel<16, 8><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
+      reverse_max_kernel<16, 8><<<grid, kWarps * 32, list_smem(16), st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
                                                            doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
                                                            cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
     } else if (k <= 32) {
-      reverse_max_kernel<32, 8><<<grid, kWarps * 32, 0, st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
+      reverse_max_kernel<32, 8><<<grid, kWarps * 32, list_smem(32), st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
                                                            doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
                                                            cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
     } else {
