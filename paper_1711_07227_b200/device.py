@@ -83,6 +83,7 @@ class DeviceCSR:
     vals: torch.Tensor
     n_cols: int
     host_offsets: np.ndarray
+    host_cols: np.ndarray | None = None  # kept for small (query-side) sets: row-order planning
 
     @property
     def n_rows(self) -> int:
@@ -99,8 +100,10 @@ class DeviceCSR:
             raise CorpusError(f"{name}: every row must hold at least one word")
         if int(offs[0]) != 0 or len(x.column_ids) != int(offs[-1]) or len(x.values) != int(offs[-1]):
             raise CorpusError(f"{name}: offset/array length mismatch")
-        return cls(to_device(offs, torch.int64), to_device(x.column_ids, torch.int32),
-                   to_device(x.values, torch.float32), int(x.n_cols), offs)
+        cols = np.asarray(x.column_ids, dtype=np.int32)
+        return cls(to_device(offs, torch.int64), to_device(cols, torch.int32),
+                   to_device(x.values, torch.float32), int(x.n_cols), offs,
+                   cols if cols.size <= (1 << 22) else None)
 
 
 class PreparedEmbeddings:
@@ -282,8 +285,22 @@ class Restricted:
     a_norms: torch.Tensor
 
     @classmethod
-    def build(cls, x: DeviceCSR, prep: PreparedEmbeddings) -> "Restricted":
-        remap, used, v_e = restrict(x.cols, x.n_cols)
+    def build(cls, x: DeviceCSR, prep: PreparedEmbeddings, first_use_order: bool = False) -> "Restricted":
+        """Restriction of ``x`` to its own words.  With ``first_use_order`` the
+        restricted rows are numbered by first appearance in x's CSR instead of by
+        ascending word id: any row order gives identical values (the reference's
+        restricted ids only name rows), and this one makes each row of x touch a
+        nearly contiguous block of Z rows (DRAM-friendly gathers in reverse_max)."""
+        if first_use_order and x.host_cols is not None:
+            words, first = np.unique(x.host_cols, return_index=True)
+            order = words[np.argsort(first, kind="stable")].astype(np.int32)
+            rank = np.full(x.n_cols, -1, dtype=np.int32)
+            rank[order] = np.arange(len(order), dtype=np.int32)
+            used = to_device(order, torch.int32)
+            remap = to_device(rank, torch.int32)
+            v_e = len(order)
+        else:
+            remap, used, v_e = restrict(x.cols, x.n_cols)
         A, an = gather_rows(prep, used, "A")
         return cls(x, remap, used, v_e, remap_ids(x.cols, remap), A, an)
 
@@ -338,7 +355,7 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         res1 = Restricted.build(x1, prep)
         d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
         del res1
-    res2 = Restricted.build(x2, prep)
+    res2 = Restricted.build(x2, prep, first_use_order=True)
     batch = reverse_batch_docs(n1, res2.v_e, z2_budget_bytes)
     ho = x1.host_offsets
     max_words = max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
