@@ -200,8 +200,12 @@ def run_ours(args, cfg):
     calls = {n: c - calls0.get(n, 0) for n, c in _lib.CALLS.items()}
     ksum = _lib.profile_read()
     _lib.profile_reset(False)
-    # reverse pipeline: 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse) + top-k merge
-    launches = (_lib.launches(calls) + 5 * ksum.get("reverse_max", {"launches": 0})["launches"]) // args.steps
+    # reverse pipeline: 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse), counted from
+    # its reverse_max launches; calibrated against the ncu launch list (profiles/r01_launches_c2.csv)
+    rev_batches = ksum.get("reverse_max", {"launches": 0})["launches"]
+    if world > 1:
+        rev_batches = rev_batches  # per-rank count; the line reports rank 0's launches
+    launches = (_lib.launches(calls) + _lib.REVERSE_KERNELS_PER_BATCH * rev_batches) // args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

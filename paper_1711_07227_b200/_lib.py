@@ -70,12 +70,13 @@ _VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lc
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".
 KERNELS_PER_CALL = {
     "lcrw_max_sqnorm": 1, "lcrw_scale_from_max_sqnorm": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
-    "lcrw_row_classes": 12, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
+    "lcrw_row_classes": 13, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
     "lcrw_reverse_max": 1, "lcrw_topk_segments": 1, "lcrw_topk_sort": 7,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse);
-# bench.py adds those from the batch count.
+# bench.py adds those from the batch count (= its reverse_max launches).
+REVERSE_KERNELS_PER_BATCH = 6
 
 CALLS: dict[str, int] = {}
 

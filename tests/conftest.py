@@ -18,6 +18,7 @@ LCRWMD_CASES = ["small_m16", "m300", "clustered", "self_queries", "dup_rows", "r
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the CUDA C ABI)")
+    config.addinivalue_line("markers", "slow: full-size (BASELINE configs[1]) GPU parity, ~1 min")
 
 
 def load_case(name):

@@ -251,3 +251,31 @@ def test_sharded_pipeline_emulated_ranks():
         ci = torch.cat(parts_i, 1).contiguous()
         gd, gi = device.topk_rows(cd, ci, x2.n_rows, cd.shape[1], k)
         assert torch.equal(gd, want_d) and torch.equal(gi, want_i), W
+
+
+@pytest.mark.slow
+def test_c2_full_size_sampled_parity():
+    """BASELINE configs[1] at full size (1M docs x 1k queries, V=100k, m=300):
+    sampled entries of the symmetric matrix vs the oracle on the sampled subsets
+    (subset invariance), and fused top-k == top-k of the full matrix."""
+    import torch
+    from paper_1711_07227_b200 import device, synthetic as S
+    V = 100_000
+    E = S.embeddings(V, 300, seed=0)
+    x1 = S.histograms(1_000_000, V, 50, seed=1)
+    x2 = S.histograms(1000, V, 50, seed=2)
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    full = device.symmetric(d1, d2, prep, None)  # (1M, 1k) on device, 4 GB
+    rng = np.random.default_rng(5)
+    di = np.sort(rng.choice(1_000_000, 256, replace=False))
+    qj = np.sort(rng.choice(1000, 16, replace=False))
+    got = full[torch.as_tensor(di, device=full.device)][:, torch.as_tensor(qj, device=full.device)].cpu().numpy()
+    ref = O.lcrwmd_full(x1.take_rows(di), x2.take_rows(qj), E, threads=O.default_threads())
+    ok, err = rel_close(got, ref, RTOL, ATOL)
+    assert ok, err
+    td, ti = device.symmetric(d1, d2, prep, 10)
+    fd, fi = device.topk_rows(full.t().contiguous(),
+                              torch.arange(1_000_000, device=full.device).repeat(1000, 1).contiguous(),
+                              1000, 1_000_000, 10)
+    assert torch.equal(td, fd) and torch.equal(ti, fi)
