@@ -155,7 +155,7 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     E, x1, x2 = make_data(cfg)
     k = cfg["k"]
@@ -170,7 +170,7 @@ def run_ours(args, cfg):
 
     def step():
         prep = device.PreparedEmbeddings(Ed)
-        if world == 1:
+        if world == 1 and not args.force_sharded:
             return device.symmetric(dx1, dx2, prep, k, z2_budget_bytes=args.z2_mb << 20, chunk_docs=args.chunk)
         return parallel.sharded_topk(dx1, lo, n1, dx2, prep, k)
 
@@ -225,7 +225,7 @@ def run_ours(args, cfg):
     d2h = n2 * k * (4 + 8)
 
     def e2e_step():
-        if world == 1:
+        if world == 1 and not args.force_sharded:
             return distances.lcrwmd_topk_arrays(hx1, hx2, hE, k)
         return parallel.sharded_topk_host(hx1, lo, n1, hx2, hE, k)
 
@@ -248,7 +248,7 @@ def run_ours(args, cfg):
         barrier()
 
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
     pk, pk_kind = peaks()
@@ -291,7 +291,7 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample_rate(E, x1, x2, k, args.cpu_seconds)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -339,6 +339,8 @@ def main():
     ap.add_argument("--ref-docs", type=int, default=96)
     ap.add_argument("--z2-mb", type=int, default=4096, help="reverse Z2 batch budget (MiB)")
     ap.add_argument("--chunk", type=int, default=512, help="docs per reverse top-k candidate chunk")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the multi-GPU code path (NCCL process group) even with one rank")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
