@@ -94,14 +94,24 @@ size_t smem_bytes(int n_kb, int stages) {
 // ---------------------------------------------------------------------------
 constexpr float kInf = __builtin_huge_valf();
 
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3 on sm_100a
+  return r;
+}
+
 template <int A, int B>
-struct RangeMin {  // min(v[A..B]) as a balanced tree (B >= A)
+struct RangeMin {  // min(v[A..B]) as a balanced ternary tree of 3-input mins (B >= A)
   __device__ __forceinline__ static float run(const float (&v)[32]) {
-    if constexpr (A == B) {
+    constexpr int n = B - A + 1;
+    if constexpr (n == 1) {
       return v[A];
+    } else if constexpr (n == 2) {
+      return fminf(v[A], v[B]);
     } else {
-      constexpr int M = (A + B) / 2;
-      return fminf(RangeMin<A, M>::run(v), RangeMin<M + 1, B>::run(v));
+      constexpr int m1 = A + n / 3 - 1 + (n % 3 > 0 ? 1 : 0);
+      constexpr int m2 = m1 + n / 3 + (n % 3 > 1 ? 1 : 0);
+      return fmin3(RangeMin<A, m1>::run(v), RangeMin<m1 + 1, m2>::run(v), RangeMin<m2 + 1, B>::run(v));
     }
   }
 };
