@@ -171,7 +171,7 @@ def run_ours(args, cfg):
     def step():
         prep = device.PreparedEmbeddings(Ed)
         if world == 1 and not args.force_sharded:
-            return device.symmetric(dx1, dx2, prep, k, z2_budget_bytes=args.z2_mb << 20, chunk_docs=args.chunk)
+            return device.symmetric(dx1, dx2, prep, k, z2_budget_bytes=args.z2_mb << 20)
         return parallel.sharded_topk(dx1, lo, n1, dx2, prep, k)
 
     def barrier():
@@ -200,11 +200,9 @@ def run_ours(args, cfg):
     calls = {n: c - calls0.get(n, 0) for n, c in _lib.CALLS.items()}
     ksum = _lib.profile_read()
     _lib.profile_reset(False)
-    # reverse pipeline: 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse), counted from
-    # its reverse_max launches; calibrated against the ncu launch list (profiles/r01_launches_c2.csv)
-    rev_batches = ksum.get("reverse_max", {"launches": 0})["launches"]
-    if world > 1:
-        rev_batches = rev_batches  # per-rank count; the line reports rank 0's launches
+    # reverse pipeline: 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels), counted
+    # from its reverse_panels launches; calibrated against the ncu launch list (profiles/)
+    rev_batches = ksum.get("reverse_panels", {"launches": 0})["launches"]
     launches = (_lib.launches(calls) + _lib.REVERSE_KERNELS_PER_BATCH * rev_batches) // args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -260,8 +258,9 @@ def run_ours(args, cfg):
     achieved_tf = rev_flops / (rev["ms"] / args.steps * 1e-3) / 1e12
     fwd_flops = 2.0 * int(np.unique(x1s.column_ids).size) * x2.nnz * cfg["dim"]
     spmm_bytes = 8.0 * (x1s.n_rows + 1) + 8.0 * x1s.nnz + 4.0 * x1s.nnz * n2
-    rev_bytes = 4.0 * x2.nnz * x1s.n_rows + 4.0 * n2 * x1s.n_rows
-    work = {"phase1": fwd_flops, "phase1_rev": rev_flops, "spmm": spmm_bytes, "reverse_max": rev_bytes}
+    # reverse_panels streams every Z2 panel once (4 * v_e2 bytes per doc), reads D1 and writes D
+    rev_bytes = 4.0 * v_e2 * x1s.n_rows + 8.0 * n2 * x1s.n_rows
+    work = {"phase1": fwd_flops, "phase1_rev": rev_flops, "spmm": spmm_bytes, "reverse_panels": rev_bytes}
     peak_tf = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
     pairs = n1 * n2
     value = pairs / (ms * 1e-3)
@@ -338,7 +337,6 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-docs", type=int, default=96)
     ap.add_argument("--z2-mb", type=int, default=4096, help="reverse Z2 batch budget (MiB)")
-    ap.add_argument("--chunk", type=int, default=512, help="docs per reverse top-k candidate chunk")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU code path (NCCL process group) even with one rank")
     args = ap.parse_args()

@@ -148,26 +148,40 @@ int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* 
                      int64_t ld_out, int k, float* cand_d, int64_t* cand_i, int64_t n_chunks_total,
                      int64_t chunk_base, int chunk_docs, void* stream);
 
-/* Whole reverse direction in one call (distances.py:263-264 + top-k): docs in
- * batches of batch_docs (multiple of 32); per batch gather -> segment plan ->
- * lcrw_phase1 (32-doc Z2 panels) -> lcrw_zero_identical -> lcrw_reverse_max,
+/* Reverse direction, panel-streaming form: one CTA per (32-doc Z2 panel, group
+ * of lcrw_reverse_panels_group() queries) streams the panel's word rows through
+ * shared memory in lcrw_reverse_panels_tile_rows()-row tiles and scatters the
+ * query nonzeros (a word-major list, see below) into fp32 per-query
+ * accumulators; writes D[q * ld_q + (doc_base + j) * ld_doc] = max(D1, D2) for
+ * the batch's docs j < n_docs.  D1 in 8-query panels (d1_ld_panel = 8 * n1).
+ * Entry list: for each query group g, tile t (rows [t*T, t*T+T)) and warp w,
+ * entries e_off[(g*n_tiles + t)*W + w] .. +1 (W = lcrw_reverse_panels_warps()),
+ * each e_pack = (row - t*T) << 16 | (q - g*G) with weight e_x; a warp owns the
+ * queries with (q - g*G) % W == w, so accumulation order is deterministic. */
+int lcrw_reverse_panels_tile_rows(void);
+int lcrw_reverse_panels_group(void);
+int lcrw_reverse_panels_warps(void);
+int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs, int64_t doc_base,
+                        const uint32_t* e_pack, const float* e_x, const int32_t* e_off, int64_t n_q,
+                        const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
+                        void* stream);
+
+/* Whole reverse direction in one call (distances.py:263-264): docs in batches
+ * of batch_docs (multiple of 32); per batch gather -> segment plan ->
+ * lcrw_phase1 (32-doc Z2 panels) -> lcrw_zero_identical -> lcrw_reverse_panels,
  * enqueued from C++ on `stream`.  doc_offsets_host is the host copy of
  * doc_offsets (batch planning); doc_cols are global E ids, rep/next/remap as in
- * lcrw_zero_identical; (q_offs, q_cols, q_vals) the query CSR with ids
- * restricted to A's rows.  Workspace from lcrw_reverse_workspace with
- * max_batch_words = max words over batches; n_chunks_total from
- * lcrw_reverse_chunks. */
+ * lcrw_zero_identical.  Writes D = max(D1, D2) for all docs (see
+ * lcrw_reverse_panels).  Workspace from lcrw_reverse_workspace with
+ * max_batch_words = max words over batches. */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
 int64_t lcrw_reverse_chunks(int64_t n_docs, int64_t batch_docs, int chunk_docs);
-int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB,
-                          const float* e_norms, int m, int kp, const float* scale, const int64_t* doc_offsets,
-                          const int64_t* doc_offsets_host, int64_t n_docs, const int32_t* doc_cols,
-                          const int32_t* rep, const int32_t* next, const int32_t* remap, const int64_t* q_offs,
-                          const int32_t* q_cols, const float* q_vals, int64_t n_q, const float* D1,
-                          int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k,
-                          float* cand_d, int64_t* cand_i, int64_t n_chunks_total, int64_t id_offset,
-                          int64_t batch_docs, int chunk_docs, int range_cols, void* ws, size_t ws_bytes,
-                          void* stream);
+int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
+                          const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
+                          int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
+                          const int32_t* remap, const uint32_t* e_pack, const float* e_x, const int32_t* e_off,
+                          int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
+                          int64_t batch_docs, int range_cols, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k
@@ -175,6 +189,9 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
  * entries.  k <= 1024 (lcrw_topk_sort handles any k for one segment). */
 int lcrw_topk_segments(const float* d, const int64_t* ids, int64_t n_seg, int64_t seg_len, int k,
                        float* out_d, int64_t* out_i, void* stream);
+/* per-row top-k of a row-major matrix (row stride ld) with implicit ids id_base + column */
+int lcrw_topk_rows(const float* d, int64_t ld, int64_t n_rows, int64_t row_len, int64_t id_base, int k,
+                   float* out_d, int64_t* out_i, void* stream);
 int lcrw_topk_sort_workspace(int64_t n, size_t* bytes);
 /* full (distance, id) sort of one segment of n candidates; writes the first k */
 int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, float* out_d, int64_t* out_i,

@@ -186,6 +186,124 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
 
 constexpr int list_smem(int kmax) { return 2 * kWarps * kmax * 32 * 4; }
 
+// ---------------------------------------------------------------------------
+// Reverse direction, panel-streaming form.  One CTA per (32-doc Z2 panel,
+// group of <= 1024 queries): the panel's word rows are streamed through shared
+// memory in 256-row tiles (cp.async, sequential 32 KB reads -- each Z2 byte is
+// read from HBM once), and a word-major list of the query nonzeros scatters
+// x * Z2[w, 32 docs] into per-query fp32 accumulators in shared memory.  Each
+// query is owned by one warp (q % 16), so accumulation order is fixed (tile,
+// then row): results are deterministic.  The symmetric combine max(D1, D2) is
+// written query-major (128-byte rows) for the final per-query top-k.
+// ---------------------------------------------------------------------------
+constexpr int kRpWarps = 16;   // consumer warps (+1 producer warp)
+constexpr int kRpTile = 128;   // Z2 rows per staged tile (16 KB)
+constexpr int kRpStages = 4;
+constexpr int kRpGroup = 1024; // queries per CTA
+
+__global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
+    reverse_panels_kernel(const float* __restrict__ Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs,
+                          int64_t doc_base, const uint32_t* __restrict__ e_pack, const float* __restrict__ e_x,
+                          const int32_t* __restrict__ e_off, int n_tiles, int64_t n_q, const float* __restrict__ D1,
+                          int64_t d1_ld_panel, float* __restrict__ D, int64_t ld_q, int64_t ld_doc) {
+  extern __shared__ __align__(16) float rp_smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t p = blockIdx.x;
+  const int g = blockIdx.y;
+  const int64_t q0 = (int64_t)g * kRpGroup;
+  const int nq = (int)min((int64_t)kRpGroup, n_q - q0);
+  float* acc = rp_smem;                                              // [kRpGroup][32]
+  float* tiles = rp_smem + (size_t)kRpGroup * 32;                    // [kRpStages][kRpTile][32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + kRpStages * kRpTile * 32);
+  uint64_t* empty = full + kRpStages;
+  int32_t* offs = reinterpret_cast<int32_t*>(empty + kRpStages);    // [n_tiles * W + 1]
+  const int32_t* goff = e_off + (int64_t)g * n_tiles * kRpWarps;
+  for (int i = threadIdx.x; i <= n_tiles * kRpWarps; i += blockDim.x) offs[i] = __ldg(goff + i);
+  for (int i = threadIdx.x; i < nq * 32; i += blockDim.x) acc[i] = 0.f;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRpStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kRpWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const float* zp = Z2 + p * z_panel;
+
+  if (warp == kRpWarps) {
+    // ---- producer: stream the panel's rows, kRpStages tiles ahead ----
+    if (lane == 0) {
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % kRpStages;
+        mbar_wait(empty + st, ((t / kRpStages) & 1) ^ 1);
+        const int64_t r0 = (int64_t)t * kRpTile;
+        const uint32_t bytes = (uint32_t)min((int64_t)kRpTile, a_rows - r0) * 128u;
+        mbar_expect_tx(full + st, bytes);
+        bulk_load(tiles + st * kRpTile * 32, zp + r0 * 32, bytes, full + st);
+      }
+    }
+  } else {
+    // ---- consumers: scatter this warp's query nonzeros of each tile ----
+    int e0 = offs[warp], e1 = offs[warp + 1];
+    uint32_t pre_p = lane < e1 - e0 ? __ldg(e_pack + e0 + lane) : 0u;
+    float pre_x = lane < e1 - e0 ? __ldg(e_x + e0 + lane) : 0.f;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int st = t % kRpStages;
+      // next tile's entry window and first 32 entries (latency hidden behind this tile)
+      const int ne0 = t + 1 < n_tiles ? offs[(t + 1) * kRpWarps + warp] : 0;
+      const int ne1 = t + 1 < n_tiles ? offs[(t + 1) * kRpWarps + warp + 1] : 0;
+      const uint32_t nxt_p = lane < ne1 - ne0 ? __ldg(e_pack + ne0 + lane) : 0u;
+      const float nxt_x = lane < ne1 - ne0 ? __ldg(e_x + ne0 + lane) : 0.f;
+      mbar_wait(full + st, (t / kRpStages) & 1);
+      const float* tile = tiles + st * kRpTile * 32;
+      uint32_t cur_p = pre_p;
+      float cur_x = pre_x;
+      for (int eb = e0; eb < e1; eb += 32) {
+        if (eb != e0) {  // rare: more than 32 entries for this (tile, warp)
+          cur_p = lane < e1 - eb ? __ldg(e_pack + eb + lane) : 0u;
+          cur_x = lane < e1 - eb ? __ldg(e_x + eb + lane) : 0.f;
+        }
+        const int cnt = min(32, e1 - eb);
+        for (int i = 0; i < cnt; ++i) {
+          const uint32_t pk = __shfl_sync(0xffffffffu, cur_p, i);
+          const float x = __shfl_sync(0xffffffffu, cur_x, i);
+          float* a = acc + (pk & 0xFFFFu) * 32 + lane;
+          *a = fmaf(x, tile[(pk >> 16) * 32 + lane], *a);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      e0 = ne0;
+      e1 = ne1;
+      pre_p = nxt_p;
+      pre_x = nxt_x;
+    }
+  }
+  __syncthreads();
+
+  // symmetric combine with D1 (8-query panels: D1[(q >> 3) * ld_panel + j * 8 + (q & 7)])
+  const int64_t j = p * 32 + lane;
+  const bool valid = j < n_docs;
+  const int64_t jg = doc_base + j;
+  for (int qp = warp; qp * 8 < nq; qp += kRpWarps + 1) {
+    const int64_t qg = q0 + qp * 8;
+    float d1v[8];
+    if (valid) {
+      const float4* src = reinterpret_cast<const float4*>(D1 + (qg >> 3) * d1_ld_panel + jg * 8);
+      const float4 a = __ldg(src), b = __ldg(src + 1);
+      d1v[0] = a.x; d1v[1] = a.y; d1v[2] = a.z; d1v[3] = a.w;
+      d1v[4] = b.x; d1v[5] = b.y; d1v[6] = b.z; d1v[7] = b.w;
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      const int ql = qp * 8 + qq;
+      if (valid && ql < nq) D[(qg + qq) * ld_q + jg * ld_doc] = fmaxf(d1v[qq], acc[ql * 32 + lane]);
+    }
+  }
+}
+
+
 }  // namespace p2
 }  // namespace lcrw
 
@@ -216,6 +334,44 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
 }
 
 int lcrw_reverse_chunk_docs(void) { return kDefaultChunkDocs; }
+
+int lcrw_reverse_panels_tile_rows(void) { return kRpTile; }
+int lcrw_reverse_panels_group(void) { return kRpGroup; }
+int lcrw_reverse_panels_warps(void) { return kRpWarps; }
+
+int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs, int64_t doc_base,
+                        const uint32_t* e_pack, const float* e_x, const int32_t* e_off, int64_t n_q,
+                        const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
+                        void* stream) {
+  LCRW_REQUIRE(n_q >= 0 && n_docs >= 0 && a_rows >= 0, "lcrw_reverse_panels: bad shape");
+  if (n_q == 0 || n_docs == 0) return LCRW_OK;
+  LCRW_REQUIRE(Z2 && e_pack && e_x && e_off && D1 && D, "lcrw_reverse_panels: null pointer");
+  LCRW_REQUIRE(z_panel == a_rows * 32 && (reinterpret_cast<uintptr_t>(Z2) & 15) == 0,
+               "lcrw_reverse_panels: Z2 must be 16-byte aligned 32-doc panels (z_panel = 32 * a_rows)");
+  const int n_tiles = (int)ceil_div(a_rows, kRpTile);
+  const int64_t panels = ceil_div(n_docs, 32);
+  const int64_t groups = ceil_div(n_q, kRpGroup);
+  LCRW_REQUIRE(panels < (1ll << 31) && groups < 65536, "lcrw_reverse_panels: grid too large");
+  const int fixed = (kRpGroup * 32 + kRpStages * kRpTile * 32) * 4 + 2 * kRpStages * 8;
+  const int smem = fixed + (n_tiles * kRpWarps + 1) * 4;
+  const int smem_max = 227 * 1024;
+  if (smem > smem_max) {
+    set_error("lcrw_reverse_panels: query vocabulary of %lld rows needs %d B of shared memory", (long long)a_rows, smem);
+    return LCRW_ERR_UNSUPPORTED;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(reverse_panels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(reverse_panels_kernel)");
+    attr = true;
+  }
+  cudaStream_t st = as_stream(stream);
+  ProfScope prof(st, "reverse_panels");
+  reverse_panels_kernel<<<dim3((unsigned)panels, (unsigned)groups), (kRpWarps + 1) * 32, smem, st>>>(
+      Z2, z_panel, a_rows, n_docs, doc_base, e_pack, e_x, e_off, n_tiles, n_q, D1, d1_ld_panel, D, ld_q, ld_doc);
+  LCRW_CHECK_LAUNCH("reverse_panels_kernel");
+  return LCRW_OK;
+}
 
 int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
                      const float* Z2, int64_t z_panel, int z_shift, int64_t n_docs, int64_t doc_base, int64_t id_offset,

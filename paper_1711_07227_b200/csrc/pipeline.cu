@@ -8,7 +8,7 @@
 //   plan     segment-end bitmap + column ranges             (segments = docs)
 //   phase1   Z2[doc, w] = min_t |E_w - T_t|                 (tcgen05, 32-doc panels)
 //   zeros    Z2[doc, w] = 0 where doc holds a word identical to w
-//   reverse  D = max(D1, spmm(Xq, Z2)) -> per (query, doc chunk) top-k
+//   reverse  D[q, doc] = max(D1, spmm(Xq, Z2)), panel-streaming (query-major D)
 // The loop runs in C++ so a batch costs a handful of launch calls, not Python.
 #include "common.cuh"
 
@@ -73,17 +73,15 @@ int64_t lcrw_reverse_chunks(int64_t n_docs, int64_t batch_docs, int chunk_docs) 
   return n;
 }
 
-int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB,
-                          const float* e_norms, int m, int kp, const float* scale, const int64_t* doc_offsets,
-                          const int64_t* doc_offsets_host, int64_t n_docs, const int32_t* doc_cols, const int32_t* rep,
-                          const int32_t* next, const int32_t* remap, const int64_t* q_offs, const int32_t* q_cols,
-                          const float* q_vals, int64_t n_q, const float* D1, int64_t d1_ld_row, int64_t d1_ld_panel,
-                          float* dout, int64_t ld_out, int k, float* cand_d, int64_t* cand_i, int64_t n_chunks_total,
-                          int64_t id_offset, int64_t batch_docs, int chunk_docs, int range_cols, void* ws,
-                          size_t ws_bytes, void* stream) {
+int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
+                          const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
+                          int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
+                          const int32_t* remap, const uint32_t* e_pack, const float* e_x, const int32_t* e_off,
+                          int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
+                          int64_t batch_docs, int range_cols, void* ws, size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
-  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && rep && ws, "lcrw_reverse_pipeline: null pointer");
+  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && rep && ws && D, "lcrw_reverse_pipeline: null pointer");
   LCRW_REQUIRE(batch_docs > 0 && (batch_docs % (1 << kZShift)) == 0,
                "lcrw_reverse_pipeline: batch_docs must be a positive multiple of 32");
   int64_t max_words = 0;
@@ -94,10 +92,6 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
   }
   const Layout L = layout(a_rows, kp, batch_docs, max_words);
   LCRW_REQUIRE(ws_bytes >= L.total, "lcrw_reverse_pipeline: workspace too small (use lcrw_reverse_workspace)");
-  if (!dout) {
-    LCRW_REQUIRE(lcrw_reverse_chunks(n_docs, batch_docs, chunk_docs) == n_chunks_total,
-                 "lcrw_reverse_pipeline: n_chunks_total != lcrw_reverse_chunks(...)");
-  }
   char* base = static_cast<char*>(ws);
   uint16_t* T = reinterpret_cast<uint16_t*>(base + L.T);
   uint32_t* mask = reinterpret_cast<uint32_t*>(base + L.mask);
@@ -105,7 +99,6 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
   float* Z2 = reinterpret_cast<float*>(base + L.Z);
   const int64_t z_panel = a_rows << kZShift;
   cudaStream_t st = as_stream(stream);
-  int64_t chunk_base = 0;
   int status;
   for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
@@ -120,11 +113,9 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;
-    if ((status = lcrw_reverse_max(q_offs, q_cols, q_vals, n_q, Z2, z_panel, kZShift, nd, j0, id_offset, D1, d1_ld_row,
-                                   d1_ld_panel, dout, ld_out, k, cand_d, cand_i, n_chunks_total, chunk_base,
-                                   chunk_docs, stream)))
+    if ((status = lcrw_reverse_panels(Z2, z_panel, a_rows, nd, j0, e_pack, e_x, e_off, n_q, D1, d1_ld_panel, D, ld_q,
+                                      ld_doc, stream)))
       return status;
-    chunk_base += ceil_div(nd, chunk_docs);
   }
   return LCRW_OK;
 }

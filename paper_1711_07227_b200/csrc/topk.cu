@@ -49,14 +49,15 @@ __device__ void bitonic_sort(uint32_t* key, int64_t* id) {
 }
 
 __global__ void __launch_bounds__(kThreads)
-    topk_segments_kernel(const float* __restrict__ d, const int64_t* __restrict__ ids, int64_t seg_len, int k, int kp,
-                         float* __restrict__ out_d, int64_t* __restrict__ out_i) {
+    topk_segments_kernel(const float* __restrict__ d, const int64_t* __restrict__ ids, int64_t ld, int64_t seg_len,
+                         int64_t id_base, int k, int kp, float* __restrict__ out_d, int64_t* __restrict__ out_i) {
   __shared__ uint32_t key[kBuf];
   __shared__ int64_t idb[kBuf];
   __shared__ int count;
   const int64_t seg = blockIdx.x;
-  const float* ds = d + seg * seg_len;
-  const int64_t* is = ids + seg * seg_len;
+  // ids == NULL: implicit ids id_base + position (rows of a distance matrix)
+  const float* ds = d + seg * ld;
+  const int64_t* is = ids ? ids + seg * ld : nullptr;
   for (int i = threadIdx.x; i < kBuf; i += blockDim.x) {
     key[i] = 0xFFFFFFFFu;
     idb[i] = INT64_MAX;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t i = base + threadIdx.x;
     if (i < seg_len) {
       const uint32_t kk = float_key(ds[i]);
-      const int64_t ii = is[i];
+      const int64_t ii = is ? is[i] : id_base + i;
       if (less(kk, ii, thr_k, thr_i)) {
         const int pos = atomicAdd(&count, 1);
         key[kp + pos] = kk;
@@ -143,8 +144,28 @@ int lcrw_topk_segments(const float* d, const int64_t* ids, int64_t n_seg, int64_
   LCRW_REQUIRE(n_seg < (1ll << 31), "lcrw_topk_segments: too many segments");
   int kp = 1;
   while (kp < k) kp <<= 1;
-  topk_segments_kernel<<<(unsigned)n_seg, kThreads, 0, as_stream(stream)>>>(d, ids, seg_len, k, kp, out_d, out_i);
+  topk_segments_kernel<<<(unsigned)n_seg, kThreads, 0, as_stream(stream)>>>(d, ids, seg_len, seg_len, 0, k, kp,
+                                                                             out_d, out_i);
   LCRW_CHECK_LAUNCH("topk_segments_kernel");
+  return LCRW_OK;
+}
+
+int lcrw_topk_rows(const float* d, int64_t ld, int64_t n_rows, int64_t row_len, int64_t id_base, int k,
+                   float* out_d, int64_t* out_i, void* stream) {
+  LCRW_REQUIRE(k >= 1, "k must be >= 1");
+  LCRW_REQUIRE(n_rows >= 0 && row_len >= 0 && ld >= row_len, "lcrw_topk_rows: bad shape");
+  if (n_rows == 0 || row_len == 0) return LCRW_OK;
+  if (k > 1024) {
+    set_error("lcrw_topk_rows: k=%d > 1024", k);
+    return LCRW_ERR_UNSUPPORTED;
+  }
+  LCRW_REQUIRE(d && out_d && out_i, "lcrw_topk_rows: null pointer");
+  LCRW_REQUIRE(n_rows < (1ll << 31), "lcrw_topk_rows: too many rows");
+  int kp = 1;
+  while (kp < k) kp <<= 1;
+  topk_segments_kernel<<<(unsigned)n_rows, kThreads, 0, as_stream(stream)>>>(d, nullptr, ld, row_len, id_base, k, kp,
+                                                                             out_d, out_i);
+  LCRW_CHECK_LAUNCH("topk_segments_kernel (rows)");
   return LCRW_OK;
 }
 

@@ -84,6 +84,7 @@ class DeviceCSR:
     n_cols: int
     host_offsets: np.ndarray
     host_cols: np.ndarray | None = None  # kept for small (query-side) sets: row-order planning
+    host_vals: np.ndarray | None = None
 
     @property
     def n_rows(self) -> int:
@@ -101,9 +102,10 @@ class DeviceCSR:
         if int(offs[0]) != 0 or len(x.column_ids) != int(offs[-1]) or len(x.values) != int(offs[-1]):
             raise CorpusError(f"{name}: offset/array length mismatch")
         cols = np.asarray(x.column_ids, dtype=np.int32)
-        return cls(to_device(offs, torch.int64), to_device(cols, torch.int32),
-                   to_device(x.values, torch.float32), int(x.n_cols), offs,
-                   cols if cols.size <= (1 << 22) else None)
+        vals = np.asarray(x.values, dtype=np.float32)
+        small = cols.size <= (1 << 22)
+        return cls(to_device(offs, torch.int64), to_device(cols, torch.int32), to_device(vals, torch.float32),
+                   int(x.n_cols), offs, cols if small else None, vals if small else None)
 
 
 class PreparedEmbeddings:
@@ -283,6 +285,7 @@ class Restricted:
     cols_r: torch.Tensor
     A: torch.Tensor
     a_norms: torch.Tensor
+    host_rank: np.ndarray | None = None  # host copy of remap (first-use order only)
 
     @classmethod
     def build(cls, x: DeviceCSR, prep: PreparedEmbeddings, first_use_order: bool = False) -> "Restricted":
@@ -300,9 +303,10 @@ class Restricted:
             remap = to_device(rank, torch.int32)
             v_e = len(order)
         else:
+            rank = None
             remap, used, v_e = restrict(x.cols, x.n_cols)
         A, an = gather_rows(prep, used, "A")
-        return cls(x, remap, used, v_e, remap_ids(x.cols, remap), A, an)
+        return cls(x, remap, used, v_e, remap_ids(x.cols, remap), A, an, rank)
 
 
 def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
@@ -332,7 +336,31 @@ def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR,
 
 
 REVERSE_Z2_BYTES = 4 << 30   # Z2 batch budget (docs per batch = budget / (4 * v_e2), multiple of 32)
-REVERSE_CHUNK_DOCS = 512     # docs per (query, chunk) top-k candidate list
+
+
+def query_entries(x: DeviceCSR, rank: np.ndarray, a_rows: int):
+    """Word-major entry list of the query CSR for lcrw_reverse_panels (include/lcrwmd.h).
+
+    Sorted by (query group, 256-row tile, owning warp, row, query); built on the
+    host from the (small) query set -- index planning, no arithmetic."""
+    T = int(_lib.value("lcrw_reverse_panels_tile_rows"))
+    G = int(_lib.value("lcrw_reverse_panels_group"))
+    W = int(_lib.value("lcrw_reverse_panels_warps"))
+    n_q = x.n_rows
+    n_tiles = (a_rows + T - 1) // T
+    n_groups = (n_q + G - 1) // G
+    q = np.repeat(np.arange(n_q, dtype=np.int64), np.diff(x.host_offsets))
+    r = rank[x.host_cols].astype(np.int64)
+    g, ql = q // G, q % G
+    t, rl, w = r // T, r % T, ql % W
+    order = np.lexsort((ql, r, w, t, g))
+    key = ((g * n_tiles + t) * W + w)[order]
+    counts = np.bincount(key, minlength=n_groups * n_tiles * W)
+    off = np.zeros(n_groups * n_tiles * W + 1, dtype=np.int32)
+    np.cumsum(counts, out=off[1:])
+    pack = ((rl << 16) | ql)[order].astype(np.uint32)
+    xv = x.host_vals[order].astype(np.float32)
+    return (to_device(pack.view(np.int32), torch.int32), to_device(xv, torch.float32), to_device(off, torch.int32))
 
 
 def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BYTES) -> int:
@@ -342,11 +370,10 @@ def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BY
 
 
 def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
-              z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0,
-              chunk_docs: int = REVERSE_CHUNK_DOCS):
+              z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0):
     """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, k) dists, ids).
 
-    ``d1`` (8-segment panels) may be supplied by a caller that computed the
+    ``d1`` (8-query panels) may be supplied by a caller that computed the
     forward direction itself (parallel.py); ``id_offset`` shifts returned doc ids."""
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
@@ -355,7 +382,10 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         res1 = Restricted.build(x1, prep)
         d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
         del res1
+    if x2.host_cols is None:
+        raise ValueError("query set too large for the host-planned reverse pass")
     res2 = Restricted.build(x2, prep, first_use_order=True)
+    e_pack, e_x, e_off = query_entries(x2, res2.host_rank, res2.v_e)
     batch = reverse_batch_docs(n1, res2.v_e, z2_budget_bytes)
     ho = x1.host_offsets
     max_words = max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
@@ -363,26 +393,27 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     _lib.call("lcrw_reverse_workspace", res2.v_e, prep.kp, batch, max_words, C.byref(ws_bytes))
     ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
     if k is None:
-        dout = torch.empty(n1 * n2, dtype=torch.float32, device=dev)
-        cand_d = cand_i = None
-        n_chunks = 0
+        D = torch.empty(n1 * n2, dtype=torch.float32, device=dev)  # reference orientation (n1, n2)
+        ld_q, ld_doc = 1, n2
     else:
-        if k > 32:
-            raise NotImplementedError("fused top-k supports k <= 32")
-        dout = None
-        n_chunks = int(_lib.value("lcrw_reverse_chunks", n1, batch, chunk_docs))
-        cand_d = torch.empty(n2 * n_chunks * k, dtype=torch.float32, device=dev)
-        cand_i = torch.empty(n2 * n_chunks * k, dtype=torch.int64, device=dev)
+        D = torch.empty(n2 * n1, dtype=torch.float32, device=dev)  # query-major for the per-query top-k
+        ld_q, ld_doc = n1, 1
     rep, nxt = prep.representatives(x1.cols)
     host_offs = np.ascontiguousarray(ho, dtype=np.int64)
-    _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), _p(prep.norms),
-              prep.k_eff, prep.kp, _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1,
-              _p(x1.cols), _p(rep), _p(nxt), _p(res2.remap), _p(x2.offsets), _p(res2.cols_r), _p(x2.vals), n2,
-              _p(d1), 8, 8 * n1, _p(dout), n2, k or 0, _p(cand_d), _p(cand_i), n_chunks, id_offset, batch,
-              chunk_docs, 0, _p(ws), ws_bytes.value, st)
+    _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), prep.k_eff, prep.kp,
+              _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
+              _p(nxt), _p(res2.remap), _p(e_pack), _p(e_x), _p(e_off), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
+              batch, 0, _p(ws), ws_bytes.value, st)
+    del ws
     if k is None:
-        return dout.view(n1, n2)
-    return topk_rows(cand_d, cand_i, n2, n_chunks * k, k)
+        return D.view(n1, n2)
+    if k > 1024:
+        raise NotImplementedError("k > 1024")
+    kk = min(k, n1)
+    out_d = torch.empty((n2, k), dtype=torch.float32, device=dev)
+    out_i = torch.empty((n2, k), dtype=torch.int64, device=dev)
+    _lib.call("lcrw_topk_rows", _p(D), n1, n2, n1, id_offset, k, _p(out_d), _p(out_i), st)
+    return out_d[:, :kk], out_i[:, :kk]
 
 
 def nearest_word_distances(E, Q) -> torch.Tensor:
