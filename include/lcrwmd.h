@@ -45,7 +45,7 @@ const char* lcrw_last_error(void);
 int lcrw_sm_count(int* out);
 
 /* Optional launch profiler (benchmarking): when enabled, instrumented launches
- * (phase1 / phase1_rev / spmm / reverse_max) are bracketed by CUDA events on
+ * (phase1 / phase1_rev / spmm / reverse_panels) are bracketed by CUDA events on
  * their stream; lcrw_profile_get waits for record i and returns its name and
  * elapsed milliseconds. */
 int lcrw_profile_reset(int enable);
@@ -134,20 +134,6 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
               int64_t z_panel, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
               int64_t ld_row, int64_t ld_panel, void* stream);
 
-/* Reverse direction + symmetric combine (distances.py:263-264): for queries q
- * (rows of the restricted query CSR) and local docs j < n_docs of a batch,
- * D2 = spmm(Xq, Z2) and D = max(D1[doc_base + j, q], D2).  D1 is addressed like
- * spmm's output (d1_ld_row, d1_ld_panel).  Either writes D[(doc_base+j) * ld_out
- * + q] (dout != NULL), or per (query, doc-chunk) top-k candidates into
- * cand_d/cand_i[(q * n_chunks_total + chunk_base + chunk) * k + r] with ids
- * id_offset + doc_base + j (id_offset = the shard's first global doc). */
-int lcrw_reverse_chunk_docs(void);
-int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
-                     const float* Z2, int64_t z_panel, int z_shift, int64_t n_docs, int64_t doc_base,
-                     int64_t id_offset, const float* D1, int64_t d1_ld_row, int64_t d1_ld_panel, float* dout,
-                     int64_t ld_out, int k, float* cand_d, int64_t* cand_i, int64_t n_chunks_total,
-                     int64_t chunk_base, int chunk_docs, void* stream);
-
 /* Reverse direction, panel-streaming form: one CTA per (32-doc Z2 panel, group
  * of lcrw_reverse_panels_group() queries) streams the panel's word rows through
  * shared memory in lcrw_reverse_panels_tile_rows()-row tiles and scatters the
@@ -175,7 +161,6 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
  * lcrw_reverse_panels).  Workspace from lcrw_reverse_workspace with
  * max_batch_words = max words over batches. */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
-int64_t lcrw_reverse_chunks(int64_t n_docs, int64_t batch_docs, int chunk_docs);
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,

@@ -46,11 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_phase1": (I32, [P, P, I64, P, I64, I32, I32, P, I64, I64, P, P, I64, P, P, I64, I32, P]),
     "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, I32, P]),
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P]),
-    "lcrw_reverse_chunk_docs": (I32, []),
-    "lcrw_reverse_max": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P, I64, I32, P, P, I64, I64,
-                               I32, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
-    "lcrw_reverse_chunks": (I64, [I64, I64, I32]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I32, I32, P, P, P, I64, P, P, P, P, P, P, P, I64, P, I64, P, I64,
                                     I64, I64, I32, P, SZ, P]),
     "lcrw_reverse_panels_tile_rows": (I32, []),
@@ -68,7 +64,7 @@ SIGNATURES: dict[str, tuple] = {
 
 # functions returning a value rather than a status
 _VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
-                "lcrw_endmask_words", "lcrw_plan_ranges", "lcrw_reverse_chunk_docs", "lcrw_reverse_chunks",
+                "lcrw_endmask_words", "lcrw_plan_ranges", 
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
                 "lcrw_profile_count"}
 
@@ -78,11 +74,11 @@ KERNELS_PER_CALL = {
     "lcrw_max_sqnorm": 1, "lcrw_scale_from_max_sqnorm": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
     "lcrw_row_classes": 13, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
-    "lcrw_reverse_max": 1, "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 1,
+    "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 1,
     "lcrw_reverse_panels": 1,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels);
-# bench.py adds those from the batch count (= its reverse_max launches).
+# bench.py adds those from the batch count (= its reverse_panels launches).
 REVERSE_KERNELS_PER_BATCH = 6
 
 CALLS: dict[str, int] = {}

@@ -1,6 +1,6 @@
 // Phase 2 of LC-RWMD (kernels.py:174-198 spmm, distances.py:203) and the
-// reverse direction's fused symmetric combine + per-query top-k
-// (distances.py:263-264, kernels.py:210-223).
+// reverse direction's Phase 2 with the fused symmetric combine
+// (distances.py:263-264); the per-query top-k over the result is in topk.cu.
 //
 // Both kernels read Z in the 8-segment panel layout written by Phase 1
 // (Z[(s>>3)*z_panel + row*8 + (s&7)]) so that a warp's lanes touch whole
@@ -14,7 +14,6 @@ namespace p2 {
 
 constexpr int kWarps = 8;
 constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
-constexpr int kDefaultChunkDocs = 256;  // reverse: docs per block (one candidate list per warp)
 
 // ---------------------------------------------------------------------------
 // CSR x panelled Z: one warp per CSR row, 4 consecutive segments per lane.
@@ -60,131 +59,6 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
   }
 }
-
-// ---------------------------------------------------------------------------
-// Reverse direction: D2[q, j] = sum_{w in q} x_qw Z2[j, w]; D = max(D1, D2).
-// Block = 8 warps = 8 queries; lanes walk the block's doc chunk.
-// ---------------------------------------------------------------------------
-template <int KMAX, int G>
-__global__ void __launch_bounds__(kWarps * 32, 3)
-    reverse_max_kernel(const int64_t* __restrict__ q_offs, const int32_t* __restrict__ q_cols,
-                       const float* __restrict__ q_vals, int64_t n_q, const float* __restrict__ Z2, int64_t z_panel,
-                       int64_t n_docs, int64_t doc_base, int64_t id_offset, const float* __restrict__ D1,
-                       int64_t d1_ld_row, int64_t d1_ld_panel, float* __restrict__ dout, int64_t ld_out, int k,
-                       float* __restrict__ cand_d, int64_t* __restrict__ cand_i, int64_t n_chunks_total,
-                       int64_t chunk_base, int chunk_docs) {
-  // Z2 in 32-doc panels: Z2[(j >> 5) * z_panel + (w << 5) + (j & 31)], so one
-  // (word, 32-doc group) is a single 128-byte line.  Each lane owns G doc groups
-  // (G * 32 docs per pass); the G line loads of the next nonzero are issued
-  // before the current one is accumulated.  grid: x = query panel (fastest),
-  // y = doc chunk, so resident blocks share one chunk whose Z2 panels stay in L2.
-  // Per-lane sorted candidate lists live in shared memory (column per lane, no
-  // bank conflicts); only the current k-th distance/id is kept in registers.
-  extern __shared__ float s_lists[];  // [kWarps][KMAX][32] distances, then [kWarps][KMAX][32] ids
-  const int lane = threadIdx.x & 31;
-  const int wrp = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * kWarps + wrp;
-  if (q >= n_q) return;  // warp-uniform; no block-level synchronisation below
-  const int64_t chunk = blockIdx.y;
-  const int64_t j_begin = chunk * chunk_docs;
-  const int64_t j_end = min(n_docs, j_begin + chunk_docs);
-  const int64_t lo = q_offs[q], hi = q_offs[q + 1];
-  const float* d1q = D1 + (q >> 3) * d1_ld_panel + (q & 7);
-  float (*kd)[32] = reinterpret_cast<float (*)[32]>(s_lists + wrp * KMAX * 32);
-  int32_t (*ki)[32] = reinterpret_cast<int32_t (*)[32]>(s_lists + (kWarps + wrp) * KMAX * 32);
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i) {
-    kd[i][lane] = __int_as_float(0x7f800000);
-    ki[i][lane] = 0x7fffffff;
-  }
-  float thr_d = __int_as_float(0x7f800000);
-  int32_t thr_i = 0x7fffffff;
-
-  for (int64_t jb = j_begin; jb < j_end; jb += 32 * G) {
-    double acc[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = 0.0;
-    const float* zb = Z2 + (jb >> 5) * z_panel + lane;
-    const int ng = (int)min((int64_t)G, (j_end - jb + 31) >> 5);  // doc groups present in this pass
-    for (int64_t base = lo; base < hi; base += 32) {
-      const int cnt = (int)min((int64_t)32, hi - base);
-      const int32_t my_w = lane < cnt ? __ldg(q_cols + base + lane) : 0;
-      const float my_x = lane < cnt ? __ldg(q_vals + base + lane) : 0.f;
-      float z[G];
-      {
-        const float* zw = zb + ((int64_t)__shfl_sync(0xffffffffu, my_w, 0) << 5);
-#pragma unroll
-        for (int g = 0; g < G; ++g) z[g] = g < ng ? __ldg(zw + g * z_panel) : 0.f;
-      }
-      for (int t = 0; t < cnt; ++t) {
-        float zn[G];
-        const int tn = t + 1 < cnt ? t + 1 : t;
-        const float* zw = zb + ((int64_t)__shfl_sync(0xffffffffu, my_w, tn) << 5);
-#pragma unroll
-        for (int g = 0; g < G; ++g) zn[g] = (g < ng && t + 1 < cnt) ? __ldg(zw + g * z_panel) : 0.f;
-        const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = fma(x, (double)z[g], acc[g]);
-#pragma unroll
-        for (int g = 0; g < G; ++g) z[g] = zn[g];
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t jl = jb + 32 * g + lane;
-      if (g < ng && jl < j_end) {
-        const int64_t jg = doc_base + jl;
-        const float d = fmaxf(__ldg(d1q + jg * d1_ld_row), (float)acc[g]);
-        if (dout) {
-          dout[jg * ld_out + q] = d;
-        } else if (d < thr_d || (d == thr_d && (int32_t)jg < thr_i)) {
-          // sorted insertion into this lane's smem list (rare once the list fills)
-          float cd = d;
-          int32_t ci = (int32_t)jg;
-          for (int i = 0; i < KMAX; ++i) {
-            const float od = kd[i][lane];
-            const int32_t oi = ki[i][lane];
-            if (cd < od || (cd == od && ci < oi)) {
-              kd[i][lane] = cd;
-              ki[i][lane] = ci;
-              cd = od;
-              ci = oi;
-            }
-          }
-          thr_d = kd[KMAX - 1][lane];
-          thr_i = ki[KMAX - 1][lane];
-        }
-      }
-    }
-  }
-  if (dout) return;
-
-  // warp-level merge of 32 sorted lane lists -> k smallest (distance, id)
-  const int64_t slot = (q * n_chunks_total + chunk_base + chunk) * (int64_t)k;
-  int head = 0;
-  for (int r = 0; r < k; ++r) {
-    const float hd = head < KMAX ? kd[head][lane] : __int_as_float(0x7f800000);
-    const int32_t hi_ = head < KMAX ? ki[head][lane] : 0x7fffffff;
-    float bd = hd;
-    int32_t bi = hi_;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float od = __shfl_xor_sync(0xffffffffu, bd, o);
-      const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (od < bd || (od == bd && oi < bi)) {
-        bd = od;
-        bi = oi;
-      }
-    }
-    if (hd == bd && hi_ == bi) ++head;
-    if (lane == 0) {
-      cand_d[slot + r] = bd;
-      cand_i[slot + r] = bi == 0x7fffffff ? INT64_MAX : (int64_t)bi + id_offset;
-    }
-  }
-}
-
-constexpr int list_smem(int kmax) { return 2 * kWarps * kmax * 32 * 4; }
 
 // ---------------------------------------------------------------------------
 // Reverse direction, panel-streaming form.  One CTA per (32-doc Z2 panel,
@@ -333,7 +207,6 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
   return LCRW_OK;
 }
 
-int lcrw_reverse_chunk_docs(void) { return kDefaultChunkDocs; }
 
 int lcrw_reverse_panels_tile_rows(void) { return kRpTile; }
 int lcrw_reverse_panels_group(void) { return kRpGroup; }
@@ -370,53 +243,6 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
   reverse_panels_kernel<<<dim3((unsigned)panels, (unsigned)groups), (kRpWarps + 1) * 32, smem, st>>>(
       Z2, z_panel, a_rows, n_docs, doc_base, e_pack, e_x, e_off, n_tiles, n_q, D1, d1_ld_panel, D, ld_q, ld_doc);
   LCRW_CHECK_LAUNCH("reverse_panels_kernel");
-  return LCRW_OK;
-}
-
-int lcrw_reverse_max(const int64_t* q_offs, const int32_t* q_cols, const float* q_vals, int64_t n_q,
-                     const float* Z2, int64_t z_panel, int z_shift, int64_t n_docs, int64_t doc_base, int64_t id_offset,
-                     const float* D1,
-                     int64_t d1_ld_row, int64_t d1_ld_panel, float* dout, int64_t ld_out, int k, float* cand_d,
-                     int64_t* cand_i, int64_t n_chunks_total, int64_t chunk_base, int chunk_docs, void* stream) {
-  LCRW_REQUIRE(n_q >= 0 && n_docs >= 0, "lcrw_reverse_max: bad shape");
-  if (n_q == 0 || n_docs == 0) return LCRW_OK;
-  LCRW_REQUIRE(q_offs && q_cols && q_vals && Z2 && D1, "lcrw_reverse_max: null pointer");
-  LCRW_REQUIRE(doc_base + n_docs < (1ll << 31), "lcrw_reverse_max: doc ids must fit in int32");
-  LCRW_REQUIRE(chunk_docs >= 32 && chunk_docs % 32 == 0, "lcrw_reverse_max: chunk_docs must be a positive multiple of 32");
-  const int64_t gx = ceil_div(n_q, kWarps);        // query panels
-  const int64_t gy = ceil_div(n_docs, chunk_docs);  // doc chunks
-  LCRW_REQUIRE(gy < 65536, "lcrw_reverse_max: too many doc chunks for one launch");
-  LCRW_REQUIRE(z_shift == 5, "lcrw_reverse_max: Z2 must use 32-segment panels (z_shift = 5)");
-  dim3 grid((unsigned)gx, (unsigned)gy);
-  cudaStream_t st = as_stream(stream);
-  ProfScope prof(st, "reverse_max");
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(reverse_max_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem(16));
-    cudaFuncSetAttribute(reverse_max_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, list_smem(32));
-    attrs = true;
-  }
-  if (dout) {
-    reverse_max_kernel<16, 8><<<grid, kWarps * 32, list_smem(16), st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs, doc_base,
-                                                         id_offset, D1, d1_ld_row, d1_ld_panel, dout, ld_out, 0, nullptr,
-                                                         nullptr, 0, 0, chunk_docs);
-  } else {
-    LCRW_REQUIRE(k >= 1 && cand_d && cand_i, "lcrw_reverse_max: top-k mode needs k >= 1 and candidate buffers");
-    LCRW_REQUIRE(chunk_base + gy <= n_chunks_total, "lcrw_reverse_max: chunk_base + chunks > n_chunks_total");
-    if (k <= 16) {
-      reverse_max_kernel<16, 8><<<grid, kWarps * 32, list_smem(16), st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
-                                                           doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
-                                                           cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
-    } else if (k <= 32) {
-      reverse_max_kernel<32, 8><<<grid, kWarps * 32, list_smem(32), st>>>(q_offs, q_cols, q_vals, n_q, Z2, z_panel, n_docs,
-                                                           doc_base, id_offset, D1, d1_ld_row, d1_ld_panel, nullptr, 0, k,
-                                                           cand_d, cand_i, n_chunks_total, chunk_base, chunk_docs);
-    } else {
-      set_error("lcrw_reverse_max: fused top-k supports k <= 32 (got %d); use the full-matrix path", k);
-      return LCRW_ERR_UNSUPPORTED;
-    }
-  }
-  LCRW_CHECK_LAUNCH("reverse_max_kernel");
   return LCRW_OK;
 }
 

@@ -63,16 +63,6 @@ int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t m
   return LCRW_OK;
 }
 
-int64_t lcrw_reverse_chunks(int64_t n_docs, int64_t batch_docs, int chunk_docs) {
-  if (n_docs < 0 || batch_docs <= 0 || chunk_docs <= 0) return -1;
-  int64_t n = 0;
-  for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
-    const int64_t nd = (n_docs - j0) < batch_docs ? (n_docs - j0) : batch_docs;
-    n += ceil_div(nd, chunk_docs);
-  }
-  return n;
-}
-
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,

@@ -292,8 +292,9 @@ class Restricted:
         """Restriction of ``x`` to its own words.  With ``first_use_order`` the
         restricted rows are numbered by first appearance in x's CSR instead of by
         ascending word id: any row order gives identical values (the reference's
-        restricted ids only name rows), and this one makes each row of x touch a
-        nearly contiguous block of Z rows (DRAM-friendly gathers in reverse_max)."""
+        restricted ids only name rows), and this one keeps each row of x's words
+        in a nearly contiguous block of Z rows (its entries cluster in few
+        lcrw_reverse_panels tiles)."""
         if first_use_order and x.host_cols is not None:
             words, first = np.unique(x.host_cols, return_index=True)
             order = words[np.argsort(first, kind="stable")].astype(np.int32)
