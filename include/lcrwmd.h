@@ -159,14 +159,17 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
  * doc_offsets (batch planning); doc_cols are global E ids, rep/next/remap as in
  * lcrw_zero_identical.  Writes D = max(D1, D2) for all docs (see
  * lcrw_reverse_panels).  Workspace from lcrw_reverse_workspace with
- * max_batch_words = max words over batches. */
+ * max_batch_words = max words over batches.  d1_ready (cudaEvent_t or NULL):
+ * the stream waits on it before the first read of D1, so the forward direction
+ * can run concurrently on another stream with the reverse Phase 1. */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_pack, const float* e_x, const int32_t* e_off,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, void* ws, size_t ws_bytes, void* stream);
+                          int64_t batch_docs, int range_cols, void* d1_ready, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k

@@ -48,7 +48,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I32, I32, P, P, P, I64, P, P, P, P, P, P, P, I64, P, I64, P, I64,
-                                    I64, I64, I32, P, SZ, P]),
+                                    I64, I64, I32, P, P, SZ, P]),
     "lcrw_reverse_panels_tile_rows": (I32, []),
     "lcrw_reverse_panels_group": (I32, []),
     "lcrw_reverse_panels_warps": (I32, []),

@@ -68,7 +68,8 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_pack, const float* e_x, const int32_t* e_off,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, void* ws, size_t ws_bytes, void* stream) {
+                          int64_t batch_docs, int range_cols, void* d1_ready, void* ws, size_t ws_bytes,
+                          void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
   LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && rep && ws && D, "lcrw_reverse_pipeline: null pointer");
@@ -103,6 +104,10 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;
+    if (j0 == 0 && d1_ready) {  // D1 may still be in flight on another stream (forward direction)
+      cudaError_t e = cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d1_ready), 0);
+      if (e != cudaSuccess) return cuda_status(e, "cudaStreamWaitEvent (D1 ready)");
+    }
     if ((status = lcrw_reverse_panels(Z2, z_panel, a_rows, nd, j0, e_pack, e_x, e_off, n_q, D1, d1_ld_panel, D, ld_q,
                                       ld_doc, stream)))
       return status;

@@ -379,6 +379,7 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
     st = _stream()
+    d1_ready = None  # (a side-stream forward pass measured slower: persistent kernels contend for SMs)
     if d1 is None:
         res1 = Restricted.build(x1, prep)
         d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
@@ -404,7 +405,8 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), prep.k_eff, prep.kp,
               _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
               _p(nxt), _p(res2.remap), _p(e_pack), _p(e_x), _p(e_off), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
-              batch, 0, _p(ws), ws_bytes.value, st)
+              batch, 0, C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value,
+              st)
     del ws
     if k is None:
         return D.view(n1, n2)
