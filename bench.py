@@ -250,6 +250,8 @@ def run_ours(args, cfg):
             dist.destroy_process_group()
         return
     pk, pk_kind = peaks()
+    tpath = ROOT / "profiles" / "roofline_traffic.json"
+    traffic = json.loads(tpath.read_text())["dram_bytes_per_launch"] if tpath.exists() and args.config == "c2" else None
     rev = ksum.get("phase1_rev", {"ms": float("nan"), "launches": 1})
     per_launch_ms = rev["ms"] / max(rev["launches"], 1)
     # algorithmic FLOPs of the reverse Phase 1 per step: 2 * v_e2 * (doc words) * m, K = m unpadded
@@ -276,7 +278,8 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": d2h, "api": "paper_1711_07227_b200.distances.lcrwmd_topk (pinned host arrays)"},
         "roofline": {"kernel": "phase1_kernel (reverse direction, tcgen05 f16 GEMM + fused segmented min)",
                      "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak_tf, "traffic": None,
+                     "frac": achieved_tf / peak_tf, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/roofline_traffic.json)",
                      "peak_source": f"{pk_kind} bf16_tflops_sustained (dense f16 = bf16 rate)",
                      "per_launch_ms": per_launch_ms, "launches_per_step": rev["launches"] / args.steps,
                      "share_of_step": rev["ms"] / args.steps / ms},
@@ -335,7 +338,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-docs", type=int, default=96)
+    ap.add_argument("--ref-docs", type=int, default=1024,
+                    help="resident docs per reference-arm step (x all queries)")
     ap.add_argument("--z2-mb", type=int, default=4096, help="reverse Z2 batch budget (MiB)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU code path (NCCL process group) even with one rank")
