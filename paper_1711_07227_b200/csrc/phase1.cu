@@ -52,7 +52,7 @@ constexpr int kMmaWarp = kEpiWarps + 1;       // 9
 constexpr int kAllocWarp = kEpiWarps + 2;     // 10
 constexpr int kThreads = 32 * (kEpiWarps + 3);
 constexpr uint32_t kIdesc = umma_idesc_f16(2 * BM, BN);
-constexpr int kMaxKb = 7;                     // m <= 448
+constexpr int kMaxKb = 8;                     // operand K <= 512 (m <= 509 with the 3 norm columns)
 
 struct Params {
   const float* a_norms;
@@ -570,10 +570,12 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
                "lcrw_phase1: operands must be 16-byte aligned");
   const int n_kb = kp / BK;
   if (n_kb > kMaxKb) {
-    set_error("lcrw_phase1: embedding dimension %d > %d unsupported", m, kMaxKb * BK);
+    set_error("lcrw_phase1: operand K = %d (embedding dimension + 3 norm columns) > %d unsupported", m,
+              kMaxKb * BK);
     return LCRW_ERR_UNSUPPORTED;
   }
-  const int stages = n_kb <= 5 ? 8 : 6;
+  // A K-blocks + B stages within ~208 KB of shared memory
+  const int stages = n_kb <= 5 ? 8 : 13 - n_kb;
   Params p;
   p.a_norms = a_norms;
   p.endmask = endmask;
@@ -601,7 +603,9 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   const size_t smem = smem_bytes(n_kb, stages);
   static bool attr_set = false;
   if (!attr_set) {
-    const size_t mx = smem_bytes(kMaxKb, 6) > smem_bytes(5, 8) ? smem_bytes(kMaxKb, 6) : smem_bytes(5, 8);
+    size_t mx = smem_bytes(5, 8);
+    for (int kb = 6; kb <= kMaxKb; ++kb)
+      if (smem_bytes(kb, 13 - kb) > mx) mx = smem_bytes(kb, 13 - kb);
     cudaError_t e = cudaFuncSetAttribute(phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(phase1_kernel)");
     attr_set = true;

@@ -279,3 +279,89 @@ def test_c2_full_size_sampled_parity():
                               torch.arange(1_000_000, device=full.device).repeat(1000, 1).contiguous(),
                               1000, 1_000_000, 10)
     assert torch.equal(td, fd) and torch.equal(ti, fi)
+
+
+# --- edge cases ----------------------------------------------------------------
+
+def _rand_set(rng, n, V, lo, hi):
+    from paper_1711_07227_b200.corpus import HistogramSet
+    rows = []
+    for _ in range(n):
+        h = int(rng.integers(lo, hi + 1))
+        ids = np.sort(rng.choice(V, size=min(h, V), replace=False)).astype(np.int32)
+        u = rng.random(len(ids)) + 0.1
+        rows.append((ids, (u / u.sum()).astype(np.float32)))
+    return HistogramSet.from_rows(rows, V)
+
+
+def test_k_larger_than_docs_and_single_rows():
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(41)
+    E = rng.standard_normal((60, 300)).astype(np.float32)
+    x1 = _rand_set(rng, 5, 60, 1, 9)
+    x2 = _rand_set(rng, 3, 60, 1, 9)
+    ref = O.lcrwmd_full(x1, x2, E)
+    res = D.lcrwmd_topk(x1, x2, E, 10)
+    assert all(len(r.ids) == 5 for r in res)
+    _check_topk([r.distances for r in res], [r.ids for r in res], ref, 10)
+    one = D.lcrwmd_full(x1.slice_rows(0, 1), x2.slice_rows(0, 1), E).values
+    ok, err = rel_close(one, ref[:1, :1], RTOL, ATOL)
+    assert ok, err
+
+
+def test_very_long_segments_cross_tiles_and_ranges():
+    """Docs of up to 3000 words: Phase-1 segments span many 256-column tiles and
+    exceed the column-range size, exercising the carried running minimum."""
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(42)
+    V = 6000
+    E = rng.standard_normal((V, 300)).astype(np.float32)
+    x1 = _rand_set(rng, 40, V, 1, 3000)
+    x2 = _rand_set(rng, 6, V, 500, 2500)
+    ref = O.lcrwmd_full(x1, x2, E, threads=8)
+    got = D.lcrwmd_full(x1, x2, E).values
+    ok, err = rel_close(got, ref, RTOL, ATOL)
+    assert ok, err
+    qv = E[rng.choice(V, 1500, replace=False)]
+    ok, err = rel_close(D.nearest_word_distances(E, qv), O.nearest_word_distances(E, qv), RTOL, 1e-4)
+    assert ok, err
+
+
+def test_many_queries_multiple_groups():
+    """More than 1024 queries: the reverse pass splits queries into groups."""
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(43)
+    V = 2000
+    E = rng.standard_normal((V, 64)).astype(np.float32)
+    x1 = _rand_set(rng, 300, V, 5, 40)
+    x2 = _rand_set(rng, 1500, V, 5, 40)
+    ref = O.lcrwmd_full(x1, x2, E, threads=8)
+    got = D.lcrwmd_full(x1, x2, E).values
+    ok, err = rel_close(got, ref, RTOL, 1e-5 * float(np.sqrt((E.astype(np.float64) ** 2).sum(1).max())))
+    assert ok, err
+    res = D.lcrwmd_topk(x1, x2, E, 7)
+    _check_topk([r.distances for r in res], [r.ids for r in res], ref, 7,
+                1e-5 * float(np.sqrt((E.astype(np.float64) ** 2).sum(1).max())))
+
+
+@pytest.mark.parametrize("m", [1, 448, 509])
+def test_dimension_extremes(m):
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(44 + m)
+    V = 400
+    E = rng.standard_normal((V, m)).astype(np.float32)
+    x1 = _rand_set(rng, 30, V, 1, 20)
+    x2 = _rand_set(rng, 5, V, 1, 20)
+    ref = O.lcrwmd_full(x1, x2, E)
+    got = D.lcrwmd_full(x1, x2, E).values
+    ok, err = rel_close(got, ref, RTOL, _atol(E))
+    assert ok, (m, err)
+
+
+def test_dimension_too_large_is_reported():
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(45)
+    E = rng.standard_normal((50, 510)).astype(np.float32)
+    x1 = _rand_set(rng, 4, 50, 1, 5)
+    with pytest.raises(NotImplementedError, match="unsupported"):
+        D.lcrwmd_full(x1, x1, E)
