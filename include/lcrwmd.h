@@ -134,23 +134,32 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
               int64_t z_panel, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
               int64_t ld_row, int64_t ld_panel, void* stream);
 
-/* Reverse direction, panel-streaming form: one CTA per (32-doc Z2 panel, group
- * of lcrw_reverse_panels_group() queries) streams the panel's word rows through
- * shared memory in lcrw_reverse_panels_tile_rows()-row tiles and scatters the
- * query nonzeros (a word-major list, see below) into fp32 per-query
- * accumulators; writes D[q * ld_q + (doc_base + j) * ld_doc] = max(D1, D2) for
- * the batch's docs j < n_docs.  D1 in 8-query panels (d1_ld_panel = 8 * n1).
- * Entry list: for each query group g, tile t (rows [t*T, t*T+T)) and warp w,
- * entries e_off[(g*n_tiles + t)*W + w] .. +1 (W = lcrw_reverse_panels_warps()),
- * each e_pack = (row - t*T) << 16 | (q - g*G) with weight e_x; a warp owns the
- * queries with (q - g*G) % W == w, so accumulation order is deterministic. */
+/* Reverse direction, panel-streaming form: work item = (32-doc Z2 panel, group
+ * of G = lcrw_reverse_panels_group() queries); persistent CTAs stream each
+ * panel's word rows through shared memory in T = lcrw_reverse_panels_tile_rows()
+ * row tiles and scatter the query nonzeros (the plan below) into fp32
+ * per-query accumulators; writes D[q * ld_q + (doc_base + j) * ld_doc] =
+ * max(D1, D2) for the batch's docs j < n_docs.  D1 in 8-query panels
+ * (d1_ld_panel = 8 * n1).
+ * Plan (replaces the word-major traversal of distances.py:203 for the
+ * reverse sets): for each query group g and tile t (rows [t*T, t*T+T)) one
+ * block of 32-bit words at e_blk + e_tile[g*n_tiles + t] (16-byte aligned,
+ * e_tile has n_groups*n_tiles + 1 entries, the last = total words):
+ *   W = lcrw_reverse_panels_warps() list ends (entries, cumulative), then the
+ *   entries, two words each: ((row - t*T) * 128 << 18 | (q - g*G) * 128, bits of x)
+ *   (byte offsets of the Z2 tile row and of the query's accumulator row).
+ * Warp w's list is entries [end[w-1], end[w]); a warp owns the queries with
+ * (q - g*G) % W == w, so accumulation order is deterministic.  Every list
+ * holds a multiple of I = lcrw_reverse_panels_ilp() entries and each aligned
+ * group of I entries names I distinct queries; padding entries use query G
+ * (a scratch row) with weight 0. */
 int lcrw_reverse_panels_tile_rows(void);
 int lcrw_reverse_panels_group(void);
 int lcrw_reverse_panels_warps(void);
+int lcrw_reverse_panels_ilp(void);
 int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs, int64_t doc_base,
-                        const uint32_t* e_pack, const float* e_x, const int32_t* e_off, int64_t n_q,
-                        const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                        void* stream);
+                        const uint32_t* e_blk, const int64_t* e_tile, int64_t n_q, const float* D1,
+                        int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, void* stream);
 
 /* Whole reverse direction in one call (distances.py:263-264): docs in batches
  * of batch_docs (multiple of 32); per batch gather -> segment plan ->
@@ -166,7 +175,7 @@ int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t m
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
-                          const int32_t* remap, const uint32_t* e_pack, const float* e_x, const int32_t* e_off,
+                          const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
                           int64_t batch_docs, int range_cols, void* d1_ready, void* ws, size_t ws_bytes,
                           void* stream);

@@ -47,12 +47,13 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, I32, P]),
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
-    "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I32, I32, P, P, P, I64, P, P, P, P, P, P, P, I64, P, I64, P, I64,
+    "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
                                     I64, I64, I32, P, P, SZ, P]),
     "lcrw_reverse_panels_tile_rows": (I32, []),
     "lcrw_reverse_panels_group": (I32, []),
     "lcrw_reverse_panels_warps": (I32, []),
-    "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, P, I64, P, I64, P, I64, I64, P]),
+    "lcrw_reverse_panels_ilp": (I32, []),
+    "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, I64, P, I64, P, I64, I64, P]),
     "lcrw_topk_rows": (I32, [P, I64, I64, I64, I64, I32, P, P, P]),
     "lcrw_profile_reset": (I32, [I32]),
     "lcrw_profile_count": (I64, []),
@@ -66,7 +67,7 @@ SIGNATURES: dict[str, tuple] = {
 _VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
                 "lcrw_endmask_words", "lcrw_plan_ranges", 
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
-                "lcrw_profile_count"}
+                "lcrw_reverse_panels_ilp",                 "lcrw_profile_count"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".

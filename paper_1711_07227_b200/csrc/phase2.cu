@@ -61,40 +61,48 @@ __global__ void __launch_bounds__(kWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
-// Reverse direction, panel-streaming form.  One CTA per (32-doc Z2 panel,
-// group of <= 1024 queries): the panel's word rows are streamed through shared
-// memory in 256-row tiles (cp.async, sequential 32 KB reads -- each Z2 byte is
-// read from HBM once), and a word-major list of the query nonzeros scatters
-// x * Z2[w, 32 docs] into per-query fp32 accumulators in shared memory.  Each
-// query is owned by one warp (q % 16), so accumulation order is fixed (tile,
-// then row): results are deterministic.  The symmetric combine max(D1, D2) is
-// written query-major (128-byte rows) for the final per-query top-k.
+// Reverse direction, panel-streaming form.  Work item = (32-doc Z2 panel,
+// group of <= 1024 queries); persistent CTAs (one per SM) loop over items.
+// A producer warp streams each panel's word rows through a ring of 16 KB
+// shared-memory tiles with 1-D TMA bulk copies -- each Z2 byte is read from
+// HBM once, with an L2 prefetch running kRpAhead tiles ahead of the ring --
+// and, into the same stage, the tile's block of the query plan (per-warp list
+// ends + entries).  16 consumer warps scatter the entries, x * Z2[w, 32 docs],
+// into per-query fp32 accumulators in shared memory.  Each query is owned by
+// one warp ((q - q0) % 16), so its accumulation order is fixed by the plan:
+// results are deterministic.  The plan packs every (tile, warp) list into
+// groups of four entries of distinct queries, so a group's four accumulator
+// read-modify-writes are independent and issue back to back.  The symmetric
+// combine max(D1, D2) is written query-major (128-byte rows) for the
+// per-query top-k.
 // ---------------------------------------------------------------------------
-constexpr int kRpWarps = 16;   // consumer warps (+1 producer warp)
-constexpr int kRpTile = 128;   // Z2 rows per staged tile (16 KB)
-constexpr int kRpStages = 4;
-constexpr int kRpGroup = 1024; // queries per CTA
+constexpr int kRpWarps = 16;     // consumer warps (+1 producer warp)
+constexpr int kRpTile = 128;     // Z2 rows per staged tile (16 KB)
+constexpr int kRpStages = 5;
+constexpr int kRpGroup = 1024;   // queries per work item
+constexpr int kRpIlp = 4;        // entries per independent group (plan invariant)
+constexpr int kRpBlkWords = 512;   // staged plan block per tile: 16 list ends + up to 248 entries (2 KB)
+constexpr int kRpBlkEntries = (kRpBlkWords - kRpWarps) / 2;
+constexpr int kRpAhead = 8;      // L2 prefetch distance (tiles)
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 
 __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
     reverse_panels_kernel(const float* __restrict__ Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs,
-                          int64_t doc_base, const uint32_t* __restrict__ e_pack, const float* __restrict__ e_x,
-                          const int32_t* __restrict__ e_off, int n_tiles, int64_t n_q, const float* __restrict__ D1,
-                          int64_t d1_ld_panel, float* __restrict__ D, int64_t ld_q, int64_t ld_doc) {
+                          int64_t doc_base, const uint32_t* __restrict__ e_blk, const int64_t* __restrict__ e_tile,
+                          int n_tiles, int64_t n_q, const float* __restrict__ D1, int64_t d1_ld_panel,
+                          float* __restrict__ D, int64_t ld_q, int64_t ld_doc, int64_t n_panels, int64_t n_items) {
   extern __shared__ __align__(16) float rp_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t p = blockIdx.x;
-  const int g = blockIdx.y;
-  const int64_t q0 = (int64_t)g * kRpGroup;
-  const int nq = (int)min((int64_t)kRpGroup, n_q - q0);
-  float* acc = rp_smem;                                              // [kRpGroup][32]
-  float* tiles = rp_smem + (size_t)kRpGroup * 32;                    // [kRpStages][kRpTile][32]
-  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + kRpStages * kRpTile * 32);
+  float* acc = rp_smem;                                                  // [kRpGroup + 1][32] (+1: padding row)
+  float* tiles = acc + (kRpGroup + 1) * 32;                              // [kRpStages][kRpTile][32]
+  uint32_t* blks = reinterpret_cast<uint32_t*>(tiles + kRpStages * kRpTile * 32);  // [kRpStages][kRpBlkWords]
+  uint64_t* full = reinterpret_cast<uint64_t*>(blks + kRpStages * kRpBlkWords);
   uint64_t* empty = full + kRpStages;
-  int32_t* offs = reinterpret_cast<int32_t*>(empty + kRpStages);    // [n_tiles * W + 1]
-  const int32_t* goff = e_off + (int64_t)g * n_tiles * kRpWarps;
-  for (int i = threadIdx.x; i <= n_tiles * kRpWarps; i += blockDim.x) offs[i] = __ldg(goff + i);
-  for (int i = threadIdx.x; i < nq * 32; i += blockDim.x) acc[i] = 0.f;
+  for (int i = threadIdx.x; i < (kRpGroup + 1) * 32; i += blockDim.x) acc[i] = 0.f;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRpStages; ++i) {
       mbar_init(full + i, 1);
@@ -103,77 +111,132 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  const float* zp = Z2 + p * z_panel;
 
   if (warp == kRpWarps) {
-    // ---- producer: stream the panel's rows, kRpStages tiles ahead ----
-    if (lane == 0) {
-      for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % kRpStages;
-        mbar_wait(empty + st, ((t / kRpStages) & 1) ^ 1);
-        const int64_t r0 = (int64_t)t * kRpTile;
-        const uint32_t bytes = (uint32_t)min((int64_t)kRpTile, a_rows - r0) * 128u;
-        mbar_expect_tx(full + st, bytes);
-        bulk_load(tiles + st * kRpTile * 32, zp + r0 * 32, bytes, full + st);
+    // ---- producer warp: lane 0 issues, the lanes fetch plan offsets 32 tiles at a time ----
+    uint32_t it = 0;
+    int64_t pf_item = blockIdx.x;  // L2 prefetch cursor (item, tile), kRpAhead tiles ahead
+    int pf_t = 0;
+    auto prefetch_next = [&]() {
+      if (pf_item >= n_items) return;
+      const int64_t r0 = (int64_t)pf_t * kRpTile;
+      const uint32_t bytes = (uint32_t)min((int64_t)kRpTile, a_rows - r0) * 128u;
+      if (lane == 0) bulk_prefetch_l2(Z2 + (pf_item % n_panels) * z_panel + r0 * 32, bytes);
+      if (++pf_t == n_tiles) {
+        pf_t = 0;
+        pf_item += gridDim.x;
+      }
+    };
+    for (int i = 0; i < kRpAhead; ++i) prefetch_next();
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int64_t p = item % n_panels;
+      const int64_t g = item / n_panels;
+      const float* zp = Z2 + p * z_panel;
+      const int64_t* tb = e_tile + g * n_tiles;
+      // D1 lines of this item, needed by the consumers' combine at the end
+      {
+        const int64_t q0 = g * kRpGroup;
+        const int nqp = (int)((min((int64_t)kRpGroup, n_q - q0) + 7) / 8);
+        const int64_t j0 = doc_base + p * 32;
+        const uint32_t dbytes = (uint32_t)min((int64_t)32, n_docs - p * 32) * 32u;
+        for (int qp = lane; qp < nqp; qp += 32) bulk_prefetch_l2(D1 + ((q0 >> 3) + qp) * d1_ld_panel + j0 * 8, dbytes);
+      }
+      int64_t b_lo = 0, b_hi = 0;
+      for (int t = 0; t < n_tiles; ++t, ++it) {
+        if ((t & 31) == 0) {  // plan block offsets of tiles t .. t+32
+          const int n = min(33, n_tiles + 1 - t);
+          b_lo = lane < n ? __ldg(tb + t + lane) : 0;
+          b_hi = lane == 0 && n == 33 ? __ldg(tb + t + 32) : 0;  // the 33rd offset
+        }
+        const int64_t blk0 = __shfl_sync(0xffffffffu, b_lo, t & 31);
+        const int64_t blk1 = (t & 31) == 31 ? __shfl_sync(0xffffffffu, b_hi, 0)
+                                            : __shfl_sync(0xffffffffu, b_lo, (t & 31) + 1);
+        const uint32_t st = it % kRpStages;
+        mbar_wait(empty + st, ((it / kRpStages) & 1) ^ 1);
+        if (lane == 0) {
+          const int64_t r0 = (int64_t)t * kRpTile;
+          const uint32_t zbytes = (uint32_t)min((int64_t)kRpTile, a_rows - r0) * 128u;
+          const uint32_t bbytes = (uint32_t)min((int64_t)kRpBlkWords, blk1 - blk0) * 4u;
+          mbar_expect_tx(full + st, zbytes + bbytes);
+          bulk_load(tiles + st * kRpTile * 32, zp + r0 * 32, zbytes, full + st);
+          bulk_load(blks + st * kRpBlkWords, e_blk + blk0, bbytes, full + st);
+        }
+        prefetch_next();
+        __syncwarp();
       }
     }
-  } else {
-    // ---- consumers: scatter this warp's query nonzeros of each tile ----
-    int e0 = offs[warp], e1 = offs[warp + 1];
-    uint32_t pre_p = lane < e1 - e0 ? __ldg(e_pack + e0 + lane) : 0u;
-    float pre_x = lane < e1 - e0 ? __ldg(e_x + e0 + lane) : 0.f;
-    for (int t = 0; t < n_tiles; ++t) {
-      const int st = t % kRpStages;
-      // next tile's entry window and first 32 entries (latency hidden behind this tile)
-      const int ne0 = t + 1 < n_tiles ? offs[(t + 1) * kRpWarps + warp] : 0;
-      const int ne1 = t + 1 < n_tiles ? offs[(t + 1) * kRpWarps + warp + 1] : 0;
-      const uint32_t nxt_p = lane < ne1 - ne0 ? __ldg(e_pack + ne0 + lane) : 0u;
-      const float nxt_x = lane < ne1 - ne0 ? __ldg(e_x + ne0 + lane) : 0.f;
-      mbar_wait(full + st, (t / kRpStages) & 1);
+    return;
+  }
+
+  // ---- consumers ----
+  uint32_t it = 0;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int64_t p = item % n_panels;
+    const int64_t g = item / n_panels;
+    const int64_t q0 = g * kRpGroup;
+    const int nq = (int)min((int64_t)kRpGroup, n_q - q0);
+    for (int t = 0; t < n_tiles; ++t, ++it) {
+      const uint32_t st = it % kRpStages;
+      mbar_wait(full + st, (it / kRpStages) & 1);
       const float* tile = tiles + st * kRpTile * 32;
-      uint32_t cur_p = pre_p;
-      float cur_x = pre_x;
-      for (int eb = e0; eb < e1; eb += 32) {
-        if (eb != e0) {  // rare: more than 32 entries for this (tile, warp)
-          cur_p = lane < e1 - eb ? __ldg(e_pack + eb + lane) : 0u;
-          cur_x = lane < e1 - eb ? __ldg(e_x + eb + lane) : 0.f;
+      const uint32_t* blk = blks + st * kRpBlkWords;
+      const int e0 = warp ? (int)blk[warp - 1] : 0;
+      const int e1 = (int)blk[warp];
+      const uint4* ent = reinterpret_cast<const uint4*>(blk + kRpWarps);  // 2 entries per uint4
+      const char* tile_lane = reinterpret_cast<const char*>(tile + lane);
+      char* acc_lane = reinterpret_cast<char*>(acc + lane);
+      // entry word: (row * 128) << 18 | query * 128 -- byte offsets of the tile row and accumulator row
+      auto scatter = [&](uint4 ab, uint4 cd) {
+        const uint32_t pk[kRpIlp] = {ab.x, ab.z, cd.x, cd.z};
+        const float x[kRpIlp] = {__uint_as_float(ab.y), __uint_as_float(ab.w), __uint_as_float(cd.y),
+                                 __uint_as_float(cd.w)};
+        float* a[kRpIlp];
+        float z[kRpIlp], v[kRpIlp];
+#pragma unroll
+        for (int j = 0; j < kRpIlp; ++j) {
+          a[j] = reinterpret_cast<float*>(acc_lane + (pk[j] & 0x3FFFFu));
+          z[j] = *reinterpret_cast<const float*>(tile_lane + (pk[j] >> 18));
+          v[j] = *a[j];
         }
-        const int cnt = min(32, e1 - eb);
-        for (int i = 0; i < cnt; ++i) {
-          const uint32_t pk = __shfl_sync(0xffffffffu, cur_p, i);
-          const float x = __shfl_sync(0xffffffffu, cur_x, i);
-          float* a = acc + (pk & 0xFFFFu) * 32 + lane;
-          *a = fmaf(x, tile[(pk >> 16) * 32 + lane], *a);
-        }
+#pragma unroll
+        for (int j = 0; j < kRpIlp; ++j) *a[j] = fmaf(x[j], z[j], v[j]);
+      };
+      const int e_mid = min(e1, kRpBlkEntries / kRpIlp * kRpIlp);
+      int i = e0;
+      for (; i < e_mid; i += kRpIlp) scatter(ent[i >> 1], ent[(i >> 1) + 1]);
+      if (i < e1) {  // rare: the tile's plan block exceeds the staged part; the rest comes from global
+        const uint4* gent = reinterpret_cast<const uint4*>(e_blk + __ldg(e_tile + g * n_tiles + t) + kRpWarps);
+        for (; i < e1; i += kRpIlp) scatter(__ldg(gent + (i >> 1)), __ldg(gent + (i >> 1) + 1));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st);
-      e0 = ne0;
-      e1 = ne1;
-      pre_p = nxt_p;
-      pre_x = nxt_x;
     }
-  }
-  __syncthreads();
+    named_bar_sync(1, kRpWarps * 32);  // all scatters of this item are in acc
 
-  // symmetric combine with D1 (8-query panels: D1[(q >> 3) * ld_panel + j * 8 + (q & 7)])
-  const int64_t j = p * 32 + lane;
-  const bool valid = j < n_docs;
-  const int64_t jg = doc_base + j;
-  for (int qp = warp; qp * 8 < nq; qp += kRpWarps + 1) {
-    const int64_t qg = q0 + qp * 8;
-    float d1v[8];
-    if (valid) {
-      const float4* src = reinterpret_cast<const float4*>(D1 + (qg >> 3) * d1_ld_panel + jg * 8);
-      const float4 a = __ldg(src), b = __ldg(src + 1);
-      d1v[0] = a.x; d1v[1] = a.y; d1v[2] = a.z; d1v[3] = a.w;
-      d1v[4] = b.x; d1v[5] = b.y; d1v[6] = b.z; d1v[7] = b.w;
-    }
+    // symmetric combine with D1 (8-query panels: D1[(q >> 3) * ld_panel + j * 8 + (q & 7)]); re-zero acc
+    const int64_t j = p * 32 + lane;
+    const bool valid = j < n_docs;
+    const int64_t jg = doc_base + j;
+    for (int qp = warp; qp * 8 < nq; qp += kRpWarps) {
+      const int64_t qg = q0 + qp * 8;
+      float d1v[8];
+      if (valid) {
+        const float4* src = reinterpret_cast<const float4*>(D1 + (qg >> 3) * d1_ld_panel + jg * 8);
+        const float4 lo4 = __ldg(src), hi4 = __ldg(src + 1);
+        d1v[0] = lo4.x; d1v[1] = lo4.y; d1v[2] = lo4.z; d1v[3] = lo4.w;
+        d1v[4] = hi4.x; d1v[5] = hi4.y; d1v[6] = hi4.z; d1v[7] = hi4.w;
+      }
 #pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      const int ql = qp * 8 + qq;
-      if (valid && ql < nq) D[(qg + qq) * ld_q + jg * ld_doc] = fmaxf(d1v[qq], acc[ql * 32 + lane]);
+      for (int qq = 0; qq < 8; ++qq) {
+        const int ql = qp * 8 + qq;
+        if (ql < nq) {
+          float* a = acc + ql * 32 + lane;
+          if (valid) D[(qg + qq) * ld_q + jg * ld_doc] = fmaxf(d1v[qq], *a);
+          *a = 0.f;
+        }
+      }
     }
+    named_bar_sync(1, kRpWarps * 32);  // acc is zero again before the next item's scatter
   }
 }
 
@@ -211,37 +274,35 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
 int lcrw_reverse_panels_tile_rows(void) { return kRpTile; }
 int lcrw_reverse_panels_group(void) { return kRpGroup; }
 int lcrw_reverse_panels_warps(void) { return kRpWarps; }
+int lcrw_reverse_panels_ilp(void) { return kRpIlp; }
 
 int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs, int64_t doc_base,
-                        const uint32_t* e_pack, const float* e_x, const int32_t* e_off, int64_t n_q,
-                        const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                        void* stream) {
+                        const uint32_t* e_blk, const int64_t* e_tile, int64_t n_q, const float* D1,
+                        int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, void* stream) {
   LCRW_REQUIRE(n_q >= 0 && n_docs >= 0 && a_rows >= 0, "lcrw_reverse_panels: bad shape");
   if (n_q == 0 || n_docs == 0) return LCRW_OK;
-  LCRW_REQUIRE(Z2 && e_pack && e_x && e_off && D1 && D, "lcrw_reverse_panels: null pointer");
-  LCRW_REQUIRE(z_panel == a_rows * 32 && (reinterpret_cast<uintptr_t>(Z2) & 15) == 0,
-               "lcrw_reverse_panels: Z2 must be 16-byte aligned 32-doc panels (z_panel = 32 * a_rows)");
-  const int n_tiles = (int)ceil_div(a_rows, kRpTile);
+  LCRW_REQUIRE(Z2 && e_blk && e_tile && D1 && D, "lcrw_reverse_panels: null pointer");
+  LCRW_REQUIRE(z_panel == a_rows * 32 && (reinterpret_cast<uintptr_t>(Z2) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(e_blk) & 15) == 0 && (reinterpret_cast<uintptr_t>(D1) & 15) == 0,
+               "lcrw_reverse_panels: Z2 (32-doc panels, z_panel = 32 * a_rows), e_blk and D1 must be 16-byte aligned");
+  const int64_t n_tiles = ceil_div(a_rows, kRpTile);
   const int64_t panels = ceil_div(n_docs, 32);
   const int64_t groups = ceil_div(n_q, kRpGroup);
-  LCRW_REQUIRE(panels < (1ll << 31) && groups < 65536, "lcrw_reverse_panels: grid too large");
-  const int fixed = (kRpGroup * 32 + kRpStages * kRpTile * 32) * 4 + 2 * kRpStages * 8;
-  const int smem = fixed + (n_tiles * kRpWarps + 1) * 4;
-  const int smem_max = 227 * 1024;
-  if (smem > smem_max) {
-    set_error("lcrw_reverse_panels: query vocabulary of %lld rows needs %d B of shared memory", (long long)a_rows, smem);
-    return LCRW_ERR_UNSUPPORTED;
-  }
+  LCRW_REQUIRE(n_tiles < (1 << 30), "lcrw_reverse_panels: query vocabulary too large");
+  const int smem = ((kRpGroup + 1) * 32 + kRpStages * kRpTile * 32 + kRpStages * kRpBlkWords) * 4 + 2 * kRpStages * 8;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(reverse_panels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaError_t e = cudaFuncSetAttribute(reverse_panels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(reverse_panels_kernel)");
     attr = true;
   }
+  const int64_t items = panels * groups;
+  const int64_t grid = items < sm_count() ? items : sm_count();
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "reverse_panels");
-  reverse_panels_kernel<<<dim3((unsigned)panels, (unsigned)groups), (kRpWarps + 1) * 32, smem, st>>>(
-      Z2, z_panel, a_rows, n_docs, doc_base, e_pack, e_x, e_off, n_tiles, n_q, D1, d1_ld_panel, D, ld_q, ld_doc);
+  reverse_panels_kernel<<<(unsigned)grid, (kRpWarps + 1) * 32, smem, st>>>(
+      Z2, z_panel, a_rows, n_docs, doc_base, e_blk, e_tile, (int)n_tiles, n_q, D1, d1_ld_panel, D, ld_q, ld_doc,
+      panels, items);
   LCRW_CHECK_LAUNCH("reverse_panels_kernel");
   return LCRW_OK;
 }

@@ -66,7 +66,7 @@ int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t m
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
-                          const int32_t* remap, const uint32_t* e_pack, const float* e_x, const int32_t* e_off,
+                          const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
                           int64_t batch_docs, int range_cols, void* d1_ready, void* ws, size_t ws_bytes,
                           void* stream) {
@@ -108,7 +108,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
       cudaError_t e = cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d1_ready), 0);
       if (e != cudaSuccess) return cuda_status(e, "cudaStreamWaitEvent (D1 ready)");
     }
-    if ((status = lcrw_reverse_panels(Z2, z_panel, a_rows, nd, j0, e_pack, e_x, e_off, n_q, D1, d1_ld_panel, D, ld_q,
+    if ((status = lcrw_reverse_panels(Z2, z_panel, a_rows, nd, j0, e_blk, e_tile, n_q, D1, d1_ld_panel, D, ld_q,
                                       ld_doc, stream)))
       return status;
   }

@@ -285,19 +285,18 @@ class Restricted:
     cols_r: torch.Tensor
     A: torch.Tensor
     a_norms: torch.Tensor
-    host_rank: np.ndarray | None = None  # host copy of remap (first-use order only)
+    host_rank: np.ndarray | None = None  # host copy of remap (host_plan only)
 
     @classmethod
-    def build(cls, x: DeviceCSR, prep: PreparedEmbeddings, first_use_order: bool = False) -> "Restricted":
-        """Restriction of ``x`` to its own words.  With ``first_use_order`` the
-        restricted rows are numbered by first appearance in x's CSR instead of by
-        ascending word id: any row order gives identical values (the reference's
-        restricted ids only name rows), and this one keeps each row of x's words
-        in a nearly contiguous block of Z rows (its entries cluster in few
-        lcrw_reverse_panels tiles)."""
-        if first_use_order and x.host_cols is not None:
-            words, first = np.unique(x.host_cols, return_index=True)
-            order = words[np.argsort(first, kind="stable")].astype(np.int32)
+    def build(cls, x: DeviceCSR, prep: PreparedEmbeddings, host_plan: bool = False) -> "Restricted":
+        """Restriction of ``x`` to its own words (ascending word id, as
+        corpus.py:417).  With ``host_plan`` the restriction is computed from the
+        host copy of x's ids (a small query set) so that the remap is also
+        available on the host for planning lcrw_reverse_panels.  Ascending ids
+        scatter each query's words over the Z2 tiles, which balances the
+        per-(tile, warp) entry lists of that kernel."""
+        if host_plan and x.host_cols is not None:
+            order = np.unique(x.host_cols).astype(np.int32)
             rank = np.full(x.n_cols, -1, dtype=np.int32)
             rank[order] = np.arange(len(order), dtype=np.int32)
             used = to_device(order, torch.int32)
@@ -340,28 +339,74 @@ REVERSE_Z2_BYTES = 4 << 30   # Z2 batch budget (docs per batch = budget / (4 * v
 
 
 def query_entries(x: DeviceCSR, rank: np.ndarray, a_rows: int):
-    """Word-major entry list of the query CSR for lcrw_reverse_panels (include/lcrwmd.h).
+    """Device copy of plan_query_entries for x (host ids of a DeviceCSR): (e_blk, e_tile)."""
+    blk, tile = plan_query_entries(x.host_offsets, x.host_cols, x.host_vals, rank, a_rows, *reverse_panels_geometry())
+    return to_device(blk.view(np.int32), torch.int32), to_device(tile, torch.int64)
 
-    Sorted by (query group, 256-row tile, owning warp, row, query); built on the
-    host from the (small) query set -- index planning, no arithmetic."""
-    T = int(_lib.value("lcrw_reverse_panels_tile_rows"))
-    G = int(_lib.value("lcrw_reverse_panels_group"))
-    W = int(_lib.value("lcrw_reverse_panels_warps"))
-    n_q = x.n_rows
+
+def reverse_panels_geometry() -> tuple[int, int, int, int]:
+    """(tile rows T, query group G, warps W, group size I) of lcrw_reverse_panels."""
+    return tuple(int(_lib.value(f"lcrw_reverse_panels_{n}")) for n in ("tile_rows", "group", "warps", "ilp"))
+
+
+def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, rank: np.ndarray, a_rows: int,
+                       T: int, G: int, W: int, I: int):
+    """Word-major plan of the query CSR for lcrw_reverse_panels (include/lcrwmd.h).
+
+    One block of uint32 words per (query group, T-row tile): W cumulative list
+    ends, then the entries (two words: (row - t*T) << 16 | (q - g*G), bits of
+    x) of the W per-warp lists (warp = local query % W).  Each list is laid out
+    in groups of I entries naming distinct queries: its entries, sorted by
+    (query, row), fill G_l = max(ceil(n/I), max multiplicity of a query) groups
+    column-major (entry i -> group i % G_l, slot i // G_l), so repeated queries
+    land in distinct groups; empty slots are padding (scratch query G, weight
+    0).  Returns (blocks uint32, block word offsets int64 [n_groups*n_tiles+1]).
+    Built on the host from the (small) query set -- index planning, no
+    arithmetic."""
+    if T > 128 or G > 1024:
+        raise ValueError("plan encoding holds rows < 128 and queries <= 1024")
+    n_q = len(offsets) - 1
     n_tiles = (a_rows + T - 1) // T
     n_groups = (n_q + G - 1) // G
-    q = np.repeat(np.arange(n_q, dtype=np.int64), np.diff(x.host_offsets))
-    r = rank[x.host_cols].astype(np.int64)
+    n_lists = n_groups * n_tiles * W
+    q = np.repeat(np.arange(n_q, dtype=np.int64), np.diff(offsets))
+    r = rank[cols].astype(np.int64)
     g, ql = q // G, q % G
     t, rl, w = r // T, r % T, ql % W
-    order = np.lexsort((ql, r, w, t, g))
-    key = ((g * n_tiles + t) * W + w)[order]
-    counts = np.bincount(key, minlength=n_groups * n_tiles * W)
-    off = np.zeros(n_groups * n_tiles * W + 1, dtype=np.int32)
-    np.cumsum(counts, out=off[1:])
-    pack = ((rl << 16) | ql)[order].astype(np.uint32)
-    xv = x.host_vals[order].astype(np.float32)
-    return (to_device(pack.view(np.int32), torch.int32), to_device(xv, torch.float32), to_device(off, torch.int32))
+    key = (g * n_tiles + t) * W + w
+    order = np.lexsort((rl, ql, key))
+    key, ql, rl = key[order], ql[order], rl[order]
+    xv = np.asarray(vals)[order].astype(np.float32)
+    n = np.bincount(key, minlength=n_lists)
+    start = np.zeros(n_lists + 1, dtype=np.int64)
+    np.cumsum(n, out=start[1:])
+    idx = np.arange(key.size, dtype=np.int64) - start[key]           # position inside its list
+    new_run = np.ones(key.size, dtype=bool)                          # (list, query) runs -> max multiplicity
+    new_run[1:] = (key[1:] != key[:-1]) | (ql[1:] != ql[:-1])
+    run_len = np.bincount(np.cumsum(new_run) - 1)
+    mult = np.zeros(n_lists, dtype=np.int64)
+    np.maximum.at(mult, key[new_run], run_len)
+    groups = np.maximum((n + I - 1) // I, mult)
+    lens = (groups * I).reshape(n_groups * n_tiles, W)               # padded list lengths (entries)
+    ends = np.cumsum(lens, axis=1)                                   # per-block cumulative list ends
+    blk_words = W + 2 * ends[:, -1]
+    blk_words = (blk_words + 3) // 4 * 4                             # 16-byte aligned blocks
+    tile_off = np.zeros(n_groups * n_tiles + 1, dtype=np.int64)
+    np.cumsum(blk_words, out=tile_off[1:])
+    words = np.zeros(tile_off[-1], dtype=np.uint32)
+    hdr = tile_off[:-1, None] + np.arange(W)
+    words[hdr.ravel()] = ends.ravel().astype(np.uint32)
+    list_start = np.zeros(n_lists, dtype=np.int64)                   # first entry of each list inside its block
+    list_start.reshape(-1, W)[:, 1:] = ends[:, :-1]
+    ent_base = tile_off[:-1].repeat(W) + W + 2 * list_start          # word offset of each list's first entry
+    # every slot starts as padding (scratch query G, weight 0), then the real entries
+    flat = lens.ravel()
+    pos = np.arange(flat.sum(), dtype=np.int64) - np.repeat(np.cumsum(flat) - flat, flat)
+    words[np.repeat(ent_base, flat) + 2 * pos] = np.uint32(G * 128)
+    slot = ent_base[key] + 2 * ((idx % groups[key]) * I + idx // groups[key])
+    words[slot] = (((rl * 128) << 18) | (ql * 128)).astype(np.uint32)
+    words[slot + 1] = xv.view(np.uint32)
+    return words, tile_off
 
 
 def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BYTES) -> int:
@@ -386,8 +431,8 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         del res1
     if x2.host_cols is None:
         raise ValueError("query set too large for the host-planned reverse pass")
-    res2 = Restricted.build(x2, prep, first_use_order=True)
-    e_pack, e_x, e_off = query_entries(x2, res2.host_rank, res2.v_e)
+    res2 = Restricted.build(x2, prep, host_plan=True)
+    e_blk, e_tile = query_entries(x2, res2.host_rank, res2.v_e)
     batch = reverse_batch_docs(n1, res2.v_e, z2_budget_bytes)
     ho = x1.host_offsets
     max_words = max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
@@ -404,7 +449,7 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     host_offs = np.ascontiguousarray(ho, dtype=np.int64)
     _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), prep.k_eff, prep.kp,
               _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
-              _p(nxt), _p(res2.remap), _p(e_pack), _p(e_x), _p(e_off), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
+              _p(nxt), _p(res2.remap), _p(e_blk), _p(e_tile), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
               batch, 0, C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value,
               st)
     del ws

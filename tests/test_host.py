@@ -124,3 +124,48 @@ def test_no_oracle_import_in_product():
     """The product package must never import the test oracle."""
     for p in (ROOT / "paper_1711_07227_b200").rglob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", p.read_text(), re.M), p
+
+
+@pytest.mark.parametrize("n_q,h,V", [(1000, 50, 100_000), (70, 300, 2000), (2100, 20, 5000), (3, 1, 10)])
+def test_reverse_entry_plan_invariants(n_q, h, V):
+    """lcrw_reverse_panels plan (include/lcrwmd.h): 16-byte aligned blocks per (group,
+    tile), W cumulative list ends, every nonzero exactly once in its (group, tile,
+    warp) list, lists a multiple of I long, each aligned group of I names distinct
+    queries, padding = scratch query G with weight 0."""
+    from paper_1711_07227_b200.device import plan_query_entries
+    T, G, W, I = 128, 1024, 16, 4
+    x = S.histograms(n_q, V, h, seed=7)
+    offs, cols, vals = np.asarray(x.row_offsets), np.asarray(x.column_ids), np.asarray(x.values)
+    used = np.unique(cols)
+    rank = np.full(V, -1, np.int32)
+    rank[used] = np.arange(len(used))
+    words, tile_off = plan_query_entries(offs, cols, vals, rank, len(used), T, G, W, I)
+    n_tiles = (len(used) + T - 1) // T
+    n_groups = (n_q + G - 1) // G
+    assert tile_off.shape == (n_groups * n_tiles + 1,) and tile_off[0] == 0 and tile_off[-1] == words.size
+    assert np.all(tile_off % 4 == 0)
+    seen = []
+    for B in range(n_groups * n_tiles):
+        g, t = divmod(B, n_tiles)
+        blk = words[tile_off[B]:tile_off[B + 1]]
+        ends = blk[:W].astype(np.int64)
+        assert np.all(np.diff(np.concatenate([[0], ends])) % I == 0)
+        assert W + 2 * ends[-1] <= blk.size < W + 2 * ends[-1] + 4
+        ent = blk[W:W + 2 * ends[-1]].reshape(-1, 2)
+        for w in range(W):
+            lo = ends[w - 1] if w else 0
+            for b in range(lo, ends[w], I):
+                qs = ((ent[b:b + I, 0] & 0x3FFFF) >> 7).astype(np.int64)
+                real = qs != G
+                assert len(set(qs[real].tolist())) == int(real.sum())
+                assert np.all(ent[b:b + I, 1][~real] == 0)
+                for e in range(b, b + I):
+                    if not real[e - b]:
+                        continue
+                    assert ent[e, 0] & 0x7F == 0 and (ent[e, 0] >> 18) & 0x7F == 0
+                    ql, rl = int((ent[e, 0] & 0x3FFFF) >> 7), int(ent[e, 0] >> 25)
+                    assert ql % W == w and rl < T
+                    seen.append((g * G + ql, t * T + rl, float(ent[e, 1:2].view(np.float32)[0])))
+    q = np.repeat(np.arange(n_q), np.diff(offs))
+    want = sorted(zip(q.tolist(), rank[cols].tolist(), vals.astype(np.float32).tolist()))
+    assert sorted(seen) == want
