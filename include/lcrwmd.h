@@ -127,11 +127,13 @@ int lcrw_zero_identical(const int64_t* seg_offsets, int64_t n_seg, const int32_t
 /* ---- Phase 2 (kernels.py:174-198 spmm/spmv; distances.py:203) -----------
  * out[i, s] = sum_p x[i, p] * Z[s, col[i, p]] in fp64, rounded once to f32,
  * for s < n_seg; out addressed out[i * ld_row + (s >> 3) * ld_panel + (s & 7)].
+ * Z in (1 << z_shift)-segment panels, 2 <= z_shift <= 7 (lcrw_phase1 layout):
+ * Z[s, w] = Z[(s >> z_shift) * z_panel + (w << z_shift) + (s & mask)].
  * Z may be split into vocabulary blocks of z_block_rows rows (the multi-GPU
  * all-gather of per-rank Phase-1 slices): row w lives at block w / z_block_rows,
  * z_block_stride floats apart; z_block_rows <= 0 means one block. */
 int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
-              int64_t z_panel, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
+              int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
               int64_t ld_row, int64_t ld_panel, void* stream);
 
 /* Reverse direction, panel-streaming form: work item = (32-doc Z2 panel, group

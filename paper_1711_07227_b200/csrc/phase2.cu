@@ -17,15 +17,18 @@ constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
 
 // ---------------------------------------------------------------------------
 // CSR x panelled Z: one warp per CSR row, 4 consecutive segments per lane.
+// Z holds (1 << zs)-segment panels (2 <= zs <= 7): with zs = 7 a warp's 128
+// segments of one word row are one contiguous 512-byte run (four 128-byte
+// lines per nonzero), with zs = 3 they are 16 separate 32-byte sectors.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarps * 32)
     spmm_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ cols, const float* __restrict__ vals,
-                int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int64_t z_block_rows,
+                int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int zs, int64_t z_block_rows,
                 int64_t z_block_stride, int64_t n_seg, float* __restrict__ out, int64_t ld_row, int64_t ld_panel) {
   const int lane = threadIdx.x & 31;
   const int64_t q0 = (int64_t)blockIdx.y * kSegPerBlock + lane * 4;
   const bool active = q0 < n_seg;
-  const float* zq = Z + (q0 >> 3) * z_panel + (q0 & 7);
+  const float* zq = Z + (q0 >> zs) * z_panel + (q0 & ((1 << zs) - 1));
   const uint32_t zbr = (uint32_t)min(z_block_rows, (int64_t)0xFFFFFFFF);
   for (int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); i < n_rows; i += (int64_t)gridDim.x * kWarps) {
     const int64_t lo = offs[i], hi = offs[i + 1];
@@ -36,7 +39,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       const float my_x = lane < cnt ? __ldg(vals + base + lane) : 0.f;
       // vocabulary-sliced Z (multi-GPU all-gather): row w lives in block w / z_block_rows
       const uint32_t blk = my_c / zbr;
-      const int64_t my_off = (int64_t)blk * z_block_stride + (int64_t)(my_c - blk * zbr) * 8;
+      const int64_t my_off = (int64_t)blk * z_block_stride + ((int64_t)(my_c - blk * zbr) << zs);
       for (int t = 0; t < cnt; ++t) {
         const int64_t zoff = __shfl_sync(0xffffffffu, my_off, t);
         const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
@@ -203,7 +206,13 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
       };
       const int e_mid = min(e1, kRpBlkEntries / kRpIlp * kRpIlp);
       int i = e0;
-      for (; i < e_mid; i += kRpIlp) scatter(ent[i >> 1], ent[(i >> 1) + 1]);
+      {
+        const uint4* ep = ent + (e0 >> 1);
+        const uint4* const ep_end = ent + (max(e0, e_mid) >> 1);
+#pragma unroll 2
+        for (; ep < ep_end; ep += 2) scatter(ep[0], ep[1]);
+        i = max(e0, e_mid);
+      }
       if (i < e1) {  // rare: the tile's plan block exceeds the staged part; the rest comes from global
         const uint4* gent = reinterpret_cast<const uint4*>(e_blk + __ldg(e_tile + g * n_tiles + t) + kRpWarps);
         for (; i < e1; i += kRpIlp) scatter(__ldg(gent + (i >> 1)), __ldg(gent + (i >> 1) + 1));
@@ -250,13 +259,14 @@ using namespace lcrw::p2;
 extern "C" {
 
 int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
-              int64_t z_panel, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
+              int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
               int64_t ld_row, int64_t ld_panel, void* stream) {
   LCRW_REQUIRE(n_rows >= 0 && n_seg >= 0, "lcrw_spmm: bad shape");
   if (n_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(offs && cols && vals && Z && out, "lcrw_spmm: null pointer");
-  LCRW_REQUIRE(z_panel % 8 == 0 && z_block_stride % 8 == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0,
-               "lcrw_spmm: Z must be 16-byte aligned with z_panel, z_block_stride % 8 == 0");
+  LCRW_REQUIRE(z_shift >= 2 && z_shift <= 7, "lcrw_spmm: z_shift must be in [2, 7]");
+  LCRW_REQUIRE(z_panel % 4 == 0 && z_block_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0,
+               "lcrw_spmm: Z must be 16-byte aligned with z_panel, z_block_stride % 4 == 0");
   if (z_block_rows <= 0) z_block_rows = INT64_MAX;
   const int64_t gy = ceil_div(n_seg, kSegPerBlock);
   LCRW_REQUIRE(gy < 65536, "lcrw_spmm: too many segments for one launch");
@@ -265,7 +275,7 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
   if (gx > cap) gx = cap;
   ProfScope prof(as_stream(stream), "spmm");
   spmm_kernel<<<dim3((unsigned)gx, (unsigned)gy), kWarps * 32, 0, as_stream(stream)>>>(
-      offs, cols, vals, n_rows, Z, z_panel, z_block_rows, z_block_stride, n_seg, out, ld_row, ld_panel);
+      offs, cols, vals, n_rows, Z, z_panel, z_shift, z_block_rows, z_block_stride, n_seg, out, ld_row, ld_panel);
   LCRW_CHECK_LAUNCH("spmm_kernel");
   return LCRW_OK;
 }

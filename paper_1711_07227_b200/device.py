@@ -218,10 +218,17 @@ def _range_cols(b_rows: int, a_rows: int) -> int:
     return int(min(32768, max(1024, (want + 255) // 256 * 256)))
 
 
+def spmm_z_shift(n_seg: int) -> int:
+    """Panel width (log2) of a Z read by lcrw_spmm: 128-segment panels make each
+    nonzero's Z row one contiguous 512-byte run; small segment counts keep 8."""
+    return 7 if n_seg > 64 else 3
+
+
 def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
            b_rows: int, seg_offsets: torch.Tensor, n_seg: int, prep: PreparedEmbeddings,
-           range_cols: int | None = None) -> tuple[torch.Tensor, int]:
-    """Z (8-segment panels, z_panel = 8 * a_rows) of distances.py:147-178, without the exact-zero pass."""
+           range_cols: int | None = None, z_shift: int = 3) -> tuple[torch.Tensor, int]:
+    """Z ((1 << z_shift)-segment panels, z_panel = a_rows << z_shift) of distances.py:147-178,
+    without the exact-zero pass."""
     dev = A.device
     st = _stream()
     rc = range_cols or _range_cols(b_rows, a_rows)
@@ -229,11 +236,12 @@ def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
     endmask = torch.empty(int(_lib.value("lcrw_endmask_words", b_rows)), dtype=torch.int32, device=dev)
     range_seg = torch.empty(n_ranges + 1, dtype=torch.int32, device=dev)
     _lib.call("lcrw_segment_plan", _p(seg_offsets), 0, n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
-    z_panel = 8 * max(a_rows, 1)
-    Z = torch.empty(((n_seg + 7) // 8) * z_panel, dtype=torch.float32, device=dev)
+    w = 1 << z_shift
+    z_panel = w * max(a_rows, 1)
+    Z = torch.empty(((n_seg + w - 1) // w) * z_panel, dtype=torch.float32, device=dev)
     _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), b_rows, prep.k_eff, prep.kp,
-              _p(seg_offsets), 0, n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel, 3,
-              st)
+              _p(seg_offsets), 0, n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel,
+              z_shift, st)
     return Z, z_panel
 
 
@@ -243,8 +251,8 @@ def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel, z_shift: int
 
 
 def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel,
-         z_block_rows: int = 0, z_block_stride: int = 0) -> None:
-    _lib.call("lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, z_block_rows,
+         z_block_rows: int = 0, z_block_stride: int = 0, z_shift: int = 3) -> None:
+    _lib.call("lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, z_shift, z_block_rows,
               z_block_stride, n_seg, _p(out), ld_row, ld_panel, _stream())
 
 
@@ -310,12 +318,12 @@ class Restricted:
 
 
 def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
-                      n_seg: int) -> tuple[torch.Tensor, int]:
+                      n_seg: int, z_shift: int = 3) -> tuple[torch.Tensor, int]:
     """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros)."""
     B, _ = gather_rows(prep, word_ids, "B")
-    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, word_ids.numel(), seg_offsets, n_seg, prep)
+    Z, zp = phase1(res.A, res.a_norms, res.v_e, B, word_ids.numel(), seg_offsets, n_seg, prep, z_shift=z_shift)
     rep, nxt = prep.representatives(word_ids)
-    zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp)
+    zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp, z_shift)
     return Z, zp
 
 
@@ -324,14 +332,15 @@ def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR,
 
     layout "rows" -> row-major (n_res, n_q); "panels" -> out[(q>>3)*8*n_res + i*8 + (q&7)]."""
     n_res, n_q = res.csr.n_rows, queries.n_rows
-    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q)
+    zs = spmm_z_shift(n_q)
+    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q, zs)
     if layout == "rows":
         out = torch.empty(n_res * max(n_q, 1), dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = n_q, 8
     else:
         out = torch.empty(((n_q + 7) // 8) * 8 * n_res, dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = 8, 8 * n_res
-    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel)
+    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel, z_shift=zs)
     return out
 
 

@@ -7,7 +7,7 @@ contiguous shards + topk_merge):
   E, X2 and the query batch are replicated;
 * forward Phase 1: rank r computes Z1 for its vocabulary slice
   [r*R, (r+1)*R) of the full vocabulary, R = ceil(V / world), and the slices
-  are all-gathered over NVLink (NCCL) into [world][panels][R][8]; the SpMM of
+  are all-gathered over NVLink (NCCL) into [world][panels][R][W]; the SpMM of
   the local doc shard reads it through the blocked addressing of lcrw_spmm;
 * reverse direction (the dominant cost): fully local -- each rank's docs are
   the "queries" of the reverse pass against the replicated X2;
@@ -79,31 +79,37 @@ def gather_candidates(d: torch.Tensor, i: torch.Tensor, group=None):
 # ---------------------------------------------------------------------------
 
 def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) -> tuple[torch.Tensor, int]:
-    """This rank's forward Phase-1 slice: Z1 rows [v0, v1) as (panels, R, 8), zero padded."""
+    """This rank's forward Phase-1 slice: Z1 rows [v0, v1) as (panels, R, W), zero padded,
+    W = 1 << device.spmm_z_shift(n_q) segments per panel."""
     n_q = dx2.n_rows
     v0, v1, R = vocab_slice(prep.V, rank, world)
     rows = v1 - v0
     dev = dx2.cols.device
-    panels = (n_q + 7) // 8
-    zl = torch.zeros((panels, R, 8), dtype=torch.float32, device=dev)
+    zs = device.spmm_z_shift(n_q)
+    W = 1 << zs
+    panels = (n_q + W - 1) // W
+    zl = torch.zeros((panels, R, W), dtype=torch.float32, device=dev)
     if rows > 0:
         B, _ = device.gather_rows(prep, dx2.cols, "B")
-        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, dx2.nnz, dx2.offsets, n_q, prep)
+        Z, zp = device.phase1(prep.EhA[v0:v1], prep.norms[v0:v1], rows, B, dx2.nnz, dx2.offsets, n_q, prep,
+                              z_shift=zs)
         remap = torch.full((prep.V,), -1, dtype=torch.int32, device=dev)
         remap[v0:v1] = torch.arange(rows, dtype=torch.int32, device=dev)
         rep, nxt = prep.representatives(dx2.cols)
-        device.zero_identical(dx2.offsets, n_q, rep, nxt, remap, Z, zp)
-        zl[:, :rows, :] = Z.view(panels, rows, 8)
+        device.zero_identical(dx2.offsets, n_q, rep, nxt, remap, Z, zp, zs)
+        zl[:, :rows, :] = Z.view(panels, rows, W)
     return zl, R
 
 
 def d1_from_slices(dx1: DeviceCSR, zall: torch.Tensor, R: int, n_q: int) -> torch.Tensor:
-    """Forward SpMM of the local shard against all-gathered slices [world][panels][R][8]."""
+    """Forward SpMM of the local shard against all-gathered slices [world][panels][R][W]."""
     n1 = dx1.n_rows
-    panels = (n_q + 7) // 8
-    out = torch.empty(panels * 8 * max(n1, 1), dtype=torch.float32, device=zall.device)
-    device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, 8 * R, n_q, out, 8, 8 * n1,
-                z_block_rows=R, z_block_stride=panels * R * 8)
+    W = zall.shape[-1]
+    zs = W.bit_length() - 1
+    panels = zall.shape[1]
+    out = torch.empty(((n_q + 7) // 8) * 8 * max(n1, 1), dtype=torch.float32, device=zall.device)
+    device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, W * R, n_q, out, 8, 8 * n1,
+                z_block_rows=R, z_block_stride=panels * R * W, z_shift=zs)
     return out
 
 
@@ -111,7 +117,7 @@ def forward_d1(dx1: DeviceCSR, dx2: DeviceCSR, prep: PreparedEmbeddings, group=N
     """D1 (panels, local docs) with Phase 1 split by vocabulary slice + Z1 all-gather."""
     rank, world = _world()
     zl, R = z1_slice(dx2, prep, rank, world)
-    zall = allgather_slices(zl, group)  # [world][panels][R][8]
+    zall = allgather_slices(zl, group)  # [world][panels][R][W]
     return d1_from_slices(dx1, zall, R, dx2.n_rows)
 
 
