@@ -18,21 +18,25 @@
 // reads and L2->SM TMA bytes) relative to a single-CTA M = 128 tile and doubles
 // the MMA time each staged byte covers.
 //
-// Work unit = (pair of 128-row m-tiles, column range of ~range_cols B rows
-// bounded by segment boundaries).  Segments may straddle N tiles: the running
-// minimum is carried in registers across the tiles of a unit, and ranges never
-// cut a segment, so every Z entry is written exactly once (no atomics, no
-// initialisation pass).
+// Work unit = (pair of 128-row m-tiles, two consecutive column ranges of
+// ~range_cols B rows each, bounded by segment boundaries).  The two ranges of a
+// unit ("halves") are interleaved tile by tile and each owns one of the two TMEM
+// accumulator buffers: half h's tiles always land in buffer h and are reduced by
+// epilogue warp group h, so a segment's running minimum never leaves the
+// registers of the warp that reduces it (ranges never cut a segment), every Z
+// entry is written exactly once, and there is no atomic, initialisation pass
+// or cross-warp hand-off.
 //
 // Warp roles (352 threads per CTA): w0..w7 epilogue (TMEM lane quarter = warp % 4,
-// column half = warp / 4, one A row per thread), w8 TMA producer, w9 MMA issuer
-// (leader CTA only), w10 TMEM allocator.
+// accumulator buffer / unit half = warp / 4, one A row per thread), w8 TMA
+// producer, w9 MMA issuer (leader CTA only), w10 TMEM allocator.
 #include <cstdio>
 
 #include "common.cuh"
 
 #ifndef LCRW_EPI_MODE
-#define LCRW_EPI_MODE 0  // experiment switch: 1 = skip segment minima, 2 = also skip TMEM loads
+#define LCRW_EPI_MODE 0  // experiment switch: 1 = skip segment minima, 2 = also skip TMEM loads,
+                         // 3 = also no B traffic, 5 = minima but no Z stores
 #endif
 
 namespace lcrw {
@@ -44,7 +48,7 @@ constexpr int BN_HALF = BN / 2;
 constexpr int BK = 64;                        // f16 elements per K block (128 B rows)
 constexpr int A_KB_BYTES = BM * BK * 2;       // 16 KB
 constexpr int B_STAGE_BYTES = BN_HALF * BK * 2;  // 16 KB per CTA
-constexpr int kEpiWarps = 8;                  // two per TMEM lane quarter: each owns one 128-column half
+constexpr int kEpiWarps = 8;                  // two groups (accumulator buffers) x four TMEM lane quarters
 // Warp roles.  The schedulers favour higher warp ids, so the single-lane TMA and
 // MMA issuers sit above the epilogue warps and are never starved by them.
 constexpr int kProducerWarp = kEpiWarps;      // 8
@@ -67,7 +71,7 @@ struct Params {
   int z_shift;       // Z panel width = 1 << z_shift segments
   int a_rows;
   int n_mpairs;      // 256-row A tiles
-  int n_ranges;
+  int n_ranges;      // column ranges; a work unit takes two consecutive ones
   int n_kb;
   int n_kmma;
   int stages;
@@ -77,16 +81,49 @@ struct Params {
 struct Smem {
   uint32_t A, B;       // shared-window addresses (1024-aligned)
   uint64_t* bars;      // a_full, a_empty, b_full[S], b_empty[S], t_full[2], t_empty[2]
-  uint64_t* hand;      // [2 dirs][4 quarters][2 parities] carry hand-off barriers
-  float* carry;        // [2 dirs][4 quarters][2 parities][32] running minima
   uint32_t* tmem_slot;
 };
 
-constexpr int kHandBars = 2 * 4 * 2;
-
 size_t smem_bytes(int n_kb, int stages) {
-  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + (2 + 2 * stages + 4) * 8 +
-         kHandBars * 8 + kHandBars * 32 * 4 + 16;
+  return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + (2 + 2 * stages + 4) * 8 + 16;
+}
+
+// a work unit's two halves: half h = columns [c[h], c[h+1]), first segment s[h] (scalars, no
+// dynamically indexed arrays, so the struct stays in registers)
+struct Unit {
+  int64_t c0, c1, c2;
+  int s0, s1;
+  int n0, n1;  // BN-column tiles per half
+  __device__ __forceinline__ int64_t cb(int h) const { return h ? c1 : c0; }
+  __device__ __forceinline__ int64_t ce(int h) const { return h ? c2 : c1; }
+  __device__ __forceinline__ int sb(int h) const { return h ? s1 : s0; }
+};
+
+__device__ __forceinline__ bool unit_plan(const Params& p, int64_t u, Unit& U) {
+  const int rp = (int)(u / p.n_mpairs);
+  const int r0 = 2 * rp, r1 = min(2 * rp + 1, p.n_ranges), r2 = min(2 * rp + 2, p.n_ranges);
+  const int s0 = p.range_seg[r0], s1 = p.range_seg[r1], s2 = p.range_seg[r2];
+  if (s0 == s2) return false;
+  U.c0 = p.seg_offsets[s0] - p.seg_base;
+  U.c1 = p.seg_offsets[s1] - p.seg_base;
+  U.c2 = p.seg_offsets[s2] - p.seg_base;
+  U.s0 = s0;
+  U.s1 = s1;
+  U.n0 = (int)((U.c1 - U.c0 + BN - 1) / BN);
+  U.n1 = (int)((U.c2 - U.c1 + BN - 1) / BN);
+  return true;
+}
+
+// interleaved tile order of a unit: i -> (half, tile index within the half)
+__device__ __forceinline__ void unit_tile(const Unit& U, int i, int& h, int& k) {
+  const int both = 2 * min(U.n0, U.n1);
+  if (i < both) {
+    h = i & 1;
+    k = i >> 1;
+  } else {
+    h = U.n0 > U.n1 ? 0 : 1;
+    k = (both >> 1) + (i - both);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -156,16 +193,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   sm.B = sm.A + p.n_kb * A_KB_BYTES;
   uint8_t* tail = base + p.n_kb * A_KB_BYTES + p.stages * B_STAGE_BYTES;
   sm.bars = reinterpret_cast<uint64_t*>(tail);
-  sm.hand = sm.bars + 2 + 2 * p.stages + 4;
-  sm.carry = reinterpret_cast<float*>(sm.hand + kHandBars);
-  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.carry + kHandBars * 32);
+  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.bars + 2 + 2 * p.stages + 4);
 
   uint64_t* a_full = sm.bars + 0;   // leader: A tiles of both CTAs landed
   uint64_t* a_empty = sm.bars + 1;  // both: the unit's MMAs retired (commit multicast)
   uint64_t* b_full = sm.bars + 2;   // leader: B halves of both CTAs landed
   uint64_t* b_empty = sm.bars + 2 + p.stages;  // both: stage consumed (commit multicast)
   uint64_t* t_full = sm.bars + 2 + 2 * p.stages;  // both: accumulator ready (commit multicast)
-  uint64_t* t_empty = sm.bars + 4 + 2 * p.stages;  // leader: 8 epilogue warps drained it
+  uint64_t* t_empty = sm.bars + 4 + 2 * p.stages;  // leader: the buffer's 4 epilogue warps (x2 CTAs) drained it
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -185,9 +220,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(t_full + i, 1);
-      mbar_init(t_empty + i, 2 * kEpiWarps);
+      mbar_init(t_empty + i, kEpiWarps);  // 4 warps per buffer in each of the 2 CTAs
     }
-    for (int i = 0; i < kHandBars; ++i) mbar_init(sm.hand + i, 1);
     fence_mbar_init();
   }
   if (warp == kAllocWarp) {
@@ -199,7 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_slot;
 
-  const int64_t n_units = (int64_t)p.n_ranges * p.n_mpairs;
+  const int64_t n_units = (int64_t)((p.n_ranges + 1) / 2) * p.n_mpairs;
 
   if (warp == kProducerWarp) {
     // ============================ TMA producer (both CTAs) ============================
@@ -211,21 +245,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t stage = 0, phase = 0, a_phase = 0;
       int64_t b_loads = 0;
       for (int64_t u = pair; u < n_units; u += n_pairs) {
-        const int range = (int)(u / p.n_mpairs);
+        Unit U;
+        if (!unit_plan(p, u, U)) continue;
         const int mp = (int)(u % p.n_mpairs);
-        const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
-        if (s0 == s1) continue;
-        const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
         mbar_wait(a_empty, a_phase ^ 1);
         a_phase ^= 1;
         if (leader) mbar_expect_tx(a_full, 2 * p.n_kb * A_KB_BYTES);
         for (int kb = 0; kb < p.n_kb; ++kb)
           tma_load_2d_2sm(&tmA, a_full_l, smem_raw + (sm.A - smem_u32(smem_raw)) + kb * A_KB_BYTES, kb * BK,
                           mp * 2 * BM + (int)rank * BM, pol_a);
-        for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
+        const int n_tiles = U.n0 + U.n1;
+        for (int i = 0; i < n_tiles; ++i) {
+          int h, k;
+          unit_tile(U, i, h, k);
+          const int64_t c0 = U.cb(h) + (int64_t)k * BN;
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_empty + stage, phase ^ 1);
-#if LCRW_EPI_MODE >= 3
+#if LCRW_EPI_MODE == 3
             if (b_loads >= p.stages) {  // experiment: ring filled once, then no more B traffic
               if (leader) mbar_arrive(b_full + stage);
             } else
@@ -249,24 +285,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ============================ MMA issuer (leader CTA) =============================
     // The whole warp walks the loop (warp-uniform state); one elected lane issues.
     if (leader) {
-      uint32_t stage = 0, phase = 0, a_phase = 0, acc = 0, acc_phase = 0;
+      uint32_t stage = 0, phase = 0, a_phase = 0, e_phase = 0;  // e_phase bit h: t_empty[h] parity
       const uint64_t a_desc0 = umma_desc_sw128(sm.A);
       const uint64_t b_desc0 = umma_desc_sw128(sm.B);
       const int last_nk = p.n_kmma - 4 * (p.n_kb - 1);  // MMAs in the last K block (1..4)
       for (int64_t u = pair; u < n_units; u += n_pairs) {
-        const int range = (int)(u / p.n_mpairs);
-        const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
-        if (s0 == s1) continue;
-        const int64_t c_begin = p.seg_offsets[s0] - p.seg_base, c_end = p.seg_offsets[s1] - p.seg_base;
+        Unit U;
+        if (!unit_plan(p, u, U)) continue;
         mbar_wait(a_full, a_phase);
         a_phase ^= 1;
         tc_fence_after();
-        for (int64_t c0 = c_begin; c0 < c_end; c0 += BN) {
-#if LCRW_EPI_MODE < 4
-          mbar_wait(t_empty + acc, acc_phase ^ 1);
+        const int n_tiles = U.n0 + U.n1;
+        for (int i = 0; i < n_tiles; ++i) {
+          int h, k;
+          unit_tile(U, i, h, k);
+#if LCRW_EPI_MODE != 4
+          mbar_wait(t_empty + h, ((e_phase >> h) & 1) ^ 1);
 #endif
+          e_phase ^= 1u << h;
           tc_fence_after();
-          const uint32_t d_tmem = tmem + acc * BN;
+          const uint32_t d_tmem = tmem + h * BN;
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_full + stage, phase);
             tc_fence_after();
@@ -284,219 +322,113 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               phase ^= 1;
             }
           }
-          umma_commit_2sm_mc_elect(t_full + acc, 0x3);  // accumulator ready in both CTAs' TMEM
-          acc ^= 1;
-          if (acc == 0) acc_phase ^= 1;
+          umma_commit_2sm_mc_elect(t_full + h, 0x3);  // accumulator h ready in both CTAs' TMEM
         }
         umma_commit_2sm_mc_elect(a_empty, 0x3);  // A tiles reusable once the unit's MMAs retire
       }
     }
   } else if (warp < kEpiWarps) {
     // ============================ epilogue (both CTAs) ================================
-    // Warp (quarter q, half h) owns TMEM lanes [32q, 32q+32) and columns [128h, 128h+128)
-    // of every tile.  Segment minima that straddle halves are stitched with a carry
-    // hand-off: half 0 of tile t -> half 1 of tile t (dir 0), half 1 of tile t -> half 0
-    // of tile t+1 (dir 1).  A half that contains a segment end publishes its tail
-    // minimum immediately and only waits for its predecessor to emit its head segment.
-    const int quarter = warp & 3;  // TMEM lane quarter accessible to this warp
-    const int half = warp >> 2;
+    // Warp (quarter q, group h) owns TMEM lanes [32q, 32q+32) (= 32 A rows, one per
+    // lane) of accumulator buffer h, i.e. of every tile of each unit's half h.  The
+    // segment structure is the same for all rows, so every branch below is warp-uniform.
+    const int quarter = warp & 3;
+    const int grp = warp >> 2;
     const float inv_scale = p.scale[1];
-    const uint32_t t_empty_l = mapa_shared(smem_u32(t_empty), 0);
+    const uint32_t t_empty_l = mapa_shared(smem_u32(t_empty + grp), 0);
     const int zs = p.z_shift;
-    const int64_t zmask = (1ll << zs) - 1;
-    auto hbar = [&](int dir, int par) { return sm.hand + (dir * 4 + quarter) * 2 + par; };
-    auto hslot = [&](int dir, int par) { return sm.carry + ((dir * 4 + quarter) * 2 + par) * 32; };
-
-    // tile iterator over this pair's units (skips empty ranges)
-    int64_t u = pair - n_pairs, c_begin = 0, c_end = 0, c0 = 0;
-    auto next_tile = [&](int64_t& uu, int64_t& cb, int64_t& ce, int64_t& cc) -> int {
-      // returns 0 = done, 1 = same unit, 2 = new unit
-      if (uu >= 0 && cc + BN < ce) {
-        cc += BN;
-        return 1;
-      }
-      for (uu += n_pairs; uu < n_units; uu += n_pairs) {
-        const int range = (int)(uu / p.n_mpairs);
-        const int s0 = p.range_seg[range], s1 = p.range_seg[range + 1];
-        if (s0 == s1) continue;
-        cb = p.seg_offsets[s0] - p.seg_base;
-        ce = p.seg_offsets[s1] - p.seg_base;
-        cc = cb;
-        return 2;
-      }
-      return 0;
-    };
-    // a tile's segment-end bits: lane i < 8 holds the word of columns [32 i, 32 i + 32)
-    auto fetch_mask = [&](int64_t cc) -> uint32_t {
+    const uint32_t zw = 1u << zs;
+    // a tile's segment-end bits: lane i < 8 holds the word of columns [c + 32 i, c + 32 i + 32)
+    auto fetch_mask = [&](int64_t c) -> uint32_t {
       uint32_t w = 0;
       if (lane < BN / 32) {
-        const int64_t bit = cc + lane * 32;
+        const int64_t bit = c + lane * 32;
         const uint32_t lo = __ldg(p.endmask + (bit >> 5));
         const uint32_t hi = __ldg(p.endmask + (bit >> 5) + 1);
         w = __funnelshift_r(lo, hi, (uint32_t)(bit & 31));
       }
       return w;
     };
-
-    int kind = next_tile(u, c_begin, c_end, c0);
-    uint32_t pm = kind ? fetch_mask(c0) : 0u;
-    uint32_t acc = 0, acc_phase = 0, tcount = 0;
-    bool valid = false;
-    float nE = 0.f;
-    float* zrow = p.Z;
-    int64_t s_tile = 0;
-    while (kind) {
-      if (kind == 2) {  // first tile of a unit
-        const int mp = (int)(u % p.n_mpairs);
-        const int range = (int)(u / p.n_mpairs);
-        const int row = mp * 2 * BM + (int)rank * BM + quarter * 32 + lane;
-        valid = row < p.a_rows;
-        nE = valid ? __ldg(p.a_norms + row) : 0.f;
-        zrow = p.Z + ((int64_t)row << zs);
-        s_tile = p.range_seg[range];
-      }
-      const bool unit_start = kind == 2;
-      const int ncols = (int)min((int64_t)BN, c_end - c0);
-      // segment-end bits of this tile, restricted to its columns
-      uint32_t wmask = __shfl_sync(0xffffffffu, pm, lane & 7);
-      {
-        const int lim = ncols - (lane & 7) * 32;
-        wmask = lim >= 32 ? wmask : (lim <= 0 ? 0u : (wmask & ((1u << lim) - 1u)));
-      }
-      const int ends0 = __popc(__shfl_sync(0xffffffffu, wmask, 0)) + __popc(__shfl_sync(0xffffffffu, wmask, 1)) +
-                        __popc(__shfl_sync(0xffffffffu, wmask, 2)) + __popc(__shfl_sync(0xffffffffu, wmask, 3));
-      const int ends1 = __popc(__shfl_sync(0xffffffffu, wmask, 4)) + __popc(__shfl_sync(0xffffffffu, wmask, 5)) +
-                        __popc(__shfl_sync(0xffffffffu, wmask, 6)) + __popc(__shfl_sync(0xffffffffu, wmask, 7));
-      // prefetch the next tile's segment bits while this tile is processed
-      int64_t nu = u, ncb = c_begin, nce = c_end, nc0 = c0;
-      const int nkind = next_tile(nu, ncb, nce, nc0);
-      if (nkind) pm = fetch_mask(nc0);
-
-      int64_t s = s_tile + (half ? ends0 : 0);  // first segment ending in (or after) my half
-      const int64_t s_head = s;
-      float head = kInf, run = kInf;
-      bool have_end = false;
-      auto emit = [&](int64_t seg, float segmin) {
-        if (valid) {
-          float d;
-          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(fmaxf(segmin + nE, 0.f)));
-          zrow[(seg >> zs) * p.z_panel + (seg & zmask)] = d * inv_scale;
+    uint32_t phase = 0;
+    for (int64_t u = pair; u < n_units; u += n_pairs) {
+      Unit U;
+      if (!unit_plan(p, u, U)) continue;
+      const int64_t c_lo = U.cb(grp), c_hi = U.ce(grp);
+      if (c_lo == c_hi) continue;
+      const int mp = (int)(u % p.n_mpairs);
+      const int row = mp * 2 * BM + (int)rank * BM + quarter * 32 + lane;
+      const bool valid = row < p.a_rows;
+      const float nE = valid ? __ldg(p.a_norms + row) : 0.f;
+      // output cursor: segment s = U.sb(grp) + emitted so far, Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))]
+      const int64_t s_first = U.sb(grp);
+      float* zp = p.Z + (s_first >> zs) * p.z_panel + ((int64_t)row << zs);
+      uint32_t s_in = (uint32_t)s_first & (zw - 1);
+      float run = kInf;
+      auto emit = [&](float segmin) {
+        float d;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(fmaxf(segmin + nE, 0.f)));
+#if LCRW_EPI_MODE == 5
+        if (d < -1.f)  // experiment: never true -- the global store is skipped
+#endif
+        if (valid) zp[s_in] = d * inv_scale;
+        if (++s_in == zw) {
+          s_in = 0;
+          zp += p.z_panel;
         }
       };
-      // segment end inside my half: the first one closes the head (emitted after the hand-off)
-      auto close = [&](float segmin) {
-        if (!have_end) {
-          head = segmin;
-          have_end = true;
-        } else {
-          emit(s, segmin);
+      uint32_t pm = fetch_mask(c_lo);
+      for (int64_t c0 = c_lo; c0 < c_hi; c0 += BN) {
+        const int ncols = (int)min((int64_t)BN, c_hi - c0);
+        uint32_t wmask = pm;
+        {
+          const int lim = ncols - lane * 32;
+          wmask = lim >= 32 ? wmask : (lim <= 0 ? 0u : (wmask & ((1u << lim) - 1u)));
         }
-        ++s;
-      };
-
-      const int my_cols = min(BN_HALF, ncols - half * BN_HALF);
-      mbar_wait(t_full + acc, acc_phase);
-      tc_fence_after();
-      const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * BN_HALF;
+        if (c0 + BN < c_hi) pm = fetch_mask(c0 + BN);  // next tile's bits, latency hidden behind this one
+        mbar_wait(t_full + grp, phase);
+        tc_fence_after();
+        const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + grp * BN;
+        const int nch = (ncols + 31) >> 5;
 #pragma unroll 1
-      for (int ch = 0; ch < BN_HALF / 32; ++ch) {
-        if (ch * 32 >= my_cols) break;
-        uint32_t raw[32];
-#if LCRW_EPI_MODE >= 2
-        if (ch >= 0) { run = fminf(run, (float)ch); continue; }
-#endif
+        for (int ch = 0; ch < nch; ++ch) {
+          uint32_t raw[32];
+          tmem_ld_32x32b_x32(t_base + ch * 32, raw);
+          tmem_wait_ld();
+          // the accumulator holds v_j = |B_j|^2 - 2 A.B_j (norm columns folded into K)
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
+          uint32_t mask = __shfl_sync(0xffffffffu, wmask, ch);
 #if LCRW_EPI_MODE == 1
-        tmem_ld_32x32b_x32(t_base + ch * 32, raw);
-        tmem_wait_ld();
-        run = fminf(run, fminf(__uint_as_float(raw[0]), __uint_as_float(raw[31])));
-        continue;
+          run = fminf(run, fminf(v[0], v[31]));
+          if (mask) { emit(run); run = kInf; }
+          continue;
 #endif
-        tmem_ld_32x32b_x32(t_base + ch * 32, raw);
-        tmem_wait_ld();
-
-        // the accumulator already holds v_j = |B_j|^2 - 2 A.B_j (norm columns folded into K)
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
-        const int lim = my_cols - ch * 32;
-        uint32_t mask = __shfl_sync(0xffffffffu, wmask, half * 4 + ch);
-        if (lim < 32) {  // columns >= lim belong to the next range
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j >= lim) v[j] = kInf;
-        }
-        const int nb_ends = __popc(mask);
-        if (nb_ends == 0) {
-          run = fminf(run, RangeMin<0, 31>::run(v));
-        } else if (nb_ends == 1) {
-          float pre, suf;
-          split_switch(__ffs(mask) - 1, v, pre, suf);
-          close(fminf(run, pre));
-          run = suf;
-        } else {
-          int start = 0;
-          while (mask) {
-            const int e = __ffs(mask) - 1;
-            mask &= mask - 1u;
-            const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
-            close(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
-            run = kInf;
-            start = e + 1;
+          if (mask == 0) {
+            run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
+          } else if ((mask & (mask - 1u)) == 0) {  // exactly one segment end in the chunk
+            float pre, suf;
+            split_switch(__ffs(mask) - 1, v, pre, suf);
+            emit(fminf(run, pre));
+            run = suf;
+          } else {
+            int start = 0;
+            while (mask) {
+              const int e = __ffs(mask) - 1;
+              mask &= mask - 1u;
+              const uint32_t upto = e == 31 ? 0xFFFFFFFFu : ((2u << e) - 1u);
+              emit(fminf(run, masked_min(v, upto & (0xFFFFFFFFu << start))));
+              run = kInf;
+              start = e + 1;
+            }
+            run = start < 32 ? masked_min(v, 0xFFFFFFFFu << start) : kInf;
           }
-          if (start < 32) run = masked_min(v, 0xFFFFFFFFu << start);
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster_relaxed(t_empty_l + acc * 8);  // leader's t_empty[acc]
-
-      // ---- carry hand-off: pred -> me (dir = 1 - half), me -> succ (dir = half) ----
-      const int par = tcount & 1;
-      const int in_dir = half ? 0 : 1;
-      const int in_par = half ? par : (par ^ 1);          // half 0 reads tile t-1's half 1
-      const uint32_t in_phase = half ? (tcount >> 1) & 1 : ((tcount - 1) >> 1) & 1;
-      const bool has_pred = half ? true : (tcount > 0);
-      auto publish = [&](float carry_out) {
-        float* slot = hslot(half, par);
-        slot[lane] = carry_out;
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(hbar(half, par));
-      };
-      auto receive = [&]() -> float {
-        if (!has_pred) return kInf;
-        mbar_wait(hbar(in_dir, in_par), in_phase);
-        const float c = hslot(in_dir, in_par)[lane];
-        return (half == 0 && unit_start) ? kInf : c;  // a unit starts with no open segment
-      };
-      // Half 0 publishes before receiving (its tail does not depend on the carry);
-      // half 1 always receives first, which keeps every hand-off barrier at most one
-      // phase ahead of its consumer (an mbarrier parity wait cannot skip a phase).
-      if (half == 0 && have_end) {
-        publish(run);
-        emit(s_head, fminf(receive(), head));
-      } else {
-        const float cin = receive();
-        if (have_end) {
-          emit(s_head, fminf(cin, head));
-          publish(run);
-        } else {
-          publish(fminf(cin, run));
-        }
+        if (lane == 0) mbar_arrive_cluster_relaxed(t_empty_l);  // leader's t_empty[grp]
+        phase ^= 1;
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-      ++tcount;
-      s_tile += ends0 + ends1;
-      u = nu;
-      c_begin = ncb;
-      c_end = nce;
-      c0 = nc0;
-      kind = nkind;
-    }
-    // drain: half 0 consumes the last hand-off of half 1 so no arrival is left pending
-    if (half == 0 && tcount > 0) {
-      const int lp = (tcount - 1) & 1;
-      mbar_wait(hbar(1, lp), ((tcount - 1) >> 1) & 1);
     }
   }
 
@@ -610,7 +542,7 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(phase1_kernel)");
     attr_set = true;
   }
-  const int64_t n_units = (int64_t)n_ranges * p.n_mpairs;
+  const int64_t n_units = (int64_t)((n_ranges + 1) / 2) * p.n_mpairs;
   const int64_t pairs = sm_count() / 2;
   const int grid = 2 * (int)(n_units < pairs ? n_units : pairs);
   ProfScope prof(stream, tag);

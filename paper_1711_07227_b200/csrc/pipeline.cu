@@ -29,7 +29,7 @@ int auto_range_cols(int64_t b_rows, int64_t a_rows) {
   int64_t want = n_mtiles * b_rows / (8 * (int64_t)sm_count());
   want = (want + 255) / 256 * 256;
   if (want < 1024) want = 1024;
-  if (want > 32768) want = 32768;
+  if (want > 16384) want = 16384;  // a work unit takes two ranges
   return (int)want;
 }
 

@@ -215,7 +215,7 @@ def gather_rows(prep: PreparedEmbeddings, ids: torch.Tensor, side: str):
 def _range_cols(b_rows: int, a_rows: int) -> int:
     n_mtiles = max(1, (a_rows + 127) // 128)
     want = (n_mtiles * b_rows) // (8 * sm_count())
-    return int(min(32768, max(1024, (want + 255) // 256 * 256)))
+    return int(min(16384, max(1024, (want + 255) // 256 * 256)))  # a work unit takes two ranges
 
 
 def spmm_z_shift(n_seg: int) -> int:
