@@ -404,6 +404,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (mask) { emit(run); run = kInf; }
           continue;
 #endif
+#if LCRW_EPI_MODE == 6
+          run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
+          if (mask) { emit(run); run = kInf; }
+          continue;
+#endif
+#if LCRW_EPI_MODE == 7
+          if (mask == 0) {
+            run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
+          } else {
+            float pre, suf;
+            split_switch(__ffs(mask) - 1, v, pre, suf);
+            emit(fminf(run, pre));
+            run = suf;
+          }
+          continue;
+#endif
           if (mask == 0) {
             run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
           } else if ((mask & (mask - 1u)) == 0) {  // exactly one segment end in the chunk
