@@ -164,15 +164,17 @@ __device__ __forceinline__ void split_at(const float (&v)[32], float& pre, float
   }
 }
 
-template <int P = 0>
+#include "split_ptx.inc"
+
+// exactly one segment end at the warp-uniform column p: one indirect branch through a
+// 32-entry PTX jump table (gen_split.py), each target a pair of 3-input-min trees
 __device__ __forceinline__ void split_switch(int p, const float (&v)[32], float& pre, float& suf) {
-  if constexpr (P < 32) {
-    if (p == P) {
-      split_at<P>(v, pre, suf);
-      return;
-    }
-    split_switch<P + 1>(p, v, pre, suf);
-  }
+  asm(LCRW_SPLIT_PTX
+      : "=f"(pre), "=f"(suf)
+      : "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]), "r"(p));
 }
 
 __device__ __forceinline__ float masked_min(const float (&v)[32], uint32_t sel) {
