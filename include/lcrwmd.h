@@ -188,9 +188,12 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
  * entries.  k <= 1024 (lcrw_topk_sort handles any k for one segment). */
 int lcrw_topk_segments(const float* d, const int64_t* ids, int64_t n_seg, int64_t seg_len, int k,
                        float* out_d, int64_t* out_i, void* stream);
-/* per-row top-k of a row-major matrix (row stride ld) with implicit ids id_base + column */
+/* per-row top-k of a row-major matrix (row stride ld) with implicit ids id_base + column;
+ * rows longer than 16384 with k <= 32 go through per-chunk warp lists and a merge, in a
+ * workspace of lcrw_topk_rows_workspace() bytes (0 = none needed, ws may be NULL) */
+int lcrw_topk_rows_workspace(int64_t n_rows, int64_t row_len, int k, size_t* bytes);
 int lcrw_topk_rows(const float* d, int64_t ld, int64_t n_rows, int64_t row_len, int64_t id_base, int k,
-                   float* out_d, int64_t* out_i, void* stream);
+                   float* out_d, int64_t* out_i, void* ws, size_t ws_bytes, void* stream);
 int lcrw_topk_sort_workspace(int64_t n, size_t* bytes);
 /* full (distance, id) sort of one segment of n candidates; writes the first k */
 int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, float* out_d, int64_t* out_i,

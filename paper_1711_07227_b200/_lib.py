@@ -54,7 +54,8 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_reverse_panels_warps": (I32, []),
     "lcrw_reverse_panels_ilp": (I32, []),
     "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, I64, P, I64, P, I64, I64, P]),
-    "lcrw_topk_rows": (I32, [P, I64, I64, I64, I64, I32, P, P, P]),
+    "lcrw_topk_rows_workspace": (I32, [I64, I64, I32, P]),
+    "lcrw_topk_rows": (I32, [P, I64, I64, I64, I64, I32, P, P, P, SZ, P]),
     "lcrw_profile_reset": (I32, [I32]),
     "lcrw_profile_count": (I64, []),
     "lcrw_profile_get": (I32, [I64, C.c_char_p, I32, P]),
@@ -75,7 +76,7 @@ KERNELS_PER_CALL = {
     "lcrw_max_sqnorm": 1, "lcrw_scale_from_max_sqnorm": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
     "lcrw_row_classes": 13, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
-    "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 1,
+    "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
     "lcrw_reverse_panels": 1,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels);

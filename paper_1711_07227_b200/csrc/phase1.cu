@@ -42,6 +42,13 @@
 namespace lcrw {
 namespace p1 {
 
+#ifdef LCRW_P1_STATS
+// experiment instrumentation (variants/build_stats.sh; not in the shipped build): cycle
+// counters [0] epilogue wait t_full, [1] epilogue tile work, [3] epilogue tiles,
+// [4] MMA wait t_empty, [5] MMA wait b_full, [6] MMA tiles
+__device__ unsigned long long g_p1_stats[8];
+#endif
+
 constexpr int BM = 128;                       // A rows per CTA (TMEM lanes); the pair covers 256
 constexpr int BN = 256;                       // B rows per pair tile (MMA N); 128 staged per CTA
 constexpr int BN_HALF = BN / 2;
@@ -302,13 +309,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           int h, k;
           unit_tile(U, i, h, k);
 #if LCRW_EPI_MODE != 4
+#ifdef LCRW_P1_STATS
+          const long long _t0 = clock64();
+#endif
           mbar_wait(t_empty + h, ((e_phase >> h) & 1) ^ 1);
+#ifdef LCRW_P1_STATS
+          if (lane == 0) {
+            atomicAdd(&g_p1_stats[4], (unsigned long long)(clock64() - _t0));
+            atomicAdd(&g_p1_stats[6], 1ull);
+          }
+#endif
 #endif
           e_phase ^= 1u << h;
           tc_fence_after();
           const uint32_t d_tmem = tmem + h * BN;
           for (int kb = 0; kb < p.n_kb; ++kb) {
+#ifdef LCRW_P1_STATS
+            const long long _t1 = clock64();
+#endif
             mbar_wait(b_full + stage, phase);
+#ifdef LCRW_P1_STATS
+            if (lane == 0) atomicAdd(&g_p1_stats[5], (unsigned long long)(clock64() - _t1));
+#endif
             tc_fence_after();
             // descriptor start-address field counts 16-byte units: +2 per 32-byte K step
             const uint64_t ad = a_desc0 + (uint64_t)(kb * (A_KB_BYTES >> 4));
@@ -387,7 +409,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           wmask = lim >= 32 ? wmask : (lim <= 0 ? 0u : (wmask & ((1u << lim) - 1u)));
         }
         if (c0 + BN < c_hi) pm = fetch_mask(c0 + BN);  // next tile's bits, latency hidden behind this one
+#ifdef LCRW_P1_STATS
+        const long long _tw = clock64();
+#endif
         mbar_wait(t_full + grp, phase);
+#ifdef LCRW_P1_STATS
+        const long long _tc = clock64();
+        if (lane == 0) {
+          atomicAdd(&g_p1_stats[0], (unsigned long long)(_tc - _tw));
+          atomicAdd(&g_p1_stats[3], 1ull);
+        }
+#endif
         tc_fence_after();
         const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + grp * BN;
         const int nch = (ncols + 31) >> 5;
@@ -409,17 +441,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #if LCRW_EPI_MODE == 6
           run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
           if (mask) { emit(run); run = kInf; }
-          continue;
-#endif
-#if LCRW_EPI_MODE == 7
-          if (mask == 0) {
-            run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
-          } else {
-            float pre, suf;
-            split_switch(__ffs(mask) - 1, v, pre, suf);
-            emit(fminf(run, pre));
-            run = suf;
-          }
           continue;
 #endif
           if (mask == 0) {
@@ -446,6 +467,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_relaxed(t_empty_l);  // leader's t_empty[grp]
         phase ^= 1;
+#ifdef LCRW_P1_STATS
+        if (lane == 0) atomicAdd(&g_p1_stats[1], (unsigned long long)(clock64() - _tc));
+#endif
       }
     }
   }
@@ -571,6 +595,17 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
 
 }  // namespace p1
 }  // namespace lcrw
+
+#ifdef LCRW_P1_STATS
+extern "C" int lcrw_p1_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, lcrw::p1::g_p1_stats, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(lcrw::p1::g_p1_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 extern "C" int lcrw_phase1(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B,
                            int64_t b_rows, int m, int kp, const int64_t* seg_offsets,

@@ -103,6 +103,83 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Rows with k <= 32, pass 1: one warp per kChunkW-column chunk of a row keeps the
+// chunk's k best (key, id) sorted across lanes 0..k-1; a batch of 32 elements costs
+// one comparison per lane against the running k-th plus a ballot, and the rare
+// candidates are inserted with two shuffles.  Pass 2 (topk_segments_kernel) merges
+// the per-chunk lists.  Exact: a row's k best are among its chunks' k best.
+// ---------------------------------------------------------------------------
+constexpr int kChunkW = 8192;
+constexpr int kWarpsTk = 8;
+
+__global__ void __launch_bounds__(kWarpsTk * 32)
+    topk_rows_chunks_kernel(const float* __restrict__ d, int64_t ld, int64_t n_rows, int64_t row_len,
+                            int64_t id_base, int k, int64_t n_chunks, bool vec4, float* __restrict__ cand_d,
+                            int64_t* __restrict__ cand_i) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * kWarpsTk + (threadIdx.x >> 5);
+  if (w >= n_rows * n_chunks) return;
+  const int64_t row = w / n_chunks, chunk = w - row * n_chunks;
+  const int64_t c0 = chunk * kChunkW, c1 = min(row_len, c0 + kChunkW);
+  const float* dr = d + row * ld;
+  uint32_t my_k = 0xFFFFFFFFu;
+  int64_t my_i = INT64_MAX;
+  uint32_t thr_k = 0xFFFFFFFFu;
+  int64_t thr_i = INT64_MAX;
+  auto offer = [&](uint32_t key, int64_t id, bool ok) {
+    uint32_t bal = __ballot_sync(0xffffffffu, ok && less(key, id, thr_k, thr_i));
+    while (bal) {
+      const int src = __ffs(bal) - 1;
+      bal &= bal - 1u;
+      const uint32_t nk = __shfl_sync(0xffffffffu, key, src);
+      const int64_t ni = __shfl_sync(0xffffffffu, id, src);
+      if (!less(nk, ni, thr_k, thr_i)) continue;  // the threshold moved since the ballot
+      const int pos = __popc(__ballot_sync(0xffffffffu, lane < k && less(my_k, my_i, nk, ni)));
+      const uint32_t uk = __shfl_up_sync(0xffffffffu, my_k, 1);
+      const int64_t ui = __shfl_up_sync(0xffffffffu, my_i, 1);
+      if (lane > pos && lane < k) {
+        my_k = uk;
+        my_i = ui;
+      }
+      if (lane == pos) {
+        my_k = nk;
+        my_i = ni;
+      }
+      thr_k = __shfl_sync(0xffffffffu, my_k, k - 1);
+      thr_i = __shfl_sync(0xffffffffu, my_i, k - 1);
+    }
+  };
+  if (vec4) {  // 16-byte aligned rows: 128 columns per warp step, next step's load in flight
+    int64_t c = c0 + lane * 4;
+    float4 cur = c + 3 < c1 ? __ldg(reinterpret_cast<const float4*>(dr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t base = c0; base < c1; base += 128) {
+      const int64_t cn = base + 128 + lane * 4;
+      const float4 nxt = cn + 3 < c1 ? __ldg(reinterpret_cast<const float4*>(dr + cn)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      c = base + lane * 4;
+      if (c + 3 >= c1 && c < c1) {  // ragged end of the chunk
+        cur.x = dr[c];
+        if (c + 1 < c1) cur.y = dr[c + 1];
+        if (c + 2 < c1) cur.z = dr[c + 2];
+      }
+      offer(float_key(cur.x), id_base + c, c < c1);
+      offer(float_key(cur.y), id_base + c + 1, c + 1 < c1);
+      offer(float_key(cur.z), id_base + c + 2, c + 2 < c1);
+      offer(float_key(cur.w), id_base + c + 3, c + 3 < c1);
+      cur = nxt;
+    }
+  } else {
+    for (int64_t base = c0; base < c1; base += 32) {
+      const int64_t c = base + lane;
+      offer(c < c1 ? float_key(dr[c]) : 0xFFFFFFFFu, id_base + c, c < c1);
+    }
+  }
+  if (lane < k) {
+    cand_d[w * k + lane] = key_float(my_k);
+    cand_i[w * k + lane] = my_i;
+  }
+}
+
 __global__ void keys_kernel(const float* __restrict__ d, const int64_t* __restrict__ perm, int64_t n,
                             uint32_t* __restrict__ keys) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -150,8 +227,17 @@ int lcrw_topk_segments(const float* d, const int64_t* ids, int64_t n_seg, int64_
   return LCRW_OK;
 }
 
+static int64_t topk_rows_chunks(int64_t row_len) { return (row_len + kChunkW - 1) / kChunkW; }
+
+int lcrw_topk_rows_workspace(int64_t n_rows, int64_t row_len, int k, size_t* bytes) {
+  LCRW_REQUIRE(n_rows >= 0 && row_len >= 0 && k >= 1 && bytes, "lcrw_topk_rows_workspace: bad arguments");
+  const size_t n = (size_t)n_rows * topk_rows_chunks(row_len) * k;
+  *bytes = (k <= 32 && row_len > 2 * kChunkW) ? (n * 4 + 255) / 256 * 256 + n * 8 : 0;
+  return LCRW_OK;
+}
+
 int lcrw_topk_rows(const float* d, int64_t ld, int64_t n_rows, int64_t row_len, int64_t id_base, int k,
-                   float* out_d, int64_t* out_i, void* stream) {
+                   float* out_d, int64_t* out_i, void* ws, size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(k >= 1, "k must be >= 1");
   LCRW_REQUIRE(n_rows >= 0 && row_len >= 0 && ld >= row_len, "lcrw_topk_rows: bad shape");
   if (n_rows == 0 || row_len == 0) return LCRW_OK;
@@ -161,11 +247,35 @@ int lcrw_topk_rows(const float* d, int64_t ld, int64_t n_rows, int64_t row_len, 
   }
   LCRW_REQUIRE(d && out_d && out_i, "lcrw_topk_rows: null pointer");
   LCRW_REQUIRE(n_rows < (1ll << 31), "lcrw_topk_rows: too many rows");
+  cudaStream_t st = as_stream(stream);
   int kp = 1;
   while (kp < k) kp <<= 1;
-  topk_segments_kernel<<<(unsigned)n_rows, kThreads, 0, as_stream(stream)>>>(d, nullptr, ld, row_len, id_base, k, kp,
-                                                                             out_d, out_i);
-  LCRW_CHECK_LAUNCH("topk_segments_kernel (rows)");
+  size_t need = 0;
+  lcrw_topk_rows_workspace(n_rows, row_len, k, &need);
+  if (need == 0) {  // short rows or k > 32: one CTA per row
+    topk_segments_kernel<<<(unsigned)n_rows, kThreads, 0, st>>>(d, nullptr, ld, row_len, id_base, k, kp, out_d,
+                                                                 out_i);
+    LCRW_CHECK_LAUNCH("topk_segments_kernel (rows)");
+    return LCRW_OK;
+  }
+  LCRW_REQUIRE(ws && ws_bytes >= need, "lcrw_topk_rows: workspace too small (use lcrw_topk_rows_workspace)");
+  const int64_t n_chunks = topk_rows_chunks(row_len);
+  const int64_t n_cand = n_chunks * k;
+  float* cand_d = static_cast<float*>(ws);
+  int64_t* cand_i = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + ((size_t)n_rows * n_cand * 4 + 255) / 256 * 256);
+  const bool vec4 = (ld % 4 == 0) && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
+  const int64_t warps = n_rows * n_chunks;
+  const int64_t blocks = (warps + kWarpsTk - 1) / kWarpsTk;
+  LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_topk_rows: too many chunks");
+  {
+    ProfScope prof(st, "topk_rows");
+    topk_rows_chunks_kernel<<<(unsigned)blocks, kWarpsTk * 32, 0, st>>>(d, ld, n_rows, row_len, id_base, k, n_chunks,
+                                                                        vec4, cand_d, cand_i);
+    LCRW_CHECK_LAUNCH("topk_rows_chunks_kernel");
+    topk_segments_kernel<<<(unsigned)n_rows, kThreads, 0, st>>>(cand_d, cand_i, n_cand, n_cand, 0, k, kp, out_d,
+                                                                 out_i);
+    LCRW_CHECK_LAUNCH("topk_segments_kernel (chunk merge)");
+  }
   return LCRW_OK;
 }
 

@@ -265,6 +265,16 @@ def topk_rows(d: torch.Tensor, ids: torch.Tensor, n_seg: int, seg_len: int, k: i
     return out_d[:, :kk], out_i[:, :kk]
 
 
+def topk_matrix_rows(D: torch.Tensor, n_rows: int, row_len: int, ld: int, id_base: int, k: int,
+                     out_d: torch.Tensor, out_i: torch.Tensor) -> None:
+    """Per-row k smallest (distance, id_base + column) of a row-major matrix (lcrw_topk_rows)."""
+    ws_bytes = C.c_size_t(0)
+    _lib.call("lcrw_topk_rows_workspace", n_rows, row_len, k, C.byref(ws_bytes))
+    ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=D.device)
+    _lib.call("lcrw_topk_rows", _p(D), ld, n_rows, row_len, id_base, k, _p(out_d), _p(out_i), _p(ws),
+              ws_bytes.value, _stream())
+
+
 def topk_sort(d: torch.Tensor, ids: torch.Tensor, k: int):
     n = d.numel()
     ws_bytes = C.c_size_t(0)
@@ -469,7 +479,7 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     kk = min(k, n1)
     out_d = torch.empty((n2, k), dtype=torch.float32, device=dev)
     out_i = torch.empty((n2, k), dtype=torch.int64, device=dev)
-    _lib.call("lcrw_topk_rows", _p(D), n1, n2, n1, id_offset, k, _p(out_d), _p(out_i), st)
+    topk_matrix_rows(D, n2, n1, n1, id_offset, k, out_d, out_i)
     return out_d[:, :kk], out_i[:, :kk]
 
 

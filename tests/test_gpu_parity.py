@@ -365,3 +365,26 @@ def test_dimension_too_large_is_reported():
     x1 = _rand_set(rng, 4, 50, 1, 5)
     with pytest.raises(NotImplementedError, match="unsupported"):
         D.lcrwmd_full(x1, x1, E)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,row_len", [(1, 100_003), (10, 100_003), (32, 98_304), (33, 100_003), (10, 98_304)])
+def test_topk_matrix_rows_long_rows_with_ties(k, row_len):
+    """lcrw_topk_rows (kernels.py:210-223 per row): chunked warp lists + merge for long rows;
+    quantised values make ties common, so the (distance, id) tie-break is exercised."""
+    import torch
+    from paper_1711_07227_b200 import device
+    rng = np.random.default_rng(k)
+    n_rows, id_base = 7, 5_000   # row_len % 4 == 0 takes the float4 path
+    D = np.round(rng.random((n_rows, row_len)) * 300).astype(np.float32)   # values 0..300: many ties
+    D[3, :] = 1.0                                                          # an all-tie row
+    Dd = torch.from_numpy(D).cuda()
+    od = torch.empty((n_rows, k), dtype=torch.float32, device="cuda")
+    oi = torch.empty((n_rows, k), dtype=torch.int64, device="cuda")
+    device.topk_matrix_rows(Dd, n_rows, row_len, row_len, id_base, k, od, oi)
+    od, oi = od.cpu().numpy(), oi.cpu().numpy()
+    for r in range(n_rows):
+        cols = np.arange(row_len)
+        order = np.lexsort((cols, D[r]))[:k]
+        assert np.array_equal(oi[r], order + id_base), r
+        assert np.array_equal(od[r], D[r, order]), r
