@@ -274,6 +274,147 @@ def rwmd_quadratic(x1, x2, embeddings) -> np.ndarray:
     return out
 
 
+def rwmd_bounds(x1, x2, embeddings):
+    """distances.py:78-114: (bound1, bound2) = the two one-sided bounds, (n1, n2) each.
+    bound1 is the forward LC-RWMD direction, bound2 the reverse one transposed
+    (the two-phase form equals the quadratic one value for value)."""
+    x1, x2 = as_csr(x1), as_csr(x2)
+    e = np.asarray(embeddings)
+    x1r, e1, _ = restrict_vocabulary(x1, e)
+    x2r, e2, _ = restrict_vocabulary(x2, e)
+    return one_direction(x1r, e1, e, x2), one_direction(x2r, e2, e, x1).T
+
+
+def pairwise_euclidean(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """kernels.py:113-130 (identical rows -> exactly 0, kernels.py:91-92)."""
+    a = np.atleast_2d(np.asarray(a))
+    b = np.atleast_2d(np.asarray(b))
+    ga, gb = _row_groups(a.astype(np.float32), b.astype(np.float32))
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    return _euclid_block(a64, squared_norms(a64), b64, squared_norms(b64), ga, gb)
+
+
+def centroids(x, embeddings) -> np.ndarray:
+    """kernels.py:201-203 (= spmm of X by E)."""
+    return spmm(as_csr(x), np.asarray(embeddings))
+
+
+def wcd_block(x1, x2, embeddings) -> np.ndarray:
+    """distances.py:59-71: centroid distances for all pairs."""
+    return pairwise_euclidean(centroids(x1, embeddings), centroids(x2, embeddings))
+
+
+# ---------------------------------------------------------------------------
+# Exact mover's distance (emd.py) -- successive shortest paths, restated
+# ---------------------------------------------------------------------------
+EMD_FEAS_TOL = 1e-9      # emd.py:33
+EMD_PRUNE_SLACK = 1e-6   # emd.py:39
+
+
+def solve_emd_objective(supply, demand, cost) -> float:
+    """emd.py:120-194: successive shortest augmenting paths with node potentials
+    (multi-source Dijkstra over reduced costs clamped at 0, lowest-index ties);
+    returns the objective.  Restated with the reference's order of operations
+    and tolerances.  Where the reference raises "no augmenting path" because the
+    float32-normalised totals differ by more than 1e-9 (emd.py:153-162), this
+    stops once either side is exhausted -- the behaviour the CUDA solver has."""
+    s = np.asarray(supply, dtype=np.float64).copy()
+    d = np.asarray(demand, dtype=np.float64).copy()
+    c = np.ascontiguousarray(cost, dtype=np.float64)
+    h1, h2 = c.shape
+    n = h1 + h2
+    flow = np.zeros((h1, h2))
+    phi = np.zeros(n)
+    while s.sum() > EMD_FEAS_TOL and d.sum() > EMD_FEAS_TOL:
+        dist = np.full(n, np.inf)
+        parent = np.full(n, -1, dtype=np.int64)
+        dist[:h1][s > EMD_FEAS_TOL] = 0.0
+        done = np.zeros(n, dtype=bool)
+        for _ in range(n):
+            u = int(np.argmin(np.where(done, np.inf, dist)))
+            if done[u] or not np.isfinite(dist[u]):
+                break
+            done[u] = True
+            if u < h1:
+                rc = np.maximum(c[u] + phi[u] - phi[h1:], 0.0)
+                cand = dist[u] + rc
+                better = (cand < dist[h1:]) & ~done[h1:]
+                dist[h1:][better] = cand[better]
+                parent[h1:][better] = u
+            else:
+                q = u - h1
+                rc = np.maximum(phi[u] - phi[:h1] - c[:, q], 0.0)
+                cand = dist[u] + rc
+                better = (flow[:, q] > EMD_FEAS_TOL) & (cand < dist[:h1]) & ~done[:h1]
+                dist[:h1][better] = cand[better]
+                parent[:h1][better] = u
+        sink = np.where(d > EMD_FEAS_TOL, dist[h1:], np.inf)
+        t = int(np.argmin(sink))
+        if not np.isfinite(sink[t]):
+            break
+        phi += np.minimum(dist, sink[t])
+        node, bott = h1 + t, d[t]
+        while parent[node] != -1:
+            prev = int(parent[node])
+            if node < h1:
+                bott = min(bott, flow[node, prev - h1])
+            node = prev
+        root = node
+        bott = min(bott, s[root])
+        node = h1 + t
+        while parent[node] != -1:
+            prev = int(parent[node])
+            if node >= h1:
+                flow[prev, node - h1] += bott
+            else:
+                flow[node, prev - h1] -= bott
+            node = prev
+        s[root] -= bott
+        d[t] -= bott
+    return float(np.sum(flow * c))
+
+
+def wmd(x1_ids, x1_w, x2_ids, x2_w, embeddings) -> float:
+    """emd.py:199-211: exact WMD over the pairwise word distances of the two documents."""
+    e = np.asarray(embeddings)
+    cost = pairwise_euclidean(e[x1_ids], e[x2_ids]).astype(np.float64)
+    return solve_emd_objective(np.asarray(x1_w, np.float64), np.asarray(x2_w, np.float64), cost)
+
+
+def prefiltered_topk_wmd(x1, q_ids, q_w, embeddings, k):
+    """emd.py:214-261: exact top-k WMD, candidates in ascending (LC-RWMD bound, id) order,
+    the k best seed a cutoff, stop at the first bound above cutoff*(1+1e-6)+1e-12."""
+    x1 = as_csr(x1)
+    e = np.asarray(embeddings)
+    n1 = x1.n_rows
+    q = CSR(np.array([0, len(q_ids)], np.int64), np.asarray(q_ids, np.int32), np.asarray(q_w, np.float32),
+            x1.n_cols)
+    bounds = lcrwmd_full(x1, q, e)[:, 0].astype(np.float64)
+    order = np.lexsort((np.arange(n1), bounds))
+
+    def row(i):
+        lo, hi = int(x1.row_offsets[i]), int(x1.row_offsets[i + 1])
+        return x1.column_ids[lo:hi], x1.values[lo:hi]
+
+    top = []
+    for idx in order[:k]:
+        top.append((wmd(*row(int(idx)), q_ids, q_w, e), int(idx)))
+    solves = k
+    top.sort()
+    cutoff = top[-1][0]
+    for pos in range(k, n1):
+        idx = int(order[pos])
+        if bounds[idx] > cutoff * (1.0 + EMD_PRUNE_SLACK) + 1e-12:
+            break
+        dist = wmd(*row(idx), q_ids, q_w, e)
+        solves += 1
+        if (dist, idx) < top[-1]:
+            top[-1] = (dist, idx)
+            top.sort()
+            cutoff = top[-1][0]
+    return np.array([t[0] for t in top]), np.array([t[1] for t in top], np.int64), solves
+
+
 # ---------------------------------------------------------------------------
 # Top-k (kernels.py:210-232)
 # ---------------------------------------------------------------------------

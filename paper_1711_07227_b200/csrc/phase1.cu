@@ -445,6 +445,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
           if (mask == 0) {
             run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
+          } else if (mask == 0xFFFFFFFFu) {  // every column closes a segment (pairwise distances)
+            emit(fminf(run, v[0]));
+#pragma unroll
+            for (int j = 1; j < 32; ++j) emit(v[j]);
+            run = kInf;
           } else if ((mask & (mask - 1u)) == 0) {  // exactly one segment end in the chunk
             float pre, suf;
             split_switch(__ffs(mask) - 1, v, pre, suf);

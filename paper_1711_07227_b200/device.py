@@ -502,6 +502,101 @@ def nearest_word_distances(E, Q) -> torch.Tensor:
     return Z[: zp].view(prep.V, 8)[:, 0]
 
 
+# ---------------------------------------------------------------------------
+# rows next to the hot path: pairwise distances, centroids, WCD, both bounds
+# ---------------------------------------------------------------------------
+
+
+def pairwise(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """kernels.py:113-130 on the tensor cores: (na, nb) Euclidean distances between rows.
+
+    The Phase-1 kernel with every b row its own segment: A = a's operand rows,
+    B = b's, one shared power-of-two scale and exact-identity classes over
+    a U b, so identical rows give exactly 0 as in the reference (kernels.py:91-92)."""
+    na, nb = int(a.shape[0]), int(b.shape[0])
+    dev = a.device
+    out = torch.zeros((na, nb), dtype=torch.float32, device=dev)
+    if na == 0 or nb == 0:
+        return out
+    prep = PreparedEmbeddings(torch.cat([a, b], dim=0))
+    ids = torch.arange(na, na + nb, dtype=torch.int32, device=dev)
+    seg = torch.arange(nb + 1, dtype=torch.int64, device=dev)
+    Z, zp = phase1(prep.EhA[:na], prep.norms[:na], na, prep.EhB[na:na + nb], nb, seg, nb, prep, z_shift=3)
+    remap = torch.full((na + nb,), -1, dtype=torch.int32, device=dev)
+    remap[:na] = torch.arange(na, dtype=torch.int32, device=dev)
+    rep, nxt = prep.representatives(ids)
+    zero_identical(seg, nb, rep, nxt, remap, Z, zp, 3)
+    panels = (nb + 7) // 8
+    return Z[: panels * zp].view(panels, na, 8).permute(1, 0, 2).reshape(na, panels * 8)[:, :nb].contiguous()
+
+
+def centroids(x: DeviceCSR, E: torch.Tensor) -> torch.Tensor:
+    """kernels.py:201-203: X . E with fp64 products and sums in ascending nonzero order,
+    rounded once (lcrw_spmm; bitwise equal to the reference)."""
+    V, m = int(E.shape[0]), int(E.shape[1])
+    zs = spmm_z_shift(m)
+    w = 1 << zs
+    mp = (m + w - 1) // w * w
+    Ep = torch.zeros((V, mp), dtype=torch.float32, device=E.device)
+    Ep[:, :m] = E
+    Zp = Ep.view(V, mp // w, w).permute(1, 0, 2).contiguous()  # (1 << zs)-dimension panels
+    out = torch.empty((max(x.n_rows, 1), m), dtype=torch.float32, device=E.device)
+    spmm(x.offsets, x.cols, x.vals, x.n_rows, Zp, w * V, m, out, m, 8, z_shift=zs)
+    return out[: x.n_rows]
+
+
+def one_sided_rows(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings) -> torch.Tensor:
+    """bound1 of distances.py:78-114 (= lcrwmd_batched): (n1, n2) row-major."""
+    res = Restricted.build(x1, prep)
+    out = one_direction(res, prep, x2, layout="rows")
+    return out[: x1.n_rows * x2.n_rows].view(x1.n_rows, x2.n_rows)
+
+
+def reverse_rows(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings) -> torch.Tensor:
+    """bound2 of distances.py:78-114: the reverse direction alone, (n1, n2), through the
+    symmetric pipeline with D1 = -inf (its max-combine then passes D2 through)."""
+    n1, n2 = x1.n_rows, x2.n_rows
+    d1 = torch.full((((n2 + 7) // 8) * 8 * max(n1, 1),), float("-inf"), dtype=torch.float32, device=x1.cols.device)
+    return symmetric(x1, x2, prep, None, d1=d1)
+
+
+def load_index(path) -> tuple[DeviceCSR, torch.Tensor, list[str]]:
+    """LCRW v1 index (corpus.py:17-25, 460-489) straight into HBM: the file is read once
+    into a pinned host buffer and each section is copied asynchronously from it
+    (no intermediate numpy arrays for the big sections).  Returns (DeviceCSR of the
+    stored set, f32 embeddings (v_e, m) on the device, words)."""
+    from pathlib import Path as _Path
+    from .corpus import _index_words, index_layout
+    dev = require_cuda()
+    nbytes = _Path(path).stat().st_size
+    buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    with open(path, "rb") as fh:
+        got = fh.readinto(memoryview(buf.numpy()))
+    if got != nbytes:
+        raise CorpusError(f"{path}: short read")
+    host = buf.numpy()
+    v_e, n, m, sec = index_layout(host, path)
+
+    def section(name, dtype):
+        off, nb = sec[name]
+        return buf[off:off + nb].view(dtype)
+
+    offs_h = section("offsets", torch.int64).numpy().copy()
+    if n and np.any(np.diff(offs_h) <= 0):
+        raise CorpusError(f"{path}: every row must hold at least one word")
+    cols = section("ids", torch.int32).to(dev, non_blocking=True)
+    vals = section("values", torch.float32).to(dev, non_blocking=True)
+    E = section("embeddings", torch.float32).view(v_e, m).to(dev, non_blocking=True)
+    offs = torch.from_numpy(offs_h).to(dev)
+    nnz = int(offs_h[-1])
+    small = nnz <= (1 << 22)
+    host_cols = section("ids", torch.int32).numpy().copy() if small else None
+    host_vals = section("values", torch.float32).numpy().copy() if small else None
+    words = _index_words(host, sec["words"][0], v_e, path)
+    torch.cuda.current_stream().synchronize()  # the pinned buffer is released on return
+    return DeviceCSR(offs, cols, vals, v_e, offs_h, host_cols, host_vals), E, words
+
+
 def restrict_vocabulary_host(x: HistogramSet, embeddings):
     """corpus.restrict_vocabulary on the GPU; returns host (set, E rows, remap)."""
     dx = DeviceCSR.upload(x, "hist_set")

@@ -9,6 +9,12 @@ Same names, signatures, return types and errors as
   (csrc/phase2.cu);
 * symmetric combine (distances.py:264) fused into the reverse-direction SpMM.
 
+Next to the path: ``wcd_block`` (distances.py:59-71, centroids by
+the SpMM kernel + pairwise distances by the Phase-1 kernel) and
+``rwmd_bounds`` / ``rwmd_quadratic`` (distances.py:78-130): the quadratic
+relaxation equals the two-phase one value for value, so
+both bounds come from the LC-RWMD kernels.
+
 ``lcrwmd_topk`` is the one extension: the symmetric bound reduced to each
 query's k nearest resident documents without materialising the n1 x n2
 matrix (the reference leaves top-k to callers, kernels.py:210-232).
@@ -35,6 +41,37 @@ def _check_space(x: HistogramSet, embeddings, name: str) -> None:
     rows = embeddings.shape[0]
     if x.n_cols != rows:
         raise ValueError(f"{name}: histogram columns ({x.n_cols}) do not match embedding rows ({rows})")
+
+
+def wcd_block(x1: HistogramSet, x2: HistogramSet, embeddings: np.ndarray, row_block: int = DEFAULT_ROW_BLOCK,
+              col_block: int = DEFAULT_COL_BLOCK) -> DistanceBlock:
+    """Word centroid distances for all pairs, (n1, n2) (distances.py:59-71)."""
+    _check_space(x1, embeddings, "x1")
+    _check_space(x2, embeddings, "x2")
+    E = device.to_device(np.asarray(embeddings, dtype=np.float32), torch.float32)
+    c1 = device.centroids(device.DeviceCSR.upload(x1, "x1"), E)
+    c2 = device.centroids(device.DeviceCSR.upload(x2, "x2"), E)
+    return DistanceBlock(device.pairwise(c1, c2).cpu().numpy())
+
+
+def rwmd_bounds(x1: HistogramSet, x2: HistogramSet, embeddings: np.ndarray, row_block: int = DEFAULT_ROW_BLOCK,
+                col_block: int = DEFAULT_COL_BLOCK) -> tuple[np.ndarray, np.ndarray]:
+    """Both one-sided relaxation bounds for all pairs as (n1, n2) f32 arrays (distances.py:78-114):
+    bound1 = x1 rows' mass to the nearest words of each x2 row, bound2 the swapped direction."""
+    _check_space(x1, embeddings, "x1")
+    _check_space(x2, embeddings, "x2")
+    prep = device.PreparedEmbeddings(embeddings)
+    dx1, dx2 = device.DeviceCSR.upload(x1, "x1"), device.DeviceCSR.upload(x2, "x2")
+    b1 = device.one_sided_rows(dx1, dx2, prep).cpu().numpy()
+    b2 = device.reverse_rows(dx1, dx2, prep).cpu().numpy()
+    return b1, b2
+
+
+def rwmd_quadratic(x1: HistogramSet, x2: HistogramSet, embeddings: np.ndarray, row_block: int = DEFAULT_ROW_BLOCK,
+                   col_block: int = DEFAULT_COL_BLOCK) -> DistanceBlock:
+    """Symmetric relaxed bound max(bound1, bound2) (distances.py:117-130)."""
+    b1, b2 = rwmd_bounds(x1, x2, embeddings, row_block, col_block)
+    return DistanceBlock(np.maximum(b1, b2))
 
 
 def nearest_word_distances(embeddings: np.ndarray, query_vectors: np.ndarray,

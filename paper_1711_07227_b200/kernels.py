@@ -9,6 +9,9 @@ kernels through the C ABI (include/lcrwmd.h):
                                     to f32 -- bitwise equal to the reference for equal z.
 * ``topk_select`` / ``topk_merge`` -> lcrw_topk_segments / lcrw_topk_sort
                                     (kernels.py:210-232): ascending (distance, id).
+* ``pairwise_euclidean``           -> lcrw_phase1 with one segment per b row
+                                    (kernels.py:113-130), f16 operands as on the hot path.
+* ``centroids``                    -> lcrw_spmm of X by E (kernels.py:201-203), bitwise.
 
 ``row_block`` / ``col_block`` are accepted for compatibility; tiling never
 changes results (kernels.py:6-10) and the GPU tiles are compile-time.
@@ -91,6 +94,28 @@ def spmv(x: HistogramSet, z: np.ndarray) -> np.ndarray:
     if z.ndim != 1:
         raise ValueError("spmv expects a 1-d right-hand side")
     return spmm(x, z[:, None])[:, 0]
+
+
+def pairwise_euclidean(a: np.ndarray, b: np.ndarray, row_block: int = DEFAULT_ROW_BLOCK,
+                       col_block: int = DEFAULT_COL_BLOCK, row_start: int = 0, col_start: int = 0) -> DistanceBlock:
+    """All-pairs Euclidean distances between the rows of a and b (kernels.py:113-130)."""
+    a = np.atleast_2d(np.asarray(a))
+    b = np.atleast_2d(np.asarray(b))
+    if a.shape[1] != b.shape[1]:
+        raise ValueError(f"dimension mismatch: {a.shape[1]} vs {b.shape[1]}")
+    ad = device.to_device(np.asarray(a, dtype=np.float32), torch.float32)
+    bd = device.to_device(np.asarray(b, dtype=np.float32), torch.float32)
+    return DistanceBlock(device.pairwise(ad, bd).cpu().numpy(), row_start=row_start, col_start=col_start)
+
+
+def centroids(x: HistogramSet, embeddings: np.ndarray) -> np.ndarray:
+    """Weighted average of each row's embedding vectors, float32 (n, m) (kernels.py:201-203)."""
+    e = np.asarray(embeddings)
+    if e.shape[0] != x.n_cols:
+        raise ValueError(f"dimension mismatch: {x.n_cols} columns vs {e.shape[0]} rows")
+    if x.n_rows == 0:
+        return np.zeros((0, e.shape[1]), dtype=np.float32)
+    return device.centroids(device.DeviceCSR.upload(x, "x"), device.to_device(e, torch.float32)).cpu().numpy()
 
 
 def topk_select(distances: np.ndarray, ids: np.ndarray, k: int) -> TopKResult:

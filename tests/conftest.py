@@ -42,3 +42,24 @@ def rel_close(a, b, rtol=1e-4, atol=1e-6):
     b = np.asarray(b, dtype=np.float64)
     return np.all(np.abs(a - b) <= rtol * np.abs(b) + atol), float(
         np.max(np.abs(a - b) / (np.abs(b) + atol / rtol)) if a.size else 0.0)
+
+
+WIDEN_CASES = ["small_m16", "m300", "clustered", "dup_rows"]
+
+
+def load_widen(name):
+    """(base golden, widen golden, x1, x2, dyadic xd1, dyadic xd2) for SURVEY §8f rows."""
+    from paper_1711_07227_b200.corpus import HistogramSet
+
+    z, x1, x2 = load_case(name)
+    w = np.load(GOLDEN / f"widen_{name}.npz")
+
+    def hs(p):
+        return HistogramSet(w[f"{p}_offsets"], w[f"{p}_ids"], w[f"{p}_vals"], int(w[f"{p}_ncols"]))
+
+    return z, w, x1, x2, hs("xd1"), hs("xd2")
+
+
+@pytest.fixture(params=WIDEN_CASES)
+def widen_case(request):
+    return (request.param, *load_widen(request.param))

@@ -100,7 +100,87 @@ def case_topk():
     print("topk")
 
 
-if __name__ == "__main__":
+def case_widen(name):
+    """Reference outputs for the rows next to the hot path: WCD, both
+    one-sided RWMD bounds, centroids, pairwise distances, exact WMD and the
+    RWMD-prefiltered exact top-k, and the LCRW index file bytes."""
+    import tempfile
+    corpus, distances, kernels = _ref()
+    from movers import emd
+    z = np.load(OUT / f"{name}.npz")
+
+    def hs(p_):
+        return corpus.HistogramSet(z[f"{p_}_offsets"], z[f"{p_}_ids"], z[f"{p_}_vals"], int(z[f"{p_}_ncols"]))
+
+    E, x1, x2 = z["E"], hs("x1"), hs("x2")
+    out = {}
+    out["wcd"] = distances.wcd_block(x1, x2, E).values
+    out["c1"] = kernels.centroids(x1, E)
+    out["pair"] = kernels.pairwise_euclidean(E[:17], E[5:40]).values
+    b1, b2 = distances.rwmd_bounds(x1, x2, E)
+    out["b1"], out["b2"] = b1, b2
+    out["quadratic"] = distances.rwmd_quadratic(x1, x2, E).values
+    # exact WMD / prefiltered top-k on dyadic-weight copies of the sets: the reference
+    # solver (emd.py:153-162) raises when float32-normalised supply and demand totals
+    # differ by more than 1e-9, which happens for about half of general histograms
+    def dyadic(hs_, seed):
+        r = np.random.default_rng(seed)
+        rows = []
+        for i in range(hs_.n_rows):
+            q = hs_.row(i)
+            c = r.integers(1, 9, len(q.word_ids)).astype(np.int64)
+            c[0] += (-int(c.sum())) % 64          # total = multiple of 64 ...
+            tot = int(c.sum())
+            scale = 1 << int(np.ceil(np.log2(tot)))
+            c[0] += scale - tot                   # ... = a power of two: weights exact in f32
+            rows.append((q.word_ids, (c / scale).astype(np.float32)))
+        return corpus.HistogramSet.from_rows(rows, hs_.n_cols)
+    xd1, xd2 = dyadic(x1, 1), dyadic(x2, 2)
+    out.update(_pack("xd1", xd1))
+    out.update(_pack("xd2", xd2))
+    n_w = min(6, xd1.n_rows)
+    out["wmd0"] = np.array([emd.wmd(xd1.row(i), xd2.row(0), E) for i in range(n_w)])
+    k = 4
+    for j in range(min(2, xd2.n_rows)):
+        r, solves = emd.prefiltered_topk_wmd(xd1, xd2.row(j), E, k)
+        out[f"pf{j}_d"], out[f"pf{j}_i"], out[f"pf{j}_solves"] = r.distances, r.ids, np.int64(solves)
+    x1r, e1, _ = corpus.restrict_vocabulary(x1, E)
+    words = [f"w{i}_\u00e9" for i in range(e1.shape[0])]
+    with tempfile.TemporaryDirectory() as td:
+        f = Path(td) / "x.lcrw"
+        corpus.write_index_file(f, x1r, e1, words)
+        out["index_bytes"] = np.frombuffer(f.read_bytes(), dtype=np.uint8)
+    np.savez_compressed(OUT / f"widen_{name}.npz", **out)
+    print("widen", name, {k_: v.shape for k_, v in out.items() if hasattr(v, "shape")})
+
+
+def case_emd():
+    """solve_emd on small transport problems, including degenerate ones."""
+    from movers import emd
+    _ref()
+    rng = np.random.default_rng(21)
+    out = {}
+    shapes = [(1, 1), (1, 5), (5, 1), (3, 3), (7, 4), (12, 12), (30, 25), (60, 45)]
+    for i, (h1, h2) in enumerate(shapes):
+        s_ = rng.random(h1) + 0.05
+        d_ = rng.random(h2) + 0.05
+        s_ /= s_.sum()
+        d_ /= d_.sum()
+        c = rng.random((h1, h2)) * 10
+        if i == 3:
+            c = np.round(c)  # ties
+        plan = emd.solve_emd(emd.TransportProblem(s_, d_, c))
+        out[f"s{i}"], out[f"d{i}"], out[f"c{i}"] = s_, d_, c
+        out[f"obj{i}"] = np.float64(plan.objective)
+    np.savez_compressed(OUT / "emd.npz", **out)
+    print("emd", len(shapes))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "widen":
+    for nm in ("small_m16", "m300", "clustered", "dup_rows"):
+        case_widen(nm)
+    case_emd()
+elif __name__ == "__main__":
     case_lcrwmd("small_m16", seed=11, n1=60, n2=12, vocab=400, m=16, hlo=1, hhi=20, quadratic=True)
     case_lcrwmd("m300", seed=12, n1=48, n2=8, vocab=500, m=300, hlo=20, hhi=60)
     case_lcrwmd("clustered", seed=13, n1=40, n2=8, vocab=500, m=64, hlo=5, hhi=30, clustered=True)

@@ -388,3 +388,56 @@ def test_topk_matrix_rows_long_rows_with_ties(k, row_len):
         order = np.lexsort((cols, D[r]))[:k]
         assert np.array_equal(oi[r], order + id_base), r
         assert np.array_equal(od[r], D[r, order]), r
+
+
+@pytest.mark.gpu
+def test_load_index_to_device(tmp_path):
+    """device.load_index: the reference-written LCRW file lands in HBM bitwise, and the
+    symmetric bound computed from it equals the one from the host arrays."""
+    import torch
+    from paper_1711_07227_b200 import corpus as Cc, device, distances
+    g = np.load(GOLDEN / "widen_m300.npz")
+    f = tmp_path / "x.lcrw"
+    f.write_bytes(g["index_bytes"].tobytes())
+    hs, E, words = Cc.read_index_file(f)
+    dx, Ed, w2 = device.load_index(f)
+    assert w2 == words and dx.n_cols == hs.n_cols and dx.n_rows == hs.n_rows
+    assert np.array_equal(dx.offsets.cpu().numpy(), hs.row_offsets)
+    assert np.array_equal(dx.cols.cpu().numpy(), hs.column_ids)
+    assert np.array_equal(dx.vals.cpu().numpy(), hs.values)
+    assert torch.equal(Ed.cpu(), torch.from_numpy(E))
+    q = hs.take_rows([0, 3, 5])
+    a = distances.lcrwmd_full(hs, q, E).values
+    b = distances.lcrwmd_full(hs, q, Ed.cpu().numpy()).values
+    assert np.array_equal(a, b)
+
+
+def _abs_tol(*mats):
+    return 1e-5 * max(float(np.sqrt((np.asarray(M, np.float64) ** 2).sum(1).max())) for M in mats)
+
+
+@pytest.mark.gpu
+def test_widen_rows_gpu(widen_case):
+    """SURVEY §8f rows on the GPU vs the reference's golden outputs:
+    centroids (bitwise), pairwise_euclidean and wcd_block (Phase-1 kernel, singleton
+    segments), rwmd_bounds / rwmd_quadratic (both LC-RWMD directions)."""
+    corpus, distances, kernels = _pkg()
+    name, z, w, x1, x2, _, _ = widen_case
+    E = z["E"]
+    c1 = kernels.centroids(x1, E)
+    assert np.array_equal(c1, w["c1"]), name
+    pair = kernels.pairwise_euclidean(E[:17], E[5:40]).values
+    ok, err = rel_close(pair, w["pair"], RTOL, _abs_tol(E))
+    assert ok, (name, "pair", err)
+    assert np.all(pair[np.arange(5, 17), np.arange(0, 12)] == 0.0)  # identical rows -> exactly 0
+    wcd = distances.wcd_block(x1, x2, E).values
+    ok, err = rel_close(wcd, w["wcd"], RTOL, _abs_tol(w["c1"]))
+    assert ok, (name, "wcd", err)
+    b1, b2 = distances.rwmd_bounds(x1, x2, E)
+    for got, key in ((b1, "b1"), (b2, "b2")):
+        ok, err = rel_close(got, w[key], RTOL, _abs_tol(E))
+        assert ok, (name, key, err)
+    q = distances.rwmd_quadratic(x1, x2, E).values
+    ok, err = rel_close(q, w["quadratic"], RTOL, _abs_tol(E))
+    assert ok, (name, "quadratic", err)
+    assert np.array_equal(q, distances.lcrwmd_full(x1, x2, E).values)

@@ -169,3 +169,53 @@ def test_reverse_entry_plan_invariants(n_q, h, V):
     q = np.repeat(np.arange(n_q), np.diff(offs))
     want = sorted(zip(q.tolist(), rank[cols].tolist(), vals.astype(np.float32).tolist()))
     assert sorted(seen) == want
+
+
+@pytest.mark.parametrize("name", ["small_m16", "m300", "clustered", "dup_rows"])
+def test_index_file_matches_reference_bytes(name, tmp_path):
+    """LCRW v1 (corpus.py:17-25, 433-489): reading the reference-written file and writing
+    it back reproduces the reference's bytes exactly (tests/golden/widen_*.npz)."""
+    g = np.load(ROOT / "tests" / "golden" / f"widen_{name}.npz")
+    ref = g["index_bytes"].tobytes()
+    f = tmp_path / "ref.lcrw"
+    f.write_bytes(ref)
+    hs, E, words = C.read_index_file(f)
+    assert hs.row_offsets.dtype == np.int64 and hs.column_ids.dtype == np.int32 and E.dtype == np.float32
+    assert hs.n_cols == E.shape[0] == len(words) and words[0] == "w0_é"
+    C.write_index_file(tmp_path / "ours.lcrw", hs, E, words)
+    assert (tmp_path / "ours.lcrw").read_bytes() == ref
+
+
+def test_index_file_errors(tmp_path):
+    hs = C.HistogramSet.from_rows([(np.array([0, 2], np.int32), np.array([0.5, 0.5], np.float32))], 3)
+    E = np.arange(6, dtype=np.float32).reshape(3, 2)
+    with pytest.raises(C.CorpusError, match="inconsistent index"):
+        C.write_index_file(tmp_path / "x", hs, E, ["a", "b"])
+    C.write_index_file(tmp_path / "x", hs, E, ["a", "b", "c"])
+    raw = (tmp_path / "x").read_bytes()
+    (tmp_path / "m").write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(C.CorpusError, match="bad magic"):
+        C.read_index_file(tmp_path / "m")
+    (tmp_path / "v").write_bytes(raw[:4] + struct.pack("<I", 2) + raw[8:])
+    with pytest.raises(C.CorpusError, match="unsupported format version 2"):
+        C.read_index_file(tmp_path / "v")
+    (tmp_path / "t").write_bytes(raw[:60])
+    with pytest.raises(C.CorpusError, match="truncated"):
+        C.read_index_file(tmp_path / "t")
+    hs2, E2, w2 = C.read_index_file(tmp_path / "x")
+    assert np.array_equal(hs2.column_ids, hs.column_ids) and np.array_equal(E2, E) and w2 == ["a", "b", "c"]
+
+
+def test_read_corpus_and_labels(tmp_path):
+    """corpus.py:196-237: plain text (line-number ids, blank lines skipped), JSONL, errors."""
+    (tmp_path / "p.txt").write_text("Hello, World!\n\n  the CAT sat.  \n")
+    ids, docs = C.read_corpus(tmp_path / "p.txt")
+    assert ids == ["0", "2"] and docs == [["hello", "world"], ["the", "cat", "sat"]]
+    (tmp_path / "j.jsonl").write_text('{"id": "a", "text": "x y"}\n{"text": "Z"}\n')
+    ids, docs = C.read_corpus(tmp_path / "j.jsonl")
+    assert ids == ["a", "1"] and docs == [["x", "y"], ["z"]]
+    (tmp_path / "b.jsonl").write_text('{"id": "a", "text": "x"}\n{"id": "b"}\n')
+    with pytest.raises(C.CorpusError, match=r"b.jsonl:2: bad JSONL record"):
+        C.read_corpus(tmp_path / "b.jsonl")
+    (tmp_path / "l.txt").write_text("pos\n\nneg \n")
+    assert C.read_labels(tmp_path / "l.txt") == ["pos", "neg"]

@@ -98,3 +98,40 @@ def test_spec_spmv_and_topk():
     assert list(i) == [3]
     with pytest.raises(ValueError, match="k must be >= 1"):
         O.topk_select(np.zeros(2), np.arange(2), 0)
+
+
+def test_widen_rows_oracle(widen_case):
+    """Oracle restatements of wcd_block, centroids, pairwise_euclidean, rwmd_bounds /
+    rwmd_quadratic (distances.py:59-130, kernels.py:113-130, 201-203) vs the reference."""
+    name, z, w, x1, x2, _, _ = widen_case
+    E = z["E"]
+    assert np.array_equal(O.centroids(x1, E), w["c1"])  # bitwise (fp64 SpMM)
+    for got, key in ((O.wcd_block(x1, x2, E), "wcd"), (O.pairwise_euclidean(E[:17], E[5:40]), "pair")):
+        ok, err = rel_close(got, w[key], rtol=TOL, atol=1e-7)
+        assert ok, (name, key, err)
+    b1, b2 = O.rwmd_bounds(x1, x2, E)
+    for got, key in ((b1, "b1"), (b2, "b2"), (np.maximum(b1, b2), "quadratic")):
+        ok, err = rel_close(got, w[key], rtol=TOL, atol=1e-7)
+        assert ok, (name, key, err)
+
+
+def test_emd_oracle():
+    """solve_emd restatement (emd.py:120-194) vs the reference objective, incl. 1x1, 1xn, ties."""
+    g = np.load(GOLDEN / "emd.npz")
+    for i in range(8):
+        got = O.solve_emd_objective(g[f"s{i}"], g[f"d{i}"], g[f"c{i}"])
+        assert abs(got - float(g[f"obj{i}"])) <= 1e-9 * max(1.0, abs(float(g[f"obj{i}"]))), i
+
+
+def test_wmd_prefilter_oracle(widen_case):
+    """wmd and prefiltered_topk_wmd restatements (emd.py:199-261) vs the reference."""
+    name, z, w, _, _, xd1, xd2 = widen_case
+    E = z["E"]
+    for i, ref in enumerate(w["wmd0"]):
+        q, r = xd2.row(0), xd1.row(i)
+        got = O.wmd(r.word_ids, r.weights, q.word_ids, q.weights, E)
+        assert abs(got - ref) <= 1e-6 * max(1.0, ref), (name, i, got, ref)
+    q = xd2.row(0)
+    d, ids, solves = O.prefiltered_topk_wmd(xd1, q.word_ids, q.weights, E, 4)
+    assert np.array_equal(ids, w["pf0_i"]), name
+    assert np.allclose(d, w["pf0_d"], rtol=1e-6, atol=1e-9), name
