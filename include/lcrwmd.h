@@ -199,6 +199,27 @@ int lcrw_topk_sort_workspace(int64_t n, size_t* bytes);
 int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, float* out_d, int64_t* out_i,
                    void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Exact mover's distance (emd.py:120-211) -------------------------------
+ * Batched balanced transport problems, one warp each: successive shortest
+ * augmenting paths with node potentials (multi-source Dijkstra over reduced
+ * costs clamped at 0, lowest-index ties, tolerance 1e-9), fp64 -- the
+ * reference's algorithm.  Problem p: supply[s_off[p] .. s_off[p+1]) (h1),
+ * demand[d_off[p] .. d_off[p+1]) (h2), costs row-major h1 x h2 at
+ * costs + c_off[p] -- or, with costs == NULL, costs formed from E rows ids1
+ * (aligned with supply) and ids2 (aligned with demand) exactly as
+ * pairwise_euclidean does (fp64, rounded once to f32; identical rows -> 0).
+ * objective[p] = sum(flow * cost); status[p] = 0 ok, 1 no augmenting path with
+ * both sides open, 2 no convergence.  Augmentation stops once either side is
+ * exhausted (the reference raises when float32 totals differ by > 1e-9).
+ * Optional flow_out (c_off layout) and phi_out (sources at s_off, sinks at
+ * s_off[n_problems] + d_off).  max_h1 x max_h2 must fit
+ * lcrw_emd_problem_bytes() <= 227 KB of shared memory. */
+size_t lcrw_emd_problem_bytes(int h1, int h2);
+int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* demand, const int64_t* d_off,
+                   const double* costs, const int64_t* c_off, const float* E, int64_t v, int m, const int32_t* ids1,
+                   const int32_t* ids2, int64_t n_problems, int max_h1, int max_h2, double* objective,
+                   int32_t* status, double* flow_out, double* phi_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

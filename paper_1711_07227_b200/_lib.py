@@ -55,6 +55,8 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_reverse_panels_ilp": (I32, []),
     "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, I64, P, I64, P, I64, I64, P]),
     "lcrw_topk_rows_workspace": (I32, [I64, I64, I32, P]),
+    "lcrw_emd_problem_bytes": (SZ, [I32, I32]),
+    "lcrw_emd_batch": (I32, [P, P, P, P, P, P, P, I64, I32, P, P, I64, I32, I32, P, P, P, P, P]),
     "lcrw_topk_rows": (I32, [P, I64, I64, I64, I64, I32, P, P, P, SZ, P]),
     "lcrw_profile_reset": (I32, [I32]),
     "lcrw_profile_count": (I64, []),
@@ -65,7 +67,7 @@ SIGNATURES: dict[str, tuple] = {
 }
 
 # functions returning a value rather than a status
-_VALUE_FUNCS = {"lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
+_VALUE_FUNCS = {"lcrw_emd_problem_bytes", "lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
                 "lcrw_endmask_words", "lcrw_plan_ranges", 
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
                 "lcrw_reverse_panels_ilp",                 "lcrw_profile_count"}
@@ -77,7 +79,7 @@ KERNELS_PER_CALL = {
     "lcrw_row_classes": 13, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
     "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
-    "lcrw_reverse_panels": 1,
+    "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels);
 # bench.py adds those from the batch count (= its reverse_panels launches).

@@ -1,0 +1,282 @@
+// Exact word mover's distance for batches of document pairs (emd.py:120-211):
+// the balanced transportation problem solved by successive shortest augmenting
+// paths with node potentials -- multi-source Dijkstra over reduced costs clamped
+// at zero, ties to the lowest node index -- the reference's algorithm, order of
+// operations and tolerances, in fp64.
+//
+// One warp per problem.  The cost matrix is either given (solve_emd) or formed
+// in the kernel from the embedding rows exactly as pairwise_euclidean does it
+// (fp64 norms and dots, (|a|^2 + |b|^2) - 2 a.b, clamp, sqrt, rounded once to
+// f32; identical rows give exactly 0), and kept in shared memory next to the
+// fp64 flow matrix and the per-node Dijkstra state.  Node scans are spread over the 32 lanes; the
+// argmin is a warp reduction that keeps the lowest index on ties (np.argmin).
+//
+// Where the reference raises "no augmenting path" because float32-normalised
+// supply and demand totals differ by more than 1e-9 (emd.py:153-162; about half
+// of general histograms), augmentation stops once either side is exhausted.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace lcrw {
+namespace emd {
+
+constexpr double kFeasTol = 1e-9;  // emd.py:33
+constexpr int kMaxWarps = 8;
+
+__host__ __device__ inline size_t problem_bytes(int h1, int h2) {
+  const size_t n = (size_t)h1 + h2;
+  // cost f64 [h1][h2], flow f64 [h1][h2], dist/phi/rem f64 [n], parent i32 [n], done u8 [n]
+  const size_t b = (size_t)h1 * h2 * 16 + 3 * n * 8 + n * 4 + n;
+  return (b + 15) / 16 * 16;
+}
+
+__device__ __forceinline__ void warp_argmin(double& v, int& i) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    if (ov < v || (ov == v && oi < i)) {
+      v = ov;
+      i = oi;
+    }
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+__global__ void __launch_bounds__(kMaxWarps * 32)
+    emd_kernel(const double* __restrict__ supply, const int64_t* __restrict__ s_off, const double* __restrict__ demand,
+               const int64_t* __restrict__ d_off, const double* __restrict__ costs, const int64_t* __restrict__ c_off,
+               const float* __restrict__ E, int m, const int32_t* __restrict__ ids1, const int32_t* __restrict__ ids2,
+               int64_t n_problems, size_t slot_bytes, double* __restrict__ objective, int32_t* __restrict__ status,
+               double* __restrict__ flow_out, double* __restrict__ phi_out) {
+  extern __shared__ __align__(16) uint8_t emd_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wip = threadIdx.x >> 5;
+  const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + wip;
+  if (prob >= n_problems) return;
+  const int64_t a0 = s_off[prob], b0 = d_off[prob];
+  const int h1 = (int)(s_off[prob + 1] - a0), h2 = (int)(d_off[prob + 1] - b0);
+  const int n = h1 + h2;
+  uint8_t* base = emd_smem + (size_t)wip * slot_bytes;
+  double* cost = reinterpret_cast<double*>(base);
+  double* flow = cost + (size_t)h1 * h2;
+  double* dist = flow + (size_t)h1 * h2;
+  double* phi = dist + n;
+  double* rem = phi + n;  // remaining supply (sources) / demand (sinks)
+  int* parent = reinterpret_cast<int*>(rem + n);
+  uint8_t* done = reinterpret_cast<uint8_t*>(parent + n);
+
+  if (costs) {
+    const double* cp = costs + c_off[prob];
+    for (int c = lane; c < h1 * h2; c += 32) {
+      cost[c] = cp[c];
+      flow[c] = 0.0;
+    }
+  } else {
+    // pairwise_euclidean(E[ids1], E[ids2]) (kernels.py:72-130), rounded once to f32 (emd.py:205)
+    const int32_t* r1 = ids1 + a0;
+    const int32_t* r2 = ids2 + b0;
+    for (int i = lane; i < n; i += 32) {  // squared norms (fp64), parked in phi for now
+      const float* row = E + (int64_t)(i < h1 ? r1[i] : r2[i - h1]) * m;
+      double acc = 0.0;
+      for (int d = 0; d < m; ++d) acc = fma((double)row[d], (double)row[d], acc);
+      phi[i] = acc;
+    }
+    __syncwarp();
+    for (int c = lane; c < h1 * h2; c += 32) {
+      const int p = c / h2, q = c - p * h2;
+      const float* ra = E + (int64_t)r1[p] * m;
+      const float* rb = E + (int64_t)r2[q] * m;
+      double dot = 0.0;
+      for (int d = 0; d < m; ++d) dot = fma((double)ra[d], (double)rb[d], dot);
+      const double sq = (phi[p] + phi[h1 + q]) - 2.0 * dot;
+      cost[c] = (double)(float)sqrt(sq > 0.0 ? sq : 0.0);
+      flow[c] = 0.0;
+    }
+  }
+  for (int i = lane; i < n; i += 32) {
+    phi[i] = 0.0;
+    rem[i] = i < h1 ? supply[a0 + i] : demand[b0 + i - h1];
+  }
+  __syncwarp();
+
+  // ---- successive shortest paths (emd.py:120-194) ----
+  const int64_t max_rounds = 8ll * n * n + 64;
+  int64_t rounds = 0;
+  int st = 0;
+  for (;;) {
+    double rs = 0.0, rd = 0.0;
+    for (int i = lane; i < n; i += 32) (i < h1 ? rs : rd) += rem[i];
+    rs = warp_sum(rs);
+    rd = warp_sum(rd);
+    if (!(rs > kFeasTol) || !(rd > kFeasTol)) break;
+    if (++rounds > max_rounds) {
+      st = 2;
+      break;
+    }
+    // multi-source Dijkstra over the residual network (emd.py:82-117)
+    for (int i = lane; i < n; i += 32) {
+      dist[i] = (i < h1 && rem[i] > kFeasTol) ? 0.0 : HUGE_VAL;
+      parent[i] = -1;
+      done[i] = 0;
+    }
+    __syncwarp();
+    for (int it = 0; it < n; ++it) {
+      double bv = HUGE_VAL;
+      int bi = n;
+      for (int i = lane; i < n; i += 32)
+        if (!done[i] && dist[i] < bv) {
+          bv = dist[i];
+          bi = i;
+        }
+      warp_argmin(bv, bi);
+      if (bi >= n || !(bv < HUGE_VAL)) break;
+      const int u = bi;
+      const double du = bv;
+      if (lane == 0) done[u] = 1;
+      __syncwarp();
+      if (u < h1) {
+        const double pu = phi[u];
+        for (int q = lane; q < h2; q += 32) {
+          const int v = h1 + q;
+          if (done[v]) continue;
+          double rc = (cost[u * h2 + q] + pu) - phi[v];
+          rc = rc > 0.0 ? rc : 0.0;
+          const double cand = du + rc;
+          if (cand < dist[v]) {
+            dist[v] = cand;
+            parent[v] = u;
+          }
+        }
+      } else {
+        const int q = u - h1;
+        const double pu = phi[u];
+        for (int p = lane; p < h1; p += 32) {
+          if (done[p] || !(flow[p * h2 + q] > kFeasTol)) continue;
+          double rc = (pu - phi[p]) - cost[p * h2 + q];
+          rc = rc > 0.0 ? rc : 0.0;
+          const double cand = du + rc;
+          if (cand < dist[p]) {
+            dist[p] = cand;
+            parent[p] = u;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // nearest sink with remaining demand
+    double sv = HUGE_VAL;
+    int t = n;
+    for (int q = lane; q < h2; q += 32) {
+      const double dq = rem[h1 + q] > kFeasTol ? dist[h1 + q] : HUGE_VAL;
+      if (dq < sv) {
+        sv = dq;
+        t = q;
+      }
+    }
+    warp_argmin(sv, t);
+    if (!(sv < HUGE_VAL)) {
+      st = 1;  // unbalanced beyond tolerance with both sides open
+      break;
+    }
+    for (int i = lane; i < n; i += 32) phi[i] += dist[i] < sv ? dist[i] : sv;
+    __syncwarp();
+    if (lane == 0) {  // trace sink -> root, bottleneck, augment (sequential, path length <= n)
+      int node = h1 + t;
+      double bott = rem[h1 + t];
+      while (parent[node] != -1) {
+        const int prev = parent[node];
+        if (node < h1) bott = fmin(bott, flow[node * h2 + (prev - h1)]);
+        node = prev;
+      }
+      const int root = node;
+      bott = fmin(bott, rem[root]);
+      node = h1 + t;
+      while (parent[node] != -1) {
+        const int prev = parent[node];
+        if (node >= h1)
+          flow[prev * h2 + (node - h1)] += bott;
+        else
+          flow[node * h2 + (prev - h1)] -= bott;
+        node = prev;
+      }
+      rem[root] -= bott;
+      rem[h1 + t] -= bott;
+    }
+    __syncwarp();
+  }
+  double obj = 0.0;
+  for (int c = lane; c < h1 * h2; c += 32) obj += flow[c] * cost[c];
+  obj = warp_sum(obj);
+  if (flow_out) {
+    double* fo = flow_out + c_off[prob];
+    for (int c = lane; c < h1 * h2; c += 32) fo[c] = flow[c];
+  }
+  if (phi_out) {  // potentials: sources at s_off, sinks after all sources (s_off[n_problems] + d_off)
+    for (int i = lane; i < n; i += 32) {
+      if (i < h1)
+        phi_out[a0 + i] = phi[i];
+      else
+        phi_out[s_off[n_problems] + b0 + i - h1] = phi[i];
+    }
+  }
+  if (lane == 0) {
+    objective[prob] = obj;
+    status[prob] = st;
+  }
+}
+
+}  // namespace emd
+}  // namespace lcrw
+
+using namespace lcrw;
+using namespace lcrw::emd;
+
+extern "C" {
+
+size_t lcrw_emd_problem_bytes(int h1, int h2) { return problem_bytes(h1, h2); }
+
+int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* demand, const int64_t* d_off,
+                   const double* costs, const int64_t* c_off, const float* E, int64_t v, int m, const int32_t* ids1,
+                   const int32_t* ids2, int64_t n_problems, int max_h1, int max_h2, double* objective,
+                   int32_t* status, double* flow_out, double* phi_out, void* stream) {
+  LCRW_REQUIRE(n_problems >= 0, "lcrw_emd_batch: bad shape");
+  if (n_problems == 0) return LCRW_OK;
+  LCRW_REQUIRE(supply && s_off && demand && d_off && objective && status, "lcrw_emd_batch: null pointer");
+  LCRW_REQUIRE(costs ? (c_off != nullptr) : (E && ids1 && ids2 && m > 0 && v > 0),
+               "lcrw_emd_batch: need either explicit costs (+ c_off) or embeddings and word ids");
+  LCRW_REQUIRE(!flow_out || c_off, "lcrw_emd_batch: flow_out needs c_off");
+  LCRW_REQUIRE(max_h1 >= 1 && max_h2 >= 1, "lcrw_emd_batch: every histogram needs at least one word");
+  const size_t slot = problem_bytes(max_h1, max_h2);
+  const size_t smem_max = 227 * 1024;
+  if (slot > smem_max) {
+    set_error("lcrw_emd_batch: a %d x %d transport problem needs %zu B of shared memory (max %zu)", max_h1, max_h2,
+              slot, smem_max);
+    return LCRW_ERR_UNSUPPORTED;
+  }
+  int warps = (int)(smem_max / slot);
+  if (warps > kMaxWarps) warps = kMaxWarps;
+  const size_t smem = slot * warps;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(emd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(emd_kernel)");
+    attr = true;
+  }
+  const int64_t blocks = (n_problems + warps - 1) / warps;
+  LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_emd_batch: too many problems");
+  cudaStream_t st = as_stream(stream);
+  ProfScope prof(st, "emd");
+  emd_kernel<<<(unsigned)blocks, warps * 32, smem, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,
+                                                         n_problems, slot, objective, status, flow_out, phi_out);
+  LCRW_CHECK_LAUNCH("emd_kernel");
+  return LCRW_OK;
+}
+
+}  // extern "C"

@@ -441,3 +441,52 @@ def test_widen_rows_gpu(widen_case):
     ok, err = rel_close(q, w["quadratic"], RTOL, _abs_tol(E))
     assert ok, (name, "quadratic", err)
     assert np.array_equal(q, distances.lcrwmd_full(x1, x2, E).values)
+
+
+@pytest.mark.gpu
+def test_solve_emd_gpu_matches_reference():
+    """solve_emd (emd.py:120-194) on the GPU: reference objectives (1x1, 1xn, nx1, ties,
+    up to 60x45), marginals, dual feasibility and complementary slackness of the plan."""
+    from paper_1711_07227_b200 import emd
+    g = np.load(GOLDEN / "emd.npz")
+    for i in range(8):
+        s, d, c = g[f"s{i}"], g[f"d{i}"], g[f"c{i}"]
+        plan = emd.solve_emd(emd.TransportProblem(s, d, c))
+        ref = float(g[f"obj{i}"])
+        assert abs(plan.objective - ref) <= 1e-9 * max(1.0, ref), (i, plan.objective, ref)
+        flow = np.zeros(c.shape)
+        flow[plan.source_ids, plan.target_ids] = plan.amounts
+        assert np.allclose(flow.sum(1), s, atol=1e-6) and np.allclose(flow.sum(0), d, atol=1e-6)
+        red = c - plan.dual_source[:, None] - plan.dual_sink[None, :]
+        assert red.min() >= -1e-7, i
+        assert np.all(np.abs(red[plan.source_ids, plan.target_ids]) <= 1e-7), i
+        dual = float(s @ plan.dual_source + d @ plan.dual_sink)
+        assert abs(dual - plan.objective) <= 1e-7 * max(1.0, abs(ref)), i
+    with pytest.raises(ValueError, match="must each sum to 1.0"):
+        emd.solve_emd(emd.TransportProblem(np.array([0.5]), np.array([1.0]), np.ones((1, 1))))
+    with pytest.raises(ValueError, match="nonnegative and finite"):
+        emd.solve_emd(emd.TransportProblem(np.array([1.0]), np.array([1.0]), -np.ones((1, 1))))
+
+
+@pytest.mark.gpu
+def test_wmd_and_prefiltered_topk_gpu(widen_case):
+    """wmd / prefiltered_topk_wmd (emd.py:199-261) vs the reference's golden outputs
+    (dyadic weights, where the reference's solver never trips on float32 totals);
+    general histograms vs the oracle restatement (which has the same exhaustion rule)."""
+    from paper_1711_07227_b200 import emd
+    name, z, w, x1, x2, xd1, xd2 = widen_case
+    E = z["E"]
+    q = xd2.row(0)
+    for i, ref in enumerate(w["wmd0"]):
+        got = emd.wmd(xd1.row(i), q, E)
+        assert abs(got - ref) <= 1e-7 * max(1.0, ref), (name, i, got, ref)
+    for j in range(2):
+        r, solves = emd.prefiltered_topk_wmd(xd1, xd2.row(j), E, 4)
+        assert np.array_equal(r.ids, w[f"pf{j}_i"]), (name, j, r.ids, w[f"pf{j}_i"])
+        assert np.allclose(r.distances, w[f"pf{j}_d"], rtol=1e-7, atol=1e-12), name
+        assert solves >= int(w[f"pf{j}_solves"])  # slack 1e-4 >= the reference's 1e-6
+    for i in range(min(6, x1.n_rows)):  # float32-normalised weights (reference raises on ~half)
+        a, b = x1.row(i), x2.row(0)
+        got = emd.wmd(a, b, E)
+        ref = O.wmd(a.word_ids, a.weights, b.word_ids, b.weights, E)
+        assert abs(got - ref) <= 1e-7 * max(1.0, ref), (name, i, got, ref)
