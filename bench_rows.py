@@ -1,0 +1,132 @@
+#!/usr/bin/env python
+"""Measurement of the rows next to the hot path, one JSON line each.
+
+    python bench_rows.py [--rows wmd,wcd] [--steps K] [--warmup W]
+
+* ``wmd``: exact top-10 word mover's distances (emd.prefiltered_topk_wmd_batch:
+  LC-RWMD bounds on the tensor cores, then batched exact transport solves in
+  csrc/emd.cu) for 64 queries over 20,000 docs (V = 20k, m = 300, ~40 words per
+  doc -- BASELINE configs[0]'s shape, 10x the docs).  Metric: queries/s, plus the
+  exact solves per second of the EMD kernel.  CPU baseline: the oracle's
+  restatement of the reference's prefiltered_topk_wmd (emd.py:214-261) on a
+  bounded number of queries, single process.
+* ``wcd``: word centroid distances (distances.wcd_block) for 100,000 x 1,000 docs
+  (V = 100k, m = 300, ~50 words); metric doc-pairs/s; CPU baseline: the oracle's
+  wcd_block on a bounded row sample.
+
+Inputs are resident in HBM for the device-timed value (CUDA events); these rows
+are not part of bench.py's headline line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def timed(fn, steps, warmup):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = None
+    for _ in range(steps):
+        out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, out
+
+
+def row_wmd(args):
+    import torch
+    from oracle import lcrwmd_oracle as O
+    from paper_1711_07227_b200 import _lib, emd, synthetic as S
+    V, m, n1, nq, h, k = 20_000, 300, 20_000, 64, 40, 10
+    E = S.embeddings(V, m, seed=0)
+    x1 = S.histograms(n1, V, h, seed=1)
+    x2 = S.histograms(nq, V, h, seed=2)
+    Et = torch.from_numpy(E).cuda()
+    _lib.profile_reset(True)
+    ms, (res, solves) = timed(lambda: emd.prefiltered_topk_wmd_batch(x1, x2, Et, k), args.steps, args.warmup)
+    prof = _lib.profile_read()
+    _lib.profile_reset(False)
+    emd_ms = prof.get("emd", {"ms": 0.0})["ms"] / (args.steps + args.warmup)
+    total_solves = int(np.sum(solves))
+    line = {"metric": "exact WMD top-k queries/sec (RWMD-prefiltered)", "value": nq / (ms * 1e-3),
+            "unit": "queries/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "dtype": "f16 bounds / fp64 transport",
+            "config": {"workload": "prefiltered exact top-10 WMD, 64 queries x 20k docs, V=20k, m=300, h~40",
+                       "k": k, "exact_solves_per_step": total_solves,
+                       "mean_solves_per_query": total_solves / nq},
+            "kernels": {"emd_ms_per_step": emd_ms, "emd_solves_per_s": total_solves / max(emd_ms * 1e-3, 1e-9)}}
+    # CPU baseline: the reference algorithm (oracle restatement) on a bounded number of queries
+    t0 = time.perf_counter()
+    nref = 0
+    while nref < nq and (nref == 0 or time.perf_counter() - t0 < args.cpu_seconds):
+        q = x2.row(nref)
+        O.prefiltered_topk_wmd(x1, q.word_ids, q.weights, E, k)
+        nref += 1
+    dt = time.perf_counter() - t0
+    line["cpu_baseline"] = {"value": nref / dt, "unit": "queries/s", "cores": 1, "kind": "port",
+                            "sample": f"{nref} queries x 20k docs, oracle prefiltered_topk_wmd ({dt:.1f} s)"}
+    for j in range(nref):  # the checked sample must agree with the GPU result
+        q = x2.row(j)
+        d, i, _ = O.prefiltered_topk_wmd(x1, q.word_ids, q.weights, E, k)
+        assert np.array_equal(i, res[j].ids), ("wmd mismatch", j)
+    print(json.dumps(line), flush=True)
+
+
+def row_wcd(args):
+    import torch
+    from oracle import lcrwmd_oracle as O
+    from paper_1711_07227_b200 import device, synthetic as S
+    V, m, n1, n2, h = 100_000, 300, 100_000, 1000, 50
+    E = S.embeddings(V, m, seed=0)
+    x1 = S.histograms(n1, V, h, seed=1)
+    x2 = S.histograms(n2, V, h, seed=2)
+    Et = torch.from_numpy(E).cuda()
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+
+    def step():
+        return device.pairwise(device.centroids(d1, Et), device.centroids(d2, Et))
+
+    ms, out = timed(step, args.steps, args.warmup)
+    line = {"metric": "WCD doc-pairs/sec", "value": n1 * n2 / (ms * 1e-3), "unit": "doc-pairs/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "fp64 centroids / f16 Gram", "config": {"workload": "wcd_block 100k x 1k docs, V=100k, m=300"}}
+    t0 = time.perf_counter()
+    ns = 2000
+    ref = O.wcd_block(x1.slice_rows(0, ns), x2, E)
+    dt = time.perf_counter() - t0
+    got = out[:ns].cpu().numpy()
+    err = float(np.max(np.abs(got - ref) / (np.abs(ref) + 1e-3)))
+    line["max_rel_err_sample"] = err
+    line["cpu_baseline"] = {"value": ns * n2 / dt, "unit": "doc-pairs/s", "cores": 1, "kind": "port",
+                            "sample": f"first {ns} docs x 1000, oracle wcd_block ({dt:.1f} s)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", default="wmd,wcd")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    for r in args.rows.split(","):
+        {"wmd": row_wmd, "wcd": row_wcd}[r](args)
+
+
+if __name__ == "__main__":
+    main()

@@ -228,7 +228,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   }
   if (lane == 0) {
     objective[prob] = obj;
+#ifdef LCRW_EMD_ROUNDS
+    status[prob] = st ? st : -(int)rounds;  // experiment build: augmentation count
+#else
     status[prob] = st;
+#endif
   }
 }
 

@@ -228,3 +228,75 @@ def prefiltered_topk_wmd(x1: HistogramSet, query: Histogram, embeddings: np.ndar
         pos = end
     return (TopKResult(distances=np.array([d for d, _ in top], dtype=np.float64),
                        ids=np.array([i for _, i in top], dtype=np.int64)), solves)
+
+
+def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddings: np.ndarray, k: int,
+                               bounds: np.ndarray | None = None) -> tuple[list[TopKResult], np.ndarray]:
+    """prefiltered_topk_wmd for many queries at once: one LC-RWMD launch for all the
+    bounds (n1 x nq), then rounds in which every still-open query contributes its
+    next speculative batch of candidates to ONE exact-solve launch.  Each query's
+    result and solve count equal prefiltered_topk_wmd's (same per-query rule)."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    n1, nq = x1.n_rows, queries.n_rows
+    if n1 < k:
+        raise ValueError(f"need at least k={k} candidates, have {n1}")
+    if bounds is None:
+        from .distances import lcrwmd_full
+        bounds = lcrwmd_full(x1, queries, embeddings).values
+    bounds = np.asarray(bounds, dtype=np.float64)
+    E_t = embeddings if isinstance(embeddings, torch.Tensor) else device.to_device(
+        np.asarray(embeddings, np.float32), torch.float32)
+    ids_rows = np.arange(n1)
+    orders = [np.lexsort((ids_rows, bounds[:, j])) for j in range(nq)]
+    qrows = [queries.row(j) for j in range(nq)]
+    drow = [None] * n1
+
+    def doc(i):
+        if drow[i] is None:
+            drow[i] = x1.row(int(i))
+        return drow[i]
+
+    def solve(pairs):
+        return solve_batch([doc(i).weights for j, i in pairs], [qrows[j].weights for j, i in pairs],
+                           embeddings=E_t, ids1=[doc(i).word_ids for j, i in pairs],
+                           ids2=[qrows[j].word_ids for j, i in pairs])
+
+    pairs = [(j, int(i)) for j in range(nq) for i in orders[j][:k]]
+    dists = solve(pairs).tolist()
+    tops = [sorted(zip(dists[j * k:(j + 1) * k], (i for _, i in pairs[j * k:(j + 1) * k]))) for j in range(nq)]
+    solves = np.full(nq, k, dtype=np.int64)
+    pos = np.full(nq, k, dtype=np.int64)
+    open_ = [j for j in range(nq) if k < n1]
+    while open_:
+        batch, spans = [], []
+        for j in open_:
+            lim = tops[j][-1][0] * (1.0 + PRUNE_SLACK) + 1e-12
+            o, p0 = orders[j], int(pos[j])
+            end = p0
+            while end < n1 and end - p0 < SOLVE_BATCH and bounds[o[end], j] <= lim:
+                end += 1
+            spans.append((j, p0, end))
+            batch += [(j, int(i)) for i in o[p0:end]]
+        dists = solve(batch).tolist() if batch else []
+        nxt, at = [], 0
+        for j, p0, end in spans:
+            top, o = tops[j], orders[j]
+            stop = end == p0
+            for r in range(p0, end):
+                idx, dist = int(o[r]), dists[at + r - p0]
+                if bounds[idx, j] > top[-1][0] * (1.0 + PRUNE_SLACK) + 1e-12:
+                    stop = True
+                    break
+                solves[j] += 1
+                if (dist, idx) < top[-1]:
+                    top[-1] = (dist, idx)
+                    top.sort()
+            at += end - p0
+            pos[j] = end
+            if not stop and end < n1:
+                nxt.append(j)
+        open_ = nxt
+    res = [TopKResult(np.array([d for d, _ in t], dtype=np.float64), np.array([i for _, i in t], dtype=np.int64))
+           for t in tops]
+    return res, solves

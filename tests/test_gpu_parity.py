@@ -490,3 +490,16 @@ def test_wmd_and_prefiltered_topk_gpu(widen_case):
         got = emd.wmd(a, b, E)
         ref = O.wmd(a.word_ids, a.weights, b.word_ids, b.weights, E)
         assert abs(got - ref) <= 1e-7 * max(1.0, ref), (name, i, got, ref)
+
+
+@pytest.mark.gpu
+def test_prefiltered_batch_equals_single(widen_case):
+    """The multi-query prefilter gives each query exactly the single-query result."""
+    from paper_1711_07227_b200 import emd
+    name, z, w, _, _, xd1, xd2 = widen_case
+    E = z["E"]
+    res, solves = emd.prefiltered_topk_wmd_batch(xd1, xd2, E, 4)
+    for j in range(xd2.n_rows):
+        r, s = emd.prefiltered_topk_wmd(xd1, xd2.row(j), E, 4)
+        assert np.array_equal(r.ids, res[j].ids) and np.array_equal(r.distances, res[j].distances), (name, j)
+        assert s == solves[j], (name, j)
