@@ -236,6 +236,258 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Small problems (h1 + h2 <= 32 * SLOTS): the per-node Dijkstra state lives in
+// registers, node i in lane i % 32, slot i / 32.  The argmin is three integer
+// warp reductions over the bit pattern of the (non-negative) distance and the
+// node index -- the lexicographic (distance, index) minimum of np.argmin -- which
+// is much shorter than a shuffle tree of doubles.  Same arithmetic as above.
+// ---------------------------------------------------------------------------
+template <int SLOTS>
+__global__ void __launch_bounds__(kMaxWarps * 32)
+    emd_kernel_reg(const double* __restrict__ supply, const int64_t* __restrict__ s_off,
+                   const double* __restrict__ demand, const int64_t* __restrict__ d_off,
+                   const double* __restrict__ costs, const int64_t* __restrict__ c_off, const float* __restrict__ E,
+                   int m, const int32_t* __restrict__ ids1, const int32_t* __restrict__ ids2, int64_t n_problems,
+                   size_t slot_bytes, double* __restrict__ objective, int32_t* __restrict__ status,
+                   double* __restrict__ flow_out, double* __restrict__ phi_out) {
+  extern __shared__ __align__(16) uint8_t emd_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wip = threadIdx.x >> 5;
+  const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + wip;
+  if (prob >= n_problems) return;
+  const int64_t a0 = s_off[prob], b0 = d_off[prob];
+  const int h1 = (int)(s_off[prob + 1] - a0), h2 = (int)(d_off[prob + 1] - b0);
+  const int n = h1 + h2;
+  uint8_t* base = emd_smem + (size_t)wip * slot_bytes;
+  double* cost = reinterpret_cast<double*>(base);
+  double* flow = cost + (size_t)h1 * h2;
+  double* phis = flow + (size_t)h1 * h2;              // potentials (broadcast reads)
+  int* parent = reinterpret_cast<int*>(phis + n);     // written on relaxation, read by the path trace
+
+  if (costs) {
+    const double* cp = costs + c_off[prob];
+    for (int c = lane; c < h1 * h2; c += 32) {
+      cost[c] = cp[c];
+      flow[c] = 0.0;
+    }
+  } else {
+    const int32_t* r1 = ids1 + a0;
+    const int32_t* r2 = ids2 + b0;
+    for (int i = lane; i < n; i += 32) {
+      const float* row = E + (int64_t)(i < h1 ? r1[i] : r2[i - h1]) * m;
+      double acc = 0.0;
+      for (int d = 0; d < m; ++d) acc = fma((double)row[d], (double)row[d], acc);
+      phis[i] = acc;
+    }
+    __syncwarp();
+    for (int c = lane; c < h1 * h2; c += 32) {
+      const int p = c / h2, q = c - p * h2;
+      const float* ra = E + (int64_t)r1[p] * m;
+      const float* rb = E + (int64_t)r2[q] * m;
+      double dot = 0.0;
+      for (int d = 0; d < m; ++d) dot = fma((double)ra[d], (double)rb[d], dot);
+      const double sq = (phis[p] + phis[h1 + q]) - 2.0 * dot;
+      cost[c] = (double)(float)sqrt(sq > 0.0 ? sq : 0.0);
+      flow[c] = 0.0;
+    }
+    __syncwarp();
+  }
+  double phi[SLOTS], rem[SLOTS], dist[SLOTS];
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j) {
+    const int i = lane + 32 * j;
+    phi[j] = 0.0;
+    rem[j] = i < h1 ? supply[a0 + i] : (i < n ? demand[b0 + i - h1] : 0.0);
+    if (i < n) phis[i] = 0.0;
+  }
+  __syncwarp();
+
+  const int64_t max_rounds = 8ll * n * n + 64;
+  int64_t rounds = 0;
+  int st = 0;
+  for (;;) {
+    double rs = 0.0, rd = 0.0;
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      if (i < h1) rs += rem[j];
+      else if (i < n) rd += rem[j];
+    }
+    rs = warp_sum(rs);
+    rd = warp_sum(rd);
+    if (!(rs > kFeasTol) || !(rd > kFeasTol)) break;
+    if (++rounds > max_rounds) {
+      st = 2;
+      break;
+    }
+    uint32_t done = 0;
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      dist[j] = (i < h1 && rem[j] > kFeasTol) ? 0.0 : HUGE_VAL;
+      if (i < n) parent[i] = -1;
+      if (i >= n) done |= 1u << j;
+    }
+    __syncwarp();
+    for (int it = 0; it < n; ++it) {
+      double bv = HUGE_VAL;
+      int bi = 0x7FFFFFFF;
+#pragma unroll
+      for (int j = 0; j < SLOTS; ++j)
+        if (!((done >> j) & 1u) && dist[j] < bv) {
+          bv = dist[j];
+          bi = lane + 32 * j;
+        }
+      // lexicographic (distance, index) minimum: non-negative doubles order like their bits
+      const uint32_t hi = (uint32_t)__double2hiint(bv);
+      const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+      const uint32_t lo = hi == mhi ? (uint32_t)__double2loint(bv) : 0xFFFFFFFFu;
+      const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
+      const uint32_t ix = (hi == mhi && lo == mlo) ? (uint32_t)bi : 0xFFFFFFFFu;
+      const int u = (int)__reduce_min_sync(0xffffffffu, ix);
+      const double du = __hiloint2double((int)mhi, (int)mlo);
+      if (u >= n || !(du < HUGE_VAL)) break;
+      if (lane == (u & 31)) done |= 1u << (u >> 5);
+      const double pu = phis[u];
+      if (u < h1) {
+        const double* crow = cost + u * h2;
+#pragma unroll
+        for (int j = 0; j < SLOTS; ++j) {
+          const int v = lane + 32 * j;
+          if (v < h1 || v >= n || ((done >> j) & 1u)) continue;
+          double rc = (crow[v - h1] + pu) - phi[j];
+          rc = rc > 0.0 ? rc : 0.0;
+          const double cand = du + rc;
+          if (cand < dist[j]) {
+            dist[j] = cand;
+            parent[v] = u;
+          }
+        }
+      } else {
+        const int q = u - h1;
+#pragma unroll
+        for (int j = 0; j < SLOTS; ++j) {
+          const int pn = lane + 32 * j;
+          if (pn >= h1 || ((done >> j) & 1u) || !(flow[pn * h2 + q] > kFeasTol)) continue;
+          double rc = (pu - phi[j]) - cost[pn * h2 + q];
+          rc = rc > 0.0 ? rc : 0.0;
+          const double cand = du + rc;
+          if (cand < dist[j]) {
+            dist[j] = cand;
+            parent[pn] = u;
+          }
+        }
+      }
+    }
+    // nearest sink with remaining demand
+    double sv = HUGE_VAL;
+    int t = 0x7FFFFFFF;
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      if (i >= h1 && i < n && rem[j] > kFeasTol && dist[j] < sv) {
+        sv = dist[j];
+        t = i - h1;
+      }
+    }
+    {
+      const uint32_t hi = (uint32_t)__double2hiint(sv);
+      const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+      const uint32_t lo = hi == mhi ? (uint32_t)__double2loint(sv) : 0xFFFFFFFFu;
+      const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
+      const uint32_t ix = (hi == mhi && lo == mlo) ? (uint32_t)t : 0xFFFFFFFFu;
+      t = (int)__reduce_min_sync(0xffffffffu, ix);
+      sv = __hiloint2double((int)mhi, (int)mlo);
+    }
+    if (!(sv < HUGE_VAL)) {
+      st = 1;
+      break;
+    }
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      phi[j] += dist[j] < sv ? dist[j] : sv;
+      if (i < n) phis[i] = phi[j];
+    }
+    __syncwarp();
+    // path trace (lane 0) -> bottleneck -> augment; remaining amounts live in registers,
+    // so the root and sink updates are applied by their owner lanes afterwards
+    int root = 0;
+    double bott = 0.0;
+    const int sink = h1 + t;
+    double rem_sink = 0.0;
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const double r = __shfl_sync(0xffffffffu, rem[j], sink & 31);
+      if ((sink >> 5) == j) rem_sink = r;
+    }
+    if (lane == 0) {
+      int node = sink;
+      bott = rem_sink;
+      while (parent[node] != -1) {
+        const int prev = parent[node];
+        if (node < h1) bott = fmin(bott, flow[node * h2 + (prev - h1)]);
+        node = prev;
+      }
+      root = node;
+    }
+    root = __shfl_sync(0xffffffffu, root, 0);
+    double rem_root = 0.0;
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const double r = __shfl_sync(0xffffffffu, rem[j], root & 31);
+      if ((root >> 5) == j) rem_root = r;
+    }
+    if (lane == 0) {
+      bott = fmin(bott, rem_root);
+      int node = sink;
+      while (parent[node] != -1) {
+        const int prev = parent[node];
+        if (node >= h1)
+          flow[prev * h2 + (node - h1)] += bott;
+        else
+          flow[node * h2 + (prev - h1)] -= bott;
+        node = prev;
+      }
+    }
+    bott = __shfl_sync(0xffffffffu, bott, 0);
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      if (i == root) rem[j] -= bott;
+      if (i == sink) rem[j] -= bott;
+    }
+    __syncwarp();
+  }
+  double obj = 0.0;
+  for (int c = lane; c < h1 * h2; c += 32) obj += flow[c] * cost[c];
+  obj = warp_sum(obj);
+  if (flow_out) {
+    double* fo = flow_out + c_off[prob];
+    for (int c = lane; c < h1 * h2; c += 32) fo[c] = flow[c];
+  }
+  if (phi_out) {
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      if (i < h1)
+        phi_out[a0 + i] = phi[j];
+      else if (i < n)
+        phi_out[s_off[n_problems] + b0 + i - h1] = phi[j];
+    }
+  }
+  if (lane == 0) {
+    objective[prob] = obj;
+#ifdef LCRW_EMD_ROUNDS
+    status[prob] = st ? st : -(int)rounds;
+#else
+    status[prob] = st;
+#endif
+  }
+}
+
 }  // namespace emd
 }  // namespace lcrw
 
@@ -245,6 +497,12 @@ using namespace lcrw::emd;
 extern "C" {
 
 size_t lcrw_emd_problem_bytes(int h1, int h2) { return problem_bytes(h1, h2); }
+
+static size_t problem_bytes_reg(int h1, int h2) {
+  const size_t n = (size_t)h1 + h2;
+  const size_t b = (size_t)h1 * h2 * 16 + n * 8 + n * 4;  // cost, flow, phi, parent
+  return (b + 15) / 16 * 16;
+}
 
 int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* demand, const int64_t* d_off,
                    const double* costs, const int64_t* c_off, const float* E, int64_t v, int m, const int32_t* ids1,
@@ -257,7 +515,9 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
                "lcrw_emd_batch: need either explicit costs (+ c_off) or embeddings and word ids");
   LCRW_REQUIRE(!flow_out || c_off, "lcrw_emd_batch: flow_out needs c_off");
   LCRW_REQUIRE(max_h1 >= 1 && max_h2 >= 1, "lcrw_emd_batch: every histogram needs at least one word");
-  const size_t slot = problem_bytes(max_h1, max_h2);
+  const int nmax = max_h1 + max_h2;
+  const int slots = nmax <= 32 ? 1 : nmax <= 64 ? 2 : nmax <= 96 ? 3 : nmax <= 128 ? 4 : 0;
+  const size_t slot = slots ? problem_bytes_reg(max_h1, max_h2) : problem_bytes(max_h1, max_h2);
   const size_t smem_max = 227 * 1024;
   if (slot > smem_max) {
     set_error("lcrw_emd_batch: a %d x %d transport problem needs %zu B of shared memory (max %zu)", max_h1, max_h2,
@@ -269,16 +529,29 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   const size_t smem = slot * warps;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(emd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(emd_kernel)");
+    const void* fns[5] = {(const void*)emd_kernel, (const void*)emd_kernel_reg<1>, (const void*)emd_kernel_reg<2>,
+                          (const void*)emd_kernel_reg<3>, (const void*)emd_kernel_reg<4>};
+    for (const void* f : fns) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(emd kernels)");
+    }
     attr = true;
   }
   const int64_t blocks = (n_problems + warps - 1) / warps;
   LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_emd_batch: too many problems");
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "emd");
-  emd_kernel<<<(unsigned)blocks, warps * 32, smem, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,
-                                                         n_problems, slot, objective, status, flow_out, phi_out);
+#define LCRW_EMD_LAUNCH(K)                                                                                      \
+  K<<<(unsigned)blocks, warps * 32, smem, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,   \
+                                               n_problems, slot, objective, status, flow_out, phi_out)
+  switch (slots) {
+    case 1: LCRW_EMD_LAUNCH(emd_kernel_reg<1>); break;
+    case 2: LCRW_EMD_LAUNCH(emd_kernel_reg<2>); break;
+    case 3: LCRW_EMD_LAUNCH(emd_kernel_reg<3>); break;
+    case 4: LCRW_EMD_LAUNCH(emd_kernel_reg<4>); break;
+    default: LCRW_EMD_LAUNCH(emd_kernel); break;
+  }
+#undef LCRW_EMD_LAUNCH
   LCRW_CHECK_LAUNCH("emd_kernel");
   return LCRW_OK;
 }
