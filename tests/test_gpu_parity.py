@@ -503,3 +503,47 @@ def test_prefiltered_batch_equals_single(widen_case):
         r, s = emd.prefiltered_topk_wmd(xd1, xd2.row(j), E, 4)
         assert np.array_equal(r.ids, res[j].ids) and np.array_equal(r.distances, res[j].distances), (name, j)
         assert s == solves[j], (name, j)
+
+
+@pytest.mark.gpu
+def test_engine_index_and_partition_invariance(tmp_path):
+    """SPEC.md engine (333-383): build -> save -> open is bitwise, run_query is identical
+    for P in {1, 2, 3, 5} for every method, self-exclusion drops the query's own id,
+    k = 1 without it returns the query itself at distance 0, rwmd == lc-rwmd, and the
+    pruned exact WMD equals the exhaustive one."""
+    from paper_1711_07227_b200 import corpus as Cc, engine, synthetic as S
+    rng = np.random.default_rng(3)
+    V, m = 600, 24
+    words = [f"t{i}" for i in range(V)]
+    vocab = Cc.Vocabulary.from_words(words)
+    E = S.embeddings(V, m, seed=4)
+    docs = [[words[int(t)] for t in rng.integers(0, V, int(rng.integers(3, 15)))] + ["zzz-oov"] for _ in range(37)]
+    labels = [f"L{i % 3}" for i in range(37)]
+    idx = engine.build_index(docs, vocab, E, stopwords=frozenset({"t0", "t1"}), labels=labels)
+    engine.save_index(idx, tmp_path / "i.lcrw")
+    back = engine.open_index(tmp_path / "i.lcrw")
+    assert back.words == idx.words and back.labels == labels
+    assert np.array_equal(back.embeddings, idx.embeddings)
+    assert np.array_equal(back.docs.row_offsets, idx.docs.row_offsets)
+    assert np.array_equal(back.docs.column_ids, idx.docs.column_ids)
+    assert np.array_equal(back.docs.values, idx.docs.values)
+    qids = [2, 7, 30]
+    queries = idx.docs.take_rows(qids)
+    for method in ("lc-rwmd", "rwmd", "wcd", "wmd-pruned"):
+        ref = engine.run_query(back, queries, engine.QueryPlan(method=method, k=4))
+        for P in (2, 3, 5):
+            got = engine.run_query(back, queries, engine.QueryPlan(method=method, k=4, partitions=P))
+            for a, b in zip(ref, got):
+                assert np.array_equal(a.ids, b.ids) and np.array_equal(a.distances, b.distances), (method, P)
+        own = engine.run_query(back, queries, engine.QueryPlan(method=method, k=1))
+        assert [int(t.ids[0]) for t in own] == qids and all(float(t.distances[0]) == 0.0 for t in own), method
+        ex = engine.run_query(back, queries, engine.QueryPlan(method=method, k=3, self_exclusion=True, partitions=2),
+                              query_ids=qids)
+        assert all(q not in t.ids for q, t in zip(qids, ex)) and all(len(t.ids) == 3 for t in ex), method
+    lc = engine.run_query(back, queries, engine.QueryPlan(method="lc-rwmd", k=5))
+    rw = engine.run_query(back, queries, engine.QueryPlan(method="rwmd", k=5))
+    assert all(np.array_equal(a.ids, b.ids) for a, b in zip(lc, rw))
+    ex_all = engine.run_query(back, queries, engine.QueryPlan(method="wmd", k=4, partitions=3))
+    pr = engine.run_query(back, queries, engine.QueryPlan(method="wmd-pruned", k=4))
+    for a, b in zip(ex_all, pr):
+        assert np.array_equal(a.ids, b.ids) and np.allclose(a.distances, b.distances, rtol=1e-12, atol=0)

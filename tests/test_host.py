@@ -219,3 +219,14 @@ def test_read_corpus_and_labels(tmp_path):
         C.read_corpus(tmp_path / "b.jsonl")
     (tmp_path / "l.txt").write_text("pos\n\nneg \n")
     assert C.read_labels(tmp_path / "l.txt") == ["pos", "neg"]
+
+
+def test_query_plan_validation():
+    from paper_1711_07227_b200.engine import QueryPlan
+    QueryPlan().validate()
+    with pytest.raises(ValueError, match="unknown method"):
+        QueryPlan(method="bm25").validate()
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        QueryPlan(k=0).validate()
+    with pytest.raises(ValueError, match="partitions must be >= 1"):
+        QueryPlan(partitions=0).validate()
