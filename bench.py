@@ -53,6 +53,14 @@ CONFIGS = {
                workload="symmetric LC-RWMD top-10, 2000 docs x 64 queries, V=20k, m=300, h~40 (BASELINE configs[0])"),
     "mid": dict(n_docs=100_000, n_queries=256, vocab=50_000, dim=300, h=50, k=10,
                 workload="symmetric LC-RWMD top-10, 100k docs x 256 queries, V=50k, m=300, h~50 (dev size)"),
+    # one GPU's share of BASELINE configs[3] (V = 3M, h ~ 150; 4M docs over 8 GPUs -> 500k per GPU)
+    "c4": dict(n_docs=500_000, n_queries=1000, vocab=3_000_000, dim=300, h=150, k=10,
+               workload="symmetric LC-RWMD top-10, 500k docs (one of 8 shards of 4M) x 1k queries, V=3M, m=300, "
+                        "h~150 (BASELINE configs[3] per GPU)"),
+    # one 4k-query batch of BASELINE configs[4] on one GPU's 25k-doc shard (200k docs over 8 GPUs)
+    "c5": dict(n_docs=25_000, n_queries=4096, vocab=400_000, dim=300, h=50, k=10,
+               workload="symmetric LC-RWMD top-10, 25k docs (one of 8 shards of 200k) x a 4k-query batch, V=400k, "
+                        "m=300, h~50 (BASELINE configs[4] per GPU and batch)"),
 }
 METRIC = "symmetric RWMD doc-pair distances/sec"
 UNIT = "doc-pairs/s"
