@@ -160,6 +160,16 @@ struct RangeMin {  // min(v[A..B]) as a balanced ternary tree of 3-input mins (B
   }
 };
 
+// min(run, v[0..31]) in 17 min instructions (16 three-input): 33 -> 11 -> 4 -> 2 -> 1
+__device__ __forceinline__ float chunk_min(float run, const float (&v)[32]) {
+  const float a0 = fmin3(run, v[0], v[1]), a1 = fmin3(v[2], v[3], v[4]), a2 = fmin3(v[5], v[6], v[7]);
+  const float a3 = fmin3(v[8], v[9], v[10]), a4 = fmin3(v[11], v[12], v[13]), a5 = fmin3(v[14], v[15], v[16]);
+  const float a6 = fmin3(v[17], v[18], v[19]), a7 = fmin3(v[20], v[21], v[22]), a8 = fmin3(v[23], v[24], v[25]);
+  const float a9 = fmin3(v[26], v[27], v[28]), a10 = fmin3(v[29], v[30], v[31]);
+  const float b0 = fmin3(a0, a1, a2), b1 = fmin3(a3, a4, a5), b2 = fmin3(a6, a7, a8), b3 = fminf(a9, a10);
+  return fminf(fmin3(b0, b1, b2), b3);
+}
+
 // exactly one segment end at column P of the chunk: pre = min(v[0..P]), suf = min(v[P+1..31])
 template <int P>
 __device__ __forceinline__ void split_at(const float (&v)[32], float& pre, float& suf) {
@@ -444,17 +454,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           continue;
 #endif
           if (mask == 0) {
-            run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
-          } else if (mask == 0xFFFFFFFFu) {  // every column closes a segment (pairwise distances)
-            emit(fminf(run, v[0]));
-#pragma unroll
-            for (int j = 1; j < 32; ++j) emit(v[j]);
-            run = kInf;
+            run = chunk_min(run, v);
           } else if ((mask & (mask - 1u)) == 0) {  // exactly one segment end in the chunk
             float pre, suf;
             split_switch(__ffs(mask) - 1, v, pre, suf);
             emit(fminf(run, pre));
             run = suf;
+          } else if (mask == 0xFFFFFFFFu) {  // every column closes a segment (pairwise distances)
+            emit(fminf(run, v[0]));
+#pragma unroll
+            for (int j = 1; j < 32; ++j) emit(v[j]);
+            run = kInf;
           } else {
             int start = 0;
             while (mask) {
