@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Measurement of the rows next to the hot path, one JSON line each.
 
-    python bench_rows.py [--rows wmd,wcd] [--steps K] [--warmup W]
+    python bench_rows.py [--rows wmd,wcd,allpairs] [--steps K] [--warmup W]
 
 * ``wmd``: exact top-10 word mover's distances (emd.prefiltered_topk_wmd_batch:
   LC-RWMD bounds on the tensor cores, then batched exact transport solves in
@@ -13,6 +13,11 @@
 * ``wcd``: word centroid distances (distances.wcd_block) for 100,000 x 1,000 docs
   (V = 100k, m = 300, ~50 words); metric doc-pairs/s; CPU baseline: the oracle's
   wcd_block on a bounded row sample.
+
+* ``allpairs``: all-pairs symmetric LC-RWMD top-10 of 50,000 docs (V = 400k,
+  m = 300, ~50 words, 4k-query batches -- BASELINE configs[4]'s shape on one
+  GPU) through the forward-only all_pairs path, next to the general symmetric
+  pipeline on the same set.
 
 Inputs are resident in HBM for the device-timed value (CUDA events); these rows
 are not part of bench.py's headline line.
@@ -117,15 +122,55 @@ def row_wcd(args):
     print(json.dumps(line), flush=True)
 
 
+def row_allpairs(args):
+    """All-pairs symmetric LC-RWMD top-10 (BASELINE configs[4] shape on one GPU: V = 400k,
+    h ~ 50, 4k-query batches): forward-only all_pairs vs the general symmetric pipeline
+    on the same set."""
+    import torch
+    from paper_1711_07227_b200 import device, synthetic as S
+    V, m, n, h, k, batch = 400_000, 300, args.allpairs_n, 50, 10, 4096
+    E = S.embeddings(V, m, seed=0)
+    x = S.histograms(n, V, h, seed=1)
+    Et = torch.from_numpy(E).cuda()
+    dx = device.DeviceCSR.upload(x)
+
+    def step():
+        prep = device.PreparedEmbeddings(Et)
+        D = device.all_pairs(dx, prep, batch)
+        od = torch.empty((n, k), dtype=torch.float32, device=D.device)
+        oi = torch.empty((n, k), dtype=torch.int64, device=D.device)
+        device.topk_matrix_rows(D, n, n, n, 0, k, od, oi)
+        return od, oi
+
+    ms, (od, oi) = timed(step, args.steps, args.warmup)
+    del od, oi
+    torch.cuda.empty_cache()
+
+    def general():
+        prep = device.PreparedEmbeddings(Et)
+        return device.symmetric(dx, dx, prep, k)
+
+    gms, _ = timed(general, 1, 1)
+    line = {"metric": "all-pairs symmetric RWMD doc-pairs/sec", "value": n * n / (ms * 1e-3), "unit": "doc-pairs/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "f16 operands, fp32 accumulate, fp64 SpMM",
+            "config": {"workload": f"all-pairs symmetric LC-RWMD top-10 of {n} docs, V=400k, m=300, h~50, "
+                                   f"query batches of {batch} (BASELINE configs[4] shape, one GPU)"},
+            "general_symmetric_path": {"ms_per_step": gms, "value": n * n / (gms * 1e-3),
+                                       "note": "device.symmetric(x, x): forward + reverse per query group"}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", default="wmd,wcd")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--allpairs-n", type=int, default=50_000)
     args = ap.parse_args()
     for r in args.rows.split(","):
-        {"wmd": row_wmd, "wcd": row_wcd}[r](args)
+        {"wmd": row_wmd, "wcd": row_wcd, "allpairs": row_allpairs}[r](args)
 
 
 if __name__ == "__main__":

@@ -163,6 +163,11 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
                         const uint32_t* e_blk, const int64_t* e_tile, int64_t n_q, const float* D1,
                         int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, void* stream);
 
+/* All-pairs symmetric combine (X1 == X2, distances.py:264 with the reverse
+ * direction equal to the transposed forward one): D = max(D, D^T) in place for
+ * an n x n row-major matrix with row stride ld. */
+int lcrw_symmetrize_max(float* D, int64_t n, int64_t ld, void* stream);
+
 /* Whole reverse direction in one call (distances.py:263-264): docs in batches
  * of batch_docs (multiple of 32); per batch gather -> segment plan ->
  * lcrw_phase1 (32-doc Z2 panels) -> lcrw_zero_identical -> lcrw_reverse_panels,

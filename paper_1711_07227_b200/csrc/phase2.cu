@@ -250,6 +250,34 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
 }
 
 
+
+// ---------------------------------------------------------------------------
+// All-pairs symmetric combine (X1 == X2): the reverse direction of a pair is the
+// forward direction of the swapped pair, so D = max(D1, D1^T) in place.  One
+// 32x32 tile pair per CTA (upper-triangle tiles only), transposed through
+// shared memory so both reads and both writes are coalesced.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) symmetrize_max_kernel(float* __restrict__ D, int64_t n, int64_t ld) {
+  __shared__ float ta[32][33], tb[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  const int64_t r0 = bi * 32, c0 = bj * 32;
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = r0 + y, c = c0 + tx;
+    ta[y][tx] = (r < n && c < n) ? D[r * ld + c] : 0.f;      // tile (bi, bj)
+    const int64_t r2 = c0 + y, c2 = r0 + tx;
+    tb[y][tx] = (r2 < n && c2 < n) ? D[r2 * ld + c2] : 0.f;  // tile (bj, bi)
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = r0 + y, c = c0 + tx;
+    if (r < n && c < n) D[r * ld + c] = fmaxf(ta[y][tx], tb[tx][y]);
+    const int64_t r2 = c0 + y, c2 = r0 + tx;
+    if (r2 < n && c2 < n) D[r2 * ld + c2] = fmaxf(tb[y][tx], ta[tx][y]);
+  }
+}
+
 }  // namespace p2
 }  // namespace lcrw
 
@@ -280,6 +308,19 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
   return LCRW_OK;
 }
 
+
+int lcrw_symmetrize_max(float* D, int64_t n, int64_t ld, void* stream) {
+  LCRW_REQUIRE(n >= 0 && ld >= n, "lcrw_symmetrize_max: bad shape");
+  if (n == 0) return LCRW_OK;
+  LCRW_REQUIRE(D, "lcrw_symmetrize_max: null pointer");
+  const int64_t t = ceil_div(n, 32);
+  LCRW_REQUIRE(t < 65536, "lcrw_symmetrize_max: n too large for one launch");
+  cudaStream_t st = as_stream(stream);
+  ProfScope prof(st, "symmetrize");
+  symmetrize_max_kernel<<<dim3((unsigned)t, (unsigned)t), 256, 0, st>>>(D, n, ld);
+  LCRW_CHECK_LAUNCH("symmetrize_max_kernel");
+  return LCRW_OK;
+}
 
 int lcrw_reverse_panels_tile_rows(void) { return kRpTile; }
 int lcrw_reverse_panels_group(void) { return kRpGroup; }

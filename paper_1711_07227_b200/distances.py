@@ -140,6 +140,26 @@ def lcrwmd_topk(x1: HistogramSet, x2: HistogramSet, embeddings: np.ndarray, k: i
     return [TopKResult(d[j], i[j]) for j in range(x2.n_rows)]
 
 
+def lcrwmd_all_pairs_topk(x: HistogramSet, embeddings: np.ndarray, k: int, batch_size: int = 4096
+                          ) -> list[TopKResult]:
+    """Each row's k nearest rows of the same set under the symmetric bound
+    (= ``lcrwmd_topk(x, x, E, k)``; a row is its own nearest at distance 0).
+    Extension for all-pairs clustering (BASELINE configs[4]): only the forward
+    direction is computed, the reverse one being its transpose."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    _check_space(x, embeddings, "x")
+    prep = device.PreparedEmbeddings(embeddings)
+    D = device.all_pairs(device.DeviceCSR.upload(x, "x"), prep, batch_size)
+    n = x.n_rows
+    kk = min(k, n)
+    od = torch.empty((max(n, 1), k), dtype=torch.float32, device=D.device)
+    oi = torch.empty((max(n, 1), k), dtype=torch.int64, device=D.device)
+    device.topk_matrix_rows(D, n, n, n, 0, k, od, oi)
+    od, oi = od[:, :kk].cpu().numpy(), oi[:, :kk].cpu().numpy()
+    return [TopKResult(od[j], oi[j]) for j in range(n)]
+
+
 def lcrwmd_topk_arrays(x1, x2, embeddings, k: int, prep=None):
     """(n2, min(k, n1)) distances and int64 ids; accepts host sets or DeviceCSRs."""
     if prep is None:

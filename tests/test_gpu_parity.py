@@ -547,3 +547,25 @@ def test_engine_index_and_partition_invariance(tmp_path):
     pr = engine.run_query(back, queries, engine.QueryPlan(method="wmd-pruned", k=4))
     for a, b in zip(ex_all, pr):
         assert np.array_equal(a.ids, b.ids) and np.allclose(a.distances, b.distances, rtol=1e-12, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [4096, 37])
+def test_all_pairs_matches_symmetric(batch):
+    """lcrwmd_all_pairs_topk (forward direction only, D = max(D1, D1^T)) vs the reference
+    symmetric bound of the set against itself; exactly symmetric, zero diagonal."""
+    import torch
+    from paper_1711_07227_b200 import device
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(46)
+    V = 3000
+    E = rng.standard_normal((V, 300)).astype(np.float32)
+    x = _rand_set(rng, 230, V, 2, 60)
+    ref = O.lcrwmd_full(x, x, E, threads=8)
+    full = device.all_pairs(device.DeviceCSR.upload(x), device.PreparedEmbeddings(E), batch).cpu().numpy()
+    assert np.array_equal(full, full.T) and np.all(np.diag(full) == 0.0)
+    ok, err = rel_close(full, ref, RTOL, _atol(E))
+    assert ok, err
+    res = D.lcrwmd_all_pairs_topk(x, E, 6, batch_size=batch)
+    _check_topk([r.distances for r in res], [r.ids for r in res], ref, 6, _atol(E))
+    assert all(int(r.ids[0]) == j and float(r.distances[0]) == 0.0 for j, r in enumerate(res))
