@@ -167,6 +167,10 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
  * direction equal to the transposed forward one): D = max(D, D^T) in place for
  * an n x n row-major matrix with row stride ld. */
 int lcrw_symmetrize_max(float* D, int64_t n, int64_t ld, void* stream);
+/* Sharded all-pairs combine: D[i, j] = max(D[i, j], R[j, i]) for i < rows,
+ * j < cols (D row stride ldd, R row stride ldr). */
+int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int64_t rows, int64_t cols,
+                        void* stream);
 
 /* Whole reverse direction in one call (distances.py:263-264): docs in batches
  * of batch_docs (multiple of 32); per batch gather -> segment plan ->

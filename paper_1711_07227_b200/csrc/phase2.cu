@@ -278,6 +278,26 @@ __global__ void __launch_bounds__(256) symmetrize_max_kernel(float* __restrict__
   }
 }
 
+
+// D[i, j] = max(D[i, j], R[j, i]) for i < rows, j < cols: the sharded all-pairs combine
+// (this rank's rows against a peer's block of the forward bounds, transposed through smem).
+__global__ void __launch_bounds__(256) max_transposed_kernel(float* __restrict__ D, int64_t ldd,
+                                                             const float* __restrict__ R, int64_t ldr, int64_t rows,
+                                                             int64_t cols) {
+  __shared__ float t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+  for (int y = ty; y < 32; y += 8) {  // R rows j0 + y, columns i0 + tx
+    const int64_t j = j0 + y, i = i0 + tx;
+    t[y][tx] = (j < cols && i < rows) ? R[j * ldr + i] : 0.f;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t i = i0 + y, j = j0 + tx;
+    if (i < rows && j < cols) D[i * ldd + j] = fmaxf(D[i * ldd + j], t[tx][y]);
+  }
+}
+
 }  // namespace p2
 }  // namespace lcrw
 
@@ -319,6 +339,19 @@ int lcrw_symmetrize_max(float* D, int64_t n, int64_t ld, void* stream) {
   ProfScope prof(st, "symmetrize");
   symmetrize_max_kernel<<<dim3((unsigned)t, (unsigned)t), 256, 0, st>>>(D, n, ld);
   LCRW_CHECK_LAUNCH("symmetrize_max_kernel");
+  return LCRW_OK;
+}
+
+int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int64_t rows, int64_t cols,
+                        void* stream) {
+  LCRW_REQUIRE(rows >= 0 && cols >= 0 && ldd >= cols && ldr >= rows, "lcrw_max_transposed: bad shape");
+  if (rows == 0 || cols == 0) return LCRW_OK;
+  LCRW_REQUIRE(D && R, "lcrw_max_transposed: null pointer");
+  LCRW_REQUIRE(ceil_div(rows, 32) < 65536, "lcrw_max_transposed: too many rows for one launch");
+  cudaStream_t st = as_stream(stream);
+  max_transposed_kernel<<<dim3((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), 256, 0, st>>>(
+      D, ldd, R, ldr, rows, cols);
+  LCRW_CHECK_LAUNCH("max_transposed_kernel");
   return LCRW_OK;
 }
 

@@ -560,6 +560,31 @@ def reverse_rows(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings) -> torc
     return symmetric(x1, x2, prep, None, d1=d1)
 
 
+def forward_rows_into(res: "Restricted", prep: PreparedEmbeddings, q: DeviceCSR, D: torch.Tensor,
+                      batch: int = 4096) -> None:
+    """D[i, c] = forward bound of resident row i (res) to query c of q (distances.py:181-204),
+    written in place into the row-major (n_res, n_q) matrix D, queries in batches."""
+    n = res.csr.n_rows
+    ho = q.host_offsets
+    ld = int(D.stride(0))
+    for q0 in range(0, q.n_rows, batch):
+        q1 = min(q.n_rows, q0 + batch)
+        nq = q1 - q0
+        lo, hi = int(ho[q0]), int(ho[q1])
+        seg = q.offsets[q0:q1 + 1] - lo
+        zs = spmm_z_shift(nq)
+        Z, zp = nearest_distances(res, prep, seg, q.cols[lo:hi], nq, zs)
+        out = D.view(-1)[q0:]  # D[i, q0 + c] = out[i * ld + c]
+        spmm(res.csr.offsets, res.cols_r, res.csr.vals, n, Z, zp, nq, out, ld, 8, z_shift=zs)
+        del Z
+
+
+def max_transposed(D: torch.Tensor, R: torch.Tensor) -> None:
+    """D = max(D, R^T) in place (lcrw_max_transposed); D (rows, cols), R (cols, rows)."""
+    rows, cols = int(D.shape[0]), int(D.shape[1])
+    _lib.call("lcrw_max_transposed", _p(D), int(D.stride(0)), _p(R), int(R.stride(0)), rows, cols, _stream())
+
+
 def all_pairs(x: DeviceCSR, prep: PreparedEmbeddings, batch: int = 4096) -> torch.Tensor:
     """Symmetric LC-RWMD of a set against itself, (n, n) on the device (BASELINE configs[4]).
 
@@ -574,18 +599,7 @@ def all_pairs(x: DeviceCSR, prep: PreparedEmbeddings, batch: int = 4096) -> torc
     D = torch.empty((max(n, 1), max(n, 1)), dtype=torch.float32, device=dev)
     if n == 0:
         return D[:0, :0]
-    res = Restricted.build(x, prep)
-    ho = x.host_offsets
-    for q0 in range(0, n, batch):
-        q1 = min(n, q0 + batch)
-        nq = q1 - q0
-        lo, hi = int(ho[q0]), int(ho[q1])
-        seg = x.offsets[q0:q1 + 1] - lo
-        zs = spmm_z_shift(nq)
-        Z, zp = nearest_distances(res, prep, seg, x.cols[lo:hi], nq, zs)
-        out = D.view(-1)[q0:]  # D1[i, q0 + q] = out[i * n + q]
-        spmm(res.csr.offsets, res.cols_r, res.csr.vals, n, Z, zp, nq, out, n, 8, z_shift=zs)
-        del Z
+    forward_rows_into(Restricted.build(x, prep), prep, x, D, batch)
     _lib.call("lcrw_symmetrize_max", _p(D), n, n, _stream())
     return D
 

@@ -12,7 +12,11 @@ contiguous shards + topk_merge):
 * reverse direction (the dominant cost): fully local -- each rank's docs are
   the "queries" of the reverse pass against the replicated X2;
 * top-k: local per-query top-k, NCCL gather to rank 0, merge there
-  (kernels.py:226-232).  Results are identical for any world size: every
+  (kernels.py:226-232);
+* all-pairs (X1 == X2, BASELINE configs[4]): forward bounds of the local rows
+  against every doc, one all_to_all of the (n_r x n_s) blocks (the reverse
+  bounds are the peers' forward bounds transposed), max-combine, local top-k,
+  gather (``sharded_all_pairs_topk``).  Results are identical for any world size: every
   pair distance is computed by the same arithmetic, and the merge is exact.
 
 The collective glue (``allgather_slices``, ``gather_candidates``) is
@@ -57,6 +61,29 @@ def allgather_slices(local: torch.Tensor, group=None) -> torch.Tensor:
         dist.all_gather_into_tensor(out.view(-1), local.contiguous().view(-1), group=group)
     else:
         dist.all_gather(list(out.unbind(0)), local.contiguous(), group=group)
+    return out
+
+
+def exchange_blocks(D1: torch.Tensor, sizes: list[int], group=None) -> list[torch.Tensor]:
+    """All-pairs exchange (BASELINE configs[4]): this rank holds the forward
+    bounds of its rows against ALL docs, D1 (n_r, n); rank s needs the block D1[:, S_s]
+    (its docs as the "reverse" side of ours).  One all_to_all; returns the blocks
+    received from every rank s, each (n_s, n_r) = that rank's D1[S_s rows, S_r cols]."""
+    rank, world = _world()
+    n_r = int(D1.shape[0])
+    offs = [0]
+    for sz in sizes:
+        offs.append(offs[-1] + sz)
+    if world == 1:
+        return [D1[:, offs[0]:offs[1]]]
+    send = torch.cat([D1[:, offs[s]:offs[s + 1]].contiguous().view(-1) for s in range(world)])
+    recv = torch.empty(sum(sz * n_r for sz in sizes), dtype=D1.dtype, device=D1.device)
+    dist.all_to_all_single(recv, send, output_split_sizes=[sz * n_r for sz in sizes],
+                           input_split_sizes=[n_r * sz for sz in sizes], group=group)
+    out, at = [], 0
+    for sz in sizes:
+        out.append(recv[at:at + sz * n_r].view(sz, n_r))
+        at += sz * n_r
     return out
 
 
@@ -153,3 +180,39 @@ def sharded_topk_host(x1_shard, doc_base: int, n1_total: int, x2, E, k: int, gro
     if out is None:
         return None
     return out[0].cpu().numpy(), out[1].cpu().numpy()
+
+
+def sharded_all_pairs_topk(dx_local: DeviceCSR, dx_all: DeviceCSR, lo: int, prep: PreparedEmbeddings, k: int,
+                           batch: int = 4096, group=None):
+    """All-pairs symmetric top-k with docs sharded over ranks (BASELINE configs[4]):
+    forward bounds of the local rows against all docs (queries replicated), one
+    all_to_all of the (n_r x n_s) blocks, D[:, S_s] = max(D1[:, S_s], received^T),
+    per-row top-k with global ids, gathered to rank 0 as (n, k); None elsewhere."""
+    rank, world = _world()
+    n = dx_all.n_rows
+    sizes = [hi_ - lo_ for lo_, hi_ in (shard_range(n, r, world) for r in range(world))]
+    n_r = dx_local.n_rows
+    D = torch.empty((max(n_r, 1), n), dtype=torch.float32, device=dx_all.cols.device)
+    device.forward_rows_into(device.Restricted.build(dx_local, prep), prep, dx_all, D, batch)
+    if world == 1:  # the one block is D itself: symmetrise in place
+        device._lib.call("lcrw_symmetrize_max", device._p(D), n, n, device._stream())
+    else:
+        blocks = exchange_blocks(D[:n_r], sizes, group)
+        at = 0
+        for s, sz in enumerate(sizes):
+            device.max_transposed(D[:n_r, at:at + sz], blocks[s])
+            at += sz
+    kk = min(k, n)
+    od = torch.empty((max(n_r, 1), k), dtype=torch.float32, device=D.device)
+    oi = torch.empty((max(n_r, 1), k), dtype=torch.int64, device=D.device)
+    device.topk_matrix_rows(D, n_r, n, n, 0, k, od, oi)
+    od, oi = od[:n_r, :kk].contiguous(), oi[:n_r, :kk].contiguous()
+    if world == 1:
+        return od, oi
+    gd = [torch.empty((sz, kk), dtype=od.dtype, device=od.device) for sz in sizes] if rank == 0 else None
+    gi = [torch.empty((sz, kk), dtype=oi.dtype, device=oi.device) for sz in sizes] if rank == 0 else None
+    dist.gather(od, gd, dst=0, group=group)
+    dist.gather(oi, gi, dst=0, group=group)
+    if rank != 0:
+        return None
+    return torch.cat(gd), torch.cat(gi)

@@ -569,3 +569,38 @@ def test_all_pairs_matches_symmetric(batch):
     res = D.lcrwmd_all_pairs_topk(x, E, 6, batch_size=batch)
     _check_topk([r.distances for r in res], [r.ids for r in res], ref, 6, _atol(E))
     assert all(int(r.ids[0]) == j and float(r.distances[0]) == 0.0 for j, r in enumerate(res))
+
+
+@pytest.mark.gpu
+def test_all_pairs_sharded_emulated_ranks():
+    """Sharded all-pairs on one GPU: per-shard forward rows, the all_to_all blocks taken
+    directly, max_transposed combine -- bitwise equal to the single-set all_pairs for
+    W in {2, 3}; parallel.sharded_all_pairs_topk at world 1 equals lcrwmd_all_pairs_topk."""
+    import torch
+    from paper_1711_07227_b200 import device, parallel
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(47)
+    V = 2500
+    E = rng.standard_normal((V, 300)).astype(np.float32)
+    x = _rand_set(rng, 97, V, 2, 40)
+    prep = device.PreparedEmbeddings(E)
+    dx = device.DeviceCSR.upload(x)
+    want = device.all_pairs(dx, prep, 20)
+    n = x.n_rows
+    for W in (2, 3):
+        ranges = [parallel.shard_range(n, r, W) for r in range(W)]
+        D1 = []
+        for lo, hi in ranges:
+            d = torch.empty((hi - lo, n), dtype=torch.float32, device="cuda")
+            device.forward_rows_into(device.Restricted.build(device.DeviceCSR.upload(x.slice_rows(lo, hi)), prep),
+                                     prep, dx, d, 20)
+            D1.append(d)
+        recv = [[D1[s_][:, lo:hi].contiguous() for s_ in range(W)] for lo, hi in ranges]  # the all_to_all
+        for r in range(W):
+            for s_, (b0, b1) in enumerate(ranges):
+                device.max_transposed(D1[r][:, b0:b1], recv[r][s_])
+        got = torch.cat(D1)
+        assert torch.equal(got, want), W
+    od, oi = parallel.sharded_all_pairs_topk(dx, dx, 0, prep, 5, 20)
+    res = D.lcrwmd_all_pairs_topk(x, E, 5, batch_size=20)
+    assert np.array_equal(oi.cpu().numpy(), np.stack([r.ids for r in res]))
