@@ -175,7 +175,9 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
 /* Whole reverse direction in one call (distances.py:263-264): docs in batches
  * of batch_docs (multiple of 32); per batch gather -> segment plan ->
  * lcrw_phase1 (32-doc Z2 panels) -> lcrw_zero_identical -> lcrw_reverse_panels,
- * enqueued from C++ on `stream`.  doc_offsets_host is the host copy of
+ * enqueued from C++ on `stream` (EhB has v_rows rows; with LCRW_GATHER_B=1 in
+ * the environment the B operand rows are TMA-gathered from EhB by doc_cols
+ * inside lcrw_phase1 instead of being copied first).  doc_offsets_host is the host copy of
  * doc_offsets (batch planning); doc_cols are global E ids, rep/next/remap as in
  * lcrw_zero_identical.  Writes D = max(D1, D2) for all docs (see
  * lcrw_reverse_panels).  Workspace from lcrw_reverse_workspace with
@@ -183,7 +185,8 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
  * the stream waits on it before the first read of D1, so the forward direction
  * can run concurrently on another stream with the reverse Phase 1. */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
-int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
+int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
+                          int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,

@@ -47,7 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, I32, P]),
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
-    "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
+    "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
                                     I64, I64, I32, P, P, SZ, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),

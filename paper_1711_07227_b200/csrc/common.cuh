@@ -160,6 +160,20 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* m, uint32_t b
       : "memory");
 }
 
+// 2-SM TMA gather: 4 rows (row indices r0..r3) x one box of columns starting at c0 land as
+// 4 consecutive rows at dst in this CTA's smem (swizzled by address like a tile load);
+// completion bytes go to the barrier at the given shared::cluster address.
+__device__ __forceinline__ void tma_gather4_2sm(const CUtensorMap* m, uint32_t bar_cluster_addr, void* dst,
+                                                int32_t c0, int32_t r0, int32_t r1, int32_t r2, int32_t r3,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "l"(policy)
+      : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05: TMEM allocation, UMMA issue/commit, TMEM -> register loads
 // ---------------------------------------------------------------------------

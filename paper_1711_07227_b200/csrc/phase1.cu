@@ -75,6 +75,8 @@ struct Params {
   int64_t z_panel;
   int64_t seg_base;  // column c = seg_offsets[s] - seg_base
   int64_t b_rows;
+  const int32_t* b_ids;  // gather mode: B row c is operand row b_ids[c] (TMA gather4); NULL = rows in order
+  int32_t b_oob;         // gather mode: a row index past the operand table (zero-filled padding rows)
   int z_shift;       // Z panel width = 1 << z_shift segments
   int a_rows;
   int n_mpairs;      // 256-row A tiles
@@ -256,7 +258,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == kProducerWarp) {
     // ============================ TMA producer (both CTAs) ============================
-    if (lane == 0) {
+    // The whole warp walks the loop; lane 0 issues tile loads, every lane issues its
+    // 4-row TMA gathers in gather mode.
+    {
       const uint64_t pol_a = l2_policy_evict_last();    // A tiles are re-read by every range
       const uint64_t pol_b = l2_policy_evict_normal();  // B ranges are shared by concurrent pairs
       const uint32_t a_full_l = mapa_shared(smem_u32(a_full), 0);
@@ -269,28 +273,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int mp = (int)(u % p.n_mpairs);
         mbar_wait(a_empty, a_phase ^ 1);
         a_phase ^= 1;
-        if (leader) mbar_expect_tx(a_full, 2 * p.n_kb * A_KB_BYTES);
-        for (int kb = 0; kb < p.n_kb; ++kb)
-          tma_load_2d_2sm(&tmA, a_full_l, smem_raw + (sm.A - smem_u32(smem_raw)) + kb * A_KB_BYTES, kb * BK,
-                          mp * 2 * BM + (int)rank * BM, pol_a);
+        if (lane == 0) {
+          if (leader) mbar_expect_tx(a_full, 2 * p.n_kb * A_KB_BYTES);
+          for (int kb = 0; kb < p.n_kb; ++kb)
+            tma_load_2d_2sm(&tmA, a_full_l, smem_raw + (sm.A - smem_u32(smem_raw)) + kb * A_KB_BYTES, kb * BK,
+                            mp * 2 * BM + (int)rank * BM, pol_a);
+        }
         const int n_tiles = U.n0 + U.n1;
         for (int i = 0; i < n_tiles; ++i) {
           int h, k;
           unit_tile(U, i, h, k);
           const int64_t c0 = U.cb(h) + (int64_t)k * BN;
+          // gather mode: lane l owns B rows 4l .. 4l+3 of this CTA's half tile
+          int32_t g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+          if (p.b_ids) {
+            const int64_t cb = c0 + rank * BN_HALF + 4 * lane;
+            auto id_at = [&](int64_t c) -> int32_t { return c < p.b_rows ? __ldg(p.b_ids + c) : p.b_oob; };
+            g0 = id_at(cb);
+            g1 = id_at(cb + 1);
+            g2 = id_at(cb + 2);
+            g3 = id_at(cb + 3);
+          }
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_empty + stage, phase ^ 1);
+            if (p.b_ids) {
+              if (leader && lane == 0) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
+              tma_gather4_2sm(&tmB, b_full_l + stage * 8,
+                              smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES + lane * 4 * BK * 2,
+                              kb * BK, g0, g1, g2, g3, pol_b);
+            } else if (lane == 0) {
 #if LCRW_EPI_MODE == 3
-            if (b_loads >= p.stages) {  // experiment: ring filled once, then no more B traffic
-              if (leader) mbar_arrive(b_full + stage);
-            } else
+              if (b_loads >= p.stages) {  // experiment: ring filled once, then no more B traffic
+                if (leader) mbar_arrive(b_full + stage);
+              } else
 #endif
-            {
-              if (leader) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
-              tma_load_2d_2sm(&tmB, b_full_l + stage * 8,
-                              smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES, kb * BK,
-                              (int32_t)(c0 + rank * BN_HALF), pol_b);
+              {
+                if (leader) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
+                tma_load_2d_2sm(&tmB, b_full_l + stage * 8,
+                                smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES, kb * BK,
+                                (int32_t)(c0 + rank * BN_HALF), pol_b);
+              }
             }
+            __syncwarp();
             ++b_loads;
             if (++stage == (uint32_t)p.stages) {
               stage = 0;
@@ -545,7 +569,8 @@ namespace p1 {
 
 int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
-           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag) {
+           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids = nullptr,
+           int64_t b_table_rows = 0) {
   LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(K)");
   LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
                "lcrw_phase1: row counts must fit in int32");
@@ -575,6 +600,8 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   p.z_panel = z_panel;
   p.seg_base = seg_base;
   p.b_rows = b_rows;
+  p.b_ids = b_ids;
+  p.b_oob = (int32_t)b_table_rows;
   p.z_shift = z_shift;
   p.a_rows = (int)a_rows;
   p.n_mpairs = (int)ceil_div(a_rows, 2 * BM);
@@ -586,7 +613,8 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   CUtensorMap tmA, tmB;
   int st = make_map(&tmA, A, a_rows, kp, BM);
   if (st) return st;
-  st = make_map(&tmB, B, b_rows, kp, BN_HALF);
+  // gather mode: B is the whole operand table, rows picked by b_ids 4 at a time (box height 1)
+  st = b_ids ? make_map(&tmB, B, b_table_rows, kp, 1) : make_map(&tmB, B, b_rows, kp, BN_HALF);
   if (st) return st;
 
   const size_t smem = smem_bytes(n_kb, stages);

@@ -10,13 +10,16 @@
 //   zeros    Z2[doc, w] = 0 where doc holds a word identical to w
 //   reverse  D[q, doc] = max(D1, spmm(Xq, Z2)), panel-streaming (query-major D)
 // The loop runs in C++ so a batch costs a handful of launch calls, not Python.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace lcrw {
 namespace p1 {
 int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
-           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag);
+           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids,
+           int64_t b_table_rows);
 }
 
 namespace {
@@ -63,7 +66,8 @@ int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t m
   return LCRW_OK;
 }
 
-int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int m, int kp,
+int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
+                          int m, int kp,
                           const float* scale, const int64_t* doc_offsets, const int64_t* doc_offsets_host,
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
@@ -91,16 +95,24 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
   const int64_t z_panel = a_rows << kZShift;
   cudaStream_t st = as_stream(stream);
   int status;
+  // B operand rows straight from EhB by TMA gather4 (no T copy) when LCRW_GATHER_B=1
+  static const bool gather_b = [] {
+    const char* e = getenv("LCRW_GATHER_B");
+    return e && e[0] == '1';
+  }();
+  const int64_t v_table = v_rows;
   for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
     const int64_t nd = j1 - j0;
     const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
-    if ((status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream))) return status;
+    if (!gather_b && (status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream)))
+      return status;
     const int rc = range_cols > 0 ? range_cols : auto_range_cols(nw, a_rows);
     const int64_t n_ranges = lcrw_plan_ranges(nw, rc);
     if ((status = lcrw_segment_plan(doc_offsets + j0, lo, nd, nw, rc, mask, rs, n_ranges, stream))) return status;
-    if ((status = p1::launch(A, a_norms, a_rows, T, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs, n_ranges, scale,
-                             Z2, z_panel, kZShift, st, "phase1_rev")))
+    if ((status = p1::launch(A, a_norms, a_rows, gather_b ? EhB : T, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs,
+                             n_ranges, scale, Z2, z_panel, kZShift, st, "phase1_rev",
+                             gather_b ? doc_cols + lo : nullptr, v_table)))
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;

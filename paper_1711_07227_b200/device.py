@@ -466,7 +466,8 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         ld_q, ld_doc = n1, 1
     rep, nxt = prep.representatives(x1.cols)
     host_offs = np.ascontiguousarray(ho, dtype=np.int64)
-    _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), prep.k_eff, prep.kp,
+    _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), prep.V, prep.k_eff,
+              prep.kp,
               _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
               _p(nxt), _p(res2.remap), _p(e_blk), _p(e_tile), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
               batch, 0, C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value,
