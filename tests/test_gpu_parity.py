@@ -604,3 +604,23 @@ def test_all_pairs_sharded_emulated_ranks():
     od, oi = parallel.sharded_all_pairs_topk(dx, dx, 0, prep, 5, 20)
     res = D.lcrwmd_all_pairs_topk(x, E, 5, batch_size=20)
     assert np.array_equal(oi.cpu().numpy(), np.stack([r.ids for r in res]))
+
+
+@pytest.mark.gpu
+def test_emd_large_and_unsupported_problems():
+    """The shared-memory solver (h1 + h2 > 128) agrees with the oracle restatement; a problem
+    too large for shared memory is reported, not silently truncated."""
+    from paper_1711_07227_b200 import emd
+    rng = np.random.default_rng(48)
+    for h1, h2 in ((90, 70), (130, 20)):
+        s = rng.random(h1) + 0.05
+        d = rng.random(h2) + 0.05
+        s /= s.sum()
+        d /= d.sum()
+        c = rng.random((h1, h2)) * 5
+        plan = emd.solve_emd(emd.TransportProblem(s, d, c))
+        ref = O.solve_emd_objective(s, d, c)
+        assert abs(plan.objective - ref) <= 1e-9 * max(1.0, ref), (h1, h2, plan.objective, ref)
+    s = np.full(200, 1 / 200)
+    with pytest.raises(NotImplementedError, match="shared memory"):
+        emd.solve_emd(emd.TransportProblem(s, s, np.ones((200, 200))))
