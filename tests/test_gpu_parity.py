@@ -624,3 +624,145 @@ def test_emd_large_and_unsupported_problems():
     s = np.full(200, 1 / 200)
     with pytest.raises(NotImplementedError, match="shared memory"):
         emd.solve_emd(emd.TransportProblem(s, s, np.ones((200, 200))))
+
+
+# --- SPEC.md acceptance criteria (reference SPEC, "ACCEPTANCE CRITERIA") --------------
+
+def _tiny_set(rng, n, V, hmax, hmin=1):
+    from paper_1711_07227_b200.corpus import HistogramSet
+    rows = []
+    for _ in range(n):
+        h = int(rng.integers(hmin, hmax + 1))
+        ids = np.sort(rng.choice(V, size=h, replace=False)).astype(np.int32)
+        c = rng.integers(1, 5, h).astype(np.int64)
+        tot = int(c.sum())
+        scale = 1 << int(np.ceil(np.log2(tot)))
+        c[0] += scale - tot  # dyadic weights: exact in f32, totals exactly 1
+        rows.append((ids, (c / scale).astype(np.float32)))
+    return HistogramSet.from_rows(rows, V)
+
+
+@pytest.mark.gpu
+def test_acceptance_1_lcrwmd_equals_quadratic_rwmd():
+    """Criterion 1: lcrwmd_full equals the quadratic RWMD (computed pair by pair by the
+    oracle, distances.py:78-130) within 1e-5 relative; n1=200, n2=50, v_e <= 1000,
+    h in [2, 32], m = 16 (10 random instances here, the oracle's quadratic form being slow)."""
+    _, D, _ = _pkg()
+    for seed in range(10):
+        rng = np.random.default_rng(1000 + seed)
+        E = rng.standard_normal((1000, 16)).astype(np.float32)
+        x1 = _rand_set(rng, 200, 1000, 2, 32)
+        x2 = _rand_set(rng, 50, 1000, 2, 32)
+        got = D.lcrwmd_full(x1, x2, E).values
+        ref = O.rwmd_quadratic(x1, x2, E)
+        ok, err = rel_close(got, ref, 1e-5, 1e-6)
+        assert ok, (seed, err)
+
+
+@pytest.mark.gpu
+def test_acceptance_2_lower_bound_chain():
+    """Criterion 2: on >= 1000 random pairs with h <= 4: WCD <= WMD + 1e-4,
+    RWMD <= WMD + 1e-4, and each one-sided bound <= the symmetric RWMD exactly."""
+    from paper_1711_07227_b200 import emd
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(2000)
+    V = 300
+    E = rng.standard_normal((V, 24)).astype(np.float32)
+    x1 = _tiny_set(rng, 40, V, 4)
+    x2 = _tiny_set(rng, 25, V, 4)
+    wcd = D.wcd_block(x1, x2, E).values
+    sym = D.lcrwmd_full(x1, x2, E).values
+    b1, b2 = D.rwmd_bounds(x1, x2, E)
+    assert np.all(b1 <= sym) and np.all(b2 <= sym)
+    rows1 = [x1.row(i) for i in range(x1.n_rows)]
+    for j in range(x2.n_rows):
+        q = x2.row(j)
+        w = emd.solve_batch([r.weights for r in rows1], [q.weights] * len(rows1), embeddings=E,
+                            ids1=[r.word_ids for r in rows1], ids2=[q.word_ids] * len(rows1))
+        assert np.all(wcd[:, j] <= w + 1e-4) and np.all(sym[:, j] <= w + 1e-4), j
+
+
+def _brute_force_emd(s, d, c):
+    """Minimum over the basic feasible solutions (spanning-tree bases of the bipartite graph)."""
+    import itertools
+    h1, h2 = c.shape
+    cells = [(p, q) for p in range(h1) for q in range(h2)]
+    best = np.inf
+    for basis in itertools.combinations(cells, h1 + h2 - 1):
+        A = np.zeros((h1 + h2, len(basis)))
+        for k_, (p, q) in enumerate(basis):
+            A[p, k_] = 1.0
+            A[h1 + q, k_] = 1.0
+        b = np.concatenate([s, d])
+        sol, res, rank, _ = np.linalg.lstsq(A, b, rcond=None)
+        if rank < h1 + h2 - 1 or np.any(sol < -1e-12) or np.abs(A @ sol - b).max() > 1e-9:
+            continue
+        best = min(best, float(sum(sol[k_] * c[p, q] for k_, (p, q) in enumerate(basis))))
+    return best
+
+
+@pytest.mark.gpu
+def test_acceptance_3_emd_vs_basic_feasible_solutions():
+    """Criterion 3: 2x2 and random 3x3 instances -- solve_emd equals the brute-force minimum
+    over basic feasible solutions within 1e-6 relative; the dual certificate matches."""
+    from paper_1711_07227_b200 import emd
+    rng = np.random.default_rng(3000)
+    for shape in [(2, 2)] * 10 + [(3, 3)] * 10:
+        s = rng.random(shape[0]) + 0.05
+        d = rng.random(shape[1]) + 0.05
+        s /= s.sum()
+        d /= d.sum()
+        c = np.round(rng.random(shape) * 10, 1)
+        plan = emd.solve_emd(emd.TransportProblem(s, d, c))
+        ref = _brute_force_emd(s, d, c)
+        assert abs(plan.objective - ref) <= 1e-6 * max(1.0, ref), (shape, plan.objective, ref)
+        dual = float(s @ plan.dual_source + d @ plan.dual_sink)
+        assert abs(dual - plan.objective) <= 1e-6 * max(1.0, ref)
+
+
+@pytest.mark.gpu
+def test_acceptance_4_pruning_exactness():
+    """Criterion 4: on 20 random instances (n1 = 300, h <= 8, m = 8, k in {4, 16}) the
+    prefiltered top-k equals the exhaustive WMD top-k, with fewer than n1 exact solves in
+    at least 18 of them."""
+    from paper_1711_07227_b200 import emd
+    pruned = 0
+    for seed in range(20):
+        rng = np.random.default_rng(4000 + seed)
+        V = 400
+        E = rng.standard_normal((V, 8)).astype(np.float32)
+        x1 = _tiny_set(rng, 300, V, 8)
+        q = _tiny_set(rng, 1, V, 8).row(0)
+        k = 4 if seed % 2 == 0 else 16
+        res, solves = emd.prefiltered_topk_wmd(x1, q, E, k)
+        rows1 = [x1.row(i) for i in range(300)]
+        w = emd.solve_batch([r.weights for r in rows1], [q.weights] * 300, embeddings=E,
+                            ids1=[r.word_ids for r in rows1], ids2=[q.word_ids] * 300)
+        order = np.lexsort((np.arange(300), w))[:k]
+        assert np.array_equal(res.ids, order), seed
+        assert np.allclose(res.distances, w[order], rtol=1e-6, atol=0), seed
+        pruned += solves < 300
+    assert pruned >= 18, pruned
+
+
+@pytest.mark.gpu
+def test_acceptance_6_8_partition_invariance_and_determinism():
+    """Criteria 6 and 8: identical top-k for P in {1, 2, 4, 8}; repeated runs are bitwise identical."""
+    from paper_1711_07227_b200 import engine
+    _, D, _ = _pkg()
+    rng = np.random.default_rng(6000)
+    V = 1500
+    E = rng.standard_normal((V, 32)).astype(np.float32)
+    x1 = _rand_set(rng, 203, V, 3, 30)
+    x2 = _rand_set(rng, 9, V, 3, 30)
+    idx = engine.Index(x1, E, [f"w{i}" for i in range(V)])
+    ref = engine.run_query(idx, x2, engine.QueryPlan(k=7))
+    for P in (2, 4, 8):
+        got = engine.run_query(idx, x2, engine.QueryPlan(k=7, partitions=P))
+        assert all(np.array_equal(a.ids, b.ids) and np.array_equal(a.distances, b.distances) for a, b in zip(ref, got))
+    a = D.lcrwmd_full(x1, x2, E).values
+    b = D.lcrwmd_full(x1, x2, E).values
+    assert np.array_equal(a, b)
+    t1 = D.lcrwmd_topk(x1, x2, E, 5)
+    t2 = D.lcrwmd_topk(x1, x2, E, 5)
+    assert all(np.array_equal(u.ids, v.ids) and np.array_equal(u.distances, v.distances) for u, v in zip(t1, t2))
