@@ -766,3 +766,60 @@ def test_acceptance_6_8_partition_invariance_and_determinism():
     t1 = D.lcrwmd_topk(x1, x2, E, 5)
     t2 = D.lcrwmd_topk(x1, x2, E, 5)
     assert all(np.array_equal(u.ids, v.ids) and np.array_equal(u.distances, v.distances) for u, v in zip(t1, t2))
+
+
+def _clustered_corpus(tmp_path, n=500, topics=5, words_per_topic=60, m=16, seed=7):
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((topics, m)) * 2.0
+    words, vecs = [], []
+    for t in range(topics):
+        for w in range(words_per_topic):
+            words.append(f"t{t}w{w}")
+            vecs.append(centers[t] + rng.standard_normal(m) * 1.5)  # topics overlap: word-level matching matters
+    emb = tmp_path / "emb.txt"
+    emb.write_text(f"{len(words)} {m}\n" + "".join(
+        w + " " + " ".join(f"{x:.6f}" for x in v) + "\n" for w, v in zip(words, vecs)))
+    docs, labels = [], []
+    for i in range(n):
+        t = int(rng.integers(topics))
+        h = int(rng.integers(3, 9))
+        toks = [f"t{t}w{int(rng.integers(words_per_topic))}" if rng.random() < 0.8
+                else f"t{int(rng.integers(topics))}w{int(rng.integers(words_per_topic))}" for _ in range(h)]
+        docs.append(" ".join(toks))
+        labels.append(f"topic{t}")
+    (tmp_path / "docs.txt").write_text("\n".join(docs) + "\n")
+    (tmp_path / "labels.txt").write_text("\n".join(labels) + "\n")
+    return emb, tmp_path / "docs.txt", tmp_path / "labels.txt"
+
+
+@pytest.mark.gpu
+def test_cli_end_to_end_overlap_precision_determinism(tmp_path):
+    """SPEC.md cli + acceptance criteria 7 and 8: index -> query (byte-identical on a rerun),
+    overlap(RWMD, WMD) >= overlap(WCD, WMD) at every k on a clustered corpus (n = 500,
+    5 clusters), and same-label precision reported per bucket."""
+    import json
+    from paper_1711_07227_b200 import cli
+    emb, docs, labels = _clustered_corpus(tmp_path)
+    idx = str(tmp_path / "c.lcrw")
+    assert cli.main(["index", "--embeddings", str(emb), "--corpus", str(docs), "--labels", str(labels),
+                     "--index", idx, "--out", str(tmp_path / "i.json")]) == 0
+    assert json.loads((tmp_path / "i.json").read_text())["n"] == 500
+    q = ["query", "--index", idx, "--sample", "20", "--seed", "3", "--k", "5", "--exclude-self"]
+    assert cli.main(q + ["--out", str(tmp_path / "q1.jsonl")]) == 0
+    assert cli.main(q + ["--out", str(tmp_path / "q2.jsonl")]) == 0
+    assert (tmp_path / "q1.jsonl").read_bytes() == (tmp_path / "q2.jsonl").read_bytes()
+    recs = [json.loads(l) for l in (tmp_path / "q1.jsonl").read_text().splitlines()]
+    assert len(recs) == 20 and all(r["query"] not in r["ids"] and len(r["ids"]) == 5 for r in recs)
+    ov = {}
+    for method in ("rwmd", "wcd"):
+        out = tmp_path / f"ov_{method}.jsonl"
+        assert cli.main(["overlap", "--index", idx, "--sample", "20", "--seed", "3", "--method", method,
+                         "--reference", "wmd", "--k-pct", "1", "2", "5", "10", "--exclude-self",
+                         "--out", str(out)]) == 0
+        ov[method] = [json.loads(l)["overlap"] for l in out.read_text().splitlines()]
+    assert all(a >= b for a, b in zip(ov["rwmd"], ov["wcd"])), ov
+    out = tmp_path / "p.jsonl"
+    assert cli.main(["precision", "--index", idx, "--sample", "40", "--seed", "1", "--k", "1", "4", "16",
+                     "--out", str(out)]) == 0
+    prec = [json.loads(l) for l in out.read_text().splitlines()]
+    assert prec and all(0.0 <= r["precision"] <= 1.0 for r in prec)

@@ -230,3 +230,16 @@ def test_query_plan_validation():
         QueryPlan(k=0).validate()
     with pytest.raises(ValueError, match="partitions must be >= 1"):
         QueryPlan(partitions=0).validate()
+
+
+def test_cli_usage_and_errors(tmp_path, capsys):
+    """SPEC.md cli: bad flags exit 2, runtime errors exit 1 with a diagnostic."""
+    from paper_1711_07227_b200 import cli
+    with pytest.raises(SystemExit) as e:
+        cli.main(["query", "--method", "bm25", "--index", "x"])
+    assert e.value.code == 2
+    with pytest.raises(SystemExit) as e:
+        cli.main([])
+    assert e.value.code == 2
+    assert cli.main(["query", "--index", str(tmp_path / "missing.lcrw")]) == 1
+    assert "error:" in capsys.readouterr().err
