@@ -1,7 +1,11 @@
 #!/usr/bin/env python
 """Benchmark: symmetric LC-RWMD doc-pair distances/sec (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|mid|c4|c5]
+
+Other --config values run one GPU's share of BASELINE configs[3] (c4: V = 3M,
+h ~ 150) and [4] (c5: a 4k-query batch on a 25k-doc shard, V = 400k); the
+all-pairs path for configs[4] is measured by bench_rows.py.
 
 Workload (BASELINE.json configs[1] = SURVEY "C2"): 1M resident docs x 1k query
 docs, vocabulary 100k, m = 300, ~50 unique words/doc, top-k = 10, synthetic
