@@ -19,6 +19,13 @@
   GPU) through the forward-only all_pairs path, next to the general symmetric
   pipeline on the same set.
 
+* ``allpairs_rank``: one rank's share of BASELINE configs[4] itself (200,000
+  docs, V = 400k, 8 ranks): C = D1[:, S_0] for the 25,000-doc shard against all
+  200,000 docs, the max-combine into its output rows and their top-10 -- what
+  each GPU computes in parallel.sharded_all_pairs_topk.  The all_to_all of the
+  row blocks (17.5 GB per rank) is not part of the timed region (one GPU here);
+  the received blocks are stood in for by the rank's own rows.
+
 Inputs are resident in HBM for the device-timed value (CUDA events); these rows
 are not part of bench.py's headline line.
 """
@@ -161,6 +168,73 @@ def row_allpairs(args):
     print(json.dumps(line), flush=True)
 
 
+def row_allpairs_rank(args):
+    """Per-rank compute of sharded all-pairs at configs[4] scale (see module docstring)."""
+    import torch
+    from paper_1711_07227_b200 import device, parallel, synthetic as S
+    V, m, n, h, k, world = 400_000, 300, 200_000, 50, 10, 8
+    lo, hi = parallel.shard_range(n, 0, world)
+    n_r = hi - lo
+    E = S.embeddings(V, m, seed=0)
+    x = S.histograms(n, V, h, seed=1)
+    Et = torch.from_numpy(E).cuda()
+    dx = device.DeviceCSR.upload(x)
+    dloc = device.DeviceCSR.upload(x.slice_rows(lo, hi))
+    C = torch.empty((n, n_r), dtype=torch.float32, device="cuda")
+    Dr = torch.empty((n_r, n), dtype=torch.float32, device="cuda")
+    od = torch.empty((n_r, k), dtype=torch.float32, device="cuda")
+    oi = torch.empty((n_r, k), dtype=torch.int64, device="cuda")
+    sizes = [parallel.shard_range(n, r, world)[1] - parallel.shard_range(n, r, world)[0] for r in range(world)]
+    assert all(sz == n_r for sz in sizes)
+    t = {}
+
+    def step():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        prep = device.PreparedEmbeddings(Et)
+        device.forward_rows_into(device.Restricted.build(dx, prep), prep, dloc, C, 4096)
+        e[1].record()
+        at = 0
+        for sz in sizes:  # C[S_0] (n_r x n_r) stands in for the received block D1[S_0, S_s]
+            device.max_transposed_into(Dr[:, at:at + sz], C[lo:hi], C[at:at + sz])
+            at += sz
+        device.topk_matrix_rows(Dr, n_r, n, n, 0, k, od, oi)
+        e[2].record()
+        t.setdefault("fwd", []).append(e)
+        return od
+
+    ms, _ = timed(step, args.steps, args.warmup)
+    torch.cuda.synchronize()
+    ev = t["fwd"][-args.steps:]
+    fwd = sum(a[0].elapsed_time(a[1]) for a in ev) / len(ev)
+    comb = sum(a[1].elapsed_time(a[2]) for a in ev) / len(ev)
+    xch_bytes = (n - n_r) * n_r * 4
+    # the other orientation (the shard's rows against all docs as queries), timed once:
+    # Phase 1 is v_e(shard) x H(all) there, with v_e(shard) ~ v_e(all)
+    del Dr
+    Dold = torch.empty((n_r, n), dtype=torch.float32, device="cuda")
+    prep = device.PreparedEmbeddings(Et)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    device.forward_rows_into(device.Restricted.build(dloc, prep), prep, dx, Dold, 4096)
+    e1.record()
+    torch.cuda.synchronize()
+    old_ms = e0.elapsed_time(e1)
+    del Dold
+    line = {"metric": "all-pairs symmetric RWMD doc-pairs/sec (per-rank compute, configs[4] shard)",
+            "value": n * n / (ms * 1e-3), "unit": "doc-pairs/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "f16 operands, fp32 accumulate, fp64 SpMM",
+            "config": {"workload": "rank 0 of 8 for all-pairs top-10 of 200k docs, V=400k, m=300, h~50 "
+                                   "(BASELINE configs[4]); value = n^2 / per-rank compute time, all_to_all excluded",
+                       "n_docs": n, "shard_docs": n_r, "world": world},
+            "split_ms": {"forward_C": fwd, "combine_topk": comb},
+            "exchange_bytes_per_rank": xch_bytes,
+            "rows_orientation_forward_ms": old_ms}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", default="wmd,wcd")
@@ -170,7 +244,7 @@ def main():
     ap.add_argument("--allpairs-n", type=int, default=50_000)
     args = ap.parse_args()
     for r in args.rows.split(","):
-        {"wmd": row_wmd, "wcd": row_wcd, "allpairs": row_allpairs}[r](args)
+        {"wmd": row_wmd, "wcd": row_wcd, "allpairs": row_allpairs, "allpairs_rank": row_allpairs_rank}[r](args)
 
 
 if __name__ == "__main__":

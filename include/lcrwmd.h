@@ -167,8 +167,13 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
  * direction equal to the transposed forward one): D = max(D, D^T) in place for
  * an n x n row-major matrix with row stride ld. */
 int lcrw_symmetrize_max(float* D, int64_t n, int64_t ld, void* stream);
-/* Sharded all-pairs combine: D[i, j] = max(D[i, j], R[j, i]) for i < rows,
- * j < cols (D row stride ldd, R row stride ldr). */
+/* Sharded all-pairs combine: out[i, j] = max(A[i, j], R[j, i]) for i < rows,
+ * j < cols (row strides ldo, lda, ldr; out may equal A).  The caller passes
+ * A = the block D1[S_r, S_s] received from rank s, R = this rank's own block
+ * D1[S_s, S_r] and out = columns S_s of its output rows. */
+int lcrw_max_transposed_into(float* out, int64_t ldo, const float* A, int64_t lda, const float* R, int64_t ldr,
+                             int64_t rows, int64_t cols, void* stream);
+/* In place: D[i, j] = max(D[i, j], R[j, i]). */
 int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int64_t rows, int64_t cols,
                         void* stream);
 

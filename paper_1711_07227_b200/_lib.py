@@ -51,6 +51,7 @@ SIGNATURES: dict[str, tuple] = {
                                     I64, I64, I32, P, P, SZ, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),
+    "lcrw_max_transposed_into": (I32, [P, I64, P, I64, P, I64, I64, I64, P]),
     "lcrw_reverse_panels_tile_rows": (I32, []),
     "lcrw_reverse_panels_group": (I32, []),
     "lcrw_reverse_panels_warps": (I32, []),
@@ -82,6 +83,7 @@ KERNELS_PER_CALL = {
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
     "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
+    "lcrw_max_transposed_into": 1,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels);
 # bench.py adds those from the batch count (= its reverse_panels launches).

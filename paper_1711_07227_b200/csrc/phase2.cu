@@ -279,9 +279,10 @@ __global__ void __launch_bounds__(256) symmetrize_max_kernel(float* __restrict__
 }
 
 
-// D[i, j] = max(D[i, j], R[j, i]) for i < rows, j < cols: the sharded all-pairs combine
-// (this rank's rows against a peer's block of the forward bounds, transposed through smem).
-__global__ void __launch_bounds__(256) max_transposed_kernel(float* __restrict__ D, int64_t ldd,
+// out[i, j] = max(A[i, j], R[j, i]) for i < rows, j < cols: the sharded all-pairs combine
+// (a peer's block of the forward bounds against this rank's own block, transposed through
+// smem).  out may alias A (the in-place lcrw_max_transposed).
+__global__ void __launch_bounds__(256) max_transposed_kernel(float* out, int64_t ldo, const float* A, int64_t lda,
                                                              const float* __restrict__ R, int64_t ldr, int64_t rows,
                                                              int64_t cols) {
   __shared__ float t[32][33];
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(256) max_transposed_kernel(float* __restrict__
   __syncthreads();
   for (int y = ty; y < 32; y += 8) {
     const int64_t i = i0 + y, j = j0 + tx;
-    if (i < rows && j < cols) D[i * ldd + j] = fmaxf(D[i * ldd + j], t[tx][y]);
+    if (i < rows && j < cols) out[i * ldo + j] = fmaxf(A[i * lda + j], t[tx][y]);
   }
 }
 
@@ -342,17 +343,23 @@ int lcrw_symmetrize_max(float* D, int64_t n, int64_t ld, void* stream) {
   return LCRW_OK;
 }
 
-int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int64_t rows, int64_t cols,
-                        void* stream) {
-  LCRW_REQUIRE(rows >= 0 && cols >= 0 && ldd >= cols && ldr >= rows, "lcrw_max_transposed: bad shape");
+int lcrw_max_transposed_into(float* out, int64_t ldo, const float* A, int64_t lda, const float* R, int64_t ldr,
+                             int64_t rows, int64_t cols, void* stream) {
+  LCRW_REQUIRE(rows >= 0 && cols >= 0 && ldo >= cols && lda >= cols && ldr >= rows,
+               "lcrw_max_transposed: bad shape");
   if (rows == 0 || cols == 0) return LCRW_OK;
-  LCRW_REQUIRE(D && R, "lcrw_max_transposed: null pointer");
+  LCRW_REQUIRE(out && A && R, "lcrw_max_transposed: null pointer");
   LCRW_REQUIRE(ceil_div(rows, 32) < 65536, "lcrw_max_transposed: too many rows for one launch");
   cudaStream_t st = as_stream(stream);
   max_transposed_kernel<<<dim3((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), 256, 0, st>>>(
-      D, ldd, R, ldr, rows, cols);
+      out, ldo, A, lda, R, ldr, rows, cols);
   LCRW_CHECK_LAUNCH("max_transposed_kernel");
   return LCRW_OK;
+}
+
+int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int64_t rows, int64_t cols,
+                        void* stream) {
+  return lcrw_max_transposed_into(D, ldd, D, ldd, R, ldr, rows, cols, stream);
 }
 
 int lcrw_reverse_panels_tile_rows(void) { return kRpTile; }

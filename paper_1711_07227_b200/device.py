@@ -586,6 +586,15 @@ def max_transposed(D: torch.Tensor, R: torch.Tensor) -> None:
     _lib.call("lcrw_max_transposed", _p(D), int(D.stride(0)), _p(R), int(R.stride(0)), rows, cols, _stream())
 
 
+def max_transposed_into(out: torch.Tensor, A: torch.Tensor, R: torch.Tensor) -> None:
+    """out = max(A, R^T) (lcrw_max_transposed_into); out, A (rows, cols), R (cols, rows),
+    each row-major with its own row stride."""
+    rows, cols = int(A.shape[0]), int(A.shape[1])
+    assert tuple(out.shape) == (rows, cols) and tuple(R.shape) == (cols, rows)
+    _lib.call("lcrw_max_transposed_into", _p(out), int(out.stride(0)), _p(A), int(A.stride(0)), _p(R),
+              int(R.stride(0)), rows, cols, _stream())
+
+
 def all_pairs(x: DeviceCSR, prep: PreparedEmbeddings, batch: int = 4096) -> torch.Tensor:
     """Symmetric LC-RWMD of a set against itself, (n, n) on the device (BASELINE configs[4]).
 

@@ -13,10 +13,13 @@ contiguous shards + topk_merge):
   the "queries" of the reverse pass against the replicated X2;
 * top-k: local per-query top-k, NCCL gather to rank 0, merge there
   (kernels.py:226-232);
-* all-pairs (X1 == X2, BASELINE configs[4]): forward bounds of the local rows
-  against every doc, one all_to_all of the (n_r x n_s) blocks (the reverse
-  bounds are the peers' forward bounds transposed), max-combine, local top-k,
-  gather (``sharded_all_pairs_topk``).  Results are identical for any world size: every
+* all-pairs (X1 == X2, BASELINE configs[4]): forward bounds of EVERY doc
+  against the local docs as queries, C_r = D1[:, S_r] -- Phase 1 is then
+  v_e(all) x H(local), so the dominant work divides by the world size (the
+  other orientation, local rows against all queries, keeps v_e(local) ~ v_e and
+  does not scale) -- one all_to_all of C_r's contiguous row blocks, the
+  max-combine with the own block transposed into the local output rows, local
+  top-k, gather (``sharded_all_pairs_topk``).  Results are identical for any world size: every
   pair distance is computed by the same arithmetic, and the merge is exact.
 
 The collective glue (``allgather_slices``, ``gather_candidates``) is
@@ -64,26 +67,28 @@ def allgather_slices(local: torch.Tensor, group=None) -> torch.Tensor:
     return out
 
 
-def exchange_blocks(D1: torch.Tensor, sizes: list[int], group=None) -> list[torch.Tensor]:
+def exchange_blocks(C: torch.Tensor, sizes: list[int], group=None) -> list[torch.Tensor]:
     """All-pairs exchange (BASELINE configs[4]): this rank holds the forward
-    bounds of its rows against ALL docs, D1 (n_r, n); rank s needs the block D1[:, S_s]
-    (its docs as the "reverse" side of ours).  One all_to_all; returns the blocks
-    received from every rank s, each (n_s, n_r) = that rank's D1[S_s rows, S_r cols]."""
+    bounds of ALL docs against its own docs, C = D1[:, S_r] (n, n_r) row-major; rank s
+    needs the row block C[S_s] = D1[S_s, S_r] (contiguous, no packing).  One
+    all_to_all; returns the blocks received from every rank s, each (n_r, n_s) =
+    D1[S_r, S_s] (rank s's C rows for our docs)."""
     rank, world = _world()
-    n_r = int(D1.shape[0])
+    n_r = int(C.shape[1])
     offs = [0]
     for sz in sizes:
         offs.append(offs[-1] + sz)
     if world == 1:
-        return [D1[:, offs[0]:offs[1]]]
-    send = torch.cat([D1[:, offs[s]:offs[s + 1]].contiguous().view(-1) for s in range(world)])
-    recv = torch.empty(sum(sz * n_r for sz in sizes), dtype=D1.dtype, device=D1.device)
-    dist.all_to_all_single(recv, send, output_split_sizes=[sz * n_r for sz in sizes],
-                           input_split_sizes=[n_r * sz for sz in sizes], group=group)
+        return [C[offs[0]:offs[1]]]
+    send = C.contiguous().view(-1)
+    my = sizes[rank]
+    recv = torch.empty(sum(sz * my for sz in sizes), dtype=C.dtype, device=C.device)
+    dist.all_to_all_single(recv, send, output_split_sizes=[my * sz for sz in sizes],
+                           input_split_sizes=[sz * n_r for sz in sizes], group=group)
     out, at = [], 0
     for sz in sizes:
-        out.append(recv[at:at + sz * n_r].view(sz, n_r))
-        at += sz * n_r
+        out.append(recv[at:at + my * sz].view(my, sz))
+        at += my * sz
     return out
 
 
@@ -185,23 +190,29 @@ def sharded_topk_host(x1_shard, doc_base: int, n1_total: int, x2, E, k: int, gro
 def sharded_all_pairs_topk(dx_local: DeviceCSR, dx_all: DeviceCSR, lo: int, prep: PreparedEmbeddings, k: int,
                            batch: int = 4096, group=None):
     """All-pairs symmetric top-k with docs sharded over ranks (BASELINE configs[4]):
-    forward bounds of the local rows against all docs (queries replicated), one
-    all_to_all of the (n_r x n_s) blocks, D[:, S_s] = max(D1[:, S_s], received^T),
+    C = D1[:, S_r], the forward bounds of every doc against the local docs as queries
+    (in ``batch``-query passes), one all_to_all of C's row blocks, then
+    D[S_r, S_s] = max(D1[S_r, S_s] received, C[S_s]^T) into the local output rows,
     per-row top-k with global ids, gathered to rank 0 as (n, k); None elsewhere."""
     rank, world = _world()
     n = dx_all.n_rows
     sizes = [hi_ - lo_ for lo_, hi_ in (shard_range(n, r, world) for r in range(world))]
     n_r = dx_local.n_rows
-    D = torch.empty((max(n_r, 1), n), dtype=torch.float32, device=dx_all.cols.device)
-    device.forward_rows_into(device.Restricted.build(dx_local, prep), prep, dx_all, D, batch)
-    if world == 1:  # the one block is D itself: symmetrise in place
-        device._lib.call("lcrw_symmetrize_max", device._p(D), n, n, device._stream())
+    C = torch.empty((n, max(n_r, 1)), dtype=torch.float32, device=dx_all.cols.device)
+    if n_r:
+        device.forward_rows_into(device.Restricted.build(dx_all, prep), prep, dx_local, C, batch)
+    if world == 1:  # C is D1 itself: symmetrise in place
+        device._lib.call("lcrw_symmetrize_max", device._p(C), n, n, device._stream())
+        D = C
     else:
-        blocks = exchange_blocks(D[:n_r], sizes, group)
+        blocks = exchange_blocks(C[:, :n_r], sizes, group)
+        D = torch.empty((max(n_r, 1), n), dtype=torch.float32, device=C.device)
         at = 0
         for s, sz in enumerate(sizes):
-            device.max_transposed(D[:n_r, at:at + sz], blocks[s])
+            if n_r and sz:
+                device.max_transposed_into(D[:n_r, at:at + sz], blocks[s], C[at:at + sz, :n_r])
             at += sz
+        del C, blocks
     kk = min(k, n)
     od = torch.empty((max(n_r, 1), k), dtype=torch.float32, device=D.device)
     oi = torch.empty((max(n_r, 1), k), dtype=torch.int64, device=D.device)

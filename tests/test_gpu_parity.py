@@ -573,9 +573,10 @@ def test_all_pairs_matches_symmetric(batch):
 
 @pytest.mark.gpu
 def test_all_pairs_sharded_emulated_ranks():
-    """Sharded all-pairs on one GPU: per-shard forward rows, the all_to_all blocks taken
-    directly, max_transposed combine -- bitwise equal to the single-set all_pairs for
-    W in {2, 3}; parallel.sharded_all_pairs_topk at world 1 equals lcrwmd_all_pairs_topk."""
+    """Sharded all-pairs on one GPU: per-shard C = D1[:, S_r] (all docs against the shard's
+    docs as queries), the all_to_all row blocks taken directly, max_transposed_into
+    combine -- bitwise equal to the single-set all_pairs for W in {2, 3};
+    parallel.sharded_all_pairs_topk at world 1 equals lcrwmd_all_pairs_topk."""
     import torch
     from paper_1711_07227_b200 import device, parallel
     _, D, _ = _pkg()
@@ -587,19 +588,22 @@ def test_all_pairs_sharded_emulated_ranks():
     dx = device.DeviceCSR.upload(x)
     want = device.all_pairs(dx, prep, 20)
     n = x.n_rows
+    res_all = device.Restricted.build(dx, prep)
     for W in (2, 3):
         ranges = [parallel.shard_range(n, r, W) for r in range(W)]
-        D1 = []
+        Cs = []
         for lo, hi in ranges:
-            d = torch.empty((hi - lo, n), dtype=torch.float32, device="cuda")
-            device.forward_rows_into(device.Restricted.build(device.DeviceCSR.upload(x.slice_rows(lo, hi)), prep),
-                                     prep, dx, d, 20)
-            D1.append(d)
-        recv = [[D1[s_][:, lo:hi].contiguous() for s_ in range(W)] for lo, hi in ranges]  # the all_to_all
-        for r in range(W):
+            c = torch.empty((n, hi - lo), dtype=torch.float32, device="cuda")
+            device.forward_rows_into(res_all, prep, device.DeviceCSR.upload(x.slice_rows(lo, hi)), c, 20)
+            Cs.append(c)
+        rows = []
+        for r, (a0, a1) in enumerate(ranges):
+            out = torch.empty((a1 - a0, n), dtype=torch.float32, device="cuda")
             for s_, (b0, b1) in enumerate(ranges):
-                device.max_transposed(D1[r][:, b0:b1], recv[r][s_])
-        got = torch.cat(D1)
+                recv = Cs[s_][a0:a1].contiguous()  # what the all_to_all delivers from rank s
+                device.max_transposed_into(out[:, b0:b1], recv, Cs[r][b0:b1])
+            rows.append(out)
+        got = torch.cat(rows)
         assert torch.equal(got, want), W
     od, oi = parallel.sharded_all_pairs_topk(dx, dx, 0, prep, 5, 20)
     res = D.lcrwmd_all_pairs_topk(x, E, 5, batch_size=20)

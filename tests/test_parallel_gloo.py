@@ -71,23 +71,21 @@ def _worker(rank, world, port, q):
                 assert np.array_equal(md, want_d[j]) and np.array_equal(mi, want_i[j]), j
         else:
             assert g is None
-        # --- all-pairs (X1 == X2): forward-bound blocks exchanged with one all_to_all;
-        # max(D1, received^T) over this rank's rows equals the symmetric all-pairs matrix
+        # --- all-pairs (X1 == X2): this rank holds C = D1[:, S_r] (every doc against its
+        # docs as queries); one all_to_all of C's row blocks; max(received, C[S_s]^T)
+        # over this rank's rows equals the symmetric all-pairs matrix
         n = 23
         sizes = [hi_ - lo_ for lo_, hi_ in (parallel.shard_range(n, r, world) for r in range(world))]
         xa = S.histograms(n, V, 12, seed=5)
         D1 = O.lcrwmd_batched(xa, xa, E)  # forward bounds (n, n)
         a0, a1 = parallel.shard_range(n, rank, world)
-        mine = torch.from_numpy(np.ascontiguousarray(D1[a0:a1]))
+        mine = torch.from_numpy(np.ascontiguousarray(D1[:, a0:a1]))
         blocks = parallel.exchange_blocks(mine, sizes)
-        at = 0
-        for s_, sz in enumerate(sizes):
+        for s_ in range(world):
             b0, b1 = parallel.shard_range(n, s_, world)
-            assert np.array_equal(blocks[s_].numpy(), D1[b0:b1, a0:a1]), s_
-            at += sz
+            assert np.array_equal(blocks[s_].numpy(), D1[a0:a1, b0:b1]), s_
         sym = np.maximum(D1, D1.T)
-        got = np.concatenate([np.maximum(D1[a0:a1, parallel.shard_range(n, s_, world)[0]:
-                                            parallel.shard_range(n, s_, world)[1]], blocks[s_].numpy().T)
+        got = np.concatenate([np.maximum(blocks[s_].numpy(), mine.numpy()[slice(*parallel.shard_range(n, s_, world))].T)
                               for s_ in range(world)], axis=1)
         assert np.array_equal(got, sym[a0:a1])
         assert np.allclose(sym, O.lcrwmd_full(xa, xa, E), rtol=1e-6, atol=1e-7)
