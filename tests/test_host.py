@@ -243,3 +243,25 @@ def test_cli_usage_and_errors(tmp_path, capsys):
     assert e.value.code == 2
     assert cli.main(["query", "--index", str(tmp_path / "missing.lcrw")]) == 1
     assert "error:" in capsys.readouterr().err
+
+
+def test_product_has_no_cpu_fallback():
+    """Without a CUDA device every compute entry point raises instead of computing on the
+    host; a missing library is reported, not worked around."""
+    import subprocess
+    import sys
+    import torch
+    from paper_1711_07227_b200 import distances, kernels
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a GPU")
+    E = S.embeddings(40, 8, seed=0)
+    x = S.histograms(5, 40, 4, seed=1)
+    for call in (lambda: distances.lcrwmd_full(x, x, E), lambda: distances.lcrwmd_topk(x, x, E, 2),
+                 lambda: kernels.topk_select(np.ones(4, np.float32), np.arange(4), 2)):
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            call()
+    code = ("import os; os.environ['LCRW_LIB'] = '/nonexistent/liblcrwmd.so'\n"
+            "from paper_1711_07227_b200 import _lib\n"
+            "try:\n    _lib.load()\nexcept RuntimeError as e:\n    print('raised', e)\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.stdout.startswith("raised"), out.stdout + out.stderr
