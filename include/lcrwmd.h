@@ -186,9 +186,13 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
  * doc_offsets (batch planning); doc_cols are global E ids, rep/next/remap as in
  * lcrw_zero_identical.  Writes D = max(D1, D2) for all docs (see
  * lcrw_reverse_panels).  Workspace from lcrw_reverse_workspace with
- * max_batch_words = max words over batches.  d1_ready (cudaEvent_t or NULL):
- * the stream waits on it before the first read of D1, so the forward direction
- * can run concurrently on another stream with the reverse Phase 1. */
+ * max_batch_words = max words over batches (0 in table mode).  d1_ready
+ * (cudaEvent_t or NULL): the stream waits on it before the first read of D1, so
+ * the forward direction can run concurrently on another stream with the reverse
+ * Phase 1.  table (NULL = GEMM mode): the distance table of lcrw_table_transpose
+ * for these a_rows query-vocabulary rows and the v_rows E rows; each batch's Z2
+ * is then one lcrw_table_min (gather, plan, phase1 and zeros are skipped; rep,
+ * next, remap, EhB may be NULL). */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                           int m, int kp,
@@ -196,8 +200,24 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, void* d1_ready, void* ws, size_t ws_bytes,
-                          void* stream);
+                          int64_t batch_docs, int range_cols, const float* table, void* d1_ready, void* ws,
+                          size_t ws_bytes, void* stream);
+
+/* ---- distance-table reverse Phase 1 (table.cu) ---------------------------
+ * When nnz(X1) >> V, every (w, u) distance of the reverse Phase 1 is needed
+ * ~nnz/V times; the table holds each once.  Build: Tp = lcrw_phase1 over the
+ * a_rows query-vocabulary A rows and ALL v_rows E rows as singleton segments
+ * (z_shift 7, z_panel = 128 * a_rows) + lcrw_zero_identical, then
+ * T[(w >> 7) * v_rows * 128 + u * 128 + (w & 127)] = Tp[w, u] (128-word chunks,
+ * one 512-byte row per E row; lcrw_table_floats(a_rows, v_rows) floats).
+ * lcrw_table_min: Z2[p * z_panel + w * 32 + (d & 31)] = min over the words u of
+ * doc d of T[w, u] (32-doc panels, z_panel = 32 * a_rows; docs as lcrw_phase1's
+ * segments: doc_offsets[d] - seg_base .. into doc_cols, E ids < v_rows). */
+int lcrw_table_chunk(void);
+int64_t lcrw_table_floats(int64_t a_rows, int64_t v_rows);
+int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, float* T, void* stream);
+int lcrw_table_min(const float* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
+                   int64_t n_docs, const int32_t* doc_cols, float* Z2, int64_t z_panel, void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k

@@ -48,7 +48,11 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
-                                    I64, I64, I32, P, P, SZ, P]),
+                                    I64, I64, I32, P, P, P, SZ, P]),
+    "lcrw_table_chunk": (I32, []),
+    "lcrw_table_floats": (I64, [I64, I64]),
+    "lcrw_table_transpose": (I32, [P, I64, I64, P, P]),
+    "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, I64, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),
     "lcrw_max_transposed_into": (I32, [P, I64, P, I64, P, I64, I64, I64, P]),
@@ -73,7 +77,7 @@ SIGNATURES: dict[str, tuple] = {
 _VALUE_FUNCS = {"lcrw_emd_problem_bytes", "lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
                 "lcrw_endmask_words", "lcrw_plan_ranges", 
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
-                "lcrw_reverse_panels_ilp",                 "lcrw_profile_count"}
+                "lcrw_reverse_panels_ilp", "lcrw_profile_count", "lcrw_table_chunk", "lcrw_table_floats"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".
@@ -83,11 +87,13 @@ KERNELS_PER_CALL = {
     "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
     "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
-    "lcrw_max_transposed_into": 1,
+    "lcrw_max_transposed_into": 1, "lcrw_table_transpose": 1, "lcrw_table_min": 1,
 }
-# lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels);
-# bench.py adds those from the batch count (= its reverse_panels launches).
+# lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels)
+# in GEMM mode, 2 (table_min, reverse_panels) with a distance table; bench.py adds those from the
+# batch count (= its reverse_panels launches).
 REVERSE_KERNELS_PER_BATCH = 6
+REVERSE_KERNELS_PER_BATCH_TABLE = 2
 
 CALLS: dict[str, int] = {}
 

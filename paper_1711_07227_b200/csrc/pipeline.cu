@@ -9,6 +9,8 @@
 //   phase1   Z2[doc, w] = min_t |E_w - T_t|                 (tcgen05, 32-doc panels)
 //   zeros    Z2[doc, w] = 0 where doc holds a word identical to w
 //   reverse  D[q, doc] = max(D1, spmm(Xq, Z2)), panel-streaming (query-major D)
+// or, with a distance table (table.cu; built once per query set), the first four
+// steps are one lcrw_table_min launch (exact zeros are already in the table).
 // The loop runs in C++ so a batch costs a handful of launch calls, not Python.
 #include <cstdlib>
 
@@ -72,15 +74,15 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, void* d1_ready, void* ws, size_t ws_bytes,
-                          void* stream) {
+                          int64_t batch_docs, int range_cols, const float* table, void* d1_ready, void* ws,
+                          size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
-  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && rep && ws && D, "lcrw_reverse_pipeline: null pointer");
+  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && (rep || table) && ws && D, "lcrw_reverse_pipeline: null pointer");
   LCRW_REQUIRE(batch_docs > 0 && (batch_docs % (1 << kZShift)) == 0,
                "lcrw_reverse_pipeline: batch_docs must be a positive multiple of 32");
   int64_t max_words = 0;
-  for (int64_t j0 = 0; j0 < n_docs; j0 += batch_docs) {
+  for (int64_t j0 = 0; !table && j0 < n_docs; j0 += batch_docs) {
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
     const int64_t w = doc_offsets_host[j1] - doc_offsets_host[j0];
     if (w > max_words) max_words = w;
@@ -105,6 +107,11 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
     const int64_t nd = j1 - j0;
     const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
+    if (table) {
+      if ((status = lcrw_table_min(table, a_rows, v_rows, doc_offsets + j0, lo, nd, doc_cols + lo, Z2, z_panel,
+                                   stream)))
+        return status;
+    } else {
     if (!gather_b && (status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream)))
       return status;
     const int rc = range_cols > 0 ? range_cols : auto_range_cols(nw, a_rows);
@@ -116,6 +123,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;
+    }
     if (j0 == 0 && d1_ready) {  // D1 may still be in flight on another stream (forward direction)
       cudaError_t e = cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d1_ready), 0);
       if (e != cudaSuccess) return cuda_status(e, "cudaStreamWaitEvent (D1 ready)");

@@ -17,6 +17,7 @@ Pipeline for ``lcrwmd_topk`` / ``lcrwmd_full`` (distances.py:244-264):
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -428,6 +429,41 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
     return words, tile_off
 
 
+REVERSE_TABLE_Z2_BYTES = 16 << 30  # table mode: bigger batches, each re-streams the table once
+TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 512 B) must stay L2-resident
+
+
+def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int) -> str:
+    """"table" when the reverse Phase 1 is cheaper as a distance table + per-doc gathers
+    (table.cu): the vocabulary is small next to nnz(X1) (each (w, u) distance is then
+    needed ~nnz/V times), a 128-word chunk of it fits in L2, and the table fits in HBM;
+    else "gemm".  LCRW_REVERSE=gemm|table overrides (tests, A/B runs)."""
+    env = os.environ.get("LCRW_REVERSE", "")
+    if env in ("gemm", "table"):
+        return env
+    if v_rows * 512 > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
+        return "gemm"
+    table_bytes = 2 * int(_lib.value("lcrw_table_floats", a_rows, v_rows)) * 4
+    free, _ = torch.cuda.mem_get_info()
+    return "table" if table_bytes < free // 3 else "gemm"
+
+
+def distance_table(res2: "Restricted", prep: PreparedEmbeddings) -> torch.Tensor:
+    """The reverse Phase-1 distance table (lcrw_table_transpose layout) of the query
+    vocabulary res2 against every E row: lcrw_phase1 with singleton segments (the
+    GEMM form's operands and roles, so each entry is the value it would compute),
+    the exact zeros, then the 128-word chunk transpose."""
+    V = prep.V
+    dev = res2.A.device
+    seg = torch.arange(V + 1, dtype=torch.int64, device=dev)
+    Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=7)
+    zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, 7)
+    T = torch.empty(max(1, int(_lib.value("lcrw_table_floats", res2.v_e, V))), dtype=torch.float32, device=dev)
+    _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(T), _stream())
+    del Tp
+    return T
+
+
 def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BYTES) -> int:
     nb = max(32, budget_bytes // (4 * max(v_e2, 1)))
     nb = min(nb, max(32, n_docs))
@@ -452,9 +488,13 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         raise ValueError("query set too large for the host-planned reverse pass")
     res2 = Restricted.build(x2, prep, host_plan=True)
     e_blk, e_tile = query_entries(x2, res2.host_rank, res2.v_e)
+    mode = reverse_mode(prep.V, res2.v_e, x1.nnz)
+    table = distance_table(res2, prep) if mode == "table" else None
+    if table is not None and z2_budget_bytes == REVERSE_Z2_BYTES:
+        z2_budget_bytes = REVERSE_TABLE_Z2_BYTES
     batch = reverse_batch_docs(n1, res2.v_e, z2_budget_bytes)
     ho = x1.host_offsets
-    max_words = max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
+    max_words = 0 if table is not None else max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
     ws_bytes = C.c_size_t(0)
     _lib.call("lcrw_reverse_workspace", res2.v_e, prep.kp, batch, max_words, C.byref(ws_bytes))
     ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
@@ -464,15 +504,15 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     else:
         D = torch.empty(n2 * n1, dtype=torch.float32, device=dev)  # query-major for the per-query top-k
         ld_q, ld_doc = n1, 1
-    rep, nxt = prep.representatives(x1.cols)
+    rep, nxt = prep.representatives(x1.cols) if table is None else (None, None)
     host_offs = np.ascontiguousarray(ho, dtype=np.int64)
     _lib.call("lcrw_reverse_pipeline", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), prep.V, prep.k_eff,
               prep.kp,
               _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
               _p(nxt), _p(res2.remap), _p(e_blk), _p(e_tile), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
-              batch, 0, C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value,
-              st)
-    del ws
+              batch, 0, _p(table), C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws),
+              ws_bytes.value, st)
+    del ws, table
     if k is None:
         return D.view(n1, n2)
     if k > 1024:

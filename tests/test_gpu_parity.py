@@ -827,3 +827,62 @@ def test_cli_end_to_end_overlap_precision_determinism(tmp_path):
                      "--out", str(out)]) == 0
     prec = [json.loads(l) for l in out.read_text().splitlines()]
     assert prec and all(0.0 <= r["precision"] <= 1.0 for r in prec)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["uniform", "dup_rows", "long_docs", "m37"])
+def test_reverse_table_mode_bitwise_equals_gemm_mode(case, monkeypatch):
+    """The distance-table reverse Phase 1 (csrc/table.cu) against the GEMM form: the
+    symmetric matrix and the top-k are bitwise equal (same Phase-1 entries, exact
+    min), over several doc batches, ragged last panels, query vocabularies that are
+    not a multiple of the 128-word chunk, docs longer than 32 words and duplicated
+    embedding rows (exact zeros); and within tolerance of the oracle."""
+    import torch
+    from paper_1711_07227_b200 import device
+    rng = np.random.default_rng(60 + ["uniform", "dup_rows", "long_docs", "m37"].index(case))
+    V, m = 3000, (37 if case == "m37" else 300)
+    E = rng.standard_normal((V, m)).astype(np.float32)
+    if case == "dup_rows":
+        E[1500:1700] = E[:200]
+    hi = 150 if case == "long_docs" else 60
+    x1 = _rand_set(rng, 1111, V, 1, hi)
+    x2 = _rand_set(rng, 45, V, 1, 60)
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    out = {}
+    for mode in ("gemm", "table"):
+        monkeypatch.setenv("LCRW_REVERSE", mode)
+        full = device.symmetric(d1, d2, prep, None, z2_budget_bytes=4 * 3000 * 320)
+        td, ti = device.symmetric(d1, d2, prep, 7, z2_budget_bytes=4 * 3000 * 320)
+        out[mode] = (full, td, ti)
+    for a, b in zip(out["gemm"], out["table"]):
+        assert torch.equal(a, b)
+    di = np.sort(rng.choice(x1.n_rows, 150, replace=False))
+    ref = O.lcrwmd_full(x1.take_rows(di), x2, E, threads=8)
+    ok, err = rel_close(out["table"][0].cpu().numpy()[di], ref, RTOL, _atol(E))
+    assert ok, err
+
+
+@pytest.mark.gpu
+def test_distance_table_layout_and_zeros():
+    """lcrw_table_transpose layout: T[(w >> 7) * V * 128 + u * 128 + (w & 127)] is the
+    Phase-1 distance of query-vocabulary row w to E row u, exactly 0 for identical rows."""
+    import torch
+    from paper_1711_07227_b200 import device
+    rng = np.random.default_rng(70)
+    V, m = 700, 300
+    E = rng.standard_normal((V, m)).astype(np.float32)
+    E[600:650] = E[:50]
+    x2 = _rand_set(rng, 40, V, 5, 30)
+    prep = device.PreparedEmbeddings(E)
+    res2 = device.Restricted.build(device.DeviceCSR.upload(x2), prep)
+    T = device.distance_table(res2, prep).cpu().numpy()
+    used = np.unique(x2.column_ids)
+    assert res2.v_e == len(used)
+    w = np.arange(len(used))
+    tab = T.reshape(-1, V, 128)[w >> 7, :, w & 127]  # (v_e, V)
+    ref = O.pairwise_euclidean(E[used], E)
+    ok, err = rel_close(tab, ref, RTOL, _atol(E))
+    assert ok, err
+    same = (E[used][:, None, :] == E[None, :, :]).all(-1)
+    assert np.all(tab[same] == 0.0) and same.sum() >= len(used)
