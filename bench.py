@@ -215,7 +215,9 @@ def run_ours(args, cfg):
     # reverse pipeline: 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels), counted
     # from its reverse_panels launches; calibrated against the ncu launch list (profiles/)
     rev_batches = ksum.get("reverse_panels", {"launches": 0})["launches"]
-    launches = (_lib.launches(calls) + _lib.REVERSE_KERNELS_PER_BATCH * rev_batches) // args.steps
+    table_mode = "table_min" in ksum
+    per_batch = _lib.REVERSE_KERNELS_PER_BATCH_TABLE if table_mode else _lib.REVERSE_KERNELS_PER_BATCH
+    launches = (_lib.launches(calls) + per_batch * rev_batches) // args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -263,21 +265,51 @@ def run_ours(args, cfg):
         return
     pk, pk_kind = peaks()
     tpath = ROOT / "profiles" / "roofline_traffic.json"
-    traffic = json.loads(tpath.read_text())["dram_bytes_per_launch"] if tpath.exists() and args.config == "c2" else None
-    rev = ksum.get("phase1_rev", {"ms": float("nan"), "launches": 1})
-    per_launch_ms = rev["ms"] / max(rev["launches"], 1)
-    # algorithmic FLOPs of the reverse Phase 1 per step: 2 * v_e2 * (doc words) * m, K = m unpadded
+    traffic_all = json.loads(tpath.read_text()) if tpath.exists() and args.config == "c2" else {}
     v_e2 = int(np.unique(x2.column_ids).size)
+    # algorithmic FLOPs of a Phase-1 GEMM: 2 * rows * cols * m, K = m unpadded
     rev_flops = 2.0 * v_e2 * x1s.nnz * cfg["dim"]
-    achieved_tf = rev_flops / (rev["ms"] / args.steps * 1e-3) / 1e12
     fwd_flops = 2.0 * int(np.unique(x1s.column_ids).size) * x2.nnz * cfg["dim"]
+    table_flops = 2.0 * v_e2 * cfg["vocab"] * cfg["dim"]
+    # table_min gathers one 4-byte table entry per (query-vocabulary word, doc word) and
+    # writes one Z2 entry per (query-vocabulary word, doc)
+    table_bytes = 4.0 * v_e2 * (x1s.nnz + x1s.n_rows)
     spmm_bytes = 8.0 * (x1s.n_rows + 1) + 8.0 * x1s.nnz + 4.0 * x1s.nnz * n2
     # reverse_panels streams every Z2 panel once (4 * v_e2 bytes per doc), reads D1 and writes D
     rev_bytes = 4.0 * v_e2 * x1s.n_rows + 8.0 * n2 * x1s.n_rows
-    work = {"phase1": fwd_flops, "phase1_rev": rev_flops, "spmm": spmm_bytes, "reverse_panels": rev_bytes}
+    work = {"phase1": fwd_flops, "phase1_rev": rev_flops, "table_build": table_flops, "spmm": spmm_bytes,
+            "reverse_panels": rev_bytes, "table_min": table_bytes}
     peak_tf = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
     pairs = n1 * n2
     value = pairs / (ms * 1e-3)
+    if table_mode:  # dominant kernel: the distance-table gathers, bound by L2 bandwidth
+        tm = ksum["table_min"]
+        achieved = table_bytes / (tm["ms"] / args.steps * 1e-3) / 1e9
+        l2path = ROOT / "profiles" / "l2_gather_peak.json"
+        l2 = json.loads(l2path.read_text()) if l2path.exists() else {"gbs": float("nan"), "source": "missing"}
+        tr = traffic_all.get("table_min_kernel")
+        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 512-B rows of an L2-resident "
+                              "distance-table chunk)",
+                    "bound": "l2", "achieved": achieved, "peak": l2["gbs"], "unit": "GB/s",
+                    "frac": achieved / l2["gbs"],
+                    "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                    "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/roofline_traffic.json)",
+                    "algorithmic_bytes_per_launch": table_bytes * args.steps / tm["launches"],
+                    "peak_source": f"measured L2 gather ceiling on B200 ({l2['source']})",
+                    "hbm_peak_gbs": pk.get("hbm_gbs"), "achieved_over_hbm_peak": achieved / pk.get("hbm_gbs", 1.0),
+                    "per_launch_ms": tm["ms"] / max(tm["launches"], 1),
+                    "launches_per_step": tm["launches"] / args.steps, "share_of_step": tm["ms"] / args.steps / ms}
+    else:
+        rev = ksum.get("phase1_rev", {"ms": float("nan"), "launches": 1})
+        achieved_tf = rev_flops / (rev["ms"] / args.steps * 1e-3) / 1e12
+        tr = traffic_all.get("phase1_kernel")
+        roofline = {"kernel": "phase1_kernel (reverse direction, tcgen05 f16 GEMM + fused segmented min)",
+                    "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": achieved_tf / peak_tf, "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                    "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/roofline_traffic.json)",
+                    "peak_source": f"{pk_kind} bf16_tflops_sustained (dense f16 = bf16 rate)",
+                    "per_launch_ms": rev["ms"] / max(rev["launches"], 1),
+                    "launches_per_step": rev["launches"] / args.steps, "share_of_step": rev["ms"] / args.steps / ms}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -288,16 +320,11 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (X1 400 MB, D1 4 GB); no flush"},
         "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "paper_1711_07227_b200.distances.lcrwmd_topk (pinned host arrays)"},
-        "roofline": {"kernel": "phase1_kernel (reverse direction, tcgen05 f16 GEMM + fused segmented min)",
-                     "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak_tf, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/roofline_traffic.json)",
-                     "peak_source": f"{pk_kind} bf16_tflops_sustained (dense f16 = bf16 rate)",
-                     "per_launch_ms": per_launch_ms, "launches_per_step": rev["launches"] / args.steps,
-                     "share_of_step": rev["ms"] / args.steps / ms},
+        "roofline": roofline,
         "kernels": {n: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                        ("tflops" if n.startswith("phase1") else "gbs_algorithmic"):
-                            (work.get(n, 0.0) / (v["ms"] / args.steps * 1e-3) / (1e12 if n.startswith("phase1") else 1e9))}
+                        ("tflops" if n.startswith(("phase1", "table_build")) else "gbs_algorithmic"):
+                            (work.get(n, 0.0) / (v["ms"] / args.steps * 1e-3) /
+                             (1e12 if n.startswith(("phase1", "table_build")) else 1e9))}
                     for n, v in ksum.items()},
         "gpu_launches": launches,
         "clocks": clk,

@@ -205,14 +205,24 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
 
 /* ---- distance-table reverse Phase 1 (table.cu) ---------------------------
  * When nnz(X1) >> V, every (w, u) distance of the reverse Phase 1 is needed
- * ~nnz/V times; the table holds each once.  Build: Tp = lcrw_phase1 over the
- * a_rows query-vocabulary A rows and ALL v_rows E rows as singleton segments
- * (z_shift 7, z_panel = 128 * a_rows) + lcrw_zero_identical, then
- * T[(w >> 7) * v_rows * 128 + u * 128 + (w & 127)] = Tp[w, u] (128-word chunks,
- * one 512-byte row per E row; lcrw_table_floats(a_rows, v_rows) floats).
+ * ~nnz/V times; the table holds each once:
+ *   T[(w >> 7) * v_rows * 128 + u * 128 + (w & 127)] = |A_w - E_u|
+ * (128-word chunks, one 512-byte row per E row; lcrw_table_floats(a_rows,
+ * v_rows) floats), with exact zeros for identical rows.
+ * lcrw_distance_table builds it in one pass: lcrw_phase1 over the a_rows
+ * query-vocabulary A rows and ALL v_rows E rows (EhB) as singleton segments
+ * (seg_offsets = 0..v_rows and its lcrw_segment_plan), storing row panels
+ * directly (the same entries lcrw_phase1 computes in the GEMM form), then the
+ * zeros (canon/next classes of lcrw_row_classes, remap = E id -> A row or -1).
+ * lcrw_table_transpose builds the same layout from lcrw_phase1's z_shift-7
+ * output Tp (zeros already applied).
  * lcrw_table_min: Z2[p * z_panel + w * 32 + (d & 31)] = min over the words u of
  * doc d of T[w, u] (32-doc panels, z_panel = 32 * a_rows; docs as lcrw_phase1's
  * segments: doc_offsets[d] - seg_base .. into doc_cols, E ids < v_rows). */
+int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
+                        int m, int kp, const int64_t* seg_offsets, const uint32_t* endmask, const int32_t* range_seg,
+                        int64_t n_ranges, const float* scale, const int32_t* canon, const int32_t* next,
+                        const int32_t* remap, float* T, void* stream);
 int lcrw_table_chunk(void);
 int64_t lcrw_table_floats(int64_t a_rows, int64_t v_rows);
 int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, float* T, void* stream);

@@ -52,6 +52,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_table_chunk": (I32, []),
     "lcrw_table_floats": (I64, [I64, I64]),
     "lcrw_table_transpose": (I32, [P, I64, I64, P, P]),
+    "lcrw_distance_table": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P]),
     "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, I64, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),
@@ -88,6 +89,7 @@ KERNELS_PER_CALL = {
     "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
     "lcrw_max_transposed_into": 1, "lcrw_table_transpose": 1, "lcrw_table_min": 1,
+    "lcrw_distance_table": 2,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels)
 # in GEMM mode, 2 (table_min, reverse_panels) with a distance table; bench.py adds those from the

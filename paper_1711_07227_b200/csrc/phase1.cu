@@ -78,6 +78,7 @@ struct Params {
   const int32_t* b_ids;  // gather mode: B row c is operand row b_ids[c] (TMA gather4); NULL = rows in order
   int32_t b_oob;         // gather mode: a row index past the operand table (zero-filled padding rows)
   int z_shift;       // Z panel width = 1 << z_shift segments
+  int z_transposed;  // 1: Z[(r >> zs) * z_panel + (s << zs) + (r & (zw-1))] (row panels; distance tables)
   int a_rows;
   int n_mpairs;      // 256-row A tiles
   int n_ranges;      // column ranges; a work unit takes two consecutive ones
@@ -417,10 +418,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = mp * 2 * BM + (int)rank * BM + quarter * 32 + lane;
       const bool valid = row < p.a_rows;
       const float nE = valid ? __ldg(p.a_norms + row) : 0.f;
-      // output cursor: segment s = U.sb(grp) + emitted so far, Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))]
+      // output cursor: segment s = U.sb(grp) + emitted so far, at
+      //   Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))]   (segment panels), or
+      //   Z[(row >> zs) * z_panel + (s << zs) + (row & (zw-1))] (z_transposed: a warp's
+      //   32 rows of one segment are one coalesced 128-byte store)
       const int64_t s_first = U.sb(grp);
-      float* zp = p.Z + (s_first >> zs) * p.z_panel + ((int64_t)row << zs);
+      float* zq;
+      int64_t step, wrap;
       uint32_t s_in = (uint32_t)s_first & (zw - 1);
+      if (p.z_transposed) {
+        zq = p.Z + ((int64_t)row >> zs) * p.z_panel + (s_first << zs) + (row & (zw - 1));
+        step = zw;
+        wrap = 0;
+      } else {
+        zq = p.Z + (s_first >> zs) * p.z_panel + ((int64_t)row << zs) + s_in;
+        step = 1;
+        wrap = p.z_panel - zw;
+      }
       float run = kInf;
       auto emit = [&](float segmin) {
         float d;
@@ -428,10 +442,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #if LCRW_EPI_MODE == 5
         if (d < -1.f)  // experiment: never true -- the global store is skipped
 #endif
-        if (valid) zp[s_in] = d * inv_scale;
+        if (valid) *zq = d * inv_scale;
+        zq += step;
         if (++s_in == zw) {
           s_in = 0;
-          zp += p.z_panel;
+          zq += wrap;
         }
       };
       uint32_t pm = fetch_mask(c_lo);
@@ -570,13 +585,14 @@ namespace p1 {
 int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
            int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids = nullptr,
-           int64_t b_table_rows = 0) {
+           int64_t b_table_rows = 0, bool z_transposed = false) {
   LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(K)");
   LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
                "lcrw_phase1: row counts must fit in int32");
   LCRW_REQUIRE(n_seg >= 0 && n_ranges >= 1, "lcrw_phase1: bad segment plan");
   LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_phase1: z_shift out of range");
-  LCRW_REQUIRE(z_panel >= (a_rows << z_shift), "lcrw_phase1: z_panel must be >= a_rows << z_shift");
+  LCRW_REQUIRE(z_panel >= ((z_transposed ? n_seg : a_rows) << z_shift),
+               "lcrw_phase1: z_panel must be >= a_rows << z_shift (n_seg << z_shift transposed)");
   if (a_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(A && a_norms && B && seg_offsets && endmask && range_seg && scale && Z,
                "lcrw_phase1: null pointer");
@@ -603,6 +619,7 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   p.b_ids = b_ids;
   p.b_oob = (int32_t)b_table_rows;
   p.z_shift = z_shift;
+  p.z_transposed = z_transposed ? 1 : 0;
   p.a_rows = (int)a_rows;
   p.n_mpairs = (int)ceil_div(a_rows, 2 * BM);
   p.n_ranges = (int)n_ranges;

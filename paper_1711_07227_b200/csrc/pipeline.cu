@@ -21,7 +21,7 @@ namespace p1 {
 int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
            int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids,
-           int64_t b_table_rows);
+           int64_t b_table_rows, bool z_transposed);
 }
 
 namespace {
@@ -119,7 +119,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     if ((status = lcrw_segment_plan(doc_offsets + j0, lo, nd, nw, rc, mask, rs, n_ranges, stream))) return status;
     if ((status = p1::launch(A, a_norms, a_rows, gather_b ? EhB : T, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs,
                              n_ranges, scale, Z2, z_panel, kZShift, st, "phase1_rev",
-                             gather_b ? doc_cols + lo : nullptr, v_table)))
+                             gather_b ? doc_cols + lo : nullptr, v_table, false)))
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;

@@ -225,6 +225,18 @@ def spmm_z_shift(n_seg: int) -> int:
     return 7 if n_seg > 64 else 3
 
 
+def segment_plan(seg_offsets: torch.Tensor, n_seg: int, b_rows: int, a_rows: int, range_cols: int | None = None):
+    """(endmask, range_seg, n_ranges) of lcrw_segment_plan for segments over b_rows B rows."""
+    dev = seg_offsets.device
+    rc = range_cols or _range_cols(b_rows, a_rows)
+    n_ranges = int(_lib.value("lcrw_plan_ranges", b_rows, rc))
+    endmask = torch.empty(int(_lib.value("lcrw_endmask_words", b_rows)), dtype=torch.int32, device=dev)
+    range_seg = torch.empty(n_ranges + 1, dtype=torch.int32, device=dev)
+    _lib.call("lcrw_segment_plan", _p(seg_offsets), 0, n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges,
+              _stream())
+    return endmask, range_seg, n_ranges
+
+
 def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
            b_rows: int, seg_offsets: torch.Tensor, n_seg: int, prep: PreparedEmbeddings,
            range_cols: int | None = None, z_shift: int = 3) -> tuple[torch.Tensor, int]:
@@ -232,11 +244,7 @@ def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
     without the exact-zero pass."""
     dev = A.device
     st = _stream()
-    rc = range_cols or _range_cols(b_rows, a_rows)
-    n_ranges = int(_lib.value("lcrw_plan_ranges", b_rows, rc))
-    endmask = torch.empty(int(_lib.value("lcrw_endmask_words", b_rows)), dtype=torch.int32, device=dev)
-    range_seg = torch.empty(n_ranges + 1, dtype=torch.int32, device=dev)
-    _lib.call("lcrw_segment_plan", _p(seg_offsets), 0, n_seg, b_rows, rc, _p(endmask), _p(range_seg), n_ranges, st)
+    endmask, range_seg, n_ranges = segment_plan(seg_offsets, n_seg, b_rows, a_rows, range_cols)
     w = 1 << z_shift
     z_panel = w * max(a_rows, 1)
     Z = torch.empty(((n_seg + w - 1) // w) * z_panel, dtype=torch.float32, device=dev)
@@ -448,19 +456,26 @@ def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int) -> str:
     return "table" if table_bytes < free // 3 else "gemm"
 
 
-def distance_table(res2: "Restricted", prep: PreparedEmbeddings) -> torch.Tensor:
-    """The reverse Phase-1 distance table (lcrw_table_transpose layout) of the query
-    vocabulary res2 against every E row: lcrw_phase1 with singleton segments (the
-    GEMM form's operands and roles, so each entry is the value it would compute),
-    the exact zeros, then the 128-word chunk transpose."""
+def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: bool = False) -> torch.Tensor:
+    """The reverse Phase-1 distance table (include/lcrwmd.h, table.cu) of the query
+    vocabulary res2 against every E row: lcrw_phase1 with singleton segments (the GEMM
+    form's operands and roles, so each entry is the value it would compute) storing
+    128-row panels directly, plus the exact zeros (lcrw_distance_table).
+    ``via_transpose``: the two-pass build (segment panels + lcrw_zero_identical +
+    lcrw_table_transpose), kept as a cross-check."""
     V = prep.V
     dev = res2.A.device
     seg = torch.arange(V + 1, dtype=torch.int64, device=dev)
-    Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=7)
-    zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, 7)
     T = torch.empty(max(1, int(_lib.value("lcrw_table_floats", res2.v_e, V))), dtype=torch.float32, device=dev)
-    _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(T), _stream())
-    del Tp
+    if via_transpose:
+        Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=7)
+        zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, 7)
+        _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(T), _stream())
+        return T
+    endmask, range_seg, n_ranges = segment_plan(seg, V, V, res2.v_e)
+    _lib.call("lcrw_distance_table", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), V, prep.k_eff, prep.kp,
+              _p(seg), _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(prep.canon), _p(prep.next),
+              _p(res2.remap), _p(T), _stream())
     return T
 
 

@@ -865,8 +865,10 @@ def test_reverse_table_mode_bitwise_equals_gemm_mode(case, monkeypatch):
 
 @pytest.mark.gpu
 def test_distance_table_layout_and_zeros():
-    """lcrw_table_transpose layout: T[(w >> 7) * V * 128 + u * 128 + (w & 127)] is the
-    Phase-1 distance of query-vocabulary row w to E row u, exactly 0 for identical rows."""
+    """Distance-table layout: T[(w >> 7) * V * 128 + u * 128 + (w & 127)] is the Phase-1
+    distance of query-vocabulary row w to E row u, exactly 0 for identical rows; the
+    one-pass build (row-panel stores from the Phase-1 epilogue) equals the two-pass
+    one (segment panels, lcrw_zero_identical, lcrw_table_transpose) bitwise."""
     import torch
     from paper_1711_07227_b200 import device
     rng = np.random.default_rng(70)
@@ -877,10 +879,12 @@ def test_distance_table_layout_and_zeros():
     prep = device.PreparedEmbeddings(E)
     res2 = device.Restricted.build(device.DeviceCSR.upload(x2), prep)
     T = device.distance_table(res2, prep).cpu().numpy()
+    T2 = device.distance_table(res2, prep, via_transpose=True).cpu().numpy()
     used = np.unique(x2.column_ids)
     assert res2.v_e == len(used)
     w = np.arange(len(used))
     tab = T.reshape(-1, V, 128)[w >> 7, :, w & 127]  # (v_e, V)
+    assert np.array_equal(tab, T2.reshape(-1, V, 128)[w >> 7, :, w & 127])  # one-pass == two-pass build
     ref = O.pairwise_euclidean(E[used], E)
     ok, err = rel_close(tab, ref, RTOL, _atol(E))
     assert ok, err
