@@ -65,6 +65,10 @@ def to_device(a, dtype, non_blocking: bool = True) -> torch.Tensor:
     t = torch.from_numpy(arr)
     if t.dtype != dtype:
         t = t.to(dtype)
+    if non_blocking and not t.is_pinned() and t.numel():
+        # stage through torch's caching pinned allocator: a pageable copy would wait for
+        # every kernel already queued on the stream and leave the GPU idle meanwhile
+        t = t.pin_memory()
     return t.to(dev, non_blocking=non_blocking and t.is_pinned())
 
 
@@ -451,9 +455,9 @@ def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int) -> str:
         return env
     if v_rows * 512 > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
         return "gemm"
-    table_bytes = 2 * int(_lib.value("lcrw_table_floats", a_rows, v_rows)) * 4
-    free, _ = torch.cuda.mem_get_info()
-    return "table" if table_bytes < free // 3 else "gemm"
+    table_bytes = int(_lib.value("lcrw_table_floats", a_rows, v_rows)) * 4
+    total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory  # (mem_get_info stalls)
+    return "table" if table_bytes < total // 4 else "gemm"
 
 
 def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: bool = False) -> torch.Tensor:
