@@ -453,7 +453,7 @@ def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int) -> str:
     env = os.environ.get("LCRW_REVERSE", "")
     if env in ("gemm", "table"):
         return env
-    if v_rows * 512 > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
+    if v_rows * 4 * int(_lib.value("lcrw_table_chunk")) > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
         return "gemm"
     table_bytes = int(_lib.value("lcrw_table_floats", a_rows, v_rows)) * 4
     total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory  # (mem_get_info stalls)
@@ -472,8 +472,9 @@ def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: 
     seg = torch.arange(V + 1, dtype=torch.int64, device=dev)
     T = torch.empty(max(1, int(_lib.value("lcrw_table_floats", res2.v_e, V))), dtype=torch.float32, device=dev)
     if via_transpose:
-        Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=7)
-        zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, 7)
+        zs = int(_lib.value("lcrw_table_chunk")).bit_length() - 1
+        Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=zs)
+        zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, zs)
         _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(T), _stream())
         return T
     endmask, range_seg, n_ranges = segment_plan(seg, V, V, res2.v_e)

@@ -869,8 +869,7 @@ def test_distance_table_layout_and_zeros():
     distance of query-vocabulary row w to E row u, exactly 0 for identical rows; the
     one-pass build (row-panel stores from the Phase-1 epilogue) equals the two-pass
     one (segment panels, lcrw_zero_identical, lcrw_table_transpose) bitwise."""
-    import torch
-    from paper_1711_07227_b200 import device
+    from paper_1711_07227_b200 import _lib, device
     rng = np.random.default_rng(70)
     V, m = 700, 300
     E = rng.standard_normal((V, m)).astype(np.float32)
@@ -883,8 +882,9 @@ def test_distance_table_layout_and_zeros():
     used = np.unique(x2.column_ids)
     assert res2.v_e == len(used)
     w = np.arange(len(used))
-    tab = T.reshape(-1, V, 128)[w >> 7, :, w & 127]  # (v_e, V)
-    assert np.array_equal(tab, T2.reshape(-1, V, 128)[w >> 7, :, w & 127])  # one-pass == two-pass build
+    C = int(_lib.value("lcrw_table_chunk"))
+    tab = T.reshape(-1, V, C)[w // C, :, w % C]  # (v_e, V)
+    assert np.array_equal(tab, T2.reshape(-1, V, C)[w // C, :, w % C])  # one-pass == two-pass build
     ref = O.pairwise_euclidean(E[used], E)
     ok, err = rel_close(tab, ref, RTOL, _atol(E))
     assert ok, err
