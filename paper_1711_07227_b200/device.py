@@ -514,7 +514,8 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     table = distance_table(res2, prep) if mode == "table" else None
     if table is not None and z2_budget_bytes == REVERSE_Z2_BYTES:
         total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
-        z2_budget_bytes = max(REVERSE_Z2_BYTES, total // REVERSE_TABLE_Z2_FRACTION)
+        live = torch.cuda.memory_allocated()  # host-side counter (mem_get_info would stall the stream)
+        z2_budget_bytes = max(REVERSE_Z2_BYTES, min(total // REVERSE_TABLE_Z2_FRACTION, (total - live) // 2))
     batch = reverse_batch_docs(n1, res2.v_e, z2_budget_bytes)
     ho = x1.host_offsets
     max_words = 0 if table is not None else max(int(ho[min(n1, j0 + batch)] - ho[j0]) for j0 in range(0, n1, batch))
