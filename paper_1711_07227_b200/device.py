@@ -447,7 +447,7 @@ REVERSE_TABLE_Z2_FRACTION = 3  # table mode: Z2 batches up to 1/3 of HBM -- each
 TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 512 B) must stay L2-resident
 
 
-def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int) -> str:
+def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | None = None) -> str:
     """"table" when the reverse Phase 1 is cheaper as a distance table + per-doc gathers
     (table.cu): the vocabulary is small next to nnz(X1) (each (w, u) distance is then
     needed ~nnz/V times), a 128-word chunk of it fits in L2, and the table fits in HBM;
@@ -458,8 +458,9 @@ def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int) -> str:
     if v_rows * 4 * int(_lib.value("lcrw_table_chunk")) > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
         return "gemm"
     table_bytes = int(_lib.value("lcrw_table_floats", a_rows, v_rows)) * 4
-    total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory  # (mem_get_info stalls)
-    return "table" if table_bytes < total // 4 else "gemm"
+    if total_memory is None:  # (mem_get_info would stall the stream)
+        total_memory = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
+    return "table" if table_bytes < total_memory // 4 else "gemm"
 
 
 def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: bool = False) -> torch.Tensor:

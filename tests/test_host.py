@@ -265,3 +265,20 @@ def test_product_has_no_cpu_fallback():
             "try:\n    _lib.load()\nexcept RuntimeError as e:\n    print('raised', e)\n")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert out.stdout.startswith("raised"), out.stdout + out.stderr
+
+
+def test_reverse_mode_choice(monkeypatch):
+    """Distance table only when nnz(X1) >> V, a 128-word chunk fits L2 and the table fits
+    a quarter of HBM (include/lcrwmd.h); LCRW_REVERSE overrides."""
+    from paper_1711_07227_b200 import device
+    monkeypatch.delenv("LCRW_REVERSE", raising=False)
+    hbm = 180 << 30
+    assert device.reverse_mode(100_000, 39_300, 50_000_000, hbm) == "table"      # C2
+    assert device.reverse_mode(3_000_000, 146_000, 75_000_000, hbm) == "gemm"    # C4: chunk >> L2
+    assert device.reverse_mode(400_000, 190_000, 1_250_000, hbm) == "gemm"      # C5 shard
+    assert device.reverse_mode(20_000, 2_400, 30_000, hbm) == "gemm"            # few docs: 2V > nnz
+    assert device.reverse_mode(100_000, 39_300, 50_000_000, 40 << 30) == "gemm"  # table > HBM / 4
+    monkeypatch.setenv("LCRW_REVERSE", "gemm")
+    assert device.reverse_mode(100_000, 39_300, 50_000_000, hbm) == "gemm"
+    monkeypatch.setenv("LCRW_REVERSE", "table")
+    assert device.reverse_mode(3_000_000, 146_000, 75_000_000, hbm) == "table"
