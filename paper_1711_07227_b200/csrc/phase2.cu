@@ -172,22 +172,20 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
   }
 
   // ---- consumers ----
-  uint32_t it = 0;
+  // stage / phase tracked incrementally (no div/mod by kRpStages per tile)
+  uint32_t st = 0, ph = 0;
+  const char* acc_lane = reinterpret_cast<const char*>(acc + lane);
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int64_t p = item % n_panels;
     const int64_t g = item / n_panels;
     const int64_t q0 = g * kRpGroup;
     const int nq = (int)min((int64_t)kRpGroup, n_q - q0);
-    for (int t = 0; t < n_tiles; ++t, ++it) {
-      const uint32_t st = it % kRpStages;
-      mbar_wait(full + st, (it / kRpStages) & 1);
-      const float* tile = tiles + st * kRpTile * 32;
+    for (int t = 0; t < n_tiles; ++t) {
+      mbar_wait(full + st, ph);
+      const char* tile_lane = reinterpret_cast<const char*>(tiles + st * (kRpTile * 32) + lane);
       const uint32_t* blk = blks + st * kRpBlkWords;
       const int e0 = warp ? (int)blk[warp - 1] : 0;
       const int e1 = (int)blk[warp];
-      const uint4* ent = reinterpret_cast<const uint4*>(blk + kRpWarps);  // 2 entries per uint4
-      const char* tile_lane = reinterpret_cast<const char*>(tile + lane);
-      char* acc_lane = reinterpret_cast<char*>(acc + lane);
       // entry word: (row * 128) << 18 | query * 128 -- byte offsets of the tile row and accumulator row
       auto scatter = [&](uint4 ab, uint4 cd) {
         const uint32_t pk[kRpIlp] = {ab.x, ab.z, cd.x, cd.z};
@@ -197,28 +195,27 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
         float z[kRpIlp], v[kRpIlp];
 #pragma unroll
         for (int j = 0; j < kRpIlp; ++j) {
-          a[j] = reinterpret_cast<float*>(acc_lane + (pk[j] & 0x3FFFFu));
+          a[j] = reinterpret_cast<float*>(const_cast<char*>(acc_lane) + (pk[j] & 0x3FFFFu));
           z[j] = *reinterpret_cast<const float*>(tile_lane + (pk[j] >> 18));
           v[j] = *a[j];
         }
 #pragma unroll
         for (int j = 0; j < kRpIlp; ++j) *a[j] = fmaf(x[j], z[j], v[j]);
       };
-      const int e_mid = min(e1, kRpBlkEntries / kRpIlp * kRpIlp);
-      int i = e0;
-      {
-        const uint4* ep = ent + (e0 >> 1);
-        const uint4* const ep_end = ent + (max(e0, e_mid) >> 1);
-#pragma unroll 2
-        for (; ep < ep_end; ep += 2) scatter(ep[0], ep[1]);
-        i = max(e0, e_mid);
-      }
-      if (i < e1) {  // rare: the tile's plan block exceeds the staged part; the rest comes from global
+      constexpr int kStaged = kRpBlkEntries / kRpIlp * kRpIlp;
+      const int e_mid = e1 < kStaged ? e1 : kStaged;
+      const uint4* ep = reinterpret_cast<const uint4*>(blk + kRpWarps) + (e0 >> 1);
+      for (int i = e0; i < e_mid; i += kRpIlp, ep += 2) scatter(ep[0], ep[1]);
+      if (e1 > kStaged) {  // rare: the tile's plan block exceeds the staged part; the rest comes from global
         const uint4* gent = reinterpret_cast<const uint4*>(e_blk + __ldg(e_tile + g * n_tiles + t) + kRpWarps);
-        for (; i < e1; i += kRpIlp) scatter(__ldg(gent + (i >> 1)), __ldg(gent + (i >> 1) + 1));
+        for (int i = e0 > kStaged ? e0 : kStaged; i < e1; i += kRpIlp) scatter(__ldg(gent + (i >> 1)), __ldg(gent + (i >> 1) + 1));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st);
+      if (++st == kRpStages) {
+        st = 0;
+        ph ^= 1;
+      }
     }
     named_bar_sync(1, kRpWarps * 32);  // all scatters of this item are in acc
 
