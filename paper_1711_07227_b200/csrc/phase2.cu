@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(kWarps * 32)
 // group of <= 1024 queries); persistent CTAs (one per SM) loop over items.
 // A producer warp streams each panel's word rows through a ring of 16 KB
 // shared-memory tiles with 1-D TMA bulk copies -- each Z2 byte is read from
-// HBM once, with an L2 prefetch running kRpAhead tiles ahead of the ring --
-// and, into the same stage, the tile's block of the query plan (per-warp list
+// HBM once (an L2 bulk prefetch running ahead of the ring measured slower:
+// it competes with the ring's own bulk copies) -- and, into the same stage, the tile's block of the query plan (per-warp list
 // ends + entries).  16 consumer warps scatter the entries, x * Z2[w, 32 docs],
 // into per-query fp32 accumulators in shared memory.  Each query is owned by
 // one warp ((q - q0) % 16), so its accumulation order is fixed by the plan:
@@ -86,7 +86,6 @@ constexpr int kRpGroup = 1024;   // queries per work item
 constexpr int kRpIlp = 4;        // entries per independent group (plan invariant)
 constexpr int kRpBlkWords = 512;   // staged plan block per tile: 16 list ends + up to 248 entries (2 KB)
 constexpr int kRpBlkEntries = (kRpBlkWords - kRpWarps) / 2;
-constexpr int kRpAhead = 8;      // L2 prefetch distance (tiles)
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -118,26 +117,16 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
   if (warp == kRpWarps) {
     // ---- producer warp: lane 0 issues, the lanes fetch plan offsets 32 tiles at a time ----
     uint32_t it = 0;
-    int64_t pf_item = blockIdx.x;  // L2 prefetch cursor (item, tile), kRpAhead tiles ahead
-    int pf_t = 0;
-    auto prefetch_next = [&]() {
-      if (pf_item >= n_items) return;
-      const int64_t r0 = (int64_t)pf_t * kRpTile;
-      const uint32_t bytes = (uint32_t)min((int64_t)kRpTile, a_rows - r0) * 128u;
-      if (lane == 0) bulk_prefetch_l2(Z2 + (pf_item % n_panels) * z_panel + r0 * 32, bytes);
-      if (++pf_t == n_tiles) {
-        pf_t = 0;
-        pf_item += gridDim.x;
-      }
-    };
-    for (int i = 0; i < kRpAhead; ++i) prefetch_next();
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t p = item % n_panels;
       const int64_t g = item / n_panels;
       const float* zp = Z2 + p * z_panel;
       const int64_t* tb = e_tile + g * n_tiles;
       // D1 lines of this item, needed by the consumers' combine at the end
-      {
+#ifndef LCRW_RP_D1PF
+#define LCRW_RP_D1PF 1
+#endif
+      if (LCRW_RP_D1PF) {
         const int64_t q0 = g * kRpGroup;
         const int nqp = (int)((min((int64_t)kRpGroup, n_q - q0) + 7) / 8);
         const int64_t j0 = doc_base + p * 32;
@@ -164,7 +153,6 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
           bulk_load(tiles + st * kRpTile * 32, zp + r0 * 32, zbytes, full + st);
           bulk_load(blks + st * kRpBlkWords, e_blk + blk0, bbytes, full + st);
         }
-        prefetch_next();
         __syncwarp();
       }
     }
