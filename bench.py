@@ -13,15 +13,20 @@ docs, vocabulary 100k, m = 300, ~50 unique words/doc, top-k = 10, synthetic
 
 One step = the whole symmetric LC-RWMD top-k from HBM-resident raw inputs
 (E f32, both CSR sets): f16 operand preparation + identity classes,
-restriction of both sides, forward Phase 1 + SpMM, reverse Phase 1 + fused
-max/top-k over doc batches, final merge.  Inputs (X1 = 400 MB, D1 = 4 GB,
+restriction of both sides, forward Phase 1 + SpMM, reverse Phase 1 (at C2 the
+distance-table form: table build + per-doc gathers; --reverse gemm forces the
+GEMM form) + reverse SpMM with the max-combine over doc batches, per-query
+top-k.  Inputs (X1 = 400 MB, D1 = 4 GB,
 Z2 batches of GBs) are far larger than the 126 MB L2, so no flush is needed.
 
 `value` is device-timed (CUDA events on the launching stream, max over
 ranks); `e2e` calls the public API distances.lcrwmd_topk with pinned host
 arrays, so it includes the host->device copies of X1, X2, E and the
-device->host read of the (n2, k) result.  `roofline` is the reverse Phase-1
-kernel (the dominant one), timed live with events inside the timed region.
+device->host read of the (n2, k) result.  `roofline` is the dominant kernel,
+timed live with events inside the timed region: table_min_kernel against the
+L2 gather ceiling measured by tools/l2gather.cu (profiles/l2_gather_peak.json),
+or, on the GEMM form, the reverse phase1_kernel against the sustained tensor
+peak; `phase1_tensor` reports every Phase-1 GEMM launch against that peak.
 
 With --gpus N > 1 (torchrun, NCCL) resident docs are sharded by contiguous
 rows; Phase 1 of the forward direction is split by vocabulary slice with Z1
