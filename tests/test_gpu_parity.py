@@ -890,3 +890,28 @@ def test_distance_table_layout_and_zeros():
     assert ok, err
     same = (E[used][:, None, :] == E[None, :, :]).all(-1)
     assert np.all(tab[same] == 0.0) and same.sum() >= len(used)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V,n1,n2,hi", [(40, 70, 5, 20), (130, 33, 129, 60), (7, 40, 3, 7)])
+def test_reverse_table_mode_tiny_vocabularies(V, n1, n2, hi, monkeypatch):
+    """Distance table with vocabularies smaller than one 32-row transpose tile or one
+    128-word chunk, query vocabularies of 1..V words, docs holding most of the
+    vocabulary: bitwise equal to the GEMM form, within tolerance of the oracle."""
+    import torch
+    from paper_1711_07227_b200 import device
+    rng = np.random.default_rng(80 + V)
+    E = rng.standard_normal((V, 300)).astype(np.float32)
+    E[V - 1] = E[0]  # an identical pair
+    x1 = _rand_set(rng, n1, V, 1, min(hi, V))
+    x2 = _rand_set(rng, n2, V, 1, min(hi, V))
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    out = {}
+    for mode in ("gemm", "table"):
+        monkeypatch.setenv("LCRW_REVERSE", mode)
+        out[mode] = device.symmetric(d1, d2, prep, None)
+    assert torch.equal(out["gemm"], out["table"])
+    ref = O.lcrwmd_full(x1, x2, E, threads=8)
+    ok, err = rel_close(out["table"].cpu().numpy(), ref, RTOL, _atol(E))
+    assert ok, err
