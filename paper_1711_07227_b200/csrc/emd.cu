@@ -524,8 +524,14 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
               slot, smem_max);
     return LCRW_ERR_UNSUPPORTED;
   }
+  // one problem (warp) per block by default: a block's shared memory is one slot, so an
+  // SM holds as many problems as their slots allow (up to 32 blocks) instead of one
+  // block of kMaxWarps slots
+#ifndef LCRW_EMD_WPB
+#define LCRW_EMD_WPB 1
+#endif
   int warps = (int)(smem_max / slot);
-  if (warps > kMaxWarps) warps = kMaxWarps;
+  if (warps > LCRW_EMD_WPB) warps = LCRW_EMD_WPB;
   const size_t smem = slot * warps;
   static bool attr = false;
   if (!attr) {

@@ -22,6 +22,7 @@ torch.cuda.synchronize(); t0 = time.perf_counter()
 res, solves = emd.prefiltered_topk_wmd_batch(x1, x2, Et, k)
 torch.cuda.synchronize(); tot = (time.perf_counter() - t0) * 1e3
 prof = _lib.profile_read()
-print("total ms", round(tot, 1), "solves counted", int(solves.sum()))
+print(os.environ.get("LCRW_LIB", "in-tree"), "total ms", round(tot, 1),
+      "solves counted", int(solves.sum()), "ids", hash(tuple(int(i) for r in res for i in r.ids)))
 print("solve_batch calls (problems, wall ms):", [(n, round(t, 1)) for n, t in log])
 print("kernel profile:", {k_: (round(v["ms"], 1), v["launches"]) for k_, v in prof.items()})
