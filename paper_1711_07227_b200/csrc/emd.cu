@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 // node index -- the lexicographic (distance, index) minimum of np.argmin -- which
 // is much shorter than a shuffle tree of doubles.  Same arithmetic as above.
 // ---------------------------------------------------------------------------
-template <int SLOTS>
+template <int SLOTS, typename CT>  // CT: cost storage (float when formed in-kernel: the values are f32-rounded)
 __global__ void __launch_bounds__(kMaxWarps * 32)
     emd_kernel_reg(const double* __restrict__ supply, const int64_t* __restrict__ s_off,
                    const double* __restrict__ demand, const int64_t* __restrict__ d_off,
@@ -261,15 +261,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   const int h1 = (int)(s_off[prob + 1] - a0), h2 = (int)(d_off[prob + 1] - b0);
   const int n = h1 + h2;
   uint8_t* base = emd_smem + (size_t)wip * slot_bytes;
-  double* cost = reinterpret_cast<double*>(base);
-  double* flow = cost + (size_t)h1 * h2;
+  CT* cost = reinterpret_cast<CT*>(base);
+  double* flow = reinterpret_cast<double*>(base + ((size_t)h1 * h2 * sizeof(CT) + 7) / 8 * 8);
   double* phis = flow + (size_t)h1 * h2;              // potentials (broadcast reads)
   int* parent = reinterpret_cast<int*>(phis + n);     // written on relaxation, read by the path trace
 
   if (costs) {
     const double* cp = costs + c_off[prob];
     for (int c = lane; c < h1 * h2; c += 32) {
-      cost[c] = cp[c];
+      cost[c] = (CT)cp[c];
       flow[c] = 0.0;
     }
   } else {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       double dot = 0.0;
       for (int d = 0; d < m; ++d) dot = fma((double)ra[d], (double)rb[d], dot);
       const double sq = (phis[p] + phis[h1 + q]) - 2.0 * dot;
-      cost[c] = (double)(float)sqrt(sq > 0.0 ? sq : 0.0);
+      cost[c] = (CT)(float)sqrt(sq > 0.0 ? sq : 0.0);
       flow[c] = 0.0;
     }
     __syncwarp();
@@ -352,12 +352,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       if (lane == (u & 31)) done |= 1u << (u >> 5);
       const double pu = phis[u];
       if (u < h1) {
-        const double* crow = cost + u * h2;
+        const CT* crow = cost + u * h2;
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j) {
           const int v = lane + 32 * j;
           if (v < h1 || v >= n || ((done >> j) & 1u)) continue;
-          double rc = (crow[v - h1] + pu) - phi[j];
+          double rc = ((double)crow[v - h1] + pu) - phi[j];
           rc = rc > 0.0 ? rc : 0.0;
           const double cand = du + rc;
           if (cand < dist[j]) {
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         for (int j = 0; j < SLOTS; ++j) {
           const int pn = lane + 32 * j;
           if (pn >= h1 || ((done >> j) & 1u) || !(flow[pn * h2 + q] > kFeasTol)) continue;
-          double rc = (pu - phi[j]) - cost[pn * h2 + q];
+          double rc = (pu - phi[j]) - (double)cost[pn * h2 + q];
           rc = rc > 0.0 ? rc : 0.0;
           const double cand = du + rc;
           if (cand < dist[j]) {
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     __syncwarp();
   }
   double obj = 0.0;
-  for (int c = lane; c < h1 * h2; c += 32) obj += flow[c] * cost[c];
+  for (int c = lane; c < h1 * h2; c += 32) obj += flow[c] * (double)cost[c];
   obj = warp_sum(obj);
   if (flow_out) {
     double* fo = flow_out + c_off[prob];
@@ -498,9 +498,10 @@ extern "C" {
 
 size_t lcrw_emd_problem_bytes(int h1, int h2) { return problem_bytes(h1, h2); }
 
-static size_t problem_bytes_reg(int h1, int h2) {
+static size_t problem_bytes_reg(int h1, int h2, size_t cost_bytes) {
   const size_t n = (size_t)h1 + h2;
-  const size_t b = (size_t)h1 * h2 * 16 + n * 8 + n * 4;  // cost, flow, phi, parent
+  const size_t c = ((size_t)h1 * h2 * cost_bytes + 7) / 8 * 8;
+  const size_t b = c + (size_t)h1 * h2 * 8 + n * 8 + n * 4;  // cost, flow, phi, parent
   return (b + 15) / 16 * 16;
 }
 
@@ -517,7 +518,7 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   LCRW_REQUIRE(max_h1 >= 1 && max_h2 >= 1, "lcrw_emd_batch: every histogram needs at least one word");
   const int nmax = max_h1 + max_h2;
   const int slots = nmax <= 32 ? 1 : nmax <= 64 ? 2 : nmax <= 96 ? 3 : nmax <= 128 ? 4 : 0;
-  const size_t slot = slots ? problem_bytes_reg(max_h1, max_h2) : problem_bytes(max_h1, max_h2);
+  const size_t slot = slots ? problem_bytes_reg(max_h1, max_h2, costs ? 8 : 4) : problem_bytes(max_h1, max_h2);
   const size_t smem_max = 227 * 1024;
   if (slot > smem_max) {
     set_error("lcrw_emd_batch: a %d x %d transport problem needs %zu B of shared memory (max %zu)", max_h1, max_h2,
@@ -535,8 +536,11 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   const size_t smem = slot * warps;
   static bool attr = false;
   if (!attr) {
-    const void* fns[5] = {(const void*)emd_kernel, (const void*)emd_kernel_reg<1>, (const void*)emd_kernel_reg<2>,
-                          (const void*)emd_kernel_reg<3>, (const void*)emd_kernel_reg<4>};
+    const void* fns[9] = {(const void*)emd_kernel,
+                          (const void*)emd_kernel_reg<1, double>, (const void*)emd_kernel_reg<2, double>,
+                          (const void*)emd_kernel_reg<3, double>, (const void*)emd_kernel_reg<4, double>,
+                          (const void*)emd_kernel_reg<1, float>,  (const void*)emd_kernel_reg<2, float>,
+                          (const void*)emd_kernel_reg<3, float>,  (const void*)emd_kernel_reg<4, float>};
     for (const void* f : fns) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(emd kernels)");
@@ -550,12 +554,22 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
 #define LCRW_EMD_LAUNCH(K)                                                                                      \
   K<<<(unsigned)blocks, warps * 32, smem, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,   \
                                                n_problems, slot, objective, status, flow_out, phi_out)
-  switch (slots) {
-    case 1: LCRW_EMD_LAUNCH(emd_kernel_reg<1>); break;
-    case 2: LCRW_EMD_LAUNCH(emd_kernel_reg<2>); break;
-    case 3: LCRW_EMD_LAUNCH(emd_kernel_reg<3>); break;
-    case 4: LCRW_EMD_LAUNCH(emd_kernel_reg<4>); break;
-    default: LCRW_EMD_LAUNCH(emd_kernel); break;
+  if (costs) {
+    switch (slots) {
+      case 1: LCRW_EMD_LAUNCH((emd_kernel_reg<1, double>)); break;
+      case 2: LCRW_EMD_LAUNCH((emd_kernel_reg<2, double>)); break;
+      case 3: LCRW_EMD_LAUNCH((emd_kernel_reg<3, double>)); break;
+      case 4: LCRW_EMD_LAUNCH((emd_kernel_reg<4, double>)); break;
+      default: LCRW_EMD_LAUNCH(emd_kernel); break;
+    }
+  } else {
+    switch (slots) {
+      case 1: LCRW_EMD_LAUNCH((emd_kernel_reg<1, float>)); break;
+      case 2: LCRW_EMD_LAUNCH((emd_kernel_reg<2, float>)); break;
+      case 3: LCRW_EMD_LAUNCH((emd_kernel_reg<3, float>)); break;
+      case 4: LCRW_EMD_LAUNCH((emd_kernel_reg<4, float>)); break;
+      default: LCRW_EMD_LAUNCH(emd_kernel); break;
+    }
   }
 #undef LCRW_EMD_LAUNCH
   LCRW_CHECK_LAUNCH("emd_kernel");
