@@ -38,6 +38,7 @@ from .kernels import TopKResult
 FEASIBILITY_TOL = 1e-9
 BALANCE_TOL = 1e-6
 PRUNE_SLACK = 1e-4
+ORDER_PREFIX = 2048  # candidates ordered up front per query in prefiltered_topk_wmd_batch
 SOLVE_BATCH = 256  # speculative exact solves per GPU launch in prefiltered_topk_wmd
 
 
@@ -247,8 +248,23 @@ def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddin
     bounds = np.asarray(bounds, dtype=np.float64)
     E_t = embeddings if isinstance(embeddings, torch.Tensor) else device.to_device(
         np.asarray(embeddings, np.float32), torch.float32)
-    ids_rows = np.arange(n1)
-    orders = [np.lexsort((ids_rows, bounds[:, j])) for j in range(nq)]
+    # ascending (bound, doc id) per query.  Queries usually stop after a few hundred
+    # candidates, so only the prefix of docs whose bound is <= the (ORDER_PREFIX)-th
+    # smallest is sorted up front (all ties included, so it is an exact prefix of the
+    # full order); the full order is built only for a query that runs past it.
+    cols = np.ascontiguousarray(bounds.T)
+
+    pre_n = max(ORDER_PREFIX, k + SOLVE_BATCH)
+
+    def order_prefix(j, full=False):
+        c = cols[j]
+        if full or n1 <= pre_n:
+            return np.argsort(c, kind="stable")
+        thr = np.partition(c, pre_n)[pre_n]
+        cand = np.flatnonzero(c <= thr)
+        return cand[np.argsort(c[cand], kind="stable")]
+
+    orders = [order_prefix(j) for j in range(nq)]
     qrows = [queries.row(j) for j in range(nq)]
     drow = [None] * n1
 
@@ -272,7 +288,10 @@ def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddin
         batch, spans = [], []
         for j in open_:
             lim = tops[j][-1][0] * (1.0 + PRUNE_SLACK) + 1e-12
-            o, p0 = orders[j], int(pos[j])
+            p0 = int(pos[j])
+            if len(orders[j]) < n1 and p0 + SOLVE_BATCH >= len(orders[j]):
+                orders[j] = order_prefix(j, full=True)
+            o = orders[j]
             end = p0
             while end < n1 and end - p0 < SOLVE_BATCH and bounds[o[end], j] <= lim:
                 end += 1
