@@ -292,6 +292,19 @@ def run_ours(args, cfg):
     p1_flops = {"phase1": fwd_flops, "phase1_rev": rev_flops, "table_build": table_flops}
     p1_ms = sum(ksum[n]["ms"] for n in p1_flops if n in ksum) / args.steps
     p1_work = sum(f for n, f in p1_flops.items() if n in ksum)
+    # Phase 2 (the forward CSR SpMM and the reverse SpMM + max-combine) against the HBM peak,
+    # algorithmic bytes as SURVEY §8(d) defines them (reads of X, Z gathers / Z2 stream, D1, D)
+    p2 = {"spmm": spmm_bytes, "reverse_panels": rev_bytes}
+    p2_ms = sum(ksum[n]["ms"] for n in p2 if n in ksum) / args.steps
+    p2_bytes = sum(b for n, b in p2.items() if n in ksum)
+    hbm = pk.get("hbm_gbs")
+    phase2_hbm = {"kernels": [n for n in p2 if n in ksum], "ms_per_step": p2_ms,
+                  "achieved": p2_bytes / (p2_ms * 1e-3) / 1e9 if p2_ms else None, "peak": hbm, "unit": "GB/s",
+                  "frac": p2_bytes / (p2_ms * 1e-3) / 1e9 / hbm if p2_ms and hbm else None,
+                  "per_kernel_frac": {n: p2[n] / (ksum[n]["ms"] / args.steps * 1e-3) / 1e9 / hbm
+                                      for n in p2 if n in ksum and hbm},
+                  "note": "spmm's Z1 gathers are served partly by L2 (Z1 in L2-resident 128-query panels), so "
+                          "its algorithmic rate can exceed the HBM peak"}
     phase1_tensor = {"kernels": [n for n in p1_flops if n in ksum], "ms_per_step": p1_ms,
                      "achieved": p1_work / (p1_ms * 1e-3) / 1e12 if p1_ms else None, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": p1_work / (p1_ms * 1e-3) / 1e12 / peak_tf if p1_ms else None,
@@ -343,6 +356,7 @@ def run_ours(args, cfg):
                              (1e12 if n.startswith(("phase1", "table_build")) else 1e9))}
                     for n, v in ksum.items()},
         "phase1_tensor": phase1_tensor,
+        "phase2_hbm": phase2_hbm,
         "gpu_launches": launches,
         "clocks": clk,
     }
