@@ -145,6 +145,45 @@ def solve_batch(supplies, demands, costs=None, embeddings=None, ids1=None, ids2=
     return objs, out
 
 
+def _gather_rows(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, rows: np.ndarray):
+    """Concatenated (ids, f64 weights) of CSR rows ``rows`` plus their lengths, vectorised."""
+    lo = offsets[rows]
+    h = (offsets[rows + 1] - lo).astype(np.int64)
+    starts = np.zeros(len(rows) + 1, dtype=np.int64)
+    np.cumsum(h, out=starts[1:])
+    idx = np.repeat(lo - starts[:-1], h) + np.arange(int(starts[-1]), dtype=np.int64)
+    return cols[idx].astype(np.int32), vals[idx].astype(np.float64), h
+
+
+def solve_batch_csr(x1: HistogramSet, docs: np.ndarray, x2: HistogramSet, queries: np.ndarray, E_t) -> np.ndarray:
+    """Exact WMD of the pairs (x1 row docs[p], x2 row queries[p]) in one launch: the
+    same problems as solve_batch(..., embeddings=E_t, ids1=..., ids2=...), with the
+    per-problem arrays gathered from the two CSR sets in bulk (no per-pair Python)."""
+    n = len(docs)
+    if n == 0:
+        return np.zeros(0)
+    dev = device.require_cuda()
+    i1, w1, h1 = _gather_rows(np.asarray(x1.row_offsets), np.asarray(x1.column_ids), np.asarray(x1.values),
+                              np.asarray(docs, np.int64))
+    i2, w2, h2 = _gather_rows(np.asarray(x2.row_offsets), np.asarray(x2.column_ids), np.asarray(x2.values),
+                              np.asarray(queries, np.int64))
+    if h1.min() < 1 or h2.min() < 1:
+        raise ValueError("every histogram needs at least one word")
+    f64 = torch.float64
+    sup, dem = device.to_device(w1, f64), device.to_device(w2, f64)
+    so, do = device.to_device(_offsets(h1), torch.int64), device.to_device(_offsets(h2), torch.int64)
+    co = device.to_device(_offsets(h1 * h2), torch.int64)
+    ti1, ti2 = device.to_device(i1, torch.int32), device.to_device(i2, torch.int32)
+    v, m = int(E_t.shape[0]), int(E_t.shape[1])
+    obj = torch.empty(n, dtype=f64, device=dev)
+    status = torch.empty(n, dtype=torch.int32, device=dev)
+    _p = device._p
+    _lib.call("lcrw_emd_batch", _p(sup), _p(so), _p(dem), _p(do), None, _p(co), _p(E_t), v, m, _p(ti1), _p(ti2), n,
+              int(h1.max()), int(h2.max()), _p(obj), _p(status), None, None, device._stream())
+    _check_status(status.cpu().numpy())
+    return obj.cpu().numpy()
+
+
 def solve_emd(prob: TransportProblem) -> TransportPlan:
     """Solve the transportation problem to optimality (emd.py:120-194)."""
     prob.validate()
@@ -265,18 +304,12 @@ def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddin
         return cand[np.argsort(c[cand], kind="stable")]
 
     orders = [order_prefix(j) for j in range(nq)]
-    qrows = [queries.row(j) for j in range(nq)]
-    drow = [None] * n1
-
-    def doc(i):
-        if drow[i] is None:
-            drow[i] = x1.row(int(i))
-        return drow[i]
-
     def solve(pairs):
-        return solve_batch([doc(i).weights for j, i in pairs], [qrows[j].weights for j, i in pairs],
-                           embeddings=E_t, ids1=[doc(i).word_ids for j, i in pairs],
-                           ids2=[qrows[j].word_ids for j, i in pairs])
+        if not pairs:
+            return np.zeros(0)
+        pj = np.fromiter((j for j, _ in pairs), dtype=np.int64, count=len(pairs))
+        pi = np.fromiter((i for _, i in pairs), dtype=np.int64, count=len(pairs))
+        return solve_batch_csr(x1, pi, queries, pj, E_t)
 
     pairs = [(j, int(i)) for j in range(nq) for i in orders[j][:k]]
     dists = solve(pairs).tolist()
