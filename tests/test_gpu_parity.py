@@ -915,3 +915,24 @@ def test_reverse_table_mode_tiny_vocabularies(V, n1, n2, hi, monkeypatch):
     ref = O.lcrwmd_full(x1, x2, E, threads=8)
     ok, err = rel_close(out["table"].cpu().numpy(), ref, RTOL, _atol(E))
     assert ok, err
+
+
+@pytest.mark.gpu
+def test_solve_batch_csr_equals_solve_batch():
+    """emd.solve_batch_csr (problem arrays gathered from the CSR sets in bulk) solves the
+    same problems as solve_batch with per-pair lists: identical objectives."""
+    import torch
+    from paper_1711_07227_b200 import emd, synthetic as S
+    V = 2000
+    E = S.embeddings(V, 64, seed=90)
+    x1 = S.histograms(300, V, 20, seed=91)
+    x2 = S.histograms(7, V, 20, seed=92)
+    rng = np.random.default_rng(93)
+    docs = rng.integers(0, 300, 500)
+    qs = rng.integers(0, 7, 500)
+    Et = torch.from_numpy(E).cuda()
+    a = emd.solve_batch_csr(x1, docs, x2, qs, Et)
+    b = emd.solve_batch([x1.row(int(i)).weights for i in docs], [x2.row(int(j)).weights for j in qs],
+                        embeddings=Et, ids1=[x1.row(int(i)).word_ids for i in docs],
+                        ids2=[x2.row(int(j)).word_ids for j in qs])
+    assert np.array_equal(a, b)
