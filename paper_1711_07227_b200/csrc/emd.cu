@@ -261,9 +261,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   const int h1 = (int)(s_off[prob + 1] - a0), h2 = (int)(d_off[prob + 1] - b0);
   const int n = h1 + h2;
   uint8_t* base = emd_smem + (size_t)wip * slot_bytes;
+  // shared: costs, a positive-flow bitmask (the only flow information the relaxations
+  // need), potentials, parents; the fp64 flows themselves live in global memory
+  // (flow_out layout) and are touched only along augmenting paths and at the end
   CT* cost = reinterpret_cast<CT*>(base);
-  double* flow = reinterpret_cast<double*>(base + ((size_t)h1 * h2 * sizeof(CT) + 7) / 8 * 8);
-  double* phis = flow + (size_t)h1 * h2;              // potentials (broadcast reads)
+  uint32_t* fmask = reinterpret_cast<uint32_t*>(base + ((size_t)h1 * h2 * sizeof(CT) + 7) / 8 * 8);
+  double* phis = reinterpret_cast<double*>(fmask + (((size_t)h1 * h2 + 63) / 64) * 2);  // potentials
+  double* flow = flow_out + c_off[prob];
   int* parent = reinterpret_cast<int*>(phis + n);     // written on relaxation, read by the path trace
 
   if (costs) {
@@ -272,6 +276,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       cost[c] = (CT)cp[c];
       flow[c] = 0.0;
     }
+    for (int w = lane; w < (h1 * h2 + 31) / 32; w += 32) fmask[w] = 0u;
   } else {
     const int32_t* r1 = ids1 + a0;
     const int32_t* r2 = ids2 + b0;
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       cost[c] = (CT)(float)sqrt(sq > 0.0 ? sq : 0.0);
       flow[c] = 0.0;
     }
+    for (int w = lane; w < (h1 * h2 + 31) / 32; w += 32) fmask[w] = 0u;
     __syncwarp();
   }
   double phi[SLOTS], rem[SLOTS], dist[SLOTS];
@@ -370,7 +376,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j) {
           const int pn = lane + 32 * j;
-          if (pn >= h1 || ((done >> j) & 1u) || !(flow[pn * h2 + q] > kFeasTol)) continue;
+          const int cell = pn * h2 + q;
+          if (pn >= h1 || ((done >> j) & 1u) || !((fmask[cell >> 5] >> (cell & 31)) & 1u)) continue;
           double rc = (pu - phi[j]) - (double)cost[pn * h2 + q];
           rc = rc > 0.0 ? rc : 0.0;
           const double cand = du + rc;
@@ -445,10 +452,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       int node = sink;
       while (parent[node] != -1) {
         const int prev = parent[node];
-        if (node >= h1)
-          flow[prev * h2 + (node - h1)] += bott;
-        else
-          flow[node * h2 + (prev - h1)] -= bott;
+        const int cell = node >= h1 ? prev * h2 + (node - h1) : node * h2 + (prev - h1);
+        const double f = node >= h1 ? flow[cell] + bott : flow[cell] - bott;
+        flow[cell] = f;
+        const uint32_t bit = 1u << (cell & 31);
+        fmask[cell >> 5] = f > kFeasTol ? (fmask[cell >> 5] | bit) : (fmask[cell >> 5] & ~bit);
         node = prev;
       }
     }
@@ -464,10 +472,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   double obj = 0.0;
   for (int c = lane; c < h1 * h2; c += 32) obj += flow[c] * (double)cost[c];
   obj = warp_sum(obj);
-  if (flow_out) {
-    double* fo = flow_out + c_off[prob];
-    for (int c = lane; c < h1 * h2; c += 32) fo[c] = flow[c];
-  }
+
   if (phi_out) {
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j) {
@@ -501,7 +506,8 @@ size_t lcrw_emd_problem_bytes(int h1, int h2) { return problem_bytes(h1, h2); }
 static size_t problem_bytes_reg(int h1, int h2, size_t cost_bytes) {
   const size_t n = (size_t)h1 + h2;
   const size_t c = ((size_t)h1 * h2 * cost_bytes + 7) / 8 * 8;
-  const size_t b = c + (size_t)h1 * h2 * 8 + n * 8 + n * 4;  // cost, flow, phi, parent
+  const size_t mask = ((size_t)h1 * h2 + 63) / 64 * 8;
+  const size_t b = c + mask + n * 8 + n * 4;  // cost, positive-flow bits, phi, parent (flows: global)
   return (b + 15) / 16 * 16;
 }
 
@@ -549,7 +555,17 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   }
   const int64_t blocks = (n_problems + warps - 1) / warps;
   LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_emd_batch: too many problems");
+  LCRW_REQUIRE(!slots || c_off, "lcrw_emd_batch: c_off (per-problem h1*h2 offsets) is required");
   cudaStream_t st = as_stream(stream);
+  // the register-state kernels keep flows in global memory (flow_out layout): without a
+  // caller buffer, a stream-ordered scratch one sized for the largest problem each
+  double* scratch = nullptr;
+  if (slots && !flow_out) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                    (size_t)n_problems * max_h1 * max_h2 * sizeof(double), st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(emd flow scratch)");
+    flow_out = scratch;
+  }
   ProfScope prof(st, "emd");
 #define LCRW_EMD_LAUNCH(K)                                                                                      \
   K<<<(unsigned)blocks, warps * 32, smem, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,   \
@@ -573,6 +589,10 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   }
 #undef LCRW_EMD_LAUNCH
   LCRW_CHECK_LAUNCH("emd_kernel");
+  if (scratch) {
+    cudaError_t e = cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFreeAsync(emd flow scratch)");
+  }
   return LCRW_OK;
 }
 
