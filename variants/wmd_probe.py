@@ -9,14 +9,14 @@ x1 = S.histograms(n1, V, h, seed=1)
 x2 = S.histograms(nq, V, h, seed=2)
 Et = torch.from_numpy(E).cuda()
 emd.prefiltered_topk_wmd_batch(x1, x2, Et, k)
-orig = emd.solve_batch
+orig = emd.solve_batch_csr
 log = []
 def wrapped(*a, **kw):
     torch.cuda.synchronize(); t = time.perf_counter()
     r = orig(*a, **kw)
-    torch.cuda.synchronize(); log.append((len(a[0]), (time.perf_counter() - t) * 1e3))
+    torch.cuda.synchronize(); log.append((len(a[1]), (time.perf_counter() - t) * 1e3))
     return r
-emd.solve_batch = wrapped
+emd.solve_batch_csr = wrapped
 _lib.profile_reset(True)
 torch.cuda.synchronize(); t0 = time.perf_counter()
 res, solves = emd.prefiltered_topk_wmd_batch(x1, x2, Et, k)
