@@ -336,6 +336,18 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       if (i < n) parent[i] = -1;
       if (i >= n) done |= 1u << j;
     }
+    // sinks with remaining demand (warp-uniform bits): Dijkstra pops nodes in (distance,
+    // index) order, so the first such sink popped is the one the full search would pick,
+    // and every node not popped by then has a distance >= it -- the potential update
+    // min(dist, sv) and the path are unchanged, so the search stops there
+    uint32_t dmask[SLOTS];
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int i = lane + 32 * j;
+      dmask[j] = __ballot_sync(0xffffffffu, i >= h1 && i < n && rem[j] > kFeasTol);
+    }
+    int t_hit = -1;
+    double sv_hit = HUGE_VAL;
     __syncwarp();
     for (int it = 0; it < n; ++it) {
       double bv = HUGE_VAL;
@@ -355,6 +367,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       const int u = (int)__reduce_min_sync(0xffffffffu, ix);
       const double du = __hiloint2double((int)mhi, (int)mlo);
       if (u >= n || !(du < HUGE_VAL)) break;
+      {
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < SLOTS; ++j) w = (u >> 5) == j ? dmask[j] : w;
+        if ((w >> (u & 31)) & 1u) {
+          t_hit = u - h1;
+          sv_hit = du;
+          break;
+        }
+      }
       if (lane == (u & 31)) done |= 1u << (u >> 5);
       const double pu = phis[u];
       if (u < h1) {
@@ -391,6 +413,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     // nearest sink with remaining demand
     double sv = HUGE_VAL;
     int t = 0x7FFFFFFF;
+    if (t_hit >= 0) {
+      sv = sv_hit;
+      t = t_hit;
+    } else {
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j) {
       const int i = lane + 32 * j;
@@ -407,6 +433,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       const uint32_t ix = (hi == mhi && lo == mlo) ? (uint32_t)t : 0xFFFFFFFFu;
       t = (int)__reduce_min_sync(0xffffffffu, ix);
       sv = __hiloint2double((int)mhi, (int)mlo);
+    }
     }
     if (!(sv < HUGE_VAL)) {
       st = 1;
