@@ -126,7 +126,9 @@ def solve_batch(supplies, demands, costs=None, embeddings=None, ids1=None, ids2=
         i2 = device.to_device(np.concatenate([np.asarray(b, np.int32) for b in ids2]), torch.int32)
     obj = torch.empty(n, dtype=f64, device=dev)
     status = torch.empty(n, dtype=torch.int32, device=dev)
-    flow = torch.empty(int(c_off[-1]), dtype=f64, device=dev) if plans else None
+    # the flows are the kernels' working storage (global memory); a torch (caching
+    # allocator) buffer avoids a driver allocation per launch
+    flow = torch.empty(int(c_off[-1]), dtype=f64, device=dev)
     phi = torch.empty(int(s_off[-1] + d_off[-1]), dtype=f64, device=dev) if plans else None
     _p = device._p
     _lib.call("lcrw_emd_batch", _p(sup), _p(so), _p(dem), _p(do), _p(cost_t), _p(co), _p(E_t), v, m, _p(i1),
@@ -177,9 +179,10 @@ def solve_batch_csr(x1: HistogramSet, docs: np.ndarray, x2: HistogramSet, querie
     v, m = int(E_t.shape[0]), int(E_t.shape[1])
     obj = torch.empty(n, dtype=f64, device=dev)
     status = torch.empty(n, dtype=torch.int32, device=dev)
+    flow = torch.empty(int((h1 * h2).sum()), dtype=f64, device=dev)  # kernel working storage (cached)
     _p = device._p
     _lib.call("lcrw_emd_batch", _p(sup), _p(so), _p(dem), _p(do), None, _p(co), _p(E_t), v, m, _p(ti1), _p(ti2), n,
-              int(h1.max()), int(h2.max()), _p(obj), _p(status), None, None, device._stream())
+              int(h1.max()), int(h2.max()), _p(obj), _p(status), _p(flow), None, device._stream())
     _check_status(status.cpu().numpy())
     return obj.cpu().numpy()
 
