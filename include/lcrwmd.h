@@ -259,7 +259,10 @@ int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, flo
  * both sides open, 2 no convergence.  Augmentation stops once either side is
  * exhausted (the reference raises when float32 totals differ by > 1e-9).
  * Optional flow_out (c_off layout) and phi_out (sources at s_off, sinks at
- * s_off[n_problems] + d_off).  max_h1 x max_h2 must fit
+ * s_off[n_problems] + d_off).  c_off is required.  Problems with h1 + h2 <= 128
+ * use flow_out as their working storage; pass a buffer of c_off[n_problems]
+ * doubles -- with NULL a stream-ordered scratch is allocated per call, which
+ * costs a driver allocation each time.  max_h1 x max_h2 must fit
  * lcrw_emd_problem_bytes() <= 227 KB of shared memory. */
 size_t lcrw_emd_problem_bytes(int h1, int h2);
 int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* demand, const int64_t* d_off,
