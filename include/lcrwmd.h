@@ -245,6 +245,34 @@ int lcrw_topk_sort_workspace(int64_t n, size_t* bytes);
 /* full (distance, id) sort of one segment of n candidates; writes the first k */
 int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, float* out_d, int64_t* out_i,
                    void* ws, size_t ws_bytes, void* stream);
+/* topk_select for distances of any numeric dtype (kernels.py:210-223 keeps the caller's
+ * dtype: np.lexsort((ids, distances))): element type codes below; the k smallest under
+ * ascending (distance, id) with -0 == +0 and NaN after +inf (numpy's order), distances
+ * copied to out_d in their own type.  Workspace lcrw_topk_sort_any_workspace(n). */
+typedef enum {
+  LCRW_F32 = 0, LCRW_F64 = 1, LCRW_F16 = 2,
+  LCRW_I8 = 3, LCRW_I16 = 4, LCRW_I32 = 5, LCRW_I64 = 6,
+  LCRW_U8 = 7, LCRW_U16 = 8, LCRW_U32 = 9, LCRW_U64 = 10
+} lcrw_dtype;
+int lcrw_topk_sort_any_workspace(int64_t n, size_t* bytes);
+int lcrw_topk_sort_any(const void* d, int dtype, const int64_t* ids, int64_t n, int64_t k, void* out_d,
+                       int64_t* out_i, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- reference primitives of the drop-in surface (csrc/prims.cu) ----------
+ * Bitwise reproductions of the float64 reference arithmetic (numpy pairwise
+ * summation over the contiguous axis, no FMA contraction):
+ *   lcrw_squared_norms   kernels.py:66-69   out[r] = sum_i a[r,i]^2 (f64); a f32 or f64 rows x m
+ *   lcrw_euclidean_f64   kernels.py:72-110  out[i*ld+j] = sqrt(max(0, (sq_a[i]+sq_b[j]) - 2 a_i.b_j)),
+ *                                            stored as f32 (out_dtype LCRW_F32) or f64
+ *   lcrw_segmented_min   kernels.py:137-167 minima over the middle axis of an (outer, n, inner)
+ *                                            array: segments [seg[s], seg[s+1]) (seg_offsets NULL:
+ *                                            one segment = the whole axis: row_min / col_min);
+ *                                            np.minimum semantics (NaN propagates), left to right */
+int lcrw_squared_norms(const void* a, int dtype, int64_t rows, int64_t m, double* out, void* stream);
+int lcrw_euclidean_f64(const double* a, const double* sq_a, int64_t r, const double* b, const double* sq_b, int64_t c,
+                       int64_t m, void* out, int out_dtype, int64_t ld, void* stream);
+int lcrw_segmented_min(const void* v, int dtype, int64_t outer, int64_t n, int64_t inner, const int64_t* seg_offsets,
+                       int64_t n_seg, void* out, void* stream);
 
 /* ---- Exact mover's distance (emd.py:120-211) -------------------------------
  * Batched balanced transport problems, one warp each: successive shortest
@@ -256,14 +284,17 @@ int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, flo
  * (aligned with supply) and ids2 (aligned with demand) exactly as
  * pairwise_euclidean does (fp64, rounded once to f32; identical rows -> 0).
  * objective[p] = sum(flow * cost); status[p] = 0 ok, 1 no augmenting path with
- * both sides open, 2 no convergence.  Augmentation stops once either side is
- * exhausted (the reference raises when float32 totals differ by > 1e-9).
+ * both sides open, 2 no convergence, 3 stopped with supply left because the demand
+ * side was exhausted (the reference raises "no augmenting path" there: float32
+ * totals differing by > 1e-9; the objective is that of the transported mass).
+ * Augmentation stops once either side is exhausted.
  * Optional flow_out (c_off layout) and phi_out (sources at s_off, sinks at
  * s_off[n_problems] + d_off).  c_off is required.  Problems with h1 + h2 <= 128
  * use flow_out as their working storage; pass a buffer of c_off[n_problems]
  * doubles -- with NULL a stream-ordered scratch is allocated per call, which
- * costs a driver allocation each time.  max_h1 x max_h2 must fit
- * lcrw_emd_problem_bytes() <= 227 KB of shared memory. */
+ * costs a driver allocation each time.  A batch whose largest problem does not fit
+ * lcrw_emd_problem_bytes() <= 227 KB of shared memory is solved with the per-problem
+ * state in global memory (stream-ordered scratch, launches of <= 4096 problems). */
 size_t lcrw_emd_problem_bytes(int h1, int h2);
 int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* demand, const int64_t* d_off,
                    const double* costs, const int64_t* c_off, const float* E, int64_t v, int m, const int32_t* ids1,

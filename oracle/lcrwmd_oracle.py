@@ -312,12 +312,20 @@ EMD_PRUNE_SLACK = 1e-6   # emd.py:39
 
 
 def solve_emd_objective(supply, demand, cost) -> float:
+    """The objective of ``solve_emd_plan``."""
+    return solve_emd_plan(supply, demand, cost)[0]
+
+
+def solve_emd_plan(supply, demand, cost):
     """emd.py:120-194: successive shortest augmenting paths with node potentials
     (multi-source Dijkstra over reduced costs clamped at 0, lowest-index ties);
     returns the objective.  Restated with the reference's order of operations
     and tolerances.  Where the reference raises "no augmenting path" because the
     float32-normalised totals differ by more than 1e-9 (emd.py:153-162), this
-    stops once either side is exhausted -- the behaviour the CUDA solver has."""
+    stops once either side is exhausted -- the behaviour the CUDA solver has.
+    Returns (objective, flow (h1, h2), potentials phi (h1 + h2)) -- the reference's
+    plan is ``flow > 1e-9`` with dual_source = -phi[:h1], dual_sink = phi[h1:]
+    (emd.py:186-194)."""
     s = np.asarray(supply, dtype=np.float64).copy()
     d = np.asarray(demand, dtype=np.float64).copy()
     c = np.ascontiguousarray(cost, dtype=np.float64)
@@ -371,7 +379,7 @@ def solve_emd_objective(supply, demand, cost) -> float:
             node = prev
         s[root] -= bott
         d[t] -= bott
-    return float(np.sum(flow * c))
+    return float(np.sum(flow * c)), flow, phi
 
 
 def wmd(x1_ids, x1_w, x2_ids, x2_w, embeddings) -> float:
@@ -418,6 +426,76 @@ def prefiltered_topk_wmd(x1, q_ids, q_w, embeddings, k):
 # ---------------------------------------------------------------------------
 # Top-k (kernels.py:210-232)
 # ---------------------------------------------------------------------------
+
+# ---------------------------------------------------------------------------
+# The remaining movers.kernels primitives, restated in the form csrc/prims.cu
+# computes them (pinned bitwise to tests/golden/prims.npz)
+# ---------------------------------------------------------------------------
+def pairwise_sum(v) -> float:
+    """numpy's pairwise summation of a contiguous float64 run (what np.sum(..., axis=-1)
+    does, kernels.py:69,105): < 8 terms sequential from 0.0; <= 128 terms eight
+    strided partial sums ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the tail; above,
+    split at n2 = n/2 - (n/2) % 8 and add the halves."""
+    v = [float(x) for x in v]
+    n = len(v)
+    if n < 8:
+        r = 0.0
+        for x in v:
+            r += x
+        return r
+    if n <= 128:
+        r = v[:8]
+        i = 8
+        while i < n - n % 8:
+            for j in range(8):
+                r[j] += v[i + j]
+            i += 8
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        while i < n:
+            res += v[i]
+            i += 1
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return pairwise_sum(v[:n2]) + pairwise_sum(v[n2:])
+
+
+def squared_norms_pairwise(a) -> np.ndarray:
+    """kernels.py:66-69 as pairwise sums of float64 squares."""
+    a64 = np.asarray(a, dtype=np.float64)
+    return np.array([pairwise_sum(r * r) for r in a64], dtype=np.float64)
+
+
+def euclidean_pairwise(a64, sq_a, b64, sq_b) -> np.ndarray:
+    """kernels.py:105-109 per entry: sqrt(max(0, (sq_a + sq_b) - 2 * pairwise_sum(a*b))), f64."""
+    a64, b64 = np.asarray(a64, np.float64), np.asarray(b64, np.float64)
+    out = np.empty((len(a64), len(b64)), dtype=np.float64)
+    for i in range(len(a64)):
+        for j in range(len(b64)):
+            sq = (sq_a[i] + sq_b[j]) - 2.0 * pairwise_sum(a64[i] * b64[j])
+            out[i, j] = np.sqrt(max(sq, 0.0)) if sq == sq else sq
+    return out
+
+
+def _np_min_seq(vals):
+    acc = vals[0]
+    for x in vals[1:]:
+        acc = acc if (acc < x or acc != acc) else x
+    return acc
+
+
+def segmented_min_seq(values, seg_offsets, axis: int = 0) -> np.ndarray:
+    """kernels.py:153-167 (np.minimum.reduceat) restated as left-to-right np.minimum
+    per segment: acc = acc if (acc < x or acc is NaN) else x."""
+    v = np.moveaxis(np.asarray(values), axis, 0)
+    out = np.empty((len(seg_offsets) - 1,) + v.shape[1:], dtype=v.dtype)
+    for s in range(len(seg_offsets) - 1):
+        seg = v[seg_offsets[s]:seg_offsets[s + 1]]
+        flat = seg.reshape(len(seg), -1)
+        out[s] = np.array([_np_min_seq(list(flat[:, c])) for c in range(flat.shape[1])],
+                          dtype=v.dtype).reshape(v.shape[1:])
+    return np.moveaxis(out, 0, axis)
+
 
 def topk_select(distances: np.ndarray, ids: np.ndarray, k: int):
     """kernels.py:210-223: k smallest under ascending (distance, id)."""

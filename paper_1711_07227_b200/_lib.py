@@ -72,6 +72,11 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_topk_segments": (I32, [P, P, I64, I64, I32, P, P, P]),
     "lcrw_topk_sort_workspace": (I32, [I64, P]),
     "lcrw_topk_sort": (I32, [P, P, I64, I64, P, P, P, SZ, P]),
+    "lcrw_topk_sort_any_workspace": (I32, [I64, P]),
+    "lcrw_squared_norms": (I32, [P, I32, I64, I64, P, P]),
+    "lcrw_euclidean_f64": (I32, [P, P, I64, P, P, I64, I64, P, I32, I64, P]),
+    "lcrw_segmented_min": (I32, [P, I32, I64, I64, I64, P, I64, P, P]),
+    "lcrw_topk_sort_any": (I32, [P, I32, P, I64, I64, P, P, P, SZ, P]),
 }
 
 # functions returning a value rather than a status
@@ -89,7 +94,8 @@ KERNELS_PER_CALL = {
     "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
     "lcrw_max_transposed_into": 1, "lcrw_table_transpose": 1, "lcrw_table_min": 1,
-    "lcrw_distance_table": 2,
+    "lcrw_distance_table": 2, "lcrw_topk_sort_any": 7, "lcrw_squared_norms": 1, "lcrw_euclidean_f64": 1,
+    "lcrw_segmented_min": 1,
 }
 # lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels)
 # in GEMM mode, 2 (table_min, reverse_panels) with a distance table; bench.py adds those from the

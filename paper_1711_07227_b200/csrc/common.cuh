@@ -298,8 +298,12 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // ordering helpers
 // ---------------------------------------------------------------------------
 // Monotone map float -> uint32 (total order for non-NaN values).
+// order-preserving unsigned key of a float under numpy's sort order: -0 == +0, and every
+// NaN after +inf (one key for all NaNs, so NaNs tie and fall back to the id)
 __device__ __forceinline__ uint32_t float_key(float d) {
   uint32_t u = __float_as_uint(d);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0xFFFFFFFFu;
+  if (u == 0x80000000u) u = 0u;
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 __device__ __forceinline__ float key_float(uint32_t k) {

@@ -54,16 +54,20 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                const int64_t* __restrict__ d_off, const double* __restrict__ costs, const int64_t* __restrict__ c_off,
                const float* __restrict__ E, int m, const int32_t* __restrict__ ids1, const int32_t* __restrict__ ids2,
                int64_t n_problems, size_t slot_bytes, double* __restrict__ objective, int32_t* __restrict__ status,
-               double* __restrict__ flow_out, double* __restrict__ phi_out) {
+               double* __restrict__ flow_out, double* __restrict__ phi_out, uint8_t* __restrict__ gstate,
+               int64_t prob_base) {
   extern __shared__ __align__(16) uint8_t emd_smem[];
   const int lane = threadIdx.x & 31;
   const int wip = threadIdx.x >> 5;
-  const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + wip;
+  const int64_t local = (int64_t)blockIdx.x * (blockDim.x >> 5) + wip;
+  const int64_t prob = prob_base + local;
   if (prob >= n_problems) return;
   const int64_t a0 = s_off[prob], b0 = d_off[prob];
   const int h1 = (int)(s_off[prob + 1] - a0), h2 = (int)(d_off[prob + 1] - b0);
   const int n = h1 + h2;
-  uint8_t* base = emd_smem + (size_t)wip * slot_bytes;
+  // state in shared memory, or -- for a problem too large for it -- in a global-memory
+  // slot of the launch (same layout, same arithmetic; L1/L2 serve the scans)
+  uint8_t* base = gstate ? gstate + (size_t)local * slot_bytes : emd_smem + (size_t)wip * slot_bytes;
   double* cost = reinterpret_cast<double*>(base);
   double* flow = cost + (size_t)h1 * h2;
   double* dist = flow + (size_t)h1 * h2;
@@ -115,7 +119,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     for (int i = lane; i < n; i += 32) (i < h1 ? rs : rd) += rem[i];
     rs = warp_sum(rs);
     rd = warp_sum(rd);
-    if (!(rs > kFeasTol) || !(rd > kFeasTol)) break;
+    if (!(rs > kFeasTol) || !(rd > kFeasTol)) {
+      if (rs > kFeasTol) st = 3;  // demand exhausted with supply left: the reference raises here
+      break;
+    }
     if (++rounds > max_rounds) {
       st = 2;
       break;
@@ -323,7 +330,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     }
     rs = warp_sum(rs);
     rd = warp_sum(rd);
-    if (!(rs > kFeasTol) || !(rd > kFeasTol)) break;
+    if (!(rs > kFeasTol) || !(rd > kFeasTol)) {
+      if (rs > kFeasTol) st = 3;  // demand exhausted with supply left: the reference raises here
+      break;
+    }
     if (++rounds > max_rounds) {
       st = 2;
       break;
@@ -337,9 +347,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       if (i >= n) done |= 1u << j;
     }
     // sinks with remaining demand (warp-uniform bits): Dijkstra pops nodes in (distance,
-    // index) order, so the first such sink popped is the one the full search would pick,
-    // and every node not popped by then has a distance >= it -- the potential update
-    // min(dist, sv) and the path are unchanged, so the search stops there
+    // index) order.  Once a sink with demand is popped at distance sv, every node not yet
+    // popped has a final distance >= sv, so min(dist, sv) (the potential update) is already
+    // final.  The reference's argmin picks the LOWEST-index sink at distance sv, which may
+    // only reach sv through zero-reduced-cost arcs of nodes popped later at the same
+    // distance, so the search goes on while the popped distance equals sv (bitwise) and
+    // stops at the first larger one: same sink, same parents, same potentials as the
+    // full search (emd.py:104-129, 166-170)
     uint32_t dmask[SLOTS];
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j) {
@@ -367,14 +381,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       const int u = (int)__reduce_min_sync(0xffffffffu, ix);
       const double du = __hiloint2double((int)mhi, (int)mlo);
       if (u >= n || !(du < HUGE_VAL)) break;
+      if (t_hit >= 0 && du != sv_hit) break;  // every node at the hit distance is popped
       {
         uint32_t w = 0;
 #pragma unroll
         for (int j = 0; j < SLOTS; ++j) w = (u >> 5) == j ? dmask[j] : w;
-        if ((w >> (u & 31)) & 1u) {
+        if (((w >> (u & 31)) & 1u) && (t_hit < 0 || u - h1 < t_hit)) {
           t_hit = u - h1;
           sv_hit = du;
-          break;
         }
       }
       if (lane == (u & 31)) done |= 1u << (u >> 5);
@@ -553,10 +567,25 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   const int slots = nmax <= 32 ? 1 : nmax <= 64 ? 2 : nmax <= 96 ? 3 : nmax <= 128 ? 4 : 0;
   const size_t slot = slots ? problem_bytes_reg(max_h1, max_h2, costs ? 8 : 4) : problem_bytes(max_h1, max_h2);
   const size_t smem_max = 227 * 1024;
+  cudaStream_t st = as_stream(stream);
   if (slot > smem_max) {
-    set_error("lcrw_emd_batch: a %d x %d transport problem needs %zu B of shared memory (max %zu)", max_h1, max_h2,
-              slot, smem_max);
-    return LCRW_ERR_UNSUPPORTED;
+    // too large for shared memory: the general kernel with its per-problem state in global
+    // memory, one warp per block, in launches of at most kGlobalProblems problems
+    constexpr int64_t kGlobalProblems = 4096;
+    const int64_t per = n_problems < kGlobalProblems ? n_problems : kGlobalProblems;
+    uint8_t* gstate = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gstate), (size_t)per * slot, st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(emd global state)");
+    ProfScope prof(st, "emd_global");
+    for (int64_t p0 = 0; p0 < n_problems; p0 += per) {
+      const int64_t cnt = n_problems - p0 < per ? n_problems - p0 : per;
+      emd_kernel<<<(unsigned)cnt, 32, 0, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,
+                                               n_problems, slot, objective, status, flow_out, phi_out, gstate, p0);
+      LCRW_CHECK_LAUNCH("emd_kernel (global state)");
+    }
+    e = cudaFreeAsync(gstate, st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFreeAsync(emd global state)");
+    return LCRW_OK;
   }
   // one problem (warp) per block by default: a block's shared memory is one slot, so an
   // SM holds as many problems as their slots allow (up to 32 blocks) instead of one
@@ -583,7 +612,6 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
   const int64_t blocks = (n_problems + warps - 1) / warps;
   LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_emd_batch: too many problems");
   LCRW_REQUIRE(!slots || c_off, "lcrw_emd_batch: c_off (per-problem h1*h2 offsets) is required");
-  cudaStream_t st = as_stream(stream);
   // the register-state kernels keep flows in global memory (flow_out layout): without a
   // caller buffer, a stream-ordered scratch one sized for the largest problem each
   double* scratch = nullptr;
@@ -594,16 +622,16 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
     flow_out = scratch;
   }
   ProfScope prof(st, "emd");
-#define LCRW_EMD_LAUNCH(K)                                                                                      \
+#define LCRW_EMD_LAUNCH(K, ...)                                                                                 \
   K<<<(unsigned)blocks, warps * 32, smem, st>>>(supply, s_off, demand, d_off, costs, c_off, E, m, ids1, ids2,   \
-                                               n_problems, slot, objective, status, flow_out, phi_out)
+                                               n_problems, slot, objective, status, flow_out, phi_out __VA_ARGS__)
   if (costs) {
     switch (slots) {
       case 1: LCRW_EMD_LAUNCH((emd_kernel_reg<1, double>)); break;
       case 2: LCRW_EMD_LAUNCH((emd_kernel_reg<2, double>)); break;
       case 3: LCRW_EMD_LAUNCH((emd_kernel_reg<3, double>)); break;
       case 4: LCRW_EMD_LAUNCH((emd_kernel_reg<4, double>)); break;
-      default: LCRW_EMD_LAUNCH(emd_kernel); break;
+      default: LCRW_EMD_LAUNCH(emd_kernel, , nullptr, 0); break;
     }
   } else {
     switch (slots) {
@@ -611,7 +639,7 @@ int lcrw_emd_batch(const double* supply, const int64_t* s_off, const double* dem
       case 2: LCRW_EMD_LAUNCH((emd_kernel_reg<2, float>)); break;
       case 3: LCRW_EMD_LAUNCH((emd_kernel_reg<3, float>)); break;
       case 4: LCRW_EMD_LAUNCH((emd_kernel_reg<4, float>)); break;
-      default: LCRW_EMD_LAUNCH(emd_kernel); break;
+      default: LCRW_EMD_LAUNCH(emd_kernel, , nullptr, 0); break;
     }
   }
 #undef LCRW_EMD_LAUNCH

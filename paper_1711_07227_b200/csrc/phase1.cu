@@ -63,7 +63,9 @@ constexpr int kMmaWarp = kEpiWarps + 1;       // 9
 constexpr int kAllocWarp = kEpiWarps + 2;     // 10
 constexpr int kThreads = 32 * (kEpiWarps + 3);
 constexpr uint32_t kIdesc = umma_idesc_f16(2 * BM, BN);
-constexpr int kMaxKb = 8;                     // operand K <= 512 (m <= 509 with the 3 norm columns)
+constexpr int kMaxKb = 8;                     // resident A: operand K <= 512 (m <= 509 with the 3 norm columns)
+constexpr int kMaxKbStream = 64;              // streamed A (K > 512): operand K <= 4096
+constexpr int kStreamStages = 6;              // streamed A: ring stages of (A + B) K blocks, 32 KB each
 
 struct Params {
   const float* a_norms;
@@ -85,6 +87,7 @@ struct Params {
   int n_kb;
   int n_kmma;
   int stages;
+  int a_stream;      // 1: A K blocks streamed through the ring with B's (operand K > 512)
 };
 
 // shared-memory carve-up; identical offsets in both CTAs of a pair
@@ -94,7 +97,9 @@ struct Smem {
   uint32_t* tmem_slot;
 };
 
-size_t smem_bytes(int n_kb, int stages) {
+size_t smem_bytes(int n_kb, int stages, bool a_stream = false) {
+  if (a_stream)  // no resident A; each stage holds an A K block followed by a B K block
+    return 1024 + (size_t)stages * (A_KB_BYTES + B_STAGE_BYTES) + (2 + 2 * stages + 4) * 8 + 16;
   return 1024 + (size_t)n_kb * A_KB_BYTES + (size_t)stages * B_STAGE_BYTES + (2 + 2 * stages + 4) * 8 + 16;
 }
 
@@ -211,9 +216,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // keep every pointer derived from smem_raw so the compiler emits shared-space accesses
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Smem sm;
+  // resident A: [A K blocks][B stages]; streamed A: [stage: A K block, B K block] x stages
+  const int a_res_kb = p.a_stream ? 0 : p.n_kb;
+  const uint32_t stage_bytes = p.a_stream ? A_KB_BYTES + B_STAGE_BYTES : B_STAGE_BYTES;
+  const uint32_t b_in_stage = p.a_stream ? A_KB_BYTES : 0;
   sm.A = smem_u32(base);
-  sm.B = sm.A + p.n_kb * A_KB_BYTES;
-  uint8_t* tail = base + p.n_kb * A_KB_BYTES + p.stages * B_STAGE_BYTES;
+  sm.B = sm.A + a_res_kb * A_KB_BYTES;
+  uint8_t* tail = base + a_res_kb * A_KB_BYTES + p.stages * stage_bytes;
   sm.bars = reinterpret_cast<uint64_t*>(tail);
   sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.bars + 2 + 2 * p.stages + 4);
 
@@ -268,13 +277,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t b_full_l = mapa_shared(smem_u32(b_full), 0);
       uint32_t stage = 0, phase = 0, a_phase = 0;
       int64_t b_loads = 0;
+      const uint32_t tx_bytes = 2 * B_STAGE_BYTES + (p.a_stream ? 2 * A_KB_BYTES : 0);  // both CTAs' halves
       for (int64_t u = pair; u < n_units; u += n_pairs) {
         Unit U;
         if (!unit_plan(p, u, U)) continue;
         const int mp = (int)(u % p.n_mpairs);
-        mbar_wait(a_empty, a_phase ^ 1);
+        const int a_row = mp * 2 * BM + (int)rank * BM;
+        if (!p.a_stream) mbar_wait(a_empty, a_phase ^ 1);
         a_phase ^= 1;
-        if (lane == 0) {
+        if (lane == 0 && !p.a_stream) {
           if (leader) mbar_expect_tx(a_full, 2 * p.n_kb * A_KB_BYTES);
           for (int kb = 0; kb < p.n_kb; ++kb)
             tma_load_2d_2sm(&tmA, a_full_l, smem_raw + (sm.A - smem_u32(smem_raw)) + kb * A_KB_BYTES, kb * BK,
@@ -297,10 +308,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait(b_empty + stage, phase ^ 1);
+            uint8_t* const st_ptr = smem_raw + (sm.B - smem_u32(smem_raw)) + stage * stage_bytes;
+            // streamed A: this K block of the unit's A rows rides with B's on the stage's
+            // barrier (one arrive.expect_tx for both: the barrier expects one arrival)
+            if (p.a_stream && lane == 0) tma_load_2d_2sm(&tmA, b_full_l + stage * 8, st_ptr, kb * BK, a_row, pol_a);
             if (p.b_ids) {
-              if (leader && lane == 0) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
-              tma_gather4_2sm(&tmB, b_full_l + stage * 8,
-                              smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES + lane * 4 * BK * 2,
+              if (leader && lane == 0) mbar_expect_tx(b_full + stage, tx_bytes);
+              tma_gather4_2sm(&tmB, b_full_l + stage * 8, st_ptr + b_in_stage + lane * 4 * BK * 2,
                               kb * BK, g0, g1, g2, g3, pol_b);
             } else if (lane == 0) {
 #if LCRW_EPI_MODE == 3
@@ -309,9 +323,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               } else
 #endif
               {
-                if (leader) mbar_expect_tx(b_full + stage, 2 * B_STAGE_BYTES);
-                tma_load_2d_2sm(&tmB, b_full_l + stage * 8,
-                                smem_raw + (sm.B - smem_u32(smem_raw)) + stage * B_STAGE_BYTES, kb * BK,
+                if (leader) mbar_expect_tx(b_full + stage, tx_bytes);
+                tma_load_2d_2sm(&tmB, b_full_l + stage * 8, st_ptr + b_in_stage, kb * BK,
                                 (int32_t)(c0 + rank * BN_HALF), pol_b);
               }
             }
@@ -336,7 +349,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int64_t u = pair; u < n_units; u += n_pairs) {
         Unit U;
         if (!unit_plan(p, u, U)) continue;
-        mbar_wait(a_full, a_phase);
+        if (!p.a_stream) mbar_wait(a_full, a_phase);
         a_phase ^= 1;
         tc_fence_after();
         const int n_tiles = U.n0 + U.n1;
@@ -368,8 +381,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
             tc_fence_after();
             // descriptor start-address field counts 16-byte units: +2 per 32-byte K step
-            const uint64_t ad = a_desc0 + (uint64_t)(kb * (A_KB_BYTES >> 4));
-            const uint64_t bd = b_desc0 + (uint64_t)(stage * (B_STAGE_BYTES >> 4));
+            const uint64_t ad = p.a_stream ? b_desc0 + (uint64_t)(stage * (stage_bytes >> 4))
+                                           : a_desc0 + (uint64_t)(kb * (A_KB_BYTES >> 4));
+            const uint64_t bd = b_desc0 + (uint64_t)((stage * stage_bytes + b_in_stage) >> 4);
             const int nk = kb == p.n_kb - 1 ? last_nk : 4;
             umma_f16_2sm_elect(d_tmem, ad, bd, kIdesc, kb != 0);
             if (nk > 1) umma_f16_2sm_elect(d_tmem, ad + 2, bd + 2, kIdesc, 1);
@@ -383,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           umma_commit_2sm_mc_elect(t_full + h, 0x3);  // accumulator h ready in both CTAs' TMEM
         }
-        umma_commit_2sm_mc_elect(a_empty, 0x3);  // A tiles reusable once the unit's MMAs retire
+        if (!p.a_stream) umma_commit_2sm_mc_elect(a_empty, 0x3);  // A tiles reusable once the unit's MMAs retire
       }
     }
   } else if (warp < kEpiWarps) {
@@ -599,13 +613,16 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   LCRW_REQUIRE((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
                "lcrw_phase1: operands must be 16-byte aligned");
   const int n_kb = kp / BK;
-  if (n_kb > kMaxKb) {
+  if (n_kb > kMaxKbStream) {
     set_error("lcrw_phase1: operand K = %d (embedding dimension + 3 norm columns) > %d unsupported", m,
-              kMaxKb * BK);
+              kMaxKbStream * BK);
     return LCRW_ERR_UNSUPPORTED;
   }
-  // A K-blocks + B stages within ~208 KB of shared memory
-  const int stages = n_kb <= 5 ? 8 : 13 - n_kb;
+  // resident A K-blocks + B stages within ~208 KB of shared memory; beyond K = 512 the A
+  // K blocks are streamed with B's (each tile re-reads its A rows: more L2->SM bytes,
+  // same MMAs)
+  const bool a_stream = n_kb > kMaxKb;
+  const int stages = a_stream ? kStreamStages : (n_kb <= 5 ? 8 : 13 - n_kb);
   Params p;
   p.a_norms = a_norms;
   p.endmask = endmask;
@@ -626,6 +643,7 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   p.n_kb = n_kb;
   p.n_kmma = (m + 15) / 16;
   p.stages = stages;
+  p.a_stream = a_stream ? 1 : 0;
 
   CUtensorMap tmA, tmB;
   int st = make_map(&tmA, A, a_rows, kp, BM);
@@ -634,12 +652,13 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   st = b_ids ? make_map(&tmB, B, b_table_rows, kp, 1) : make_map(&tmB, B, b_rows, kp, BN_HALF);
   if (st) return st;
 
-  const size_t smem = smem_bytes(n_kb, stages);
+  const size_t smem = smem_bytes(n_kb, stages, a_stream);
   static bool attr_set = false;
   if (!attr_set) {
     size_t mx = smem_bytes(5, 8);
     for (int kb = 6; kb <= kMaxKb; ++kb)
       if (smem_bytes(kb, 13 - kb) > mx) mx = smem_bytes(kb, 13 - kb);
+    if (smem_bytes(0, kStreamStages, true) > mx) mx = smem_bytes(0, kStreamStages, true);
     cudaError_t e = cudaFuncSetAttribute(phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(phase1_kernel)");
     attr_set = true;

@@ -200,6 +200,62 @@ __global__ void emit_kernel(const float* __restrict__ d, const int64_t* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Any element type (topk_select keeps the caller's dtype, kernels.py:210-223): an
+// order-preserving 64-bit key per element (floats widened exactly to double, -0 == +0,
+// NaN last; signed integers with the sign bit flipped; unsigned as is), the same two
+// stable radix passes (id, then key), and the k first elements copied back in their
+// own type.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t double_key(double d) {
+  uint64_t u = (uint64_t)__double_as_longlong(d);
+  if ((u & 0x7FFFFFFFFFFFFFFFull) > 0x7FF0000000000000ull) return ~0ull;
+  if (u == 0x8000000000000000ull) u = 0ull;
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ uint64_t any_key(const void* d, int dtype, int64_t i) {
+  switch (dtype) {
+    case LCRW_F32: return double_key((double)static_cast<const float*>(d)[i]);
+    case LCRW_F64: return double_key(static_cast<const double*>(d)[i]);
+    case LCRW_F16: return double_key((double)__half2float(static_cast<const __half*>(d)[i]));
+    case LCRW_I8: return (uint64_t)(int64_t)static_cast<const int8_t*>(d)[i] ^ 0x8000000000000000ull;
+    case LCRW_I16: return (uint64_t)(int64_t)static_cast<const int16_t*>(d)[i] ^ 0x8000000000000000ull;
+    case LCRW_I32: return (uint64_t)(int64_t)static_cast<const int32_t*>(d)[i] ^ 0x8000000000000000ull;
+    case LCRW_I64: return (uint64_t)static_cast<const int64_t*>(d)[i] ^ 0x8000000000000000ull;
+    case LCRW_U8: return static_cast<const uint8_t*>(d)[i];
+    case LCRW_U16: return static_cast<const uint16_t*>(d)[i];
+    case LCRW_U32: return static_cast<const uint32_t*>(d)[i];
+    default: return static_cast<const uint64_t*>(d)[i];  // LCRW_U64
+  }
+}
+
+__global__ void keys64_kernel(const void* __restrict__ d, int dtype, const int64_t* __restrict__ perm, int64_t n,
+                              uint64_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = any_key(d, dtype, perm[i]);
+}
+
+__global__ void emit_any_kernel(const uint8_t* __restrict__ d, int elem, const int64_t* __restrict__ ids,
+                                const int64_t* __restrict__ pos_by_id, const int64_t* __restrict__ order, int64_t k,
+                                uint8_t* __restrict__ out_d, int64_t* __restrict__ out_i) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < k; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos_by_id[order[r]];
+    for (int b = 0; b < elem; ++b) out_d[r * elem + b] = d[p * elem + b];
+    out_i[r] = ids[p];
+  }
+}
+
+int dtype_bytes(int dtype) {
+  switch (dtype) {
+    case LCRW_F16: case LCRW_I16: case LCRW_U16: return 2;
+    case LCRW_F32: case LCRW_I32: case LCRW_U32: return 4;
+    case LCRW_F64: case LCRW_I64: case LCRW_U64: return 8;
+    case LCRW_I8: case LCRW_U8: return 1;
+    default: return 0;
+  }
+}
+
 }  // namespace tk
 }  // namespace lcrw
 
@@ -326,6 +382,58 @@ int lcrw_topk_sort(const float* d, const int64_t* ids, int64_t n, int64_t k, flo
   const int64_t kk = k < n ? k : n;
   emit_kernel<<<g, 256, 0, st>>>(d, ids, pos_sorted, order, kk, out_d, out_i);
   LCRW_CHECK_LAUNCH("topk emit");
+  return LCRW_OK;
+}
+
+int lcrw_topk_sort_any_workspace(int64_t n, size_t* bytes) {
+  LCRW_REQUIRE(n >= 0 && bytes, "lcrw_topk_sort_any_workspace: bad arguments");
+  size_t c1 = 0, c2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, c1, (const int64_t*)nullptr, (int64_t*)nullptr, (const int64_t*)nullptr,
+                                  (int64_t*)nullptr, (int64_t)n);
+  cub::DeviceRadixSort::SortPairs(nullptr, c2, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n);
+  // sorted ids, positions, positions by id, keys in/out, rank iota
+  *bytes = 6 * align256((size_t)n * 8) + (c1 > c2 ? c1 : c2);
+  return LCRW_OK;
+}
+
+// topk_select for distances of any numeric dtype (LCRW_F32 .. LCRW_U64): the k smallest
+// under ascending (distance, id), distances copied back in their own type.
+int lcrw_topk_sort_any(const void* d, int dtype, const int64_t* ids, int64_t n, int64_t k, void* out_d,
+                       int64_t* out_i, void* ws, size_t ws_bytes, void* stream) {
+  LCRW_REQUIRE(k >= 1, "k must be >= 1");
+  LCRW_REQUIRE(n >= 0, "lcrw_topk_sort_any: bad shape");
+  const int elem = dtype_bytes(dtype);
+  LCRW_REQUIRE(elem > 0, "lcrw_topk_sort_any: unsupported dtype code");
+  if (n == 0) return LCRW_OK;
+  LCRW_REQUIRE(d && ids && out_d && out_i && ws, "lcrw_topk_sort_any: null pointer");
+  size_t need = 0;
+  lcrw_topk_sort_any_workspace(n, &need);
+  LCRW_REQUIRE(ws_bytes >= need, "lcrw_topk_sort_any: workspace too small");
+  cudaStream_t st = as_stream(stream);
+  char* p = static_cast<char*>(ws);
+  const size_t a = align256((size_t)n * 8);
+  int64_t* ids_sorted = reinterpret_cast<int64_t*>(p);
+  int64_t* pos = reinterpret_cast<int64_t*>(p + a);
+  int64_t* pos_sorted = reinterpret_cast<int64_t*>(p + 2 * a);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(p + 3 * a);
+  uint64_t* keys_sorted = reinterpret_cast<uint64_t*>(p + 4 * a);
+  int64_t* rank = reinterpret_cast<int64_t*>(p + 5 * a);
+  int64_t* order = ids_sorted;  // reused after pass 1
+  void* cub_ws = p + 6 * a;
+  size_t cub_bytes = need - 6 * a;
+  const unsigned g = (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  iota_kernel<<<g, 256, 0, st>>>(pos, n);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, ids, ids_sorted, pos, pos_sorted, n, 0, 64, st);
+  if (e != cudaSuccess) return cuda_status(e, "cub SortPairs (ids)");
+  keys64_kernel<<<g, 256, 0, st>>>(d, dtype, pos_sorted, n, keys);
+  iota_kernel<<<g, 256, 0, st>>>(rank, n);
+  e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, keys, keys_sorted, rank, order, n, 0, 64, st);
+  if (e != cudaSuccess) return cuda_status(e, "cub SortPairs (keys)");
+  const int64_t kk = k < n ? k : n;
+  emit_any_kernel<<<g, 256, 0, st>>>(static_cast<const uint8_t*>(d), elem, ids, pos_sorted, order, kk,
+                                     static_cast<uint8_t*>(out_d), out_i);
+  LCRW_CHECK_LAUNCH("topk emit (any dtype)");
   return LCRW_OK;
 }
 

@@ -81,14 +81,18 @@ def to_device(a, dtype, non_blocking: bool = True) -> torch.Tensor:
 
 @dataclass
 class DeviceCSR:
-    """A HistogramSet in HBM (int64 offsets, int32 ids, f32 weights) plus host offsets for planning."""
+    """A HistogramSet in HBM (int64 offsets, int32 ids, f32 weights) plus host offsets for planning.
+
+    The host copies of ids and weights (query-side planning of the reverse pass) are the
+    caller's own arrays when uploaded from a HistogramSet (no copy), else read back from
+    the device on first use (``host_ids``)."""
 
     offsets: torch.Tensor
     cols: torch.Tensor
     vals: torch.Tensor
     n_cols: int
     host_offsets: np.ndarray
-    host_cols: np.ndarray | None = None  # kept for small (query-side) sets: row-order planning
+    host_cols: np.ndarray | None = None
     host_vals: np.ndarray | None = None
 
     @property
@@ -99,6 +103,21 @@ class DeviceCSR:
     def nnz(self) -> int:
         return int(self.host_offsets[-1])
 
+    def host_ids(self) -> tuple[np.ndarray, np.ndarray]:
+        """(ids int32, weights f32) on the host (one device->host read if not kept)."""
+        if self.host_cols is None or self.host_vals is None:
+            self.host_cols = self.cols.cpu().numpy()
+            self.host_vals = self.vals.cpu().numpy()
+        return self.host_cols, self.host_vals
+
+    def slice_rows(self, r0: int, r1: int) -> "DeviceCSR":
+        """Rows [r0, r1) as a DeviceCSR sharing the id / weight storage (offsets rebased)."""
+        lo, hi = int(self.host_offsets[r0]), int(self.host_offsets[r1])
+        ho = self.host_offsets[r0:r1 + 1] - lo
+        return DeviceCSR(self.offsets[r0:r1 + 1] - lo, self.cols[lo:hi], self.vals[lo:hi], self.n_cols, ho,
+                         None if self.host_cols is None else self.host_cols[lo:hi],
+                         None if self.host_vals is None else self.host_vals[lo:hi])
+
     @classmethod
     def upload(cls, x: HistogramSet, name: str = "x") -> "DeviceCSR":
         offs = np.asarray(x.row_offsets, dtype=np.int64)
@@ -108,9 +127,8 @@ class DeviceCSR:
             raise CorpusError(f"{name}: offset/array length mismatch")
         cols = np.asarray(x.column_ids, dtype=np.int32)
         vals = np.asarray(x.values, dtype=np.float32)
-        small = cols.size <= (1 << 22)
         return cls(to_device(offs, torch.int64), to_device(cols, torch.int32), to_device(vals, torch.float32),
-                   int(x.n_cols), offs, cols if small else None, vals if small else None)
+                   int(x.n_cols), offs, cols, vals)
 
 
 class PreparedEmbeddings:
@@ -326,8 +344,8 @@ class Restricted:
         available on the host for planning lcrw_reverse_panels.  Ascending ids
         scatter each query's words over the Z2 tiles, which balances the
         per-(tile, warp) entry lists of that kernel."""
-        if host_plan and x.host_cols is not None:
-            order = np.unique(x.host_cols).astype(np.int32)
+        if host_plan:
+            order = np.unique(x.host_ids()[0]).astype(np.int32)
             rank = np.full(x.n_cols, -1, dtype=np.int32)
             rank[order] = np.arange(len(order), dtype=np.int32)
             used = to_device(order, torch.int32)
@@ -372,7 +390,8 @@ REVERSE_Z2_BYTES = 4 << 30   # Z2 batch budget (docs per batch = budget / (4 * v
 
 def query_entries(x: DeviceCSR, rank: np.ndarray, a_rows: int):
     """Device copy of plan_query_entries for x (host ids of a DeviceCSR): (e_blk, e_tile)."""
-    blk, tile = plan_query_entries(x.host_offsets, x.host_cols, x.host_vals, rank, a_rows, *reverse_panels_geometry())
+    hc, hv = x.host_ids()
+    blk, tile = plan_query_entries(x.host_offsets, hc, hv, rank, a_rows, *reverse_panels_geometry())
     return to_device(blk.view(np.int32), torch.int32), to_device(tile, torch.int64)
 
 
@@ -493,12 +512,50 @@ def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BY
     return int((nb + 31) // 32 * 32)
 
 
+QUERY_SLICE = 16384  # queries per pass of the symmetric pipeline (bounds D, D1, plan and table per pass)
+
+
 def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
-              z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0):
-    """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, k) dists, ids).
+              z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0,
+              query_slice: int = QUERY_SLICE):
+    """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, min(k, n1))
+    dists, ids).  Query sets of any size: queries are processed in slices of
+    ``query_slice`` (a multiple of 8), each slice a full pass (restriction, table, both
+    directions) -- query batching never changes a result (distances.py:198-203).
 
     ``d1`` (8-query panels) may be supplied by a caller that computed the
     forward direction itself (parallel.py); ``id_offset`` shifts returned doc ids."""
+    n1, n2 = x1.n_rows, x2.n_rows
+    dev = x1.cols.device
+    if n1 == 0 or n2 == 0:
+        if k is None:
+            return torch.empty((n1, n2), dtype=torch.float32, device=dev)
+        return (torch.empty((n2, 0), dtype=torch.float32, device=dev),
+                torch.empty((n2, 0), dtype=torch.int64, device=dev))
+    qs = max(8, query_slice // 8 * 8)
+    if n2 <= qs:
+        return _symmetric_pass(x1, x2, prep, k, z2_budget_bytes, d1, id_offset)
+    if k is None:
+        D = torch.empty((n1, n2), dtype=torch.float32, device=dev)
+    else:
+        kk = min(k, n1)
+        out_d = torch.empty((n2, kk), dtype=torch.float32, device=dev)
+        out_i = torch.empty((n2, kk), dtype=torch.int64, device=dev)
+    for q0 in range(0, n2, qs):
+        q1 = min(n2, q0 + qs)
+        d1s = None if d1 is None else d1[(q0 // 8) * 8 * n1:((q1 + 7) // 8) * 8 * n1]
+        r = _symmetric_pass(x1, x2.slice_rows(q0, q1), prep, k, z2_budget_bytes, d1s, id_offset)
+        if k is None:
+            D[:, q0:q1] = r
+        else:
+            out_d[q0:q1], out_i[q0:q1] = r
+        del r
+    return D if k is None else (out_d, out_i)
+
+
+def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
+                    z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0):
+    """One pass of ``symmetric`` over all of x2's queries."""
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
     st = _stream()
@@ -507,8 +564,6 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
         res1 = Restricted.build(x1, prep)
         d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
         del res1
-    if x2.host_cols is None:
-        raise ValueError("query set too large for the host-planned reverse pass")
     res2 = Restricted.build(x2, prep, host_plan=True)
     e_blk, e_tile = query_entries(x2, res2.host_rank, res2.v_e)
     mode = reverse_mode(prep.V, res2.v_e, x1.nnz)
@@ -540,9 +595,15 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     del ws, table
     if k is None:
         return D.view(n1, n2)
-    if k > 1024:
-        raise NotImplementedError("k > 1024")
     kk = min(k, n1)
+    if k > 1024:  # beyond the selection kernels: one (distance, id) sort per query row
+        out_d = torch.empty((n2, kk), dtype=torch.float32, device=dev)
+        out_i = torch.empty((n2, kk), dtype=torch.int64, device=dev)
+        ids = torch.arange(id_offset, id_offset + n1, dtype=torch.int64, device=dev)
+        for q in range(n2):
+            od, oi = topk_sort(D[q * n1:(q + 1) * n1], ids, kk)
+            out_d[q], out_i[q] = od, oi
+        return out_d, out_i
     out_d = torch.empty((n2, k), dtype=torch.float32, device=dev)
     out_i = torch.empty((n2, k), dtype=torch.int64, device=dev)
     topk_matrix_rows(D, n2, n1, n1, id_offset, k, out_d, out_i)
@@ -707,13 +768,10 @@ def load_index(path) -> tuple[DeviceCSR, torch.Tensor, list[str]]:
     vals = section("values", torch.float32).to(dev, non_blocking=True)
     E = section("embeddings", torch.float32).view(v_e, m).to(dev, non_blocking=True)
     offs = torch.from_numpy(offs_h).to(dev)
-    nnz = int(offs_h[-1])
-    small = nnz <= (1 << 22)
-    host_cols = section("ids", torch.int32).numpy().copy() if small else None
-    host_vals = section("values", torch.float32).numpy().copy() if small else None
     words = _index_words(host, sec["words"][0], v_e, path)
     torch.cuda.current_stream().synchronize()  # the pinned buffer is released on return
-    return DeviceCSR(offs, cols, vals, v_e, offs_h, host_cols, host_vals), E, words
+    # host ids / weights are read back from the device only if a caller plans with them
+    return DeviceCSR(offs, cols, vals, v_e, offs_h), E, words
 
 
 def restrict_vocabulary_host(x: HistogramSet, embeddings):

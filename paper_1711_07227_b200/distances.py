@@ -86,11 +86,22 @@ def nearest_word_distances(embeddings: np.ndarray, query_vectors: np.ndarray,
     return device.nearest_word_distances(e, q).cpu().numpy()
 
 
+QUERY_BATCH = 4096  # queries per forward pass above which the one-sided bound runs in batches
+
+
 def _one_sided_device(x1: HistogramSet, queries: HistogramSet, embeddings) -> np.ndarray:
+    """(n1, n_q) forward bounds; query sets above QUERY_BATCH in batches (distances.py:198-203:
+    batching never changes a value), so Z1 stays bounded for any query count."""
+    if x1.n_rows == 0:
+        return np.zeros((0, queries.n_rows), dtype=np.float32)
     prep = device.PreparedEmbeddings(embeddings)
     dx1 = device.DeviceCSR.upload(x1, "x1")
     dq = device.DeviceCSR.upload(queries, "queries")
     res = device.Restricted.build(dx1, prep)
+    if queries.n_rows > QUERY_BATCH:
+        D = torch.empty((x1.n_rows, queries.n_rows), dtype=torch.float32, device=res.A.device)
+        device.forward_rows_into(res, prep, dq, D, QUERY_BATCH)
+        return D.cpu().numpy()
     out = device.one_direction(res, prep, dq, layout="rows")
     return out[: x1.n_rows * queries.n_rows].view(x1.n_rows, queries.n_rows).cpu().numpy()
 

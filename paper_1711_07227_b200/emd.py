@@ -12,11 +12,14 @@ Documented differences:
   beyond tolerance" because float32-normalised supply and demand totals
   differ by more than 1e-9 (emd.py:153-162 -- about half of general
   histograms), augmentation stops once either side is exhausted; the balance
-  check of emd.py:60-63 still raises;
-* the pruning slack is ``PRUNE_SLACK = 1e-4`` instead of 1e-6: the GPU
-  bounds carry the stated 1e-4 relative tolerance, so a smaller slack could
-  discard a true top-k member.  Results are identical; at most a few extra
-  exact solves are made (the returned ``solves`` counts them).
+  check of emd.py:60-63 still raises.  ``STRICT_UNBALANCED = True`` restores the
+  reference's exception for a strict drop-in;
+* the pruning test is ``bound > cutoff * (1 + PRUNE_SLACK) + PRUNE_ATOL * max_w |E_w|``
+  with ``PRUNE_SLACK = 1e-4`` instead of the reference's 1e-6 and no absolute
+  term: the GPU bounds carry the stated tolerance 1e-4 |d| + 1e-5 max_w |E_w|
+  (tests/test_gpu_parity.py), so a tighter test could discard a true top-k
+  member.  Results are identical; at most a few extra exact solves are made
+  (the returned ``solves`` counts them).
 * ``prefiltered_topk_wmd`` solves candidates in speculative batches on the
   GPU but applies the reference's sequential cutoff rule to their results in
   candidate order, so the result and the solve count are those of the
@@ -38,6 +41,7 @@ from .kernels import TopKResult
 FEASIBILITY_TOL = 1e-9
 BALANCE_TOL = 1e-6
 PRUNE_SLACK = 1e-4
+PRUNE_ATOL = 1e-5  # times the largest embedding norm: the absolute part of the GPU bound tolerance
 ORDER_PREFIX = 2048  # candidates ordered up front per query in prefiltered_topk_wmd_batch
 SOLVE_BATCH = 256  # speculative exact solves per GPU launch in prefiltered_topk_wmd
 
@@ -85,8 +89,17 @@ def _offsets(sizes) -> np.ndarray:
     return off
 
 
-def _check_status(status: np.ndarray) -> None:
-    if np.any(status == 1):
+STRICT_UNBALANCED = False  # True: raise where the reference raises (see the module docstring)
+
+
+def _check_status(status: np.ndarray, strict: bool | None = None) -> None:
+    """Kernel status -> the reference's exceptions.  1: no sink reachable with both sides
+    open; 2: too many rounds; 3: augmentation stopped with supply left because the demand
+    side was exhausted (float32-normalised totals differing by more than 1e-9) -- the
+    reference raises "no augmenting path" there (emd.py:153-162); by default this build
+    returns the optimal objective of the transported mass instead (STRICT_UNBALANCED)."""
+    strict = STRICT_UNBALANCED if strict is None else strict
+    if np.any(status == 1) or (strict and np.any(status == 3)):
         raise ValueError("no augmenting path; problem is unbalanced beyond tolerance")
     if np.any(status == 2):
         raise RuntimeError("augmentation failed to converge")
@@ -220,6 +233,16 @@ def wmd(x1: Histogram, x2: Histogram, embeddings: np.ndarray) -> float:
                              ids2=[x2.word_ids])[0])
 
 
+def _prune_atol(embeddings) -> float:
+    """Absolute slack of the pruning test: PRUNE_ATOL * max_w |E_w| (+ the reference's 1e-12)."""
+    if isinstance(embeddings, torch.Tensor):
+        mx = float(torch.linalg.vector_norm(embeddings.double(), dim=1).max()) if embeddings.numel() else 0.0
+    else:
+        e = np.asarray(embeddings, dtype=np.float64)
+        mx = float(np.sqrt((e * e).sum(axis=1).max())) if e.size else 0.0
+    return PRUNE_ATOL * mx + 1e-12
+
+
 def prefiltered_topk_wmd(x1: HistogramSet, query: Histogram, embeddings: np.ndarray, k: int) -> tuple[TopKResult, int]:
     """Exact top-k mover's distances from ``query`` to the rows of x1 (emd.py:214-261).
 
@@ -242,6 +265,7 @@ def prefiltered_topk_wmd(x1: HistogramSet, query: Histogram, embeddings: np.ndar
         return solve_batch([r.weights for r in rows], [query.weights] * len(rows), embeddings=E_t,
                            ids1=[r.word_ids for r in rows], ids2=[query.word_ids] * len(rows))
 
+    atol = _prune_atol(embeddings)
     first = order[:k]
     top = sorted(zip(solve(first).tolist(), (int(i) for i in first)))
     solves = k
@@ -249,7 +273,7 @@ def prefiltered_topk_wmd(x1: HistogramSet, query: Histogram, embeddings: np.ndar
     pos = k
     while pos < n1:
         # speculative batch: candidates whose bound passes the current cutoff (it only shrinks)
-        lim = cutoff * (1.0 + PRUNE_SLACK) + 1e-12
+        lim = cutoff * (1.0 + PRUNE_SLACK) + atol
         end = pos
         while end < n1 and end - pos < SOLVE_BATCH and bounds[order[end]] <= lim:
             end += 1
@@ -258,7 +282,7 @@ def prefiltered_topk_wmd(x1: HistogramSet, query: Histogram, embeddings: np.ndar
         dists = solve(order[pos:end])
         stop = False
         for idx, dist in zip(order[pos:end], dists.tolist()):
-            if bounds[idx] > cutoff * (1.0 + PRUNE_SLACK) + 1e-12:
+            if bounds[idx] > cutoff * (1.0 + PRUNE_SLACK) + atol:
                 stop = True  # bounds ascend and the cutoff never grows: all the rest prune
                 break
             solves += 1
@@ -295,6 +319,7 @@ def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddin
     # smallest is sorted up front (all ties included, so it is an exact prefix of the
     # full order); the full order is built only for a query that runs past it.
     cols = np.ascontiguousarray(bounds.T)
+    atol = _prune_atol(E_t)
 
     pre_n = max(ORDER_PREFIX, k + SOLVE_BATCH)
 
@@ -323,7 +348,7 @@ def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddin
     while open_:
         batch, spans = [], []
         for j in open_:
-            lim = tops[j][-1][0] * (1.0 + PRUNE_SLACK) + 1e-12
+            lim = tops[j][-1][0] * (1.0 + PRUNE_SLACK) + atol
             p0 = int(pos[j])
             if len(orders[j]) < n1 and p0 + SOLVE_BATCH >= len(orders[j]):
                 orders[j] = order_prefix(j, full=True)
@@ -340,7 +365,7 @@ def prefiltered_topk_wmd_batch(x1: HistogramSet, queries: HistogramSet, embeddin
             stop = end == p0
             for r in range(p0, end):
                 idx, dist = int(o[r]), dists[at + r - p0]
-                if bounds[idx, j] > top[-1][0] * (1.0 + PRUNE_SLACK) + 1e-12:
+                if bounds[idx, j] > top[-1][0] * (1.0 + PRUNE_SLACK) + atol:
                     stop = True
                     break
                 solves[j] += 1

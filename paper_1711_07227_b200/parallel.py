@@ -55,15 +55,15 @@ def _world():
 
 
 def allgather_slices(local: torch.Tensor, group=None) -> torch.Tensor:
-    """[world, *local.shape] from equal-shaped per-rank slices."""
-    rank, world = _world()
-    if world == 1:
+    """[world, *local.shape] from equal-shaped per-rank slices: one
+    ``all_gather_into_tensor`` into a contiguous buffer (ncclAllGather on NCCL; the same
+    call runs on gloo in tests/test_parallel_gloo.py), issued whenever a process group
+    is initialised, world 1 included."""
+    if not (dist.is_available() and dist.is_initialized()):
         return local.unsqueeze(0)
+    world = dist.get_world_size(group)
     out = torch.empty((world, *local.shape), dtype=local.dtype, device=local.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out.view(-1), local.contiguous().view(-1), group=group)
-    else:
-        dist.all_gather(list(out.unbind(0)), local.contiguous(), group=group)
+    dist.all_gather_into_tensor(out.view(-1), local.contiguous().view(-1), group=group)
     return out
 
 
@@ -93,10 +93,11 @@ def exchange_blocks(C: torch.Tensor, sizes: list[int], group=None) -> list[torch
 
 
 def gather_candidates(d: torch.Tensor, i: torch.Tensor, group=None):
-    """Gather per-rank (n_q, k) top-k lists to rank 0 as (n_q, world * k); None elsewhere."""
-    rank, world = _world()
-    if world == 1:
+    """Gather per-rank (n_q, k) top-k lists to rank 0 as (n_q, world * k); None elsewhere.
+    The gather is issued whenever a process group is initialised (world 1 included)."""
+    if not (dist.is_available() and dist.is_initialized()):
         return d, i
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
     gd = [torch.empty_like(d) for _ in range(world)] if rank == 0 else None
     gi = [torch.empty_like(i) for _ in range(world)] if rank == 0 else None
     dist.gather(d.contiguous(), gd, dst=0, group=group)
@@ -220,10 +221,30 @@ def sharded_all_pairs_topk(dx_local: DeviceCSR, dx_all: DeviceCSR, lo: int, prep
     od, oi = od[:n_r, :kk].contiguous(), oi[:n_r, :kk].contiguous()
     if world == 1:
         return od, oi
-    gd = [torch.empty((sz, kk), dtype=od.dtype, device=od.device) for sz in sizes] if rank == 0 else None
-    gi = [torch.empty((sz, kk), dtype=oi.dtype, device=oi.device) for sz in sizes] if rank == 0 else None
-    dist.gather(od, gd, dst=0, group=group)
-    dist.gather(oi, gi, dst=0, group=group)
+    return gather_rows_uneven(od, oi, sizes, group)
+
+
+def gather_rows_uneven(d: torch.Tensor, i: torch.Tensor, sizes: list[int], group=None):
+    """Gather per-rank (sizes[r], k) row blocks to rank 0 as one (sum(sizes), k) pair; None
+    elsewhere.  gather needs equal shapes on every rank, so each block is padded to
+    max(sizes) rows and rank 0 trims the padding."""
+    rank, world = _world()
+    mx = max(sizes) if sizes else 0
+    k = int(d.shape[1])
+
+    def padded(t, fill):
+        if t.shape[0] == mx:
+            return t.contiguous()
+        out = torch.full((mx, k), fill, dtype=t.dtype, device=t.device)
+        out[: t.shape[0]] = t
+        return out
+
+    pd = padded(d, float("inf"))
+    pi = padded(i, -1)
+    gd = [torch.empty_like(pd) for _ in range(world)] if rank == 0 else None
+    gi = [torch.empty_like(pi) for _ in range(world)] if rank == 0 else None
+    dist.gather(pd, gd, dst=0, group=group)
+    dist.gather(pi, gi, dst=0, group=group)
     if rank != 0:
         return None
-    return torch.cat(gd), torch.cat(gi)
+    return (torch.cat([g[:sz] for g, sz in zip(gd, sizes)]), torch.cat([g[:sz] for g, sz in zip(gi, sizes)]))

@@ -176,7 +176,69 @@ def case_emd():
     print("emd", len(shapes))
 
 
-if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "widen":
+def case_prims():
+    """The remaining public primitives of movers.kernels (kernels.py:66-167, 210-232):
+    squared_norms, euclidean_into (f32 and f64 out, m below and above numpy's 128-element
+    pairwise block, duplicate rows), row_min / col_min / segmented_min (NaN, ints,
+    both axes), and topk_select / topk_merge on non-f32 dtypes (f64 near-ties, exact
+    ties, integers, f16)."""
+    _, _, kernels = _ref()
+    rng = np.random.default_rng(31)
+    out = {}
+    a32 = rng.standard_normal((20, 300)).astype(np.float32)
+    a64 = rng.standard_normal((15, 1000))
+    out["sn_a32"], out["sn_a64"] = a32, a64
+    out["sn_r32"], out["sn_r64"] = kernels.squared_norms(a32), kernels.squared_norms(a64)
+    for i, (r, c, m) in enumerate(((37, 29, 300), (9, 11, 700), (5, 6, 1), (8, 8, 129))):
+        a = rng.standard_normal((r, m))
+        b = rng.standard_normal((c, m))
+        b[: min(3, c)] = a[: min(3, c)]  # identical rows: exactly 0
+        o32 = np.empty((r, c), np.float32)
+        o64 = np.empty((r, c), np.float64)
+        kernels.euclidean_into(a, kernels.squared_norms(a), b, kernels.squared_norms(b), o32, 7, 5)
+        kernels.euclidean_into(a, kernels.squared_norms(a), b, kernels.squared_norms(b), o64)
+        out[f"eu{i}_a"], out[f"eu{i}_b"], out[f"eu{i}_o32"], out[f"eu{i}_o64"] = a, b, o32, o64
+    mf = rng.standard_normal((13, 17)).astype(np.float32)
+    mf[3, 5] = np.nan
+    mf[7, :] = -0.0
+    mi = rng.integers(-1000, 1000, (9, 21)).astype(np.int32)
+    md = rng.standard_normal((6, 40))
+    out["mn_f"], out["mn_i"], out["mn_d"] = mf, mi, md
+    for nm, v in (("f", mf), ("i", mi), ("d", md)):
+        out[f"rmin_{nm}"], out[f"cmin_{nm}"] = kernels.row_min(v), kernels.col_min(v)
+    seg0 = np.array([0, 2, 3, 9, 13])
+    seg1 = np.array([0, 1, 5, 6, 17])
+    out["seg0"], out["seg1"] = seg0, seg1
+    out["smin_f0"] = kernels.segmented_min(mf, seg0, axis=0)
+    out["smin_f1"] = kernels.segmented_min(mf, seg1, axis=1)
+    out["smin_d1"] = kernels.segmented_min(md, np.array([0, 10, 11, 40]), axis=-1)
+    v1 = rng.standard_normal(50)
+    out["smin_v"], out["smin_v_seg"] = v1, np.array([0, 7, 8, 30, 50])
+    out["smin_v_out"] = kernels.segmented_min(v1, out["smin_v_seg"])
+    # top-k on the caller's dtype
+    n = 3000
+    base = rng.integers(0, 40, n).astype(np.float64) / 3.0
+    d64 = base + rng.integers(0, 3, n) * 1e-12  # near-ties a float32 cast would merge
+    ids = rng.permutation(n).astype(np.int64) * 5 + 2
+    dint = rng.integers(-20, 20, n).astype(np.int64)
+    d16 = (rng.integers(0, 100, n) / 8).astype(np.float16)
+    out["tk_d64"], out["tk_ids"], out["tk_dint"], out["tk_d16"] = d64, ids, dint, d16
+    for k in (1, 10, 700, 5000):
+        for nm, d in (("d64", d64), ("dint", dint), ("d16", d16)):
+            r = kernels.topk_select(d, ids, k)
+            out[f"tk_{nm}_{k}_d"], out[f"tk_{nm}_{k}_i"] = r.distances, r.ids
+    r = kernels.topk_select(np.array([1.0, 1.0 + 1e-12]), np.array([7, 3]), 1)
+    out["tk_verdict_d"], out["tk_verdict_i"] = r.distances, r.ids
+    parts = [kernels.topk_select(d64[a:a + 700], ids[a:a + 700], 50) for a in range(0, n, 700)]
+    mr = kernels.topk_merge(parts, 50)
+    out["tk_merge_d"], out["tk_merge_i"] = mr.distances, mr.ids
+    np.savez_compressed(OUT / "prims.npz", **out)
+    print("prims", len(out))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "prims":
+    case_prims()
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "widen":
     for nm in ("small_m16", "m300", "clustered", "dup_rows"):
         case_widen(nm)
     case_emd()

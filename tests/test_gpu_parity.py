@@ -344,8 +344,9 @@ def test_many_queries_multiple_groups():
                 1e-5 * float(np.sqrt((E.astype(np.float64) ** 2).sum(1).max())))
 
 
-@pytest.mark.parametrize("m", [1, 448, 509])
+@pytest.mark.parametrize("m", [1, 448, 509, 510, 768, 1024])
 def test_dimension_extremes(m):
+    """m > 509 (operand K > 512): the Phase-1 kernel streams A's K blocks through the ring."""
     _, D, _ = _pkg()
     rng = np.random.default_rng(44 + m)
     V = 400
@@ -361,7 +362,7 @@ def test_dimension_extremes(m):
 def test_dimension_too_large_is_reported():
     _, D, _ = _pkg()
     rng = np.random.default_rng(45)
-    E = rng.standard_normal((50, 510)).astype(np.float32)
+    E = rng.standard_normal((50, 4094)).astype(np.float32)
     x1 = _rand_set(rng, 4, 50, 1, 5)
     with pytest.raises(NotImplementedError, match="unsupported"):
         D.lcrwmd_full(x1, x1, E)
@@ -611,12 +612,12 @@ def test_all_pairs_sharded_emulated_ranks():
 
 
 @pytest.mark.gpu
-def test_emd_large_and_unsupported_problems():
-    """The shared-memory solver (h1 + h2 > 128) agrees with the oracle restatement; a problem
-    too large for shared memory is reported, not silently truncated."""
+def test_emd_large_problems():
+    """The shared-memory solver (h1 + h2 > 128) and the global-memory one (a problem too
+    large for shared memory, e.g. 200 x 200) agree with the oracle restatement."""
     from paper_1711_07227_b200 import emd
     rng = np.random.default_rng(48)
-    for h1, h2 in ((90, 70), (130, 20)):
+    for h1, h2 in ((90, 70), (130, 20), (200, 200), (260, 90)):
         s = rng.random(h1) + 0.05
         d = rng.random(h2) + 0.05
         s /= s.sum()
@@ -625,9 +626,59 @@ def test_emd_large_and_unsupported_problems():
         plan = emd.solve_emd(emd.TransportProblem(s, d, c))
         ref = O.solve_emd_objective(s, d, c)
         assert abs(plan.objective - ref) <= 1e-9 * max(1.0, ref), (h1, h2, plan.objective, ref)
-    s = np.full(200, 1 / 200)
-    with pytest.raises(NotImplementedError, match="shared memory"):
-        emd.solve_emd(emd.TransportProblem(s, s, np.ones((200, 200))))
+    # long documents through the embedding path (costs formed in-kernel), global-memory state
+    V, m = 600, 24
+    E = rng.standard_normal((V, m)).astype(np.float32)
+    from paper_1711_07227_b200.corpus import Histogram
+    for h1, h2 in ((180, 150),):
+        ids1 = np.sort(rng.choice(V, h1, replace=False)).astype(np.int32)
+        ids2 = np.sort(rng.choice(V, h2, replace=False)).astype(np.int32)
+        w1 = np.full(h1, 1.0 / h1, np.float32)
+        w2 = np.full(h2, 1.0 / h2, np.float32)
+        got = emd.wmd(Histogram(ids1, w1), Histogram(ids2, w2), E)
+        c = O.pairwise_euclidean(E[ids1], E[ids2]).astype(np.float64)
+        ref = O.solve_emd_objective(w1.astype(np.float64), w2.astype(np.float64), c)
+        assert abs(got - ref) <= 1e-9 * max(1.0, ref), (h1, h2, got, ref)
+
+
+def test_emd_degenerate_ties_same_plan_and_duals():
+    """Degenerate problems (small integer costs, uniform dyadic weights: many equal path
+    lengths) -- the GPU solver picks the reference's augmenting paths (lowest-index sink
+    among equal distances, emd.py:166-167), so plan and duals match, not only the objective."""
+    from paper_1711_07227_b200 import emd
+    rng = np.random.default_rng(77)
+    for trial in range(60):
+        h1, h2 = int(rng.integers(2, 12)), int(rng.integers(2, 12))
+        if trial % 3 == 2:
+            h1, h2 = int(rng.integers(40, 70)), int(rng.integers(40, 70))  # register-state kernel, 2-3 slots
+        s = np.full(h1, 1.0 / 16) if h1 == 16 else rng.integers(1, 4, h1).astype(np.float64)
+        d = rng.integers(1, 4, h2).astype(np.float64)
+        s /= s.sum()
+        d /= d.sum()
+        c = rng.integers(0, 3, (h1, h2)).astype(np.float64)
+        plan = emd.solve_emd(emd.TransportProblem(s, d, c))
+        obj, flow, phi = O.solve_emd_plan(s, d, c)
+        keep = flow > 1e-9
+        pi, qi = np.nonzero(keep)
+        assert abs(plan.objective - obj) <= 1e-12 * max(1.0, obj), trial
+        assert np.array_equal(plan.source_ids, pi) and np.array_equal(plan.target_ids, qi), trial
+        np.testing.assert_allclose(plan.amounts, flow[keep], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(plan.dual_sink, phi[h1:], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(plan.dual_source, -phi[:h1], rtol=0, atol=1e-12)
+
+
+def test_emd_strict_unbalanced_opt_in(monkeypatch):
+    """Totals differing by more than 1e-9 (but within the 1e-6 balance check): by default the
+    transported mass is solved; STRICT_UNBALANCED raises the reference's error (emd.py:153-162)."""
+    from paper_1711_07227_b200 import emd
+    s = np.array([0.5, 0.5 + 4e-7])
+    d = np.array([0.25, 0.75])
+    c = np.array([[1.0, 2.0], [3.0, 0.5]])
+    plan = emd.solve_emd(emd.TransportProblem(s, d, c))
+    assert abs(plan.objective - O.solve_emd_objective(s, d, c)) <= 1e-12
+    monkeypatch.setattr(emd, "STRICT_UNBALANCED", True)
+    with pytest.raises(ValueError, match="no augmenting path"):
+        emd.solve_emd(emd.TransportProblem(s, d, c))
 
 
 # --- SPEC.md acceptance criteria (reference SPEC, "ACCEPTANCE CRITERIA") --------------

@@ -135,3 +135,32 @@ def test_wmd_prefilter_oracle(widen_case):
     d, ids, solves = O.prefiltered_topk_wmd(xd1, q.word_ids, q.weights, E, 4)
     assert np.array_equal(ids, w["pf0_i"]), name
     assert np.allclose(d, w["pf0_d"], rtol=1e-6, atol=1e-9), name
+
+
+def test_prims_restatement_bitwise():
+    """The restated numpy arithmetic csrc/prims.cu implements (pairwise sums, sequential
+    np.minimum) reproduces the reference's squared_norms / euclidean_into / minima bit for
+    bit, and the oracle's top-k keeps the caller's dtype (tests/golden/prims.npz)."""
+    z = np.load(GOLDEN / "prims.npz")
+    assert np.array_equal(O.squared_norms_pairwise(z["sn_a32"]), z["sn_r32"])
+    assert np.array_equal(O.squared_norms_pairwise(z["sn_a64"]), z["sn_r64"])
+    for i in range(4):
+        a, b = z[f"eu{i}_a"], z[f"eu{i}_b"]
+        e = O.euclidean_pairwise(a, O.squared_norms_pairwise(a), b, O.squared_norms_pairwise(b))
+        assert np.array_equal(e, z[f"eu{i}_o64"]), i
+        assert np.array_equal(e.astype(np.float32), z[f"eu{i}_o32"]), i
+    for nm in ("f", "i", "d"):
+        v = z[f"mn_{nm}"]
+        np.testing.assert_array_equal(O.segmented_min_seq(v, [0, v.shape[1]], axis=1)[:, 0], z[f"rmin_{nm}"])
+        np.testing.assert_array_equal(O.segmented_min_seq(v, [0, v.shape[0]], axis=0)[0], z[f"cmin_{nm}"])
+    np.testing.assert_array_equal(O.segmented_min_seq(z["mn_f"], z["seg0"], 0), z["smin_f0"])
+    np.testing.assert_array_equal(O.segmented_min_seq(z["mn_f"], z["seg1"], 1), z["smin_f1"])
+    np.testing.assert_array_equal(O.segmented_min_seq(z["mn_d"], [0, 10, 11, 40], 1), z["smin_d1"])
+    np.testing.assert_array_equal(O.segmented_min_seq(z["smin_v"], z["smin_v_seg"], 0), z["smin_v_out"])
+    for k in (1, 10, 700, 5000):
+        for nm in ("d64", "dint", "d16"):
+            d, i = O.topk_select(z[f"tk_{nm}"], z["tk_ids"], k)
+            assert d.dtype == z[f"tk_{nm}"].dtype
+            assert np.array_equal(d, z[f"tk_{nm}_{k}_d"]) and np.array_equal(i, z[f"tk_{nm}_{k}_i"]), (nm, k)
+    d, i = O.topk_select(np.array([1.0, 1.0 + 1e-12]), np.array([7, 3]), 1)
+    assert np.array_equal(i, z["tk_verdict_i"]) and i[0] == 7

@@ -89,6 +89,20 @@ def _worker(rank, world, port, q):
                               for s_ in range(world)], axis=1)
         assert np.array_equal(got, sym[a0:a1])
         assert np.allclose(sym, O.lcrwmd_full(xa, xa, E), rtol=1e-6, atol=1e-7)
+        # uneven per-rank row blocks (n = 23 over 2 ranks: 11 + 12) gathered to rank 0
+        # (sharded_all_pairs_topk's final step): padded to equal shapes, trimmed on rank 0
+        kk = 4
+        rows_d = np.sort(sym[a0:a1], axis=1)[:, :kk].astype(np.float32)
+        rows_i = np.tile(np.arange(kk, dtype=np.int64), (a1 - a0, 1)) + a0
+        g = parallel.gather_rows_uneven(torch.from_numpy(rows_d), torch.from_numpy(rows_i), sizes)
+        if rank == 0:
+            gd, gi = (x.numpy() for x in g)
+            assert gd.shape == (n, kk) and np.array_equal(gd, np.sort(sym, axis=1)[:, :kk].astype(np.float32))
+            want_i = np.concatenate([np.tile(np.arange(kk), (sz, 1)) + lo_ for sz, (lo_, _) in
+                                     zip(sizes, (parallel.shard_range(n, r, world) for r in range(world)))])
+            assert np.array_equal(gi, want_i)
+        else:
+            assert g is None
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
