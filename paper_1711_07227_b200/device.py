@@ -407,11 +407,14 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
     One block of uint32 words per (query group, T-row tile): W cumulative list
     ends, then the entries (two words: (row - t*T) << 16 | (q - g*G), bits of
     x) of the W per-warp lists (warp = local query % W).  Each list is laid out
-    in groups of I entries naming distinct queries: its entries, sorted by
-    (query, row), fill G_l = max(ceil(n/I), max multiplicity of a query) groups
-    column-major (entry i -> group i % G_l, slot i // G_l), so repeated queries
-    land in distinct groups; empty slots are padding (scratch query G, weight
-    0).  Returns (blocks uint32, block word offsets int64 [n_groups*n_tiles+1]).
+    in groups of I entries naming distinct queries, by LEVEL: the j-th entry
+    (ascending row) of every query of the list is on level j, and level j's
+    entries (ascending query) fill ceil(n_j / I) groups, levels in order.  So
+    each query's terms are accumulated in ascending row (= word id) order
+    whatever the other queries of the set are -- the fp32 sums, and D, do not
+    depend on how the queries are batched (distances.py:198-203); empty slots
+    are padding (scratch query G, weight 0).  Returns (blocks uint32, block
+    word offsets int64 [n_groups*n_tiles+1]).
     Built on the host from the (small) query set -- index planning, no
     arithmetic."""
     if T > 128 or G > 1024:
@@ -428,16 +431,25 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
     order = np.lexsort((rl, ql, key))
     key, ql, rl = key[order], ql[order], rl[order]
     xv = np.asarray(vals)[order].astype(np.float32)
-    n = np.bincount(key, minlength=n_lists)
-    start = np.zeros(n_lists + 1, dtype=np.int64)
-    np.cumsum(n, out=start[1:])
-    idx = np.arange(key.size, dtype=np.int64) - start[key]           # position inside its list
-    new_run = np.ones(key.size, dtype=bool)                          # (list, query) runs -> max multiplicity
+    # level of an entry = its position inside its (list, query) run (ascending row)
+    new_run = np.ones(key.size, dtype=bool)
     new_run[1:] = (key[1:] != key[:-1]) | (ql[1:] != ql[:-1])
-    run_len = np.bincount(np.cumsum(new_run) - 1)
-    mult = np.zeros(n_lists, dtype=np.int64)
-    np.maximum.at(mult, key[new_run], run_len)
-    groups = np.maximum((n + I - 1) // I, mult)
+    run_id = np.cumsum(new_run) - 1
+    run_start = np.flatnonzero(new_run)
+    level = np.arange(key.size, dtype=np.int64) - run_start[run_id]
+    L = int(level.max()) + 1 if key.size else 1
+    # (list, level) cells, ascending query inside each: position p -> group p // I, slot p % I
+    order2 = np.lexsort((ql, level, key))
+    key, ql, rl, xv, level = key[order2], ql[order2], rl[order2], xv[order2], level[order2]
+    cell = key * L + level
+    n_cell = np.bincount(cell, minlength=n_lists * L)
+    cell_start = np.zeros(n_lists * L + 1, dtype=np.int64)
+    np.cumsum(n_cell, out=cell_start[1:])
+    cpos = np.arange(key.size, dtype=np.int64) - cell_start[cell]     # position inside its cell
+    g_cell = ((n_cell + I - 1) // I).reshape(n_lists, L)              # groups per (list, level)
+    g_off = np.zeros((n_lists, L), dtype=np.int64)                    # first group of each level in its list
+    np.cumsum(g_cell[:, :-1], axis=1, out=g_off[:, 1:])
+    groups = g_cell.sum(axis=1)
     lens = (groups * I).reshape(n_groups * n_tiles, W)               # padded list lengths (entries)
     ends = np.cumsum(lens, axis=1)                                   # per-block cumulative list ends
     blk_words = W + 2 * ends[:, -1]
@@ -454,7 +466,7 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
     flat = lens.ravel()
     pos = np.arange(flat.sum(), dtype=np.int64) - np.repeat(np.cumsum(flat) - flat, flat)
     words[np.repeat(ent_base, flat) + 2 * pos] = np.uint32(G * 128)
-    slot = ent_base[key] + 2 * ((idx % groups[key]) * I + idx // groups[key])
+    slot = ent_base[key] + 2 * ((g_off[key, level] + cpos // I) * I + cpos % I)
     words[slot] = (((rl * 128) << 18) | (ql * 128)).astype(np.uint32)
     words[slot + 1] = xv.view(np.uint32)
     return words, tile_off

@@ -154,6 +154,13 @@ def test_reverse_entry_plan_invariants(n_q, h, V):
         ent = blk[W:W + 2 * ends[-1]].reshape(-1, 2)
         for w in range(W):
             lo = ends[w - 1] if w else 0
+            last_row = {}  # each query's terms in ascending row order (batching-invariant fp32 sums)
+            for e in range(lo, ends[w]):
+                qv = int((ent[e, 0] & 0x3FFFF) >> 7)
+                if qv != G:
+                    rv = int(ent[e, 0] >> 25)
+                    assert rv > last_row.get(qv, -1), (B, w, qv)
+                    last_row[qv] = rv
             for b in range(lo, ends[w], I):
                 qs = ((ent[b:b + I, 0] & 0x3FFFF) >> 7).astype(np.int64)
                 real = qs != G
