@@ -35,8 +35,9 @@ gathered to rank 0 and merged (paper_1711_07227_b200/parallel.py).  Total work
 is fixed (strong scaling of C2, as BASELINE.json configs[2] describes).
 
 --impl reference times the reference algorithm (the pinned CPU oracle port,
-oracle/lcrwmd_oracle.py, all host threads) on a bounded sample of the same
-workload; rank 0 only.
+oracle/lcrwmd_oracle.py, all host threads) on bounded samples of each part of
+the same workload, extrapolated part by part to the full step (CpuSample);
+rank 0 only.  `--gpus N` outside torchrun re-launches itself as N ranks.
 """
 
 from __future__ import annotations
@@ -57,6 +58,7 @@ sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
     "c2": dict(n_docs=1_000_000, n_queries=1000, vocab=100_000, dim=300, h=50, k=10,
+               l2="inputs larger than L2 (X1 400 MB, D1 4 GB, distance table 11.8 GB); no flush",
                workload="symmetric LC-RWMD top-10, 1M docs x 1k queries, V=100k, m=300, h~50 (BASELINE configs[1])"),
     "c1": dict(n_docs=2000, n_queries=64, vocab=20_000, dim=300, h=40, k=10,
                workload="symmetric LC-RWMD top-10, 2000 docs x 64 queries, V=20k, m=300, h~40 (BASELINE configs[0])"),
@@ -64,10 +66,12 @@ CONFIGS = {
                 workload="symmetric LC-RWMD top-10, 100k docs x 256 queries, V=50k, m=300, h~50 (dev size)"),
     # one GPU's share of BASELINE configs[3] (V = 3M, h ~ 150; 4M docs over 8 GPUs -> 500k per GPU)
     "c4": dict(n_docs=500_000, n_queries=1000, vocab=3_000_000, dim=300, h=150, k=10,
+               l2="inputs larger than L2 (E 3.6 GB, X1 600 MB, Z1 12 GB); no flush",
                workload="symmetric LC-RWMD top-10, 500k docs (one of 8 shards of 4M) x 1k queries, V=3M, m=300, "
                         "h~150 (BASELINE configs[3] per GPU)"),
     # one 4k-query batch of BASELINE configs[4] on one GPU's 25k-doc shard (200k docs over 8 GPUs)
     "c5": dict(n_docs=25_000, n_queries=4096, vocab=400_000, dim=300, h=50, k=10,
+               l2="inputs larger than L2 (E 480 MB, Z1 of the batch 6.6 GB); no flush",
                workload="symmetric LC-RWMD top-10, 25k docs (one of 8 shards of 200k) x a 4k-query batch, V=400k, "
                         "m=300, h~50 (BASELINE configs[4] per GPU and batch)"),
 }
@@ -141,22 +145,88 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port, all host threads) on a bounded sample
+# CPU baseline (oracle port, all host threads): bounded samples of each part of the
+# step, each extrapolated to the full workload by its own work model
 # ---------------------------------------------------------------------------
-def cpu_sample_rate(E, x1, x2, k, target_s: float):
+class CpuSample:
+    """The reference algorithm's step (lcrwmd_full + per-query top-k, distances.py:244-264,
+    kernels.py:210-223) on the host cores, timed as four parts on bounded samples and
+    extrapolated part by part (each oracle loop is linear in its row count):
+
+      forward Phase 1   R restricted-vocabulary rows x all query words  -> x v_e1 / R
+      forward SpMM      n_s docs x all queries                          -> x n1 / n_s
+      reverse direction n_s docs as queries against the query set       -> x n1 / n_s
+      max + top-k       the n_s x n2 block, per query                   -> x n1 / n_s
+
+    (a plain "first n docs" sample would under-count the forward pass, whose vocabulary
+    restriction -- hence Phase-1 work -- grows with n until it saturates at ~V)."""
+
+    def __init__(self, E, x1, x2, k, rows: int, docs: int, threads: int):
+        from oracle import lcrwmd_oracle as O
+        self.O, self.E, self.x1, self.x2, self.k, self.threads = O, E, x1, x2, k, threads
+        self.used1 = np.unique(np.asarray(x1.column_ids))
+        self.v_e1 = int(self.used1.size)
+        self.rows = min(rows, self.v_e1)
+        self.docs = min(docs, x1.n_rows)
+        self.xs = O.as_csr(x1.slice_rows(0, self.docs))
+        self.x2c = O.as_csr(x2)
+        self.t2 = np.ascontiguousarray(E[np.asarray(x2.column_ids)])
+        self.e_rows = np.ascontiguousarray(E[self.used1[: self.rows]])
+        self.x2r, self.e2, _ = O.restrict_vocabulary(self.x2c, E)
+        self.xsr, _, _ = O.restrict_vocabulary(self.xs, E)
+        rng = np.random.default_rng(0)
+        self.z1 = rng.random((self.xsr.n_cols, x2.n_rows), dtype=np.float32)  # SpMM cost: any values
+
+    def step(self) -> dict:
+        O, th = self.O, self.threads
+        t = {}
+        t0 = time.perf_counter()
+        O.phase1(self.e_rows, self.t2, np.asarray(self.x2c.row_offsets), threads=th)
+        t["fwd_phase1"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        d1 = O.spmm(self.xsr, self.z1, threads=th)
+        t["fwd_spmm"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        d2t = O.one_direction(self.x2r, self.e2, self.E, self.xs, threads=th)
+        t["reverse"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.topk_per_query(np.maximum(d1, d2t.T), self.k)
+        t["max_topk"] = time.perf_counter() - t0
+        return t
+
+    def extrapolate(self, t: dict) -> float:
+        """Seconds for the full workload (n1 docs x n2 queries)."""
+        f_docs = self.x1.n_rows / self.docs
+        return (t["fwd_phase1"] * self.v_e1 / self.rows
+                + (t["fwd_spmm"] + t["reverse"] + t["max_topk"]) * f_docs)
+
+    def describe(self, t: dict) -> str:
+        return (f"extrapolated from bounded samples of the same workload (oracle/lcrwmd_oracle.py, "
+                f"{self.threads} threads): forward Phase 1 on {self.rows} of {self.v_e1} restricted vocabulary rows x "
+                f"all {self.x2.nnz} query words ({t['fwd_phase1']:.2f} s, x{self.v_e1 / self.rows:.1f}); "
+                f"forward SpMM, reverse direction and max+top-{self.k} on {self.docs} of {self.x1.n_rows} docs "
+                f"({t['fwd_spmm']:.2f} + {t['reverse']:.2f} + {t['max_topk']:.2f} s, "
+                f"x{self.x1.n_rows / self.docs:.0f})")
+
+
+def cpu_sample_rate(E, x1, x2, k, target_s: float, rows: int = 2048, docs: int = 512):
     from oracle import lcrwmd_oracle as O
     threads = O.default_threads()
-    n = 32
+    smp = CpuSample(E, x1, x2, k, rows, docs, threads)
+    tot = {}
+    t_start = time.perf_counter()
+    reps = 0
     while True:
-        t0 = time.perf_counter()
-        O.lcrwmd_topk(x1.slice_rows(0, n), x2, E, k, threads=threads)
-        dt = time.perf_counter() - t0
-        if dt >= target_s or n >= x1.n_rows:
+        for n_, v in smp.step().items():
+            tot[n_] = tot.get(n_, 0.0) + v
+        reps += 1
+        if time.perf_counter() - t_start >= target_s:
             break
-        n = int(min(x1.n_rows, max(2 * n, n * target_s / max(dt, 1e-3) * 0.9)))
-    return {"value": n * x2.n_rows / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {n} resident docs x all {x2.n_rows} queries of the same workload "
-                      f"(full symmetric LC-RWMD + top-{k}, oracle/lcrwmd_oracle.py, {dt:.1f} s)"}
+    avg = {n_: v / reps for n_, v in tot.items()}
+    secs = smp.extrapolate(avg)
+    return {"value": x1.n_rows * x2.n_rows / secs, "unit": UNIT, "cores": threads, "kind": "port",
+            "extrapolated": True, "seconds_full_step": secs, "parts_s": avg,
+            "sample": smp.describe(avg) + f"; {reps} repetition(s)"}
 
 
 # ---------------------------------------------------------------------------
@@ -344,9 +414,7 @@ def run_ours(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f16 operands, fp32 accumulate",
         "data": "synthetic (N(0,1) embeddings, uniform word ids; seeds 0/1/2)",
-        "config": {"workload": cfg["workload"], "n_docs": n1, "n_queries": n2, "vocab": cfg["vocab"],
-                   "dim": cfg["dim"], "h": cfg["h"], "k": k, "parallelism": f"docs sharded x{world}",
-                   "l2": "inputs larger than L2 (X1 400 MB, D1 4 GB); no flush"},
+        "config": bench_config(cfg, world),
         "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "paper_1711_07227_b200.distances.lcrwmd_topk (pinned host arrays)"},
         "roofline": roofline,
@@ -379,24 +447,47 @@ def run_reference(args, cfg):
     E, x1, x2 = make_data(cfg)
     k = cfg["k"]
     threads = O.default_threads()
-    n = args.ref_docs
-    sub = x1.slice_rows(0, n)
+    smp = CpuSample(E, x1, x2, k, args.ref_rows, args.ref_docs, threads)
     for _ in range(args.warmup):
-        O.lcrwmd_topk(sub, x2, E, k, threads=threads)
-    t0 = time.perf_counter()
+        smp.step()
+    tot = {}
     for _ in range(args.steps):
-        O.lcrwmd_topk(sub, x2, E, k, threads=threads)
-    dt = (time.perf_counter() - t0) / args.steps
-    value = n * x2.n_rows / dt
-    sample = (f"first {n} resident docs x all {x2.n_rows} queries per step (full symmetric LC-RWMD + top-{k}); "
-              f"oracle port oracle/lcrwmd_oracle.py (reference is pure Python, no compiled build)")
+        for n_, v in smp.step().items():
+            tot[n_] = tot.get(n_, 0.0) + v
+    avg = {n_: v / args.steps for n_, v in tot.items()}
+    secs = smp.extrapolate(avg)
+    value = x1.n_rows * x2.n_rows / secs
+    sample = smp.describe(avg) + "; the reference is pure Python (no compiled build): its algorithm restated in " \
+                                 "numpy, pinned to the reference's outputs (tests/golden)"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "impl": "reference",
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeds 0/1/2)",
-            "config": {"workload": cfg["workload"], "n_docs": x1.n_rows, "n_queries": x2.n_rows, "k": k},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "impl": "reference",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (N(0,1) embeddings, uniform word ids; seeds 0/1/2)",
+            "config": bench_config(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "extrapolated": True,
+                             "sample": sample, "parts_s": avg},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def bench_config(cfg, world: int) -> dict:
+    """The config object both arms print (identical keys and values)."""
+    return {"workload": cfg["workload"], "n_docs": cfg["n_docs"], "n_queries": cfg["n_queries"],
+            "vocab": cfg["vocab"], "dim": cfg["dim"], "h": cfg["h"], "k": cfg["k"],
+            "parallelism": f"docs sharded x{world}",
+            "l2": cfg.get("l2", "small inputs (not a headline config); no flush")}
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-run this command as N ranks
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -408,8 +499,10 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-docs", type=int, default=1024,
-                    help="resident docs per reference-arm step (x all queries)")
+    ap.add_argument("--ref-docs", type=int, default=512,
+                    help="sampled resident docs per reference-arm step (SpMM, reverse, top-k parts)")
+    ap.add_argument("--ref-rows", type=int, default=2048,
+                    help="sampled restricted-vocabulary rows per reference-arm step (forward Phase 1 part)")
     ap.add_argument("--z2-mb", type=int, default=4096, help="reverse Z2 batch budget (MiB)")
     ap.add_argument("--reverse", choices=["auto", "gemm", "table"], default="auto",
                     help="reverse Phase-1 form (sets LCRW_REVERSE): auto picks the distance table when "
@@ -417,6 +510,11 @@ def main():
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU code path (NCCL process group) even with one rank")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}; using WORLD_SIZE",
+              file=sys.stderr)
     if args.reverse != "auto":
         os.environ["LCRW_REVERSE"] = args.reverse
     cfg = CONFIGS[args.config]
