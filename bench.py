@@ -346,9 +346,12 @@ def run_ours(args, cfg):
     rev_flops = 2.0 * v_e2 * x1s.nnz * cfg["dim"]
     fwd_flops = 2.0 * int(np.unique(x1s.column_ids).size) * x2.nnz * cfg["dim"]
     table_flops = 2.0 * v_e2 * cfg["vocab"] * cfg["dim"]
-    # table_min gathers one 4-byte table entry per (query-vocabulary word, doc word) and
-    # writes one Z2 entry per (query-vocabulary word, doc)
-    table_bytes = 4.0 * v_e2 * (x1s.nnz + x1s.n_rows)
+    # table_min gathers, per doc word and 160-word table chunk, one 512-byte row of 3-byte keys
+    # (3.2 B per (query-vocabulary word, doc word) distance) and writes one 4-byte Z2 entry per
+    # (query-vocabulary word, doc)
+    n_chunks = -(-v_e2 // 160)
+    table_bytes = 512.0 * n_chunks * x1s.nnz + 4.0 * v_e2 * x1s.n_rows
+    table_entries = float(v_e2) * x1s.nnz
     spmm_bytes = 8.0 * (x1s.n_rows + 1) + 8.0 * x1s.nnz + 4.0 * x1s.nnz * n2
     # reverse_panels streams every Z2 panel once (4 * v_e2 bytes per doc), reads D1 and writes D
     rev_bytes = 4.0 * v_e2 * x1s.n_rows + 8.0 * n2 * x1s.n_rows
@@ -387,8 +390,8 @@ def run_ours(args, cfg):
         l2path = ROOT / "profiles" / "l2_gather_peak.json"
         l2 = json.loads(l2path.read_text()) if l2path.exists() else {"gbs": float("nan"), "source": "missing"}
         tr = traffic_all.get("table_min_kernel")
-        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 512-B rows of an L2-resident "
-                              "distance-table chunk)",
+        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 512-B rows of 24-bit keys of "
+                              "an L2-resident 160-word distance-table chunk)",
                     "bound": "l2", "achieved": achieved, "peak": l2["gbs"], "unit": "GB/s",
                     "frac": achieved / l2["gbs"],
                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
@@ -397,6 +400,7 @@ def run_ours(args, cfg):
                     "peak_source": f"measured L2 gather ceiling on B200 ({l2['source']})",
                     "hbm_peak_gbs": pk.get("hbm_gbs"), "achieved_over_hbm_peak": achieved / pk.get("hbm_gbs", 1.0),
                     "per_launch_ms": tm["ms"] / max(tm["launches"], 1),
+                    "distances_per_s": table_entries / (tm["ms"] / args.steps * 1e-3),
                     "launches_per_step": tm["launches"] / args.steps, "share_of_step": tm["ms"] / args.steps / ms}
     else:
         rev = ksum.get("phase1_rev", {"ms": float("nan"), "launches": 1})

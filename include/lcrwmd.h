@@ -189,10 +189,11 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
  * max_batch_words = max words over batches (0 in table mode).  d1_ready
  * (cudaEvent_t or NULL): the stream waits on it before the first read of D1, so
  * the forward direction can run concurrently on another stream with the reverse
- * Phase 1.  table (NULL = GEMM mode): the distance table of lcrw_table_transpose
- * for these a_rows query-vocabulary rows and the v_rows E rows; each batch's Z2
- * is then one lcrw_table_min (gather, plan, phase1 and zeros are skipped; rep,
- * next, remap, EhB may be NULL). */
+ * Phase 1.  table (NULL = GEMM mode): the packed distance table of
+ * lcrw_distance_table for these a_rows query-vocabulary rows and the v_rows E
+ * rows; each batch's Z2 is then one lcrw_table_min (gather, plan, phase1 and
+ * zeros are skipped; rep, next, remap, EhB may be NULL).  In GEMM mode Z2 is
+ * rounded through the table's 24-bit key, so both modes give the same D. */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                           int m, int kp,
@@ -200,34 +201,41 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, const float* table, void* d1_ready, void* ws,
+                          int64_t batch_docs, int range_cols, const void* table, void* d1_ready, void* ws,
                           size_t ws_bytes, void* stream);
 
 /* ---- distance-table reverse Phase 1 (table.cu) ---------------------------
  * When nnz(X1) >> V, every (w, u) distance of the reverse Phase 1 is needed
- * ~nnz/V times; the table holds each once:
- *   T[(w >> 7) * v_rows * 128 + u * 128 + (w & 127)] = |A_w - E_u|
- * (128-word chunks, one 512-byte row per E row; lcrw_table_floats(a_rows,
- * v_rows) floats), with exact zeros for identical rows.
+ * ~nnz/V times; the table holds each once, as a 24-bit order-preserving key of
+ * the scaled distance (5 exponent + 19 mantissa bits, round to nearest:
+ * relative error <= 2^-20; 0 stays 0 -- common.cuh dist_key24):
+ *   chunk c = w >> 7 of 128 query-vocabulary words, per E row u one 384-byte
+ *   row at byte ((c * v_rows) + u) * 384: 128 x u16 (key >> 8) then
+ *   128 x u8 (key & 255);  lcrw_table_bytes(a_rows, v_rows) bytes,
+ * with exact zeros for identical rows.
  * lcrw_distance_table builds it in one pass: lcrw_phase1 over the a_rows
  * query-vocabulary A rows and ALL v_rows E rows (EhB) as singleton segments
- * (seg_offsets = 0..v_rows and its lcrw_segment_plan), storing row panels
+ * (seg_offsets = 0..v_rows and its lcrw_segment_plan), storing packed rows
  * directly (the same entries lcrw_phase1 computes in the GEMM form), then the
  * zeros (canon/next classes of lcrw_row_classes, remap = E id -> A row or -1).
- * lcrw_table_transpose builds the same layout from lcrw_phase1's z_shift-7
- * output Tp (zeros already applied).
+ * lcrw_table_transpose builds the same table from lcrw_phase1's z_shift-7 f32
+ * output Tp (unscaled; zeros already applied) and scale (cross-check path).
  * lcrw_table_min: Z2[p * z_panel + w * 32 + (d & 31)] = min over the words u of
- * doc d of T[w, u] (32-doc panels, z_panel = 32 * a_rows; docs as lcrw_phase1's
- * segments: doc_offsets[d] - seg_base .. into doc_cols, E ids < v_rows). */
+ * doc d of T[w, u], decoded and unscaled (32-doc panels, z_panel = 32 * a_rows;
+ * docs as lcrw_phase1's segments: doc_offsets[d] - seg_base .. into doc_cols,
+ * E ids < v_rows).  The GEMM form of the reverse pass rounds its Z2 through the
+ * same key, so both forms give identical Z2. */
 int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                         int m, int kp, const int64_t* seg_offsets, const uint32_t* endmask, const int32_t* range_seg,
                         int64_t n_ranges, const float* scale, const int32_t* canon, const int32_t* next,
-                        const int32_t* remap, float* T, void* stream);
+                        const int32_t* remap, void* T, void* stream);
 int lcrw_table_chunk(void);
-int64_t lcrw_table_floats(int64_t a_rows, int64_t v_rows);
-int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, float* T, void* stream);
-int lcrw_table_min(const float* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
-                   int64_t n_docs, const int32_t* doc_cols, float* Z2, int64_t z_panel, void* stream);
+int64_t lcrw_table_bytes(int64_t a_rows, int64_t v_rows);
+int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const float* scale, void* T,
+                         void* stream);
+int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
+                   int64_t n_docs, const int32_t* doc_cols, const float* scale, float* Z2, int64_t z_panel,
+                   void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k

@@ -50,10 +50,10 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
                                     I64, I64, I32, P, P, P, SZ, P]),
     "lcrw_table_chunk": (I32, []),
-    "lcrw_table_floats": (I64, [I64, I64]),
-    "lcrw_table_transpose": (I32, [P, I64, I64, P, P]),
+    "lcrw_table_bytes": (I64, [I64, I64]),
+    "lcrw_table_transpose": (I32, [P, I64, I64, P, P, P]),
     "lcrw_distance_table": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P]),
-    "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, I64, P]),
+    "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, P, I64, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),
     "lcrw_max_transposed_into": (I32, [P, I64, P, I64, P, I64, I64, I64, P]),
@@ -83,7 +83,7 @@ SIGNATURES: dict[str, tuple] = {
 _VALUE_FUNCS = {"lcrw_emd_problem_bytes", "lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
                 "lcrw_endmask_words", "lcrw_plan_ranges", 
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
-                "lcrw_reverse_panels_ilp", "lcrw_profile_count", "lcrw_table_chunk", "lcrw_table_floats"}
+                "lcrw_reverse_panels_ilp", "lcrw_profile_count", "lcrw_table_chunk", "lcrw_table_bytes"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".

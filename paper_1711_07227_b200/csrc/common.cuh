@@ -310,4 +310,44 @@ __device__ __forceinline__ float key_float(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
+// ---------------------------------------------------------------------------
+// 24-bit distance keys of the reverse direction (table.cu).
+// A distance d in the scaled operand space (0 <= d < 2^8: every scaled row has
+// |x'| < 2^7) is stored as an order-preserving 24-bit key: 5 exponent bits
+// relative to 2^-23 and 19 mantissa bits, rounded to nearest (relative error
+// <= 2^-20 ~ 9.5e-7); 0 -> 0 (exact zeros stay exact), 0 < d < 2^-22 -> 1.
+// Keys compare as integers, so min over keys == key of the min, and the table
+// form and the GEMM form of the reverse Phase 1 round identically.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kKeyExpBase = 104u;  // f32 biased exponent of 2^-23
+__device__ __forceinline__ uint32_t dist_key24(float d) {
+  const uint32_t b = __float_as_uint(d);
+  if (b < ((kKeyExpBase + 1u) << 23)) return b == 0u ? 0u : 1u;
+  return (b - (kKeyExpBase << 23) + 8u) >> 4;
+}
+__device__ __forceinline__ float key24_dist(uint32_t key) {
+  return key ? __uint_as_float((key << 4) + (kKeyExpBase << 23)) : 0.f;
+}
+// packed table rows: 160 query-vocabulary words per chunk, per vocabulary word u one
+// 512-byte row of 32 16-byte groups (one 16-byte load per lane per row in table_min,
+// 3.2 bytes per distance).  Group g = four little-endian 32-bit words q0..q3 holding
+// words 5g .. 5g+4 of the chunk:
+//   q_i = key(5g + i) << 8 | byte i of key(5g + 4)      (i = 0, 1, 2; q3's low byte 0)
+// so the min of q_i over rows has key(5g + i) in its top 24 bits (no unpacking), and
+// key(5g + 4) is reassembled from the low bytes with two byte permutes.
+constexpr int kTableChunk = 160;
+constexpr int kTableKeysPerGroup = 5;
+constexpr int kTableRowBytes = 512;
+// the three bytes (low to high) of word p's key inside its row: b0, b0 + step, b0 + 2 step
+__host__ __device__ __forceinline__ void table_key_bytes(int p, int64_t& b0, int& step) {
+  const int g = p / kTableKeysPerGroup, i = p % kTableKeysPerGroup;
+  if (i < 4) {
+    b0 = 16 * g + 4 * i + 1;
+    step = 1;
+  } else {
+    b0 = 16 * g;
+    step = 4;
+  }
+}
+
 }  // namespace lcrw

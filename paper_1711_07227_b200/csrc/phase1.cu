@@ -67,6 +67,14 @@ constexpr int kMaxKb = 8;                     // resident A: operand K <= 512 (m
 constexpr int kMaxKbStream = 64;              // streamed A (K > 512): operand K <= 4096
 constexpr int kStreamStages = 6;              // streamed A: ring stages of (A + B) K blocks, 32 KB each
 
+// output forms of the epilogue
+enum ZMode : int {
+  kZPanels = 0,     // f32 Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))] (segment panels)
+  kZPanelsKey = 1,  // the same, values rounded through the 24-bit key (reverse direction, GEMM form)
+  kZTable = 2,      // packed 24-bit distance table (kTableChunk-row chunks, kTableRowBytes per
+                    // segment = vocabulary word; z_panel = bytes per chunk)
+};
+
 struct Params {
   const float* a_norms;
   const uint32_t* endmask;
@@ -80,7 +88,7 @@ struct Params {
   const int32_t* b_ids;  // gather mode: B row c is operand row b_ids[c] (TMA gather4); NULL = rows in order
   int32_t b_oob;         // gather mode: a row index past the operand table (zero-filled padding rows)
   int z_shift;       // Z panel width = 1 << z_shift segments
-  int z_transposed;  // 1: Z[(r >> zs) * z_panel + (s << zs) + (r & (zw-1))] (row panels; distance tables)
+  int z_mode;        // ZMode: Z layout / value form of the output
   int a_rows;
   int n_mpairs;      // 256-row A tiles
   int n_ranges;      // column ranges; a work unit takes two consecutive ones
@@ -434,16 +442,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float nE = valid ? __ldg(p.a_norms + row) : 0.f;
       // output cursor: segment s = U.sb(grp) + emitted so far, at
       //   Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))]   (segment panels), or
-      //   Z[(row >> zs) * z_panel + (s << zs) + (row & (zw-1))] (z_transposed: a warp's
-      //   32 rows of one segment are one coalesced 128-byte store)
+      //   packed table bytes (row / 160) * z_panel + s * 512 + table_key_bytes(row % 160)
+      //   (kZTable: a warp's 32 rows of one segment write within ~100 contiguous bytes)
       const int64_t s_first = U.sb(grp);
       float* zq;
       int64_t step, wrap;
       uint32_t s_in = (uint32_t)s_first & (zw - 1);
-      if (p.z_transposed) {
-        zq = p.Z + ((int64_t)row >> zs) * p.z_panel + (s_first << zs) + (row & (zw - 1));
-        step = zw;
-        wrap = 0;
+      uint8_t* zb = nullptr;
+      int kstep = 1;
+      if (p.z_mode == kZTable) {
+        zq = nullptr;
+        step = wrap = 0;
+        int64_t kb0;
+        table_key_bytes(row % kTableChunk, kb0, kstep);
+        zb = reinterpret_cast<uint8_t*>(p.Z) + ((int64_t)row / kTableChunk) * p.z_panel +
+             s_first * kTableRowBytes + kb0;
       } else {
         zq = p.Z + (s_first >> zs) * p.z_panel + ((int64_t)row << zs) + s_in;
         step = 1;
@@ -456,6 +469,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #if LCRW_EPI_MODE == 5
         if (d < -1.f)  // experiment: never true -- the global store is skipped
 #endif
+        if (p.z_mode == kZTable) {
+          const uint32_t key = dist_key24(d);
+          if (valid) {
+            zb[0] = (uint8_t)key;
+            zb[kstep] = (uint8_t)(key >> 8);
+            zb[2 * kstep] = (uint8_t)(key >> 16);
+          }
+          zb += kTableRowBytes;
+          return;
+        }
+        if (p.z_mode == kZPanelsKey) d = key24_dist(dist_key24(d));
         if (valid) *zq = d * inv_scale;
         zq += step;
         if (++s_in == zw) {
@@ -599,14 +623,14 @@ namespace p1 {
 int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
            int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids = nullptr,
-           int64_t b_table_rows = 0, bool z_transposed = false) {
+           int64_t b_table_rows = 0, int z_mode = kZPanels) {
   LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(K)");
   LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
                "lcrw_phase1: row counts must fit in int32");
   LCRW_REQUIRE(n_seg >= 0 && n_ranges >= 1, "lcrw_phase1: bad segment plan");
   LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_phase1: z_shift out of range");
-  LCRW_REQUIRE(z_panel >= ((z_transposed ? n_seg : a_rows) << z_shift),
-               "lcrw_phase1: z_panel must be >= a_rows << z_shift (n_seg << z_shift transposed)");
+  LCRW_REQUIRE(z_mode == kZTable ? z_panel >= n_seg * kTableRowBytes : z_panel >= (a_rows << z_shift),
+               "lcrw_phase1: z_panel must be >= a_rows << z_shift (packed table: n_seg * 384 bytes)");
   if (a_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(A && a_norms && B && seg_offsets && endmask && range_seg && scale && Z,
                "lcrw_phase1: null pointer");
@@ -636,7 +660,7 @@ int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16
   p.b_ids = b_ids;
   p.b_oob = (int32_t)b_table_rows;
   p.z_shift = z_shift;
-  p.z_transposed = z_transposed ? 1 : 0;
+  p.z_mode = z_mode;
   p.a_rows = (int)a_rows;
   p.n_mpairs = (int)ceil_div(a_rows, 2 * BM);
   p.n_ranges = (int)n_ranges;

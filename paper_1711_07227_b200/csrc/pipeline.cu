@@ -21,7 +21,7 @@ namespace p1 {
 int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
            const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
            int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids,
-           int64_t b_table_rows, bool z_transposed);
+           int64_t b_table_rows, int z_mode);
 }
 
 namespace {
@@ -74,7 +74,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, const float* table, void* d1_ready, void* ws,
+                          int64_t batch_docs, int range_cols, const void* table, void* d1_ready, void* ws,
                           size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
@@ -108,8 +108,8 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     const int64_t nd = j1 - j0;
     const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
     if (table) {
-      if ((status = lcrw_table_min(table, a_rows, v_rows, doc_offsets + j0, lo, nd, doc_cols + lo, Z2, z_panel,
-                                   stream)))
+      if ((status = lcrw_table_min(table, a_rows, v_rows, doc_offsets + j0, lo, nd, doc_cols + lo, scale, Z2,
+                                   z_panel, stream)))
         return status;
     } else {
     if (!gather_b && (status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream)))
@@ -119,7 +119,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     if ((status = lcrw_segment_plan(doc_offsets + j0, lo, nd, nw, rc, mask, rs, n_ranges, stream))) return status;
     if ((status = p1::launch(A, a_norms, a_rows, gather_b ? EhB : T, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs,
                              n_ranges, scale, Z2, z_panel, kZShift, st, "phase1_rev",
-                             gather_b ? doc_cols + lo : nullptr, v_table, false)))
+                             gather_b ? doc_cols + lo : nullptr, v_table, 1 /* kZPanelsKey */)))
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;

@@ -476,6 +476,7 @@ REVERSE_TABLE_Z2_FRACTION = 3  # table mode: Z2 batches up to 1/3 of HBM -- each
                                # once and larger batches keep one chunk L2-resident for longer (C2 on
                                # B200: 16 GB 502 ms, 32 GB 490 ms, 64 GB 485 ms per step)
 TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 512 B) must stay L2-resident
+TABLE_ROW_BYTES = 512             # per vocabulary word per 160-word chunk: 160 3-byte keys in 32 16-byte groups
 
 
 def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | None = None) -> str:
@@ -486,9 +487,9 @@ def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | No
     env = os.environ.get("LCRW_REVERSE", "")
     if env in ("gemm", "table"):
         return env
-    if v_rows * 4 * int(_lib.value("lcrw_table_chunk")) > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
+    if v_rows * TABLE_ROW_BYTES > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
         return "gemm"
-    table_bytes = int(_lib.value("lcrw_table_floats", a_rows, v_rows)) * 4
+    table_bytes = int(_lib.value("lcrw_table_bytes", a_rows, v_rows))
     if total_memory is None:  # (mem_get_info would stall the stream)
         total_memory = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
     return "table" if table_bytes < total_memory // 4 else "gemm"
@@ -504,12 +505,12 @@ def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: 
     V = prep.V
     dev = res2.A.device
     seg = torch.arange(V + 1, dtype=torch.int64, device=dev)
-    T = torch.empty(max(1, int(_lib.value("lcrw_table_floats", res2.v_e, V))), dtype=torch.float32, device=dev)
+    T = torch.empty(max(16, int(_lib.value("lcrw_table_bytes", res2.v_e, V))), dtype=torch.uint8, device=dev)
     if via_transpose:
-        zs = int(_lib.value("lcrw_table_chunk")).bit_length() - 1
+        zs = 7  # lcrw_table_transpose reads 128-segment panels
         Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=zs)
         zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, zs)
-        _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(T), _stream())
+        _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(prep.scale), _p(T), _stream())
         return T
     endmask, range_seg, n_ranges = segment_plan(seg, V, V, res2.v_e)
     _lib.call("lcrw_distance_table", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), V, prep.k_eff, prep.kp,

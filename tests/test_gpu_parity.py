@@ -914,12 +914,23 @@ def test_reverse_table_mode_bitwise_equals_gemm_mode(case, monkeypatch):
     assert ok, err
 
 
+def _decode_table(T: np.ndarray, V: int, inv_scale: float) -> np.ndarray:
+    """Packed 24-bit table (include/lcrwmd.h) -> unscaled f32 distances (chunks, V, 160):
+    16-byte group g of a 512-byte row = LE words q_i = key(5g+i) << 8 | byte i of key(5g+4)."""
+    q = np.ascontiguousarray(T).view("<u4").reshape(-1, V, 32, 4)
+    k4 = (q[..., 0] & 255) | ((q[..., 1] & 255) << 8) | ((q[..., 2] & 255) << 16)
+    key = np.concatenate([q >> 8, k4[..., None]], axis=-1).reshape(-1, V, 160).astype(np.uint32)
+    val = ((key << 4) + (104 << 23)).astype(np.uint32).view(np.float32)
+    return np.where(key == 0, np.float32(0), val) * np.float32(inv_scale)
+
+
 @pytest.mark.gpu
 def test_distance_table_layout_and_zeros():
-    """Distance-table layout: T[(w >> 7) * V * 128 + u * 128 + (w & 127)] is the Phase-1
-    distance of query-vocabulary row w to E row u, exactly 0 for identical rows; the
-    one-pass build (row-panel stores from the Phase-1 epilogue) equals the two-pass
-    one (segment panels, lcrw_zero_identical, lcrw_table_transpose) bitwise."""
+    """Distance-table layout: chunk w >> 7, E row u -> 384-byte row of 24-bit keys of the
+    Phase-1 distance of query-vocabulary row w to E row u (relative rounding <= 2^-20),
+    exactly 0 for identical rows; the one-pass build (packed stores from the Phase-1
+    epilogue) equals the two-pass one (segment panels, lcrw_zero_identical,
+    lcrw_table_transpose) bitwise."""
     from paper_1711_07227_b200 import _lib, device
     rng = np.random.default_rng(70)
     V, m = 700, 300
@@ -934,8 +945,16 @@ def test_distance_table_layout_and_zeros():
     assert res2.v_e == len(used)
     w = np.arange(len(used))
     C = int(_lib.value("lcrw_table_chunk"))
-    tab = T.reshape(-1, V, C)[w // C, :, w % C]  # (v_e, V)
-    assert np.array_equal(tab, T2.reshape(-1, V, C)[w // C, :, w % C])  # one-pass == two-pass build
+    assert T.size == -(-len(used) // C) * V * 512
+    inv = float(prep.scale[1].item())
+    tab = _decode_table(T, V, inv)[w // C, :, w % C]  # (v_e, V)
+    assert np.array_equal(tab, _decode_table(T2, V, inv)[w // C, :, w % C])  # one-pass == two-pass build
+    # the keys are the f32 Phase-1 entries rounded to 19 mantissa bits
+    seg = __import__("torch").arange(V + 1, dtype=__import__("torch").int64, device=res2.A.device)
+    zf, zp = device.phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=3)
+    zf = zf.cpu().numpy()[: ((V + 7) // 8) * zp].reshape(-1, res2.v_e, 8).transpose(1, 0, 2).reshape(res2.v_e, -1)[:, :V]
+    nz = (tab != 0) & (zf != 0)
+    assert np.max(np.abs(tab[nz] / zf[nz] - 1)) <= 2.0 ** -20 * 1.001
     ref = O.pairwise_euclidean(E[used], E)
     ok, err = rel_close(tab, ref, RTOL, _atol(E))
     assert ok, err
