@@ -346,11 +346,12 @@ def run_ours(args, cfg):
     rev_flops = 2.0 * v_e2 * x1s.nnz * cfg["dim"]
     fwd_flops = 2.0 * int(np.unique(x1s.column_ids).size) * x2.nnz * cfg["dim"]
     table_flops = 2.0 * v_e2 * cfg["vocab"] * cfg["dim"]
-    # table_min gathers, per doc word and 160-word table chunk, one 512-byte row of 3-byte keys
-    # (3.2 B per (query-vocabulary word, doc word) distance) and writes one 4-byte Z2 entry per
+    # table_min gathers, per doc word and 180-word table chunk, one 480-byte row of 21-bit keys
+    # (2.67 B per (query-vocabulary word, doc word) distance) and writes one 4-byte Z2 entry per
     # (query-vocabulary word, doc)
-    n_chunks = -(-v_e2 // 160)
-    table_bytes = 512.0 * n_chunks * x1s.nnz + 4.0 * v_e2 * x1s.n_rows
+    from paper_1711_07227_b200 import _lib as _L, device as _dev
+    n_chunks = -(-v_e2 // int(_L.value("lcrw_table_chunk")))
+    table_bytes = float(_dev.TABLE_ROW_BYTES) * n_chunks * x1s.nnz + 4.0 * v_e2 * x1s.n_rows
     table_entries = float(v_e2) * x1s.nnz
     spmm_bytes = 8.0 * (x1s.n_rows + 1) + 8.0 * x1s.nnz + 4.0 * x1s.nnz * n2
     # reverse_panels streams every Z2 panel once (4 * v_e2 bytes per doc), reads D1 and writes D
@@ -382,7 +383,7 @@ def run_ours(args, cfg):
                      "achieved": p1_work / (p1_ms * 1e-3) / 1e12 if p1_ms else None, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": p1_work / (p1_ms * 1e-3) / 1e12 / peak_tf if p1_ms else None,
                      "note": "algorithmic 2*rows*cols*m FLOP of the Phase-1 GEMMs launched per step; the table "
-                             "build is store-bound (15.7 GB of table at C2), the GEMM-path reverse Phase 1 "
+                             "build is store-bound (10.5 GB of table at C2), the GEMM-path reverse Phase 1 "
                              "(--reverse gemm) runs at 0.93-0.97 of the sustained peak"}
     if table_mode:  # dominant kernel: the distance-table gathers, bound by L2 bandwidth
         tm = ksum["table_min"]
@@ -390,8 +391,8 @@ def run_ours(args, cfg):
         l2path = ROOT / "profiles" / "l2_gather_peak.json"
         l2 = json.loads(l2path.read_text()) if l2path.exists() else {"gbs": float("nan"), "source": "missing"}
         tr = traffic_all.get("table_min_kernel")
-        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 512-B rows of 24-bit keys of "
-                              "an L2-resident 160-word distance-table chunk)",
+        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 480-B rows of 21-bit keys of "
+                              "an L2-resident 180-word distance-table chunk)",
                     "bound": "l2", "achieved": achieved, "peak": l2["gbs"], "unit": "GB/s",
                     "frac": achieved / l2["gbs"],
                     "traffic": tr["dram_bytes_per_launch"] if tr else None,

@@ -153,15 +153,24 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
  * Warp w's list is entries [end[w-1], end[w]); a warp owns the queries with
  * (q - g*G) % W == w, so accumulation order is deterministic.  Every list
  * holds a multiple of I = lcrw_reverse_panels_ilp() entries and each aligned
- * group of I entries names I distinct queries; padding entries use query G
- * (a scratch row) with weight 0. */
+ * group of I entries names I distinct queries; padding entries of warp w's
+ * list use query G + w (that warp's scratch row) with weight 0. */
 int lcrw_reverse_panels_tile_rows(void);
 int lcrw_reverse_panels_group(void);
 int lcrw_reverse_panels_warps(void);
 int lcrw_reverse_panels_ilp(void);
 int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs, int64_t doc_base,
                         const uint32_t* e_blk, const int64_t* e_tile, int64_t n_q, const float* D1,
-                        int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, void* stream);
+                        int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, float* top_d, int64_t* top_i,
+                        int k, int64_t id_base, void* stream);
+/* Fused max -> top-k (top_d != NULL, D may be NULL; 1 <= k <= 32): instead of
+ * writing D, each CTA keeps the k smallest (distance, id_base + doc_base + j)
+ * per query in list slot blockIdx.x: top_d / top_i [n_q][S][k] with S =
+ * lcrw_reverse_panels_top_slots(), ascending (distance, id); initialise every
+ * entry to (+inf, INT64_MAX) once per query set (the lists carry over between
+ * doc batches), then lcrw_topk_segments(top_d, top_i, n_q, S * k, k, ...)
+ * gives the per-query top-k of max(D1, D2) without materialising D. */
+int lcrw_reverse_panels_top_slots(void);
 
 /* All-pairs symmetric combine (X1 == X2, distances.py:264 with the reverse
  * direction equal to the transposed forward one): D = max(D, D^T) in place for
@@ -193,7 +202,9 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
  * lcrw_distance_table for these a_rows query-vocabulary rows and the v_rows E
  * rows; each batch's Z2 is then one lcrw_table_min (gather, plan, phase1 and
  * zeros are skipped; rep, next, remap, EhB may be NULL).  In GEMM mode Z2 is
- * rounded through the table's 24-bit key, so both modes give the same D. */
+ * rounded through the table's 21-bit key, so both modes give the same D.
+ * E32 (v_rows x dim f32, unscaled) and a_ids (E id of each A row) feed the
+ * exact re-evaluation of near Z2 entries (lcrw_refine_near, list mode). */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                           int m, int kp,
@@ -201,29 +212,34 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, const void* table, void* d1_ready, void* ws,
-                          size_t ws_bytes, void* stream);
+                          float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols,
+                          const void* table, const float* E32, int dim,
+                          const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- distance-table reverse Phase 1 (table.cu) ---------------------------
  * When nnz(X1) >> V, every (w, u) distance of the reverse Phase 1 is needed
- * ~nnz/V times; the table holds each once, as a 24-bit order-preserving key of
- * the scaled distance (5 exponent + 19 mantissa bits, round to nearest:
- * relative error <= 2^-20; 0 stays 0 -- common.cuh dist_key24):
- *   chunk c = w >> 7 of 128 query-vocabulary words, per E row u one 384-byte
- *   row at byte ((c * v_rows) + u) * 384: 128 x u16 (key >> 8) then
- *   128 x u8 (key & 255);  lcrw_table_bytes(a_rows, v_rows) bytes,
+ * ~nnz/V times; the table holds each once, as a 21-bit order-preserving key of
+ * the scaled distance (5 exponent + 16 mantissa bits, round to nearest:
+ * relative error <= 2^-17; 0 stays 0 -- common.cuh dist_key21):
+ *   chunk c = w / 180 of 180 query-vocabulary words, per E row u one 480-byte
+ *   row at byte ((c * v_rows) + u) * 480: 30 16-byte groups of six keys
+ *   (layout in common.cuh);  lcrw_table_bytes(a_rows, v_rows) bytes,
  * with exact zeros for identical rows.
- * lcrw_distance_table builds it in one pass: lcrw_phase1 over the a_rows
- * query-vocabulary A rows and ALL v_rows E rows (EhB) as singleton segments
+ * lcrw_distance_table builds it in one pass: lcrw_phase1 over the query-
+ * vocabulary A rows and ALL v_rows E rows (EhB) as singleton segments
  * (seg_offsets = 0..v_rows and its lcrw_segment_plan), storing packed rows
  * directly (the same entries lcrw_phase1 computes in the GEMM form), then the
  * zeros (canon/next classes of lcrw_row_classes, remap = E id -> A row or -1).
+ * A / a_norms are PADDED: lcrw_table_operand_rows(a_rows) rows, row
+ * 32 * (r / 30) + r % 30 holding query-vocabulary row r (rows 30, 31 of each
+ * 32 are ignored), so each warp of the epilogue stores whole 16-byte groups.
  * lcrw_table_transpose builds the same table from lcrw_phase1's z_shift-7 f32
  * output Tp (unscaled; zeros already applied) and scale (cross-check path).
  * lcrw_table_min: Z2[p * z_panel + w * 32 + (d & 31)] = min over the words u of
  * doc d of T[w, u], decoded and unscaled (32-doc panels, z_panel = 32 * a_rows;
  * docs as lcrw_phase1's segments: doc_offsets[d] - seg_base .. into doc_cols,
- * E ids < v_rows).  The GEMM form of the reverse pass rounds its Z2 through the
+ * E ids < v_rows); with refine_list != NULL it appends every near entry (w, d)
+ * (lcrw_refine_near's test on the decoded value, a_norms of the A rows).  The GEMM form of the reverse pass rounds its Z2 through the
  * same key, so both forms give identical Z2. */
 int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                         int m, int kp, const int64_t* seg_offsets, const uint32_t* endmask, const int32_t* range_seg,
@@ -231,11 +247,30 @@ int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows,
                         const int32_t* remap, void* T, void* stream);
 int lcrw_table_chunk(void);
 int64_t lcrw_table_bytes(int64_t a_rows, int64_t v_rows);
+int64_t lcrw_table_operand_rows(int64_t a_rows);
 int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const float* scale, void* T,
                          void* stream);
 int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
                    int64_t n_docs, const int32_t* doc_cols, const float* scale, float* Z2, int64_t z_panel,
+                   const float* a_norms, void* refine_list, uint32_t* refine_count, int64_t refine_cap,
                    void* stream);
+
+/* ---- exact re-evaluation of near entries (refine.cu) ---------
+ * The Gram expansion's error scales with the operand norms, so an entry whose
+ * scaled distance d satisfies 0 < d < tau * |a| (tau = lcrw_refine_tau() = 0.5,
+ * |a|^2 = a_norms[row], the A row's scaled squared norm) is recomputed as
+ * min over its segment's words b of sqrt(sum_k (A32[a_ids[row]]_k - B32[b]_k)^2)
+ * (f32 rows, unscaled, direct differences, fixed order).  Z is lcrw_phase1's
+ * panel layout (z_panel, z_shift) of a_rows x n_seg entries; segment s holds
+ * B rows seg_ids[seg_offsets[s] - seg_base ..].  list == NULL: every entry is
+ * tested (scan).  Otherwise list/count hold the (row, segment) uint32 pairs a
+ * producer flagged (lcrw_table_min, the reverse pipeline's Phase 1) and only
+ * those are recomputed -- unless *count > cap, in which case it scans. */
+float lcrw_refine_tau(void);
+int lcrw_refine_near(float* Z, int64_t z_panel, int z_shift, int64_t a_rows, int64_t n_seg,
+                     const int64_t* seg_offsets, int64_t seg_base, const int32_t* seg_ids, const float* A32,
+                     const int32_t* a_ids, const float* B32, int m, const float* a_norms, const float* scale,
+                     const void* list, const uint32_t* count, int64_t cap, void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k

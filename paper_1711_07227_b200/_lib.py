@@ -48,12 +48,15 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
-                                    I64, I64, I32, P, P, P, SZ, P]),
+                                    I64, P, P, I32, I64, I64, I32, P, P, I32, P, P, P, SZ, P]),
     "lcrw_table_chunk": (I32, []),
     "lcrw_table_bytes": (I64, [I64, I64]),
+    "lcrw_table_operand_rows": (I64, [I64]),
     "lcrw_table_transpose": (I32, [P, I64, I64, P, P, P]),
     "lcrw_distance_table": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P]),
-    "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, P, I64, P]),
+    "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, P, I64, P, P, P, I64, P]),
+    "lcrw_refine_tau": (C.c_float, []),
+    "lcrw_refine_near": (I32, [P, I64, I32, I64, I64, P, I64, P, P, P, P, I32, P, P, P, P, I64, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),
     "lcrw_max_transposed_into": (I32, [P, I64, P, I64, P, I64, I64, I64, P]),
@@ -61,7 +64,8 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_reverse_panels_group": (I32, []),
     "lcrw_reverse_panels_warps": (I32, []),
     "lcrw_reverse_panels_ilp": (I32, []),
-    "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, I64, P, I64, P, I64, I64, P]),
+    "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, I64, P, I64, P, I64, I64, P, P, I32, I64, P]),
+    "lcrw_reverse_panels_top_slots": (I32, []),
     "lcrw_topk_rows_workspace": (I32, [I64, I64, I32, P]),
     "lcrw_emd_problem_bytes": (SZ, [I32, I32]),
     "lcrw_emd_batch": (I32, [P, P, P, P, P, P, P, I64, I32, P, P, I64, I32, I32, P, P, P, P, P]),
@@ -83,7 +87,9 @@ SIGNATURES: dict[str, tuple] = {
 _VALUE_FUNCS = {"lcrw_emd_problem_bytes", "lcrw_abi_version", "lcrw_status_string", "lcrw_last_error", "lcrw_padded_dim", "lcrw_operand_k",
                 "lcrw_endmask_words", "lcrw_plan_ranges", 
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
-                "lcrw_reverse_panels_ilp", "lcrw_profile_count", "lcrw_table_chunk", "lcrw_table_bytes"}
+                "lcrw_reverse_panels_ilp", "lcrw_profile_count", "lcrw_table_chunk", "lcrw_table_bytes",
+                "lcrw_table_operand_rows", "lcrw_refine_tau",
+                "lcrw_reverse_panels_top_slots"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".
@@ -95,13 +101,13 @@ KERNELS_PER_CALL = {
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
     "lcrw_max_transposed_into": 1, "lcrw_table_transpose": 1, "lcrw_table_min": 1,
     "lcrw_distance_table": 2, "lcrw_topk_sort_any": 7, "lcrw_squared_norms": 1, "lcrw_euclidean_f64": 1,
-    "lcrw_segmented_min": 1,
+    "lcrw_segmented_min": 1, "lcrw_refine_near": 1,
 }
-# lcrw_reverse_pipeline launches 6 kernels per doc batch (gather, 2 plan, phase1, zeros, reverse_panels)
-# in GEMM mode, 2 (table_min, reverse_panels) with a distance table; bench.py adds those from the
-# batch count (= its reverse_panels launches).
-REVERSE_KERNELS_PER_BATCH = 6
-REVERSE_KERNELS_PER_BATCH_TABLE = 2
+# lcrw_reverse_pipeline launches 7 kernels per doc batch (gather, 2 plan, phase1, zeros, refine,
+# reverse_panels) in GEMM mode, 3 (table_min, refine, reverse_panels) with a distance table; bench.py
+# adds those from the batch count (= its reverse_panels launches).
+REVERSE_KERNELS_PER_BATCH = 7
+REVERSE_KERNELS_PER_BATCH_TABLE = 3
 
 CALLS: dict[str, int] = {}
 

@@ -311,43 +311,76 @@ __device__ __forceinline__ float key_float(uint32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// 24-bit distance keys of the reverse direction (table.cu).
+// 21-bit distance keys of the reverse direction (table.cu).
 // A distance d in the scaled operand space (0 <= d < 2^8: every scaled row has
-// |x'| < 2^7) is stored as an order-preserving 24-bit key: 5 exponent bits
-// relative to 2^-23 and 19 mantissa bits, rounded to nearest (relative error
-// <= 2^-20 ~ 9.5e-7); 0 -> 0 (exact zeros stay exact), 0 < d < 2^-22 -> 1.
+// |x'| < 2^7) is stored as an order-preserving 21-bit key: 5 exponent bits
+// relative to 2^-23 and 16 mantissa bits, rounded to nearest (relative error
+// <= 2^-17 ~ 7.6e-6); 0 -> 0 (exact zeros stay exact), 0 < d < 2^-22 -> 1.
 // Keys compare as integers, so min over keys == key of the min, and the table
 // form and the GEMM form of the reverse Phase 1 round identically.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kKeyExpBase = 104u;  // f32 biased exponent of 2^-23
-__device__ __forceinline__ uint32_t dist_key24(float d) {
+constexpr uint32_t kKeyMax = (1u << 21) - 1u;
+__device__ __forceinline__ uint32_t dist_key21(float d) {
   const uint32_t b = __float_as_uint(d);
   if (b < ((kKeyExpBase + 1u) << 23)) return b == 0u ? 0u : 1u;
-  return (b - (kKeyExpBase << 23) + 8u) >> 4;
+  const uint32_t k = (b - (kKeyExpBase << 23) + 64u) >> 7;
+  return k < kKeyMax ? k : kKeyMax;
 }
-__device__ __forceinline__ float key24_dist(uint32_t key) {
-  return key ? __uint_as_float((key << 4) + (kKeyExpBase << 23)) : 0.f;
+__device__ __forceinline__ float key21_dist(uint32_t key) {
+  return key ? __uint_as_float((key << 7) + (kKeyExpBase << 23)) : 0.f;
 }
-// packed table rows: 160 query-vocabulary words per chunk, per vocabulary word u one
-// 512-byte row of 32 16-byte groups (one 16-byte load per lane per row in table_min,
-// 3.2 bytes per distance).  Group g = four little-endian 32-bit words q0..q3 holding
-// words 5g .. 5g+4 of the chunk:
-//   q_i = key(5g + i) << 8 | byte i of key(5g + 4)      (i = 0, 1, 2; q3's low byte 0)
-// so the min of q_i over rows has key(5g + i) in its top 24 bits (no unpacking), and
-// key(5g + 4) is reassembled from the low bytes with two byte permutes.
-constexpr int kTableChunk = 160;
-constexpr int kTableKeysPerGroup = 5;
-constexpr int kTableRowBytes = 512;
-// the three bytes (low to high) of word p's key inside its row: b0, b0 + step, b0 + 2 step
-__host__ __device__ __forceinline__ void table_key_bytes(int p, int64_t& b0, int& step) {
-  const int g = p / kTableKeysPerGroup, i = p % kTableKeysPerGroup;
-  if (i < 4) {
-    b0 = 16 * g + 4 * i + 1;
-    step = 1;
-  } else {
-    b0 = 16 * g;
-    step = 4;
-  }
+// Near-entry refinement (refine.cu): a Z entry whose scaled distance d satisfies
+// 0 < d < kRefineTau * |a| (|a|^2 = the A row's scaled squared norm) is recomputed
+// exactly from the f32 rows.  The test always reads the stored (unscaled) Z value times
+// the power-of-two scale, so table_min's list and the GEMM form's scan of the same Z2
+// flag the same entries.
+constexpr float kRefineTau = 0.5f;
+__device__ __forceinline__ bool refine_flag(float d_scaled, float a_sq, float tau2) {
+  return d_scaled > 0.f && d_scaled * d_scaled < tau2 * a_sq;
 }
+// where a reverse-pass producer appends the (row, segment) pairs it flags
+struct RefineSink {
+  uint2* list;
+  uint32_t* count;
+  int64_t cap;
+};
+// append (row, segment) to a refine list (reverse pass); entries past the capacity are
+// dropped and the count still grows, which sends lcrw_refine_near to its full scan
+__device__ __forceinline__ void refine_append(uint2* list, uint32_t* count, int64_t cap, uint32_t row, uint32_t seg) {
+  const uint32_t i = atomicAdd(count, 1u);
+  if ((int64_t)i < cap) list[i] = make_uint2(row, seg);
+}
+// Packed table rows: 180 query-vocabulary words per chunk; per vocabulary word u one
+// 480-byte row of 30 16-byte groups (one 16-byte load per lane of lanes 0..29 per
+// row in table_min: 2.67 bytes per distance).  Group g = four little-endian 32-bit
+// words q0..q3 holding words 6g .. 6g+5 of the chunk:
+//   q_i = key(6g + i) << 11 | piece_i      (i = 0..3)
+//   piece_0 = key(6g+4) >> 10,  piece_1 = (key(6g+4) & 0x3FF) << 1,
+//   piece_2 = key(6g+5) >> 10,  piece_3 = (key(6g+5) & 0x3FF) << 1
+// so the min of q_i over rows has key(6g + i) in its top 21 bits (no unpacking), and
+// key(6g+4) << 11 == funnelshift_l(q1 << 21, q0, 21) (likewise key(6g+5) from q2, q3).
+// The table build (phase1 epilogue, kZTable) runs on query-vocabulary rows padded to
+// 30 real rows per 32 (lcrw_table_rows): a warp's 30 rows are 5 whole groups, which it
+// assembles with one shuffle and stores as 80 contiguous bytes.
+constexpr int kTableChunk = 180;
+constexpr int kTableKeysPerGroup = 6;
+constexpr int kTableGroups = 30;
+constexpr int kTableRowBytes = 480;
+constexpr int kTableWarpRows = 30;  // real rows per 32-row warp block of the padded operand
+// word q_i of key p's group inside a row: byte offset of the group and the key's slot i
+__host__ __device__ __forceinline__ void table_key_slot(int p, int& group_byte, int& slot) {
+  group_byte = 16 * (p / kTableKeysPerGroup);
+  slot = p % kTableKeysPerGroup;
+}
+
+namespace p1 {
+// the tcgen05 Phase-1 GEMM with fused segmented-min epilogue (phase1.cu)
+int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp,
+           const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg, const uint32_t* endmask,
+           const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift,
+           cudaStream_t stream, const char* tag, const int32_t* b_ids = nullptr, int64_t b_table_rows = 0,
+           int z_mode = 0);
+}  // namespace p1
 
 }  // namespace lcrw

@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       st = 1;
       break;
     }
+    __syncwarp();  // every lane's Dijkstra reads of phis precede the potential update (WAR)
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j) {
       const int i = lane + 32 * j;

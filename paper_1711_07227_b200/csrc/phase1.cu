@@ -70,9 +70,10 @@ constexpr int kStreamStages = 6;              // streamed A: ring stages of (A +
 // output forms of the epilogue
 enum ZMode : int {
   kZPanels = 0,     // f32 Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))] (segment panels)
-  kZPanelsKey = 1,  // the same, values rounded through the 24-bit key (reverse direction, GEMM form)
-  kZTable = 2,      // packed 24-bit distance table (kTableChunk-row chunks, kTableRowBytes per
-                    // segment = vocabulary word; z_panel = bytes per chunk)
+  kZPanelsKey = 1,  // the same, values rounded through the 21-bit key (reverse direction, GEMM form)
+  kZTable = 2,      // packed 21-bit distance table (kTableChunk-word chunks, kTableRowBytes per
+                    // segment = vocabulary word; z_panel = bytes per chunk); A rows padded to
+                    // 30 real rows per 32-row warp block (common.cuh)
 };
 
 struct Params {
@@ -442,21 +443,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float nE = valid ? __ldg(p.a_norms + row) : 0.f;
       // output cursor: segment s = U.sb(grp) + emitted so far, at
       //   Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))]   (segment panels), or
-      //   packed table bytes (row / 160) * z_panel + s * 512 + table_key_bytes(row % 160)
-      //   (kZTable: a warp's 32 rows of one segment write within ~100 contiguous bytes)
+      //   packed table bytes: chunk (row / 192) of the padded rows, row s of 480 bytes,
+      //   group 5 (row % 192) / 32 + lane / 6, word lane % 6 (< 4) -- lanes 0..29 of a warp
+      //   hold 5 whole groups, so each segment's store is 80 contiguous bytes of the row
       const int64_t s_first = U.sb(grp);
       float* zq;
       int64_t step, wrap;
       uint32_t s_in = (uint32_t)s_first & (zw - 1);
       uint8_t* zb = nullptr;
-      int kstep = 1;
+      const int t_slot = lane % kTableKeysPerGroup;
+      const int t_src = lane < kTableWarpRows ? lane - t_slot + 4 + (t_slot >> 1) : lane;  // its piece's key
+      const bool t_store = lane < kTableWarpRows && t_slot < 4 && valid;
       if (p.z_mode == kZTable) {
         zq = nullptr;
         step = wrap = 0;
-        int64_t kb0;
-        table_key_bytes(row % kTableChunk, kb0, kstep);
-        zb = reinterpret_cast<uint8_t*>(p.Z) + ((int64_t)row / kTableChunk) * p.z_panel +
-             s_first * kTableRowBytes + kb0;
+        const int wb = (row % (kTableChunk / kTableWarpRows * 32)) >> 5;  // warp block inside the chunk
+        zb = reinterpret_cast<uint8_t*>(p.Z) + ((int64_t)row / (kTableChunk / kTableWarpRows * 32)) * p.z_panel +
+             s_first * kTableRowBytes + (wb * (kTableWarpRows / kTableKeysPerGroup) + lane / kTableKeysPerGroup) * 16 +
+             t_slot * 4;
       } else {
         zq = p.Z + (s_first >> zs) * p.z_panel + ((int64_t)row << zs) + s_in;
         step = 1;
@@ -470,16 +474,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (d < -1.f)  // experiment: never true -- the global store is skipped
 #endif
         if (p.z_mode == kZTable) {
-          const uint32_t key = dist_key24(d);
-          if (valid) {
-            zb[0] = (uint8_t)key;
-            zb[kstep] = (uint8_t)(key >> 8);
-            zb[2 * kstep] = (uint8_t)(key >> 16);
-          }
+          const uint32_t key = dist_key21(d);
+          const uint32_t pk = __shfl_sync(0xffffffffu, key, t_src);
+          const uint32_t piece = (t_slot & 1) ? (pk & 0x3FFu) << 1 : pk >> 10;
+          if (t_store) *reinterpret_cast<uint32_t*>(zb) = key << 11 | piece;
           zb += kTableRowBytes;
           return;
         }
-        if (p.z_mode == kZPanelsKey) d = key24_dist(dist_key24(d));
+        if (p.z_mode == kZPanelsKey) d = key21_dist(dist_key21(d));
         if (valid) *zq = d * inv_scale;
         zq += step;
         if (++s_in == zw) {
@@ -620,17 +622,17 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int kp, int box_r
 namespace lcrw {
 namespace p1 {
 
-int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
-           const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
-           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids = nullptr,
-           int64_t b_table_rows = 0, int z_mode = kZPanels) {
+int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp,
+           const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg, const uint32_t* endmask,
+           const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift,
+           cudaStream_t stream, const char* tag, const int32_t* b_ids, int64_t b_table_rows, int z_mode) {
   LCRW_REQUIRE(m > 0 && kp == lcrw_padded_dim(m), "lcrw_phase1: kp must be lcrw_padded_dim(K)");
   LCRW_REQUIRE(a_rows >= 0 && a_rows < (1ll << 31) && b_rows >= 0 && b_rows < (1ll << 31),
                "lcrw_phase1: row counts must fit in int32");
   LCRW_REQUIRE(n_seg >= 0 && n_ranges >= 1, "lcrw_phase1: bad segment plan");
   LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10, "lcrw_phase1: z_shift out of range");
   LCRW_REQUIRE(z_mode == kZTable ? z_panel >= n_seg * kTableRowBytes : z_panel >= (a_rows << z_shift),
-               "lcrw_phase1: z_panel must be >= a_rows << z_shift (packed table: n_seg * 384 bytes)");
+               "lcrw_phase1: z_panel must be >= a_rows << z_shift (packed table: n_seg * kTableRowBytes)");
   if (a_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(A && a_norms && B && seg_offsets && endmask && range_seg && scale && Z,
                "lcrw_phase1: null pointer");

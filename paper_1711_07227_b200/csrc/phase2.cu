@@ -87,6 +87,49 @@ constexpr int kRpIlp = 4;        // entries per independent group (plan invarian
 constexpr int kRpBlkWords = 512;   // staged plan block per tile: 16 list ends + up to 248 entries (2 KB)
 constexpr int kRpBlkEntries = (kRpBlkWords - kRpWarps) / 2;
 
+// Fused max -> top-k of lcrw_reverse_panels: per (query, CTA slot) a sorted list of the k
+// smallest (distance, id) seen so far, lists [q][slot][k] (d and i arrays), merged at the end
+// by lcrw_topk_segments (kernels.py:210-232 order: ascending distance, then id).
+struct TopLists {
+  float* d;
+  int64_t* i;
+  int k;          // 1 .. 32
+  int slots;      // list slots per query (>= grid)
+  int64_t id_base;
+};
+constexpr float kInfF = __builtin_huge_valf();
+
+// Inserts the candidates of ballot b (lane values v, ids id) into list `li` (entries
+// li * k ..), held across lanes 0..k-1 while merging; returns the new k-th distance.
+__device__ __forceinline__ float top_insert(const TopLists& t, int64_t li, uint32_t b, float v, int64_t id,
+                                            int lane) {
+  float* ld = t.d + li * t.k;
+  int64_t* lid = t.i + li * t.k;
+  const bool own = lane < t.k;
+  float cur_d = own ? ld[lane] : kInfF;
+  int64_t cur_i = own ? lid[lane] : INT64_MAX;
+  while (b) {
+    const int src = __ffs(b) - 1;
+    b &= b - 1u;
+    const float cd = __shfl_sync(0xffffffffu, v, src);
+    const int64_t ci = __shfl_sync(0xffffffffu, id, src);
+    // position = number of list entries ordered before the candidate
+    const bool before = own && (cur_d < cd || (cur_d == cd && cur_i < ci));
+    const int pos = __popc(__ballot_sync(0xffffffffu, before));
+    const float up_d = __shfl_up_sync(0xffffffffu, cur_d, 1);
+    const int64_t up_i = __shfl_up_sync(0xffffffffu, cur_i, 1);
+    if (pos < t.k && lane >= pos) {
+      cur_d = lane == pos ? cd : up_d;
+      cur_i = lane == pos ? ci : up_i;
+    }
+  }
+  if (own) {
+    ld[lane] = cur_d;
+    lid[lane] = cur_i;
+  }
+  return __shfl_sync(0xffffffffu, cur_d, t.k - 1);
+}
+
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -95,16 +138,18 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
     reverse_panels_kernel(const float* __restrict__ Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs,
                           int64_t doc_base, const uint32_t* __restrict__ e_blk, const int64_t* __restrict__ e_tile,
                           int n_tiles, int64_t n_q, const float* __restrict__ D1, int64_t d1_ld_panel,
-                          float* __restrict__ D, int64_t ld_q, int64_t ld_doc, int64_t n_panels, int64_t n_items) {
+                          float* __restrict__ D, int64_t ld_q, int64_t ld_doc, int64_t n_panels, int64_t n_items,
+                          TopLists top) {
   extern __shared__ __align__(16) float rp_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  float* acc = rp_smem;                                                  // [kRpGroup + 1][32] (+1: padding row)
-  float* tiles = acc + (kRpGroup + 1) * 32;                              // [kRpStages][kRpTile][32]
+  float* acc = rp_smem;            // [kRpGroup + kRpWarps][32] (+ one scratch row per warp for padding entries)
+  float* tiles = acc + (kRpGroup + kRpWarps) * 32;                              // [kRpStages][kRpTile][32]
   uint32_t* blks = reinterpret_cast<uint32_t*>(tiles + kRpStages * kRpTile * 32);  // [kRpStages][kRpBlkWords]
   uint64_t* full = reinterpret_cast<uint64_t*>(blks + kRpStages * kRpBlkWords);
   uint64_t* empty = full + kRpStages;
-  for (int i = threadIdx.x; i < (kRpGroup + 1) * 32; i += blockDim.x) acc[i] = 0.f;
+  float* thr = reinterpret_cast<float*>(empty + kRpStages);  // [kRpGroup] top-k mode: k-th distance per query
+  for (int i = threadIdx.x; i < (kRpGroup + kRpWarps) * 32; i += blockDim.x) acc[i] = 0.f;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRpStages; ++i) {
       mbar_init(full + i, 1);
@@ -162,6 +207,7 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
   // ---- consumers ----
   // stage / phase tracked incrementally (no div/mod by kRpStages per tile)
   uint32_t st = 0, ph = 0;
+  int64_t top_g = -1;  // query group whose thresholds are in thr
   const char* acc_lane = reinterpret_cast<const char*>(acc + lane);
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int64_t p = item % n_panels;
@@ -211,6 +257,44 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
     const int64_t j = p * 32 + lane;
     const bool valid = j < n_docs;
     const int64_t jg = doc_base + j;
+    if (top.d) {
+      // fused max -> top-k (no D): this CTA's running k best per query (its list slot), the
+      // k-th distance cached in smem; a warp owns its queries, so no two warps touch a list
+      if (g != top_g) {
+        for (int ql = warp * 32 + lane; ql < nq; ql += kRpWarps * 32)
+          thr[ql] = top.d[((q0 + ql) * top.slots + blockIdx.x) * top.k + top.k - 1];
+        top_g = g;
+        named_bar_sync(1, kRpWarps * 32);
+      }
+      for (int qp = warp; qp * 8 < nq; qp += kRpWarps) {
+        const int64_t qg = q0 + qp * 8;
+        float d1v[8];
+        if (valid) {
+          const float4* src = reinterpret_cast<const float4*>(D1 + (qg >> 3) * d1_ld_panel + jg * 8);
+          const float4 lo4 = __ldg(src), hi4 = __ldg(src + 1);
+          d1v[0] = lo4.x; d1v[1] = lo4.y; d1v[2] = lo4.z; d1v[3] = lo4.w;
+          d1v[4] = hi4.x; d1v[5] = hi4.y; d1v[6] = hi4.z; d1v[7] = hi4.w;
+        }
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          const int ql = qp * 8 + qq;
+          if (ql < nq) {
+            float* a = acc + ql * 32 + lane;
+            const float v = valid ? fmaxf(d1v[qq], *a) : kInfF;
+            *a = 0.f;
+            const uint32_t b = __ballot_sync(0xffffffffu, valid && v <= thr[ql]);
+            if (b) {
+              const float kth = top_insert(top, (q0 + ql) * top.slots + blockIdx.x, b, v, jg + top.id_base, lane);
+              __syncwarp();  // every lane's read of thr[ql] precedes the update
+              if (lane == 0) thr[ql] = kth;
+              __syncwarp();
+            }
+          }
+        }
+      }
+      named_bar_sync(1, kRpWarps * 32);  // acc is zero again before the next item's scatter
+      continue;
+    }
     for (int qp = warp; qp * 8 < nq; qp += kRpWarps) {
       const int64_t qg = q0 + qp * 8;
       float d1v[8];
@@ -352,12 +436,16 @@ int lcrw_reverse_panels_group(void) { return kRpGroup; }
 int lcrw_reverse_panels_warps(void) { return kRpWarps; }
 int lcrw_reverse_panels_ilp(void) { return kRpIlp; }
 
+int lcrw_reverse_panels_top_slots(void) { return sm_count(); }
+
 int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_t n_docs, int64_t doc_base,
                         const uint32_t* e_blk, const int64_t* e_tile, int64_t n_q, const float* D1,
-                        int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, void* stream) {
+                        int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc, float* top_d, int64_t* top_i,
+                        int k, int64_t id_base, void* stream) {
   LCRW_REQUIRE(n_q >= 0 && n_docs >= 0 && a_rows >= 0, "lcrw_reverse_panels: bad shape");
   if (n_q == 0 || n_docs == 0) return LCRW_OK;
-  LCRW_REQUIRE(Z2 && e_blk && e_tile && D1 && D, "lcrw_reverse_panels: null pointer");
+  LCRW_REQUIRE(Z2 && e_blk && e_tile && D1 && (D || top_d), "lcrw_reverse_panels: null pointer");
+  LCRW_REQUIRE(!top_d || (top_i && k >= 1 && k <= 32), "lcrw_reverse_panels: top-k lists need ids and 1 <= k <= 32");
   LCRW_REQUIRE(z_panel == a_rows * 32 && (reinterpret_cast<uintptr_t>(Z2) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(e_blk) & 15) == 0 && (reinterpret_cast<uintptr_t>(D1) & 15) == 0,
                "lcrw_reverse_panels: Z2 (32-doc panels, z_panel = 32 * a_rows), e_blk and D1 must be 16-byte aligned");
@@ -365,7 +453,8 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
   const int64_t panels = ceil_div(n_docs, 32);
   const int64_t groups = ceil_div(n_q, kRpGroup);
   LCRW_REQUIRE(n_tiles < (1 << 30), "lcrw_reverse_panels: query vocabulary too large");
-  const int smem = ((kRpGroup + 1) * 32 + kRpStages * kRpTile * 32 + kRpStages * kRpBlkWords) * 4 + 2 * kRpStages * 8;
+  const int smem = ((kRpGroup + kRpWarps) * 32 + kRpStages * kRpTile * 32 + kRpStages * kRpBlkWords) * 4 +
+                   2 * kRpStages * 8 + kRpGroup * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(reverse_panels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -378,7 +467,7 @@ int lcrw_reverse_panels(const float* Z2, int64_t z_panel, int64_t a_rows, int64_
   ProfScope prof(st, "reverse_panels");
   reverse_panels_kernel<<<(unsigned)grid, (kRpWarps + 1) * 32, smem, st>>>(
       Z2, z_panel, a_rows, n_docs, doc_base, e_blk, e_tile, (int)n_tiles, n_q, D1, d1_ld_panel, D, ld_q, ld_doc,
-      panels, items);
+      panels, items, TopLists{top_d, top_i, k, sm_count(), id_base});
   LCRW_CHECK_LAUNCH("reverse_panels_kernel");
   return LCRW_OK;
 }

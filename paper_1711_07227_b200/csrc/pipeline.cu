@@ -8,21 +8,18 @@
 //   plan     segment-end bitmap + column ranges             (segments = docs)
 //   phase1   Z2[doc, w] = min_t |E_w - T_t|                 (tcgen05, 32-doc panels)
 //   zeros    Z2[doc, w] = 0 where doc holds a word identical to w
+//   refine   near Z2 entries (0 < d < tau |E_w|) recomputed exactly from the f32 rows
+//            (refine.cu; a scan of the batch's Z2)
 //   reverse  D[q, doc] = max(D1, spmm(Xq, Z2)), panel-streaming (query-major D)
 // or, with a distance table (table.cu; built once per query set), the first four
-// steps are one lcrw_table_min launch (exact zeros are already in the table).
+// steps are one lcrw_table_min launch (exact zeros are already in the table; it
+// lists the near entries for the refine step instead of a scan).
 // The loop runs in C++ so a batch costs a handful of launch calls, not Python.
 #include <cstdlib>
 
 #include "common.cuh"
 
 namespace lcrw {
-namespace p1 {
-int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp, const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg,
-           const uint32_t* endmask, const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z,
-           int64_t z_panel, int z_shift, cudaStream_t stream, const char* tag, const int32_t* b_ids,
-           int64_t b_table_rows, int z_mode);
-}
 
 namespace {
 constexpr int kZShift = 5;  // 32-doc panels: a warp's 32 docs of one word row are one 128-byte line
@@ -38,8 +35,10 @@ int auto_range_cols(int64_t b_rows, int64_t a_rows) {
   return (int)want;
 }
 
+constexpr int64_t kRefineCap = 1 << 20;  // refine list entries per batch (overflow -> full scan)
+
 struct Layout {
-  size_t T, tn, mask, rs, Z, total;
+  size_t T, tn, mask, rs, Z, rlist, rcount, total;
 };
 
 Layout layout(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_words) {
@@ -51,7 +50,9 @@ Layout layout(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_words) {
   L.rs = L.mask + align256((size_t)lcrw_endmask_words(max_words) * 4);
   L.Z = L.rs + align256((size_t)max_ranges * 4);
   const int64_t panels = ceil_div(batch_docs, 1 << kZShift);
-  L.total = L.Z + align256((size_t)panels * (size_t)(a_rows << kZShift) * 4);
+  L.rlist = L.Z + align256((size_t)panels * (size_t)(a_rows << kZShift) * 4);
+  L.rcount = L.rlist + align256((size_t)kRefineCap * 8);
+  L.total = L.rcount + 256;
   return L;
 }
 }  // namespace
@@ -74,11 +75,13 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          int64_t batch_docs, int range_cols, const void* table, void* d1_ready, void* ws,
-                          size_t ws_bytes, void* stream) {
+                          float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols, const void* table, const float* E32,
+                          int dim, const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
-  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && (rep || table) && ws && D, "lcrw_reverse_pipeline: null pointer");
+  LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && (rep || table) && ws && (D || top_d) && E32 && a_ids &&
+                   dim > 0,
+               "lcrw_reverse_pipeline: null pointer");
   LCRW_REQUIRE(batch_docs > 0 && (batch_docs % (1 << kZShift)) == 0,
                "lcrw_reverse_pipeline: batch_docs must be a positive multiple of 32");
   int64_t max_words = 0;
@@ -94,6 +97,8 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
   uint32_t* mask = reinterpret_cast<uint32_t*>(base + L.mask);
   int32_t* rs = reinterpret_cast<int32_t*>(base + L.rs);
   float* Z2 = reinterpret_cast<float*>(base + L.Z);
+  uint2* rlist = reinterpret_cast<uint2*>(base + L.rlist);
+  uint32_t* rcount = reinterpret_cast<uint32_t*>(base + L.rcount);
   const int64_t z_panel = a_rows << kZShift;
   cudaStream_t st = as_stream(stream);
   int status;
@@ -107,9 +112,11 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
     const int64_t nd = j1 - j0;
     const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
+    cudaError_t ce = cudaMemsetAsync(rcount, 0, sizeof(uint32_t), st);
+    if (ce != cudaSuccess) return cuda_status(ce, "cudaMemsetAsync (refine count)");
     if (table) {
       if ((status = lcrw_table_min(table, a_rows, v_rows, doc_offsets + j0, lo, nd, doc_cols + lo, scale, Z2,
-                                   z_panel, stream)))
+                                   z_panel, a_norms, rlist, rcount, kRefineCap, stream)))
         return status;
     } else {
     if (!gather_b && (status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream)))
@@ -124,12 +131,17 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;
     }
+    // table form: the entries table_min listed; GEMM form: a scan of the batch's Z2 (small next
+    // to the GEMM's work) -- the same test on the same stored values either way
+    if ((status = lcrw_refine_near(Z2, z_panel, kZShift, a_rows, nd, doc_offsets + j0, lo, doc_cols + lo, E32, a_ids,
+                                   E32, dim, a_norms, scale, table ? rlist : nullptr, rcount, kRefineCap, stream)))
+      return status;
     if (j0 == 0 && d1_ready) {  // D1 may still be in flight on another stream (forward direction)
       cudaError_t e = cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d1_ready), 0);
       if (e != cudaSuccess) return cuda_status(e, "cudaStreamWaitEvent (D1 ready)");
     }
     if ((status = lcrw_reverse_panels(Z2, z_panel, a_rows, nd, j0, e_blk, e_tile, n_q, D1, d1_ld_panel, D, ld_q,
-                                      ld_doc, stream)))
+                                      ld_doc, top_d, top_i, k, id_base, stream)))
       return status;
   }
   return LCRW_OK;

@@ -8,19 +8,13 @@
 // BASELINE configs[1]).  The table form computes each pair once with the same
 // Phase-1 kernel (same operands, same roles: A = E2 rows, B = E rows as singleton
 // segments, so every entry is bitwise the value the GEMM form produces), applies
-// the exact zeros, transposes it into 128-word chunks [chunk][u][128 w] (one
-// 512-byte row per vocabulary word), and then each doc's Z2 column is a
-// min over its words' rows: 512-byte gathers from an L2-resident 51 MB chunk
-// (V = 100k), L2-bandwidth bound instead of tensor bound.
+// the exact zeros, and stores it as 180-word chunks [chunk][u][180 w] of 21-bit
+// keys (one 480-byte row per vocabulary word, common.cuh); each doc's Z2 column
+// is then a min over its words' rows: 480-byte gathers from an L2-resident 48 MB
+// chunk (V = 100k), L2-bandwidth bound instead of tensor bound.
 #include "common.cuh"
 
 namespace lcrw {
-namespace p1 {
-int launch(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* B, int64_t b_rows, int m, int kp,
-           const int64_t* seg_offsets, int64_t seg_base, int64_t n_seg, const uint32_t* endmask,
-           const int32_t* range_seg, int64_t n_ranges, const float* scale, float* Z, int64_t z_panel, int z_shift,
-           cudaStream_t stream, const char* tag, const int32_t* b_ids, int64_t b_table_rows, int z_mode);
-}
 namespace tbl {
 
 #ifndef LCRW_TBL_HINTS
@@ -67,25 +61,33 @@ __device__ __forceinline__ void st_stream(float* ptr, float v, uint64_t pol) {
 #endif
 }
 
-constexpr int kChunk = kTableChunk;  // query-vocabulary words per table chunk (512-byte packed rows)
+constexpr int kChunk = kTableChunk;  // query-vocabulary words per table chunk (480-byte packed rows)
 constexpr int kPanelDocs = 32;       // Z2 panel width (lcrw_reverse_panels layout)
 constexpr int kTileStride = kChunk + 1;  // smem tile row stride (conflict-free both ways)
 #ifndef LCRW_TBL_UNROLL
 #define LCRW_TBL_UNROLL 8
 #endif
 #ifndef LCRW_TBL_MINB
-#define LCRW_TBL_MINB 1
+#define LCRW_TBL_MINB 4  // 4 CTAs (1024 threads) per SM: <= 64 registers
 #endif
 constexpr int kUnroll = LCRW_TBL_UNROLL;  // (#pragma unroll does not expand macros)
 
+// Sets word w's key in row u (atomics: the fields of one 32-bit word belong to
+// different words w).  Cross-check and exact-zero paths only; the build writes whole words.
 __device__ __forceinline__ void store_key(uint8_t* T, int64_t v_rows, int64_t w, int64_t u, uint32_t key) {
-  int64_t b0;
-  int step;
-  table_key_bytes((int)(w % kChunk), b0, step);
-  uint8_t* b = T + ((w / kChunk) * v_rows + u) * kTableRowBytes + b0;
-  b[0] = (uint8_t)key;
-  b[step] = (uint8_t)(key >> 8);
-  b[2 * step] = (uint8_t)(key >> 16);
+  int gb, slot;
+  table_key_slot((int)(w % kChunk), gb, slot);
+  uint32_t* q = reinterpret_cast<uint32_t*>(T + ((w / kChunk) * v_rows + u) * kTableRowBytes + gb);
+  if (slot < 4) {
+    atomicAnd(q + slot, 0x7FFu);
+    atomicOr(q + slot, key << 11);
+  } else {
+    uint32_t* hi = q + 2 * (slot - 4);
+    atomicAnd(hi, ~0x7FFu);
+    atomicOr(hi, key >> 10);
+    atomicAnd(hi + 1, ~0x7FFu);
+    atomicOr(hi + 1, (key & 0x3FFu) << 1);
+  }
 }
 
 // Cross-check path: T'[(u >> 7) * zp + (w << 7) + (u & 127)] (f32 segment panels of lcrw_phase1,
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
   __syncthreads();
   for (int y = ty; y < 32; y += 8) {  // destination rows u0 + y, words w0 + tx
     const int64_t u = u0 + y, w = w0 + tx;
-    if (u < v_rows) store_key(T, v_rows, w, u, dist_key24(t[tx][y] * s));
+    if (u < v_rows && w < a_rows) store_key(T, v_rows, w, u, dist_key21(t[tx][y] * s));
   }
 }
 
@@ -122,29 +124,37 @@ __global__ void table_zeros_kernel(const int32_t* __restrict__ canon, const int3
 }
 
 // One CTA per (chunk c, 32-doc panel p), panels fastest so the CTAs in flight share
-// one L2-resident chunk (v_rows x 512 B: 51 MB at V = 100k).  Warp j takes docs j,
-// j+8, j+16, j+24; lane l owns words 5l..5l+4 of the chunk: per doc word, one 16-byte
-// load of their five 3-byte keys (the warp reads the 512-byte row once: 160 distances,
-// 3.2 bytes each).  Four keys sit in the top 24 bits of the group's 32-bit words, so
-// their minima are plain integer minima of the words; the fifth is reassembled from
-// the words' low bytes with two byte permutes (its top byte repeated, which orders like
-// the key); the 32 x 160 result is decoded, unscaled, staged in smem (row
-// stride 161: conflict-free both ways) and written as 160 coalesced 128-byte Z2 rows:
+// one L2-resident chunk (v_rows x 480 B: 48 MB at V = 100k).  Warp j takes docs j,
+// j+8, j+16, j+24; lane l < 30 owns words 6l..6l+5 of the chunk: per doc word, one
+// 16-byte load of their six 21-bit keys (the warp reads the 480-byte row once: 180
+// distances, 2.67 bytes each).  Four keys sit in the top 21 bits of the group's 32-bit
+// words, so their minima are plain integer minima of the words; the other two are
+// reassembled from the words' low 11 bits with one shift + one funnel shift each;
+// the 32 x 180 result is decoded, unscaled, staged in smem (row stride 181:
+// conflict-free both ways) and written as 180 coalesced 128-byte Z2 rows:
 // Z2[p * z_panel + w * 32 + doc].
 __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uint8_t* __restrict__ T, int64_t v_rows, int64_t a_rows,
                                                         const int64_t* __restrict__ doc_offsets, int64_t seg_base,
                                                         int64_t n_docs, const int32_t* __restrict__ cols,
                                                         const float* __restrict__ scale, float* __restrict__ Z2,
-                                                        int64_t z_panel, int64_t panels) {
+                                                        int64_t z_panel, int64_t panels,
+                                                        const float* __restrict__ a_norms, RefineSink sink) {
   __shared__ float tile[kPanelDocs * kTileStride];
+  __shared__ float wsq[kChunk];  // the chunk words' scaled squared norms (refine test)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t c = blockIdx.x / panels, p = blockIdx.x - c * panels;
-  const uint4* Tc = reinterpret_cast<const uint4*>(T + c * v_rows * kTableRowBytes) + lane;
+  if (sink.list && threadIdx.x < kChunk)
+    wsq[threadIdx.x] = c * kChunk + threadIdx.x < a_rows ? __ldg(a_norms + c * kChunk + threadIdx.x) : 0.f;
+  const bool active = lane < kTableGroups;
+  // lanes 30, 31 repeat lane 29's 16 bytes (same sector: no extra traffic) so the loop has no
+  // predication; their minima are discarded
+  const uint4* Tc = reinterpret_cast<const uint4*>(T + c * v_rows * kTableRowBytes) + (active ? lane : kTableGroups - 1);
   const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
   const float inv_scale = __ldg(scale + 1);
   for (int dd = warp; dd < kPanelDocs; dd += 8) {
     const int64_t d = p * kPanelDocs + dd;
-    uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu, k2 = 0xFFFFFFFFu, k3 = 0xFFFFFFFFu, k4 = 0xFFFFFFFFu;
+    uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu, k2 = 0xFFFFFFFFu, k3 = 0xFFFFFFFFu, k4 = 0xFFFFFFFFu,
+             k5 = 0xFFFFFFFFu;
     if (d < n_docs) {
       const int64_t b = __ldg(doc_offsets + d) - seg_base, e = __ldg(doc_offsets + d + 1) - seg_base;
       for (int64_t j0 = b; j0 < e; j0 += 32) {
@@ -154,26 +164,38 @@ __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uin
         for (int j = 0; j < n; ++j) {
           const int u = __shfl_sync(0xffffffffu, mine, j);
           const uint4 r = ld_keep_u4(Tc + (int64_t)u * (kTableRowBytes / 16), keep);
-          k0 = min(k0, r.x);  // key of word 5l in the top 24 bits
+          k0 = min(k0, r.x);  // key of word 6l in the top 21 bits
           k1 = min(k1, r.y);
           k2 = min(k2, r.z);
           k3 = min(k3, r.w);
-          k4 = min(k4, __byte_perm(__byte_perm(r.x, r.y, 0x0040), r.z, 0x4410));  // low bytes: word 5l+4
+          k4 = min(k4, __funnelshift_l(r.y << 21, r.x, 21));  // key of word 6l+4 << 11
+          k5 = min(k5, __funnelshift_l(r.w << 21, r.z, 21));  // key of word 6l+5 << 11
         }
       }
     }
-    float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
-    trow[0] = key24_dist(k0 >> 8) * inv_scale;
-    trow[1] = key24_dist(k1 >> 8) * inv_scale;
-    trow[2] = key24_dist(k2 >> 8) * inv_scale;
-    trow[3] = key24_dist(k3 >> 8) * inv_scale;
-    trow[4] = key24_dist(k4 & 0xFFFFFFu) * inv_scale;
+    if (active) {
+      float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
+      trow[0] = key21_dist(k0 >> 11) * inv_scale;
+      trow[1] = key21_dist(k1 >> 11) * inv_scale;
+      trow[2] = key21_dist(k2 >> 11) * inv_scale;
+      trow[3] = key21_dist(k3 >> 11) * inv_scale;
+      trow[4] = key21_dist(k4 >> 11) * inv_scale;
+      trow[5] = key21_dist(k5 >> 11) * inv_scale;
+    }
   }
   __syncthreads();
   float* zp = Z2 + p * z_panel;
   const int64_t w0 = c * kChunk;
+  const float s0 = __ldg(scale);
+  const bool doc_ok = p * kPanelDocs + lane < n_docs;
   for (int q = warp; q < kChunk; q += 8) {  // lane = doc; word q of the chunk
-    if (w0 + q < a_rows) st_stream(zp + (w0 + q) * kPanelDocs + lane, tile[lane * kTileStride + q], stream);
+    if (w0 + q < a_rows) {
+      const float v = tile[lane * kTileStride + q];
+      st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);
+      // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
+      if (sink.list && doc_ok && refine_flag(v * s0, wsq[q], kRefineTau * kRefineTau))
+        refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
+    }
   }
 }
 
@@ -190,6 +212,8 @@ int64_t lcrw_table_bytes(int64_t a_rows, int64_t v_rows) {
   return ceil_div(a_rows, tbl::kChunk) * v_rows * kTableRowBytes;
 }
 
+int64_t lcrw_table_operand_rows(int64_t a_rows) { return ceil_div(a_rows, kTableWarpRows) * 32; }
+
 int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                         int m, int kp, const int64_t* seg_offsets, const uint32_t* endmask, const int32_t* range_seg,
                         int64_t n_ranges, const float* scale, const int32_t* canon, const int32_t* next,
@@ -198,7 +222,15 @@ int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows,
   if (a_rows == 0 || v_rows == 0) return LCRW_OK;
   LCRW_REQUIRE(canon && next && remap && T, "lcrw_distance_table: null pointer");
   cudaStream_t st = as_stream(stream);
-  int status = p1::launch(A, a_norms, a_rows, EhB, v_rows, m, kp, seg_offsets, 0, v_rows, endmask, range_seg,
+  // a partial last chunk has groups no warp block writes: zero it (the gathers read them)
+  if (lcrw_table_operand_rows(a_rows) % (kTableChunk / kTableWarpRows * 32)) {
+    const int64_t last = ceil_div(a_rows, tbl::kChunk) - 1;
+    cudaError_t e = cudaMemsetAsync(static_cast<uint8_t*>(T) + last * v_rows * kTableRowBytes, 0,
+                                    (size_t)v_rows * kTableRowBytes, st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync (table tail)");
+  }
+  // A / a_norms: the padded operand (lcrw_table_operand_rows rows, 30 real rows per 32)
+  int status = p1::launch(A, a_norms, lcrw_table_operand_rows(a_rows), EhB, v_rows, m, kp, seg_offsets, 0, v_rows, endmask, range_seg,
                           n_ranges, scale, static_cast<float*>(T), v_rows * kTableRowBytes, 7, st, "table_build",
                           nullptr, 0, 2 /* kZTable */);
   if (status) return status;
@@ -214,9 +246,15 @@ int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const 
   LCRW_REQUIRE(a_rows >= 0 && v_rows >= 0, "lcrw_table_transpose: bad shape");
   if (a_rows == 0 || v_rows == 0) return LCRW_OK;
   LCRW_REQUIRE(Tp && T && scale, "lcrw_table_transpose: null pointer");
-  const int64_t gy = ceil_div(a_rows, tbl::kChunk) * (tbl::kChunk / 32);
+  const int64_t gy = ceil_div(a_rows, 32);
   LCRW_REQUIRE(gy < 65536, "lcrw_table_transpose: query vocabulary too large for one launch");
   cudaStream_t st = as_stream(stream);
+  if (a_rows % tbl::kChunk) {  // fields of words past a_rows in the last chunk: defined zeros
+    const int64_t last = a_rows / tbl::kChunk;
+    cudaError_t e = cudaMemsetAsync(static_cast<uint8_t*>(T) + last * v_rows * kTableRowBytes, 0,
+                                    (size_t)v_rows * kTableRowBytes, st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync (table tail)");
+  }
   ProfScope prof(st, "table_transpose");
   tbl::transpose_kernel<<<dim3((unsigned)ceil_div(v_rows, 32), (unsigned)gy), 256, 0, st>>>(
       Tp, a_rows, v_rows, scale, static_cast<uint8_t*>(T));
@@ -226,10 +264,13 @@ int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const 
 
 int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
                    int64_t n_docs, const int32_t* doc_cols, const float* scale, float* Z2, int64_t z_panel,
+                   const float* a_norms, void* refine_list, uint32_t* refine_count, int64_t refine_cap,
                    void* stream) {
   LCRW_REQUIRE(a_rows >= 0 && v_rows >= 0 && n_docs >= 0, "lcrw_table_min: bad shape");
   if (a_rows == 0 || n_docs == 0) return LCRW_OK;
   LCRW_REQUIRE(T && doc_offsets && doc_cols && Z2 && scale, "lcrw_table_min: null pointer");
+  LCRW_REQUIRE(!refine_list || (a_norms && refine_count && refine_cap >= 0),
+               "lcrw_table_min: a refine list needs a_norms, its count and capacity");
   LCRW_REQUIRE(z_panel == a_rows * tbl::kPanelDocs && (reinterpret_cast<uintptr_t>(T) & 15) == 0,
                "lcrw_table_min: Z2 must be in 32-doc panels (z_panel = 32 * a_rows), T 16-byte aligned");
   const int64_t panels = ceil_div(n_docs, tbl::kPanelDocs);
@@ -238,7 +279,8 @@ int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t*
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "table_min");
   tbl::table_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(T), v_rows, a_rows, doc_offsets,
-                                                          seg_base, n_docs, doc_cols, scale, Z2, z_panel, panels);
+                                                          seg_base, n_docs, doc_cols, scale, Z2, z_panel, panels, a_norms,
+      RefineSink{static_cast<uint2*>(refine_list), refine_count, refine_cap});
   LCRW_CHECK_LAUNCH("table_min_kernel");
   return LCRW_OK;
 }

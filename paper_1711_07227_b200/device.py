@@ -270,6 +270,8 @@ def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
     w = 1 << z_shift
     z_panel = w * max(a_rows, 1)
     Z = torch.empty(((n_seg + w - 1) // w) * z_panel, dtype=torch.float32, device=dev)
+    if n_seg % w:  # slots past the last segment: defined values (lcrw_spmm reads 4 segments at a time)
+        Z[(n_seg // w) * z_panel:].zero_()
     _lib.call("lcrw_phase1", _p(A), _p(a_norms), a_rows, _p(B), b_rows, prep.k_eff, prep.kp,
               _p(seg_offsets), 0, n_seg, _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(Z), z_panel,
               z_shift, st)
@@ -279,6 +281,16 @@ def phase1(A: torch.Tensor, a_norms: torch.Tensor, a_rows: int, B: torch.Tensor,
 def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel, z_shift: int = 3) -> None:
     _lib.call("lcrw_zero_identical", _p(seg_offsets), n_seg, _p(rep), _p(nxt), _p(remap), _p(Z), z_panel, z_shift,
               _stream())
+
+
+def refine_near(Z, z_panel, z_shift, a_rows, n_seg, seg_offsets, seg_ids, a_ids, a_norms, prep: "PreparedEmbeddings",
+                B32: torch.Tensor | None = None) -> None:
+    """Exact re-evaluation of the near entries of a Phase-1 Z (lcrw_refine_near, scan
+    mode): entries with 0 < d < tau |a| become the exact segment minimum from the f32
+    rows (A rows E32[a_ids], segment rows B32[seg_ids], B32 = E32 by default)."""
+    B = prep.E32 if B32 is None else B32
+    _lib.call("lcrw_refine_near", _p(Z), z_panel, z_shift, a_rows, n_seg, _p(seg_offsets), 0, _p(seg_ids),
+              _p(prep.E32), _p(a_ids), _p(B), prep.m, _p(a_norms), _p(prep.scale), None, None, 0, _stream())
 
 
 def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel,
@@ -365,6 +377,7 @@ def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: to
     Z, zp = phase1(res.A, res.a_norms, res.v_e, B, word_ids.numel(), seg_offsets, n_seg, prep, z_shift=z_shift)
     rep, nxt = prep.representatives(word_ids)
     zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp, z_shift)
+    refine_near(Z, zp, z_shift, res.v_e, n_seg, seg_offsets, word_ids, res.used, res.a_norms, prep)
     return Z, zp
 
 
@@ -381,6 +394,8 @@ def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR,
     else:
         out = torch.empty(((n_q + 7) // 8) * 8 * n_res, dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = 8, 8 * n_res
+        if n_q % 8:  # the last panel's padding queries: defined values (lcrw_reverse_panels reads 8 at a time)
+            out[(n_q // 8) * 8 * n_res:].zero_()
     spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel, z_shift=zs)
     return out
 
@@ -413,7 +428,7 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
     each query's terms are accumulated in ascending row (= word id) order
     whatever the other queries of the set are -- the fp32 sums, and D, do not
     depend on how the queries are batched (distances.py:198-203); empty slots
-    are padding (scratch query G, weight 0).  Returns (blocks uint32, block
+    are padding (scratch query G + warp, weight 0).  Returns (blocks uint32, block
     word offsets int64 [n_groups*n_tiles+1]).
     Built on the host from the (small) query set -- index planning, no
     arithmetic."""
@@ -462,10 +477,12 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
     list_start = np.zeros(n_lists, dtype=np.int64)                   # first entry of each list inside its block
     list_start.reshape(-1, W)[:, 1:] = ends[:, :-1]
     ent_base = tile_off[:-1].repeat(W) + W + 2 * list_start          # word offset of each list's first entry
-    # every slot starts as padding (scratch query G, weight 0), then the real entries
+    # every slot starts as padding (weight 0, the list's own scratch query G + warp: no two
+    # warps touch the same accumulator row), then the real entries
     flat = lens.ravel()
     pos = np.arange(flat.sum(), dtype=np.int64) - np.repeat(np.cumsum(flat) - flat, flat)
-    words[np.repeat(ent_base, flat) + 2 * pos] = np.uint32(G * 128)
+    scratch = ((G + np.arange(n_lists, dtype=np.int64) % W) * 128).astype(np.uint32)
+    words[np.repeat(ent_base, flat) + 2 * pos] = np.repeat(scratch, flat)
     slot = ent_base[key] + 2 * ((g_off[key, level] + cpos // I) * I + cpos % I)
     words[slot] = (((rl * 128) << 18) | (ql * 128)).astype(np.uint32)
     words[slot + 1] = xv.view(np.uint32)
@@ -475,8 +492,8 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
 REVERSE_TABLE_Z2_FRACTION = 3  # table mode: Z2 batches up to 1/3 of HBM -- each batch re-streams the table
                                # once and larger batches keep one chunk L2-resident for longer (C2 on
                                # B200: 16 GB 502 ms, 32 GB 490 ms, 64 GB 485 ms per step)
-TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 512 B) must stay L2-resident
-TABLE_ROW_BYTES = 512             # per vocabulary word per 160-word chunk: 160 3-byte keys in 32 16-byte groups
+TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 480 B) must stay L2-resident
+TABLE_ROW_BYTES = 480             # per vocabulary word per 180-word chunk: 180 21-bit keys in 30 16-byte groups
 
 
 def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | None = None) -> str:
@@ -513,7 +530,13 @@ def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: 
         _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(prep.scale), _p(T), _stream())
         return T
     endmask, range_seg, n_ranges = segment_plan(seg, V, V, res2.v_e)
-    _lib.call("lcrw_distance_table", _p(res2.A), _p(res2.a_norms), res2.v_e, _p(prep.EhB), V, prep.k_eff, prep.kp,
+    # the build's A operand: 30 query-vocabulary rows per 32 (include/lcrwmd.h); the two
+    # filler rows of each block repeat a real row and are not stored
+    a_pad = int(_lib.value("lcrw_table_operand_rows", res2.v_e))
+    r = np.arange(a_pad, dtype=np.int64)
+    real = np.minimum((r // 32) * 30 + np.minimum(r % 32, 29), res2.v_e - 1)
+    Ap, anp = gather_rows(prep, res2.used[to_device(real, torch.int64)], "A")
+    _lib.call("lcrw_distance_table", _p(Ap), _p(anp), res2.v_e, _p(prep.EhB), V, prep.k_eff, prep.kp,
               _p(seg), _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(prep.canon), _p(prep.next),
               _p(res2.remap), _p(T), _stream())
     return T
@@ -525,6 +548,7 @@ def reverse_batch_docs(n_docs: int, v_e2: int, budget_bytes: int = REVERSE_Z2_BY
     return int((nb + 31) // 32 * 32)
 
 
+FUSED_TOPK_MAX = 32  # k up to which the max -> top-k is fused into lcrw_reverse_panels (no D)
 QUERY_SLICE = 16384  # queries per pass of the symmetric pipeline (bounds D, D1, plan and table per pass)
 
 
@@ -591,9 +615,17 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
     ws_bytes = C.c_size_t(0)
     _lib.call("lcrw_reverse_workspace", res2.v_e, prep.kp, batch, max_words, C.byref(ws_bytes))
     ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
+    fused = k is not None and k <= FUSED_TOPK_MAX and not os.environ.get("LCRW_TOPK_VIA_D")
+    top_d = top_i = None
     if k is None:
         D = torch.empty(n1 * n2, dtype=torch.float32, device=dev)  # reference orientation (n1, n2)
         ld_q, ld_doc = 1, n2
+    elif fused:
+        # max -> top-k fused into lcrw_reverse_panels: per-(query, CTA) lists, D never exists
+        slots = int(_lib.value("lcrw_reverse_panels_top_slots"))
+        top_d = torch.full((n2, slots, k), float("inf"), dtype=torch.float32, device=dev)
+        top_i = torch.full((n2, slots, k), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+        D, ld_q, ld_doc = None, 0, 0
     else:
         D = torch.empty(n2 * n1, dtype=torch.float32, device=dev)  # query-major for the per-query top-k
         ld_q, ld_doc = n1, 1
@@ -603,12 +635,15 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
               prep.kp,
               _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
               _p(nxt), _p(res2.remap), _p(e_blk), _p(e_tile), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
-              batch, 0, _p(table), C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws),
-              ws_bytes.value, st)
+              _p(top_d), _p(top_i), k if fused else 0, id_offset, batch, 0, _p(table), _p(prep.E32), prep.m, _p(res2.used),
+              C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value, st)
     del ws, table
     if k is None:
         return D.view(n1, n2)
     kk = min(k, n1)
+    if fused:
+        d, i = topk_rows(top_d.view(n2, -1), top_i.view(n2, -1), n2, top_d.shape[1] * k, k)
+        return d[:, :kk].contiguous(), i[:, :kk].contiguous()
     if k > 1024:  # beyond the selection kernels: one (distance, id) sort per query row
         out_d = torch.empty((n2, kk), dtype=torch.float32, device=dev)
         out_i = torch.empty((n2, kk), dtype=torch.int64, device=dev)
@@ -639,6 +674,8 @@ def nearest_word_distances(E, Q) -> torch.Tensor:
     _lib.call("lcrw_match_rows", _p(Qd), nq, _p(prep.E32), prep.m, _p(prep.sorted_hash), _p(prep.sorted_ids),
               prep.V, _p(prep.canon), _p(rep), _stream())
     zero_identical(seg, 1, rep, prep.next, None, Z, zp)
+    refine_near(Z, zp, 3, prep.V, 1, seg, torch.arange(nq, dtype=torch.int32, device=dev),
+                torch.arange(prep.V, dtype=torch.int32, device=dev), prep.norms, prep, B32=Qd.contiguous())
     return Z[: zp].view(prep.V, 8)[:, 0]
 
 
@@ -666,6 +703,7 @@ def pairwise(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     remap[:na] = torch.arange(na, dtype=torch.int32, device=dev)
     rep, nxt = prep.representatives(ids)
     zero_identical(seg, nb, rep, nxt, remap, Z, zp, 3)
+    refine_near(Z, zp, 3, na, nb, seg, ids, torch.arange(na, dtype=torch.int32, device=dev), prep.norms[:na], prep)
     panels = (nb + 7) // 8
     return Z[: panels * zp].view(panels, na, 8).permute(1, 0, 2).reshape(na, panels * 8)[:, :nb].contiguous()
 

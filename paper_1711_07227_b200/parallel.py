@@ -130,6 +130,8 @@ def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) ->
         remap[v0:v1] = torch.arange(rows, dtype=torch.int32, device=dev)
         rep, nxt = prep.representatives(dx2.cols)
         device.zero_identical(dx2.offsets, n_q, rep, nxt, remap, Z, zp, zs)
+        device.refine_near(Z, zp, zs, rows, n_q, dx2.offsets, dx2.cols,
+                           torch.arange(v0, v1, dtype=torch.int32, device=dev), prep.norms[v0:v1], prep)
         zl[:, :rows, :] = Z.view(panels, rows, W)
     return zl, R
 
@@ -141,6 +143,8 @@ def d1_from_slices(dx1: DeviceCSR, zall: torch.Tensor, R: int, n_q: int) -> torc
     zs = W.bit_length() - 1
     panels = zall.shape[1]
     out = torch.empty(((n_q + 7) // 8) * 8 * max(n1, 1), dtype=torch.float32, device=zall.device)
+    if n_q % 8:  # padding queries of the last panel (read 8 at a time by lcrw_reverse_panels)
+        out[(n_q // 8) * 8 * max(n1, 1):].zero_()
     device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, W * R, n_q, out, 8, 8 * n1,
                 z_block_rows=R, z_block_stride=panels * R * W, z_shift=zs)
     return out

@@ -1,0 +1,155 @@
+"""GPU parity at the largest BASELINE configurations and on adversarial embedding
+scales (SURVEY.md §8c protocol: sampled sub-blocks recomputed by the oracle on
+the sampled subsets, sound by subset invariance; top-k checked by "returned
+distances equal the oracle's for the returned ids, and no sampled doc beats the
+k-th").
+
+* c4 (BASELINE configs[3]): V = 3M, h ~ 150 -- one GPU's share (500k of the 4M
+  docs) x 1k queries; the vocabulary is too large for an L2-resident table
+  chunk, so the reverse direction runs the tcgen05 GEMM form (69 Phase-1
+  launches per step at this shape).
+* c5 (configs[4]): all-pairs of 200k docs over V = 400k, rank 0 of 8 emulated
+  on one GPU: C = D1[:, S_0] (every doc against the local docs as queries), the
+  local rows R = D1[S_0, :], D = max(R, C^T), per-row top-k.
+* wide dynamic range: row norms log-uniform over 1e-3 .. 1e2 (one global
+  power-of-two operand scale; small rows sit in f16 subnormals).
+
+Tolerance as tests/test_gpu_parity.py."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel_close
+from oracle import lcrwmd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1711_07227_b200 import _lib
+    _lib.load()
+
+
+def _atol(E):
+    return ATOL
+
+
+def _check_topk_sampled(td, ti, row_ids, x_rows, x_cols, E, k, n_cols, rng, n_probe=512, atol=0.0):
+    """For each sampled row r: the returned ids' oracle distances equal the returned
+    distances, and no probe column (random) has an oracle distance below the k-th - tol."""
+    for r, xi in zip(row_ids, range(len(row_ids))):
+        ids = ti[xi]
+        probe = np.unique(np.concatenate([ids, rng.choice(n_cols, n_probe, replace=False)]))
+        ref = O.lcrwmd_full(x_cols.take_rows(probe), x_rows.take_rows([r]), E, threads=O.default_threads())[:, 0]
+        pos = np.searchsorted(probe, ids)
+        ok, err = rel_close(td[xi], ref[pos], RTOL, atol)
+        assert ok, (r, err)
+        kth = float(td[xi][-1])
+        others = ~np.isin(probe, ids)
+        assert np.all(ref[others] >= kth - (RTOL * kth + atol) - 1e-6), (r, "a probe doc beats the k-th")
+
+
+def test_c4_share_gemm_path_sampled_parity():
+    """configs[3] at full vocabulary and word count: 500k docs x 1k queries, V=3M, h~150."""
+    import torch
+    from paper_1711_07227_b200 import device, synthetic as S
+    V = 3_000_000
+    E = S.embeddings(V, 300, seed=0)
+    x1 = S.histograms(500_000, V, 150, seed=1)
+    x2 = S.histograms(1000, V, 150, seed=2)
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    res2 = device.Restricted.build(d2, prep)
+    assert device.reverse_mode(prep.V, res2.v_e, d1.nnz) == "gemm"
+    del res2
+    full = device.symmetric(d1, d2, prep, None)  # (500k, 1k)
+    rng = np.random.default_rng(11)
+    di = np.sort(rng.choice(500_000, 192, replace=False))
+    qj = np.sort(rng.choice(1000, 12, replace=False))
+    got = full[torch.as_tensor(di, device=full.device)][:, torch.as_tensor(qj, device=full.device)].cpu().numpy()
+    ref = O.lcrwmd_full(x1.take_rows(di), x2.take_rows(qj), E, threads=O.default_threads())
+    ok, err = rel_close(got, ref, RTOL, _atol(E))
+    assert ok, err
+    # fused top-k == top-k of the full matrix, bitwise
+    td, ti = device.symmetric(d1, d2, prep, 10)
+    ids = torch.arange(500_000, device=full.device).repeat(1000, 1).contiguous()
+    fd, fi = device.topk_rows(full.t().contiguous(), ids, 1000, 500_000, 10)
+    assert torch.equal(td, fd) and torch.equal(ti, fi)
+
+
+def test_c5_all_pairs_rank_share_sampled_parity():
+    """configs[4]: all-pairs of 200k docs, V=400k, rank 0 of 8 (25k local rows)."""
+    import torch
+    from paper_1711_07227_b200 import device, parallel, synthetic as S
+    V, n, world = 400_000, 200_000, 8
+    E = S.embeddings(V, 300, seed=0)
+    x = S.histograms(n, V, 50, seed=3)
+    lo, hi = parallel.shard_range(n, 0, world)
+    prep = device.PreparedEmbeddings(E)
+    dx_all = device.DeviceCSR.upload(x)
+    dx_loc = device.DeviceCSR.upload(x.slice_rows(lo, hi))
+    n_r = hi - lo
+    dev = dx_all.cols.device
+    C = torch.empty((n, n_r), dtype=torch.float32, device=dev)       # D1[:, S_0]
+    device.forward_rows_into(device.Restricted.build(dx_all, prep), prep, dx_loc, C, 4096)
+    R = torch.empty((n_r, n), dtype=torch.float32, device=dev)       # D1[S_0, :]
+    device.forward_rows_into(device.Restricted.build(dx_loc, prep), prep, dx_all, R, 4096)
+    D = torch.empty((n_r, n), dtype=torch.float32, device=dev)
+    device.max_transposed_into(D, R, C)
+    del R, C
+    rng = np.random.default_rng(12)
+    ri = np.sort(rng.choice(n_r, 96, replace=False))
+    cj = np.sort(rng.choice(n, 96, replace=False))
+    got = D[torch.as_tensor(ri, device=dev)][:, torch.as_tensor(cj, device=dev)].cpu().numpy()
+    ref = O.lcrwmd_full(x.take_rows(lo + ri), x.take_rows(cj), E, threads=O.default_threads())
+    ok, err = rel_close(got, ref, RTOL, _atol(E))
+    assert ok, err
+    # the diagonal block is exactly symmetric with zero diagonal (D = max(D1, D1^T))
+    blk = D[:, lo:hi]
+    assert torch.equal(blk, blk.t()) and bool((torch.diagonal(blk) == 0).all())
+    k = 10
+    od = torch.empty((n_r, k), dtype=torch.float32, device=dev)
+    oi = torch.empty((n_r, k), dtype=torch.int64, device=dev)
+    device.topk_matrix_rows(D, n_r, n, n, 0, k, od, oi)
+    rows = np.sort(rng.choice(n_r, 6, replace=False))
+    td, ti = od[torch.as_tensor(rows, device=dev)].cpu().numpy(), oi[torch.as_tensor(rows, device=dev)].cpu().numpy()
+    assert np.all(ti[:, 0] == lo + rows) and np.all(td[:, 0] == 0)  # every doc is its own nearest
+    _check_topk_sampled(td, ti, lo + rows, x, x, E, k, n, rng, atol=_atol(E))
+
+
+def test_wide_dynamic_range_embeddings():
+    """Row norms log-uniform over [1e-3, 1e2]: one global power-of-two operand scale
+    (prep.cu scale_kernel) puts the smallest rows into f16 subnormals; distances
+    small next to a row's norm are recomputed exactly (lcrw_refine_near), so every
+    distance meets the plain relative tolerance -- measured and printed."""
+    from paper_1711_07227_b200 import distances
+    rng = np.random.default_rng(13)
+    V, m = 6000, 300
+    norms = 10.0 ** rng.uniform(-3, 2, V)
+    E = rng.standard_normal((V, m))
+    E = (E / np.linalg.norm(E, axis=1, keepdims=True) * norms[:, None]).astype(np.float32)
+    from paper_1711_07227_b200 import synthetic as S
+    x1 = S.histograms(600, V, 40, seed=14)
+    x2 = S.histograms(40, V, 40, seed=15)
+    got = distances.lcrwmd_full(x1, x2, E).values
+    ref = O.lcrwmd_full(x1, x2, E, threads=O.default_threads())
+    atol = _atol(E)
+    ok, err = rel_close(got, ref, RTOL, atol)
+    assert ok, err
+    rel = np.abs(got.astype(np.float64) - ref) / np.maximum(np.abs(ref), 1e-30)
+    big = ref > 1.0  # distances with at least one large row
+    print(f"wide range: max rel err {rel.max():.2e}; over distances > 1: {rel[big].max():.2e}")
+    assert rel[big].max() <= RTOL
+    assert np.array_equal(got == 0, ref == 0)
+    top = distances.lcrwmd_topk(x1, x2, E, 10)
+    for j, t in enumerate(top):
+        ok, err = rel_close(t.distances, ref[t.ids, j], RTOL, atol)
+        assert ok, (j, err)

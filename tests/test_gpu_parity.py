@@ -2,12 +2,14 @@
 vectors and the pinned CPU oracle.
 
 Tolerances (written here, justified in DESIGN.md §Precision):
-  * distances: |d - d_ref| <= 1e-4 * |d_ref| + 1e-5 * max_w |E_w|
+  * distances: |d - d_ref| <= 1e-4 * |d_ref| + 1e-6
     The relative term covers operand rounding (f16 = 11-bit significand, like
-    TF32-RN; split 3 x f16 below m = 64).  The absolute term is the fp32
-    tensor-core accumulation of the Gram expansion |a|^2 + |b|^2 - 2 a.b,
-    whose error scales with the norms, not the distance; it only matters for
-    near-duplicate words (clustered stress data).
+    TF32-RN; split 3 x f16 below m = 64), the fp32 tensor-core accumulation
+    of the Gram expansion and the reverse direction's 21-bit keys (2^-17).
+    The Gram expansion's error scales with the norms, not the distance, so
+    entries with d < 0.5 |a| (near-duplicate words, clustered data) are
+    recomputed exactly from the f32 rows (lcrw_refine_near); the 1e-6 only
+    absorbs values within rounding of zero.
   * exact zeros where the reference has them (identical vectors)
   * spmm / topk_select / restrict_vocabulary: bitwise
   * top-k ids: identical except where the reference's k-th and (k+1)-th
@@ -24,7 +26,7 @@ from oracle import lcrwmd_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-RTOL, ATOL = 1e-4, 1e-5
+RTOL, ATOL = 1e-4, 1e-6
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -63,7 +65,8 @@ def _check_topk(d, i, dref_full, k, ATOL=ATOL):
 
 
 def _atol(E):
-    return 1e-5 * float(np.sqrt((np.asarray(E, np.float64) ** 2).sum(1).max()))
+    """The absolute term of the tolerance: a constant 1e-6 (no norm-scaled slack)."""
+    return ATOL
 
 
 def test_golden_full_batched_onesided(golden_case):
@@ -140,7 +143,8 @@ def test_spec_known_answers():
     z0, a, _ = load_case("small_m16")
     d = D.lcrwmd_full(a, a, z0["E"]).values
     assert np.all(np.diag(d) == 0)
-    ok, err = rel_close(d, d.T, 1e-6, 1e-6)  # symmetry when X1 == X2
+    # symmetry when X1 == X2, to the reverse direction's 21-bit key rounding (2^-17 relative)
+    ok, err = rel_close(d, d.T, 1e-5, 1e-6)
     assert ok, err
 
 
@@ -171,7 +175,7 @@ def test_c1_shaped_vs_oracle(clustered):
     x2 = S.histograms(40, V, 40, seed=5)
     ref = O.lcrwmd_full(x1, x2, E, threads=8)
     got = D.lcrwmd_full(x1, x2, E).values
-    ok, err = rel_close(got, ref, RTOL, ATOL)  # strict: 1e-4 rel + 1e-5 abs at m = 300
+    ok, err = rel_close(got, ref, RTOL, ATOL)  # 1e-4 relative (+ 1e-6)
     assert ok, err
     res = D.lcrwmd_topk(x1, x2, E, 10)
     _check_topk([r.distances for r in res], [r.ids for r in res], ref, 10)
@@ -915,19 +919,22 @@ def test_reverse_table_mode_bitwise_equals_gemm_mode(case, monkeypatch):
 
 
 def _decode_table(T: np.ndarray, V: int, inv_scale: float) -> np.ndarray:
-    """Packed 24-bit table (include/lcrwmd.h) -> unscaled f32 distances (chunks, V, 160):
-    16-byte group g of a 512-byte row = LE words q_i = key(5g+i) << 8 | byte i of key(5g+4)."""
-    q = np.ascontiguousarray(T).view("<u4").reshape(-1, V, 32, 4)
-    k4 = (q[..., 0] & 255) | ((q[..., 1] & 255) << 8) | ((q[..., 2] & 255) << 16)
-    key = np.concatenate([q >> 8, k4[..., None]], axis=-1).reshape(-1, V, 160).astype(np.uint32)
-    val = ((key << 4) + (104 << 23)).astype(np.uint32).view(np.float32)
+    """Packed 21-bit table (include/lcrwmd.h, common.cuh) -> unscaled f32 distances
+    (chunks, V, 180): 16-byte group g of a 480-byte row = LE words q_i =
+    key(6g+i) << 11 | piece_i, key(6g+4) = (q0 & 0x7FF) << 10 | (q1 & 0x7FF) >> 1,
+    key(6g+5) likewise from q2, q3."""
+    q = np.ascontiguousarray(T).view("<u4").reshape(-1, V, 30, 4).astype(np.uint32)
+    k4 = ((q[..., 0] & 0x7FF) << 10) | ((q[..., 1] & 0x7FF) >> 1)
+    k5 = ((q[..., 2] & 0x7FF) << 10) | ((q[..., 3] & 0x7FF) >> 1)
+    key = np.concatenate([q >> 11, k4[..., None], k5[..., None]], axis=-1).reshape(-1, V, 180).astype(np.uint32)
+    val = ((key << 7) + (104 << 23)).astype(np.uint32).view(np.float32)
     return np.where(key == 0, np.float32(0), val) * np.float32(inv_scale)
 
 
 @pytest.mark.gpu
 def test_distance_table_layout_and_zeros():
-    """Distance-table layout: chunk w >> 7, E row u -> 384-byte row of 24-bit keys of the
-    Phase-1 distance of query-vocabulary row w to E row u (relative rounding <= 2^-20),
+    """Distance-table layout: chunk w // 180, E row u -> 480-byte row of 21-bit keys of the
+    Phase-1 distance of query-vocabulary row w to E row u (relative rounding <= 2^-17),
     exactly 0 for identical rows; the one-pass build (packed stores from the Phase-1
     epilogue) equals the two-pass one (segment panels, lcrw_zero_identical,
     lcrw_table_transpose) bitwise."""
@@ -945,16 +952,16 @@ def test_distance_table_layout_and_zeros():
     assert res2.v_e == len(used)
     w = np.arange(len(used))
     C = int(_lib.value("lcrw_table_chunk"))
-    assert T.size == -(-len(used) // C) * V * 512
+    assert C == 180 and T.size == -(-len(used) // C) * V * 480
     inv = float(prep.scale[1].item())
     tab = _decode_table(T, V, inv)[w // C, :, w % C]  # (v_e, V)
     assert np.array_equal(tab, _decode_table(T2, V, inv)[w // C, :, w % C])  # one-pass == two-pass build
-    # the keys are the f32 Phase-1 entries rounded to 19 mantissa bits
+    # the keys are the f32 Phase-1 entries rounded to 16 mantissa bits
     seg = __import__("torch").arange(V + 1, dtype=__import__("torch").int64, device=res2.A.device)
     zf, zp = device.phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=3)
     zf = zf.cpu().numpy()[: ((V + 7) // 8) * zp].reshape(-1, res2.v_e, 8).transpose(1, 0, 2).reshape(res2.v_e, -1)[:, :V]
     nz = (tab != 0) & (zf != 0)
-    assert np.max(np.abs(tab[nz] / zf[nz] - 1)) <= 2.0 ** -20 * 1.001
+    assert np.max(np.abs(tab[nz] / zf[nz] - 1)) <= 2.0 ** -17 * 1.001
     ref = O.pairwise_euclidean(E[used], E)
     ok, err = rel_close(tab, ref, RTOL, _atol(E))
     assert ok, err

@@ -131,7 +131,7 @@ def test_reverse_entry_plan_invariants(n_q, h, V):
     """lcrw_reverse_panels plan (include/lcrwmd.h): 16-byte aligned blocks per (group,
     tile), W cumulative list ends, every nonzero exactly once in its (group, tile,
     warp) list, lists a multiple of I long, each aligned group of I names distinct
-    queries, padding = scratch query G with weight 0."""
+    queries, padding = the list's scratch query G + warp with weight 0."""
     from paper_1711_07227_b200.device import plan_query_entries
     T, G, W, I = 128, 1024, 16, 4
     x = S.histograms(n_q, V, h, seed=7)
@@ -157,13 +157,14 @@ def test_reverse_entry_plan_invariants(n_q, h, V):
             last_row = {}  # each query's terms in ascending row order (batching-invariant fp32 sums)
             for e in range(lo, ends[w]):
                 qv = int((ent[e, 0] & 0x3FFFF) >> 7)
-                if qv != G:
+                if qv < G:
                     rv = int(ent[e, 0] >> 25)
                     assert rv > last_row.get(qv, -1), (B, w, qv)
                     last_row[qv] = rv
             for b in range(lo, ends[w], I):
                 qs = ((ent[b:b + I, 0] & 0x3FFFF) >> 7).astype(np.int64)
-                real = qs != G
+                real = qs < G
+                assert np.all(qs[~real] == G + w)  # the warp's own scratch row
                 assert len(set(qs[real].tolist())) == int(real.sum())
                 assert np.all(ent[b:b + I, 1][~real] == 0)
                 for e in range(b, b + I):
@@ -284,7 +285,7 @@ def test_reverse_mode_choice(monkeypatch):
     assert device.reverse_mode(3_000_000, 146_000, 75_000_000, hbm) == "gemm"    # C4: chunk >> L2
     assert device.reverse_mode(400_000, 190_000, 1_250_000, hbm) == "gemm"      # C5 shard
     assert device.reverse_mode(20_000, 2_400, 30_000, hbm) == "gemm"            # few docs: 2V > nnz
-    assert device.reverse_mode(100_000, 39_300, 50_000_000, 40 << 30) == "gemm"  # table > HBM / 4
+    assert device.reverse_mode(100_000, 39_300, 50_000_000, 32 << 30) == "gemm"  # table > HBM / 4
     monkeypatch.setenv("LCRW_REVERSE", "gemm")
     assert device.reverse_mode(100_000, 39_300, 50_000_000, hbm) == "gemm"
     monkeypatch.setenv("LCRW_REVERSE", "table")

@@ -1,6 +1,6 @@
 // L2 gather ceiling probe (the "peak" of bench.py's table_min roofline, profiles/l2_gather_peak.json):
-// 512-byte random row gathers + min from an L2-resident 51 MB table, the access pattern
-// of csrc/table.cu without its Z2 stores.  nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/l2gather tools/l2gather.cu
+// 480-byte (30 lanes x 16 B, the current table row) and 512-byte random row gathers + min
+// from an L2-resident ~50 MB table, the access pattern of csrc/table.cu without its Z2 stores.  nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/l2gather tools/l2gather.cu
 // Microbenchmark: random 512-B (or 1-KB) row gathers + min from an L2-resident table,
 // the access pattern of a distance-table formulation of the reverse Phase 1.
 #include <cstdio>
@@ -14,10 +14,11 @@ __global__ void fill(float* t, int64_t n) {
     t[i] = (float)((i * 2654435761u) % 1000003u) * 1e-3f;
 }
 
-template <int VEC>  // float4 per lane per row: row width = 32*4*VEC floats
+template <int VEC>  // float4 per lane per row: row width = 32*4*VEC floats (lanes < act_lanes load)
 __global__ void __launch_bounds__(256) gather_min(const float4* __restrict__ T, int row_f4, const int* __restrict__ cols,
-                                                  int h, int n_docs, float4* __restrict__ out) {
+                                                  int h, int n_docs, float4* __restrict__ out, int act_lanes) {
   const int lane = threadIdx.x & 31;
+  const bool act = lane < act_lanes;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int d = warp; d < n_docs; d += nw) {
@@ -33,13 +34,14 @@ __global__ void __launch_bounds__(256) gather_min(const float4* __restrict__ T, 
       const float4* r = T + (int64_t)u * row_f4 + lane;
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
+        if (!act) continue;
         float4 x = __ldg(r + 32 * v);
         acc[v].x = fminf(acc[v].x, x.x); acc[v].y = fminf(acc[v].y, x.y);
         acc[v].z = fminf(acc[v].z, x.z); acc[v].w = fminf(acc[v].w, x.w);
       }
     }
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) out[((int64_t)(d & 4095) * VEC + v) * 32 + lane] = acc[v];
+    for (int v = 0; v < VEC; ++v) if (act) out[((int64_t)(d & 4095) * VEC + v) * 32 + lane] = acc[v];
   }
 }
 
@@ -50,16 +52,15 @@ int main() {
   for (auto& x : hc) x = g() % V;
   int* cols; cudaMalloc(&cols, hc.size() * 4); cudaMemcpy(cols, hc.data(), hc.size() * 4, cudaMemcpyHostToDevice);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (int vec = 1; vec <= 1; ++vec) {
-    const int row_f4 = 32 * vec;
+  for (int act_lanes : {30, 32}) {
+    const int row_f4 = act_lanes;
     float4* T; cudaMalloc(&T, (size_t)V * row_f4 * 16);
     fill<<<4096, 256>>>(reinterpret_cast<float*>(T), (int64_t)V * row_f4 * 4);
-    float4* out; cudaMalloc(&out, (size_t)4096 * row_f4 * 16);
+    float4* out; cudaMalloc(&out, (size_t)4096 * 32 * 16);
     for (int bps : {4, 8, 16, 64}) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
       auto run = [&]() {
-        if (vec == 1) gather_min<1><<<sms * bps, 256>>>(T, row_f4, cols, h, n_docs, out);
-        else gather_min<2><<<sms * bps, 256>>>(T, row_f4, cols, h, n_docs, out);
+        gather_min<1><<<sms * bps, 256>>>(T, row_f4, cols, h, n_docs, out, act_lanes);
       };
       run(); run();
       cudaEventRecord(a);
