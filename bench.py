@@ -397,7 +397,14 @@ def run_ours(args, cfg):
                     "frac": achieved / l2["gbs"],
                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
                     "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/roofline_traffic.json)",
+                    "traffic_launch_docs": tr.get("launch_docs") if tr else None,
+                    "traffic_over_algorithmic": tr.get("traffic_over_algorithmic") if tr else None,
+                    "ncu_lts_throughput_pct": tr.get("lts_throughput_pct") if tr else None,
+                    "ncu_l2_hit_rate_pct": tr.get("lts_hit_rate_pct") if tr else None,
                     "algorithmic_bytes_per_launch": table_bytes * args.steps / tm["launches"],
+                    "algorithmic_bytes_note": "mean over the step's launches (full doc batches + the remainder); "
+                                              "traffic_over_algorithmic compares ncu's DRAM bytes with the "
+                                              "algorithmic bytes of that same full-batch launch",
                     "peak_source": f"measured L2 gather ceiling on B200 ({l2['source']})",
                     "hbm_peak_gbs": pk.get("hbm_gbs"), "achieved_over_hbm_peak": achieved / pk.get("hbm_gbs", 1.0),
                     "per_launch_ms": tm["ms"] / max(tm["launches"], 1),

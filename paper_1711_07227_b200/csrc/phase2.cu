@@ -21,6 +21,20 @@ constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
 // segments of one word row are one contiguous 512-byte run (four 128-byte
 // lines per nonzero), with zs = 3 they are 16 separate 32-byte sectors.
 // ---------------------------------------------------------------------------
+#ifndef LCRW_SPMM_UNROLL
+#define LCRW_SPMM_UNROLL 1
+#endif
+#ifndef LCRW_SPMM_ALU_CVT
+#define LCRW_SPMM_ALU_CVT 0  // measured slower (23.2 vs 20.9 ms at C2): F2F is not the limiter
+#endif
+// exact f32 -> f64 with integer ops for positive normal floats (exponent rebias 127 -> 1023,
+// mantissa shifted into place); zero, subnormals, negatives, inf and nan take cvt
+__device__ __forceinline__ double f2d_alu(float f) {
+  const uint32_t b = __float_as_uint(f);
+  if (b - 0x00800000u >= 0x7f000000u) return (double)f;
+  return __hiloint2double((int)((b >> 3) + (896u << 20)), (int)(b << 29));
+}
+constexpr int kSpmmUnroll = LCRW_SPMM_UNROLL;  // (#pragma unroll does not expand macros)
 __global__ void __launch_bounds__(kWarps * 32)
     spmm_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ cols, const float* __restrict__ vals,
                 int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int zs, int64_t z_block_rows,
@@ -40,15 +54,25 @@ __global__ void __launch_bounds__(kWarps * 32)
       // vocabulary-sliced Z (multi-GPU all-gather): row w lives in block w / z_block_rows
       const uint32_t blk = my_c / zbr;
       const int64_t my_off = (int64_t)blk * z_block_stride + ((int64_t)(my_c - blk * zbr) << zs);
+#pragma unroll kSpmmUnroll
       for (int t = 0; t < cnt; ++t) {
         const int64_t zoff = __shfl_sync(0xffffffffu, my_off, t);
         const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
         if (active) {
           const float4 z = __ldg(reinterpret_cast<const float4*>(zq + zoff));
+#if LCRW_SPMM_ALU_CVT
+          // half of the f32 -> f64 conversions on the integer pipe: F2F runs on the XU pipe,
+          // which ncu shows saturated here (profiles/r01_spmm_full.ncu-rep)
+          a0 = fma(x, (double)z.x, a0);
+          a1 = fma(x, (double)z.y, a1);
+          a2 = fma(x, f2d_alu(z.z), a2);
+          a3 = fma(x, f2d_alu(z.w), a3);
+#else
           a0 = fma(x, (double)z.x, a0);
           a1 = fma(x, (double)z.y, a1);
           a2 = fma(x, (double)z.z, a2);
           a3 = fma(x, (double)z.w, a3);
+#endif
         }
       }
     }

@@ -71,6 +71,14 @@ constexpr int kTileStride = kChunk + 1;  // smem tile row stride (conflict-free 
 #define LCRW_TBL_MINB 4  // 4 CTAs (1024 threads) per SM: <= 64 registers
 #endif
 constexpr int kUnroll = LCRW_TBL_UNROLL;  // (#pragma unroll does not expand macros)
+#ifndef LCRW_TBL_PANELS
+#define LCRW_TBL_PANELS 1
+#endif
+#ifndef LCRW_TBL_DYN
+#define LCRW_TBL_DYN 0
+#endif
+constexpr int kCtaPanels = LCRW_TBL_PANELS;        // 32-doc Z2 panels per CTA
+constexpr int kCtaDocs = kCtaPanels * kPanelDocs;  // docs per CTA
 
 // Sets word w's key in row u (atomics: the fields of one 32-bit word belong to
 // different words w).  Cross-check and exact-zero paths only; the build writes whole words.
@@ -123,78 +131,111 @@ __global__ void table_zeros_kernel(const int32_t* __restrict__ canon, const int3
   }
 }
 
-// One CTA per (chunk c, 32-doc panel p), panels fastest so the CTAs in flight share
-// one L2-resident chunk (v_rows x 480 B: 48 MB at V = 100k).  Warp j takes docs j,
-// j+8, j+16, j+24; lane l < 30 owns words 6l..6l+5 of the chunk: per doc word, one
-// 16-byte load of their six 21-bit keys (the warp reads the 480-byte row once: 180
-// distances, 2.67 bytes each).  Four keys sit in the top 21 bits of the group's 32-bit
-// words, so their minima are plain integer minima of the words; the other two are
-// reassembled from the words' low 11 bits with one shift + one funnel shift each;
-// the 32 x 180 result is decoded, unscaled, staged in smem (row stride 181:
+struct Keys {
+  uint32_t k0, k1, k2, k3, k4, k5;
+};
+// the 16-byte group of a row: four keys in the top 21 bits of the words, two reassembled
+// from the 11-bit pieces (key << 11 == funnelshift_l(q_odd << 21, q_even, 21))
+__device__ __forceinline__ void keys_min1(Keys& k, const uint4 r) {
+  k.k0 = min(k.k0, r.x);
+  k.k1 = min(k.k1, r.y);
+  k.k2 = min(k.k2, r.z);
+  k.k3 = min(k.k3, r.w);
+  k.k4 = min(k.k4, __funnelshift_l(r.y << 21, r.x, 21));
+  k.k5 = min(k.k5, __funnelshift_l(r.w << 21, r.z, 21));
+}
+// Work unit = (chunk c, kCtaPanels consecutive 32-doc panels), panels fastest, so the
+// units in flight share one L2-resident chunk (v_rows x 480 B: 48 MB at V = 100k);
+// one CTA per unit (4 resident per SM).  Warp j takes docs j, j+8, ... (LCRW_TBL_DYN=1:
+// an smem counter hands out docs one at a time -- measured neutral); lane l < 30 owns
+// words 6l..6l+5: per doc word, one 16-byte load of their six 21-bit keys (the warp reads
+// the 480-byte row once: 180 distances, 2.67 bytes each).  Four keys sit in the top 21 bits of
+// the group's words, so their minima are plain integer minima of the words; the other two
+// are reassembled from the words' low 11 bits with one shift + one funnel shift each.
+// The 32 x 180 result per panel is decoded, unscaled, staged in smem (row stride 181:
 // conflict-free both ways) and written as 180 coalesced 128-byte Z2 rows:
 // Z2[p * z_panel + w * 32 + doc].
 __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uint8_t* __restrict__ T, int64_t v_rows, int64_t a_rows,
                                                         const int64_t* __restrict__ doc_offsets, int64_t seg_base,
                                                         int64_t n_docs, const int32_t* __restrict__ cols,
                                                         const float* __restrict__ scale, float* __restrict__ Z2,
-                                                        int64_t z_panel, int64_t panels,
+                                                        int64_t z_panel, int64_t cta_units,
                                                         const float* __restrict__ a_norms, RefineSink sink) {
-  __shared__ float tile[kPanelDocs * kTileStride];
+  __shared__ float tile[kCtaDocs * kTileStride];
   __shared__ float wsq[kChunk];  // the chunk words' scaled squared norms (refine test)
+  __shared__ int next_doc;       // dynamic doc assignment: warps take the unit's docs one at a time
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c = blockIdx.x / panels, p = blockIdx.x - c * panels;
-  if (sink.list && threadIdx.x < kChunk)
-    wsq[threadIdx.x] = c * kChunk + threadIdx.x < a_rows ? __ldg(a_norms + c * kChunk + threadIdx.x) : 0.f;
   const bool active = lane < kTableGroups;
-  // lanes 30, 31 repeat lane 29's 16 bytes (same sector: no extra traffic) so the loop has no
-  // predication; their minima are discarded
-  const uint4* Tc = reinterpret_cast<const uint4*>(T + c * v_rows * kTableRowBytes) + (active ? lane : kTableGroups - 1);
   const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
   const float inv_scale = __ldg(scale + 1);
-  for (int dd = warp; dd < kPanelDocs; dd += 8) {
-    const int64_t d = p * kPanelDocs + dd;
-    uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu, k2 = 0xFFFFFFFFu, k3 = 0xFFFFFFFFu, k4 = 0xFFFFFFFFu,
-             k5 = 0xFFFFFFFFu;
-    if (d < n_docs) {
-      const int64_t b = __ldg(doc_offsets + d) - seg_base, e = __ldg(doc_offsets + d + 1) - seg_base;
-      for (int64_t j0 = b; j0 < e; j0 += 32) {
-        const int n = e - j0 < 32 ? (int)(e - j0) : 32;
-        const int mine = lane < n ? ld_stream(cols + j0 + lane, stream) : 0;
+  const float s0 = __ldg(scale);
+  {  // one work unit per CTA (a persistent loop over units measured 2.6x slower: CTAs drift
+     // apart and the chunks in flight no longer fit L2)
+    const int64_t unit = blockIdx.x;
+    const int64_t c = unit / cta_units, u0 = unit - c * cta_units;
+    const int64_t d0 = u0 * kCtaDocs;  // first doc of the unit
+    if (threadIdx.x == 0) next_doc = 8;
+    if (sink.list && threadIdx.x < kChunk)
+      wsq[threadIdx.x] = c * kChunk + threadIdx.x < a_rows ? __ldg(a_norms + c * kChunk + threadIdx.x) : 0.f;
+    __syncthreads();
+    // lanes 30, 31 repeat lane 29's 16 bytes (same sector: no extra traffic) so the loop has
+    // no predication; their minima are discarded
+    const uint4* Tc =
+        reinterpret_cast<const uint4*>(T + c * v_rows * kTableRowBytes) + (active ? lane : kTableGroups - 1);
+    for (int dd = warp; dd < kCtaDocs;) {
+      const int64_t d = d0 + dd;
+      Keys k{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+      if (d < n_docs) {
+        const int64_t b = __ldg(doc_offsets + d) - seg_base, e = __ldg(doc_offsets + d + 1) - seg_base;
+        for (int64_t j0 = b; j0 < e; j0 += 32) {
+          const int n = e - j0 < 32 ? (int)(e - j0) : 32;
+          const int mine = lane < n ? ld_stream(cols + j0 + lane, stream) : 0;
 #pragma unroll kUnroll
-        for (int j = 0; j < n; ++j) {
-          const int u = __shfl_sync(0xffffffffu, mine, j);
-          const uint4 r = ld_keep_u4(Tc + (int64_t)u * (kTableRowBytes / 16), keep);
-          k0 = min(k0, r.x);  // key of word 6l in the top 21 bits
-          k1 = min(k1, r.y);
-          k2 = min(k2, r.z);
-          k3 = min(k3, r.w);
-          k4 = min(k4, __funnelshift_l(r.y << 21, r.x, 21));  // key of word 6l+4 << 11
-          k5 = min(k5, __funnelshift_l(r.w << 21, r.z, 21));  // key of word 6l+5 << 11
+          for (int j = 0; j < n; ++j) {
+            const int u = __shfl_sync(0xffffffffu, mine, j);
+            keys_min1(k, ld_keep_u4(Tc + (int64_t)u * (kTableRowBytes / 16), keep));
+          }
         }
       }
+      if (active) {
+        float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
+        trow[0] = key21_dist(k.k0 >> 11) * inv_scale;
+        trow[1] = key21_dist(k.k1 >> 11) * inv_scale;
+        trow[2] = key21_dist(k.k2 >> 11) * inv_scale;
+        trow[3] = key21_dist(k.k3 >> 11) * inv_scale;
+        trow[4] = key21_dist(k.k4 >> 11) * inv_scale;
+        trow[5] = key21_dist(k.k5 >> 11) * inv_scale;
+      }
+#if LCRW_TBL_DYN
+      int nd = 0;
+      if (lane == 0) nd = atomicAdd(&next_doc, 1);
+      dd = __shfl_sync(0xffffffffu, nd, 0);
+#else
+      dd += 8;
+#endif
     }
-    if (active) {
-      float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
-      trow[0] = key21_dist(k0 >> 11) * inv_scale;
-      trow[1] = key21_dist(k1 >> 11) * inv_scale;
-      trow[2] = key21_dist(k2 >> 11) * inv_scale;
-      trow[3] = key21_dist(k3 >> 11) * inv_scale;
-      trow[4] = key21_dist(k4 >> 11) * inv_scale;
-      trow[5] = key21_dist(k5 >> 11) * inv_scale;
-    }
-  }
-  __syncthreads();
-  float* zp = Z2 + p * z_panel;
-  const int64_t w0 = c * kChunk;
-  const float s0 = __ldg(scale);
-  const bool doc_ok = p * kPanelDocs + lane < n_docs;
-  for (int q = warp; q < kChunk; q += 8) {  // lane = doc; word q of the chunk
-    if (w0 + q < a_rows) {
-      const float v = tile[lane * kTileStride + q];
-      st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);
-      // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
-      if (sink.list && doc_ok && refine_flag(v * s0, wsq[q], kRefineTau * kRefineTau))
-        refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
+    __syncthreads();
+    const int64_t w0 = c * kChunk;
+#pragma unroll
+    for (int pp = 0; pp < kCtaPanels; ++pp) {
+      const int64_t p = u0 * kCtaPanels + pp;
+      if (p * kPanelDocs >= n_docs) break;
+      float* zp = Z2 + p * z_panel;
+      const bool doc_ok = p * kPanelDocs + lane < n_docs;
+      const float* trow = tile + (pp * kPanelDocs + lane) * kTileStride;
+      for (int q = warp; q < kChunk; q += 8) {  // lane = doc; word q of the chunk
+        if (w0 + q < a_rows) {
+          const float v = trow[q];
+#ifndef LCRW_TBL_NOSTORE
+          st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);
+#else
+          if (v == -1.f) st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);  // experiment: stores skipped
+#endif
+          // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
+          if (sink.list && doc_ok && refine_flag(v * s0, wsq[q], kRefineTau * kRefineTau))
+            refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
+        }
+      }
     }
   }
 }
@@ -273,13 +314,14 @@ int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t*
                "lcrw_table_min: a refine list needs a_norms, its count and capacity");
   LCRW_REQUIRE(z_panel == a_rows * tbl::kPanelDocs && (reinterpret_cast<uintptr_t>(T) & 15) == 0,
                "lcrw_table_min: Z2 must be in 32-doc panels (z_panel = 32 * a_rows), T 16-byte aligned");
-  const int64_t panels = ceil_div(n_docs, tbl::kPanelDocs);
-  const int64_t blocks = ceil_div(a_rows, tbl::kChunk) * panels;
+  const int64_t units = ceil_div(n_docs, tbl::kCtaDocs);
+  const int64_t n_units = ceil_div(a_rows, tbl::kChunk) * units;
+  const int64_t blocks = n_units;
   LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_table_min: too many (chunk, panel) blocks for one launch");
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "table_min");
   tbl::table_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(T), v_rows, a_rows, doc_offsets,
-                                                          seg_base, n_docs, doc_cols, scale, Z2, z_panel, panels, a_norms,
+                                                          seg_base, n_docs, doc_cols, scale, Z2, z_panel, units, a_norms,
       RefineSink{static_cast<uint2*>(refine_list), refine_count, refine_cap});
   LCRW_CHECK_LAUNCH("table_min_kernel");
   return LCRW_OK;

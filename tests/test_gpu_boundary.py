@@ -201,3 +201,31 @@ def test_engine_wmd_keeps_f64():
             want, _ = emd.prefiltered_topk_wmd(x, q.row(j), E, 4)
             assert r.distances.dtype == np.float64
             assert np.array_equal(r.ids, want.ids) and np.array_equal(r.distances, want.distances), (method, j)
+
+
+@pytest.mark.parametrize("k", [1, 10, 32, 33])
+@pytest.mark.parametrize("reverse", ["table", "gemm"])
+def test_fused_topk_equals_topk_of_materialised_d(monkeypatch, k, reverse):
+    """The max -> top-k fused into lcrw_reverse_panels (per-(query, CTA) lists, k <= 32,
+    no D) returns exactly the (distance, id) top-k of the materialised query-major D
+    (LCRW_TOPK_VIA_D), ties included: duplicated docs give equal distances that must be
+    ordered by id (kernels.py:218-223).  k = 33 takes the D path both times."""
+    import torch
+    from paper_1711_07227_b200 import device, synthetic as S
+    monkeypatch.setenv("LCRW_REVERSE", reverse)
+    V = 4000
+    E = S.embeddings(V, 300, seed=11)
+    base = S.histograms(1500, V, 40, seed=12)
+    x1 = base.take_rows(np.concatenate([np.arange(1500), np.arange(0, 1500, 7), np.arange(3, 1500, 11)]))
+    x2 = S.histograms(40, V, 40, seed=13)
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    fd, fi = device.symmetric(d1, d2, prep, k, id_offset=5)
+    monkeypatch.setenv("LCRW_TOPK_VIA_D", "1")
+    rd, ri = device.symmetric(d1, d2, prep, k, id_offset=5)
+    assert torch.equal(fd, rd) and torch.equal(fi, ri)
+    full = device.symmetric(d1, d2, prep, None).cpu().numpy()  # (n1, n2)
+    for j in range(x2.n_rows):
+        order = np.lexsort((np.arange(x1.n_rows), full[:, j]))[:k]
+        assert np.array_equal(fi[j].cpu().numpy(), order + 5)
+        assert np.array_equal(fd[j].cpu().numpy(), full[order, j])
