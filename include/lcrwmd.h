@@ -135,6 +135,13 @@ int lcrw_zero_identical(const int64_t* seg_offsets, int64_t n_seg, const int32_t
 int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
               int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
               int64_t ld_row, int64_t ld_panel, void* stream);
+/* The same product when every Z entry is a distance -- finite, >= 0, zero or normal
+ * (lcrw_phase1 / lcrw_refine_near output) -- bitwise equal to lcrw_spmm; the f32 -> f64
+ * widening runs on the integer pipe (entries outside that domain give wrong results:
+ * use lcrw_spmm for general matrices). */
+int lcrw_spmm_dist(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
+                   int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg,
+                   float* out, int64_t ld_row, int64_t ld_panel, void* stream);
 
 /* Reverse direction, panel-streaming form: work item = (32-doc Z2 panel, group
  * of G = lcrw_reverse_panels_group() queries); persistent CTAs stream each

@@ -46,6 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_phase1": (I32, [P, P, I64, P, I64, I32, I32, P, I64, I64, P, P, I64, P, P, I64, I32, P]),
     "lcrw_zero_identical": (I32, [P, I64, P, P, P, P, I64, I32, P]),
     "lcrw_spmm": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
+    "lcrw_spmm_dist": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
                                     I64, P, P, I32, I64, I64, I32, P, P, I32, P, P, P, SZ, P]),
@@ -96,7 +97,7 @@ _VALUE_FUNCS = {"lcrw_emd_problem_bytes", "lcrw_abi_version", "lcrw_status_strin
 KERNELS_PER_CALL = {
     "lcrw_max_sqnorm": 1, "lcrw_scale_from_max_sqnorm": 1, "lcrw_prepare_rows": 1, "lcrw_gather_rows": 1,
     "lcrw_row_classes": 13, "lcrw_match_rows": 2, "lcrw_restrict": 4, "lcrw_remap_ids": 1,
-    "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1,
+    "lcrw_segment_plan": 2, "lcrw_phase1": 1, "lcrw_zero_identical": 1, "lcrw_spmm": 1, "lcrw_spmm_dist": 1,
     "lcrw_topk_segments": 1, "lcrw_topk_sort": 7, "lcrw_topk_rows": 2,
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
     "lcrw_max_transposed_into": 1, "lcrw_table_transpose": 1, "lcrw_table_min": 1,

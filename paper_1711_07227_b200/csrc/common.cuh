@@ -366,7 +366,10 @@ __device__ __forceinline__ void refine_append(uint2* list, uint32_t* count, int6
 constexpr int kTableChunk = 180;
 constexpr int kTableKeysPerGroup = 6;
 constexpr int kTableGroups = 30;
-constexpr int kTableRowBytes = 480;
+#ifndef LCRW_TABLE_ROW_BYTES
+#define LCRW_TABLE_ROW_BYTES 480
+#endif
+constexpr int kTableRowBytes = LCRW_TABLE_ROW_BYTES;  // row stride (30 groups used; 512 = 128-B aligned rows)
 constexpr int kTableWarpRows = 30;  // real rows per 32-row warp block of the padded operand
 // word q_i of key p's group inside a row: byte offset of the group and the key's slot i
 __host__ __device__ __forceinline__ void table_key_slot(int p, int& group_byte, int& slot) {

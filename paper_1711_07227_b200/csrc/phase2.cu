@@ -24,22 +24,28 @@ constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
 #ifndef LCRW_SPMM_UNROLL
 #define LCRW_SPMM_UNROLL 1
 #endif
-#ifndef LCRW_SPMM_ALU_CVT
-#define LCRW_SPMM_ALU_CVT 0  // measured slower (23.2 vs 20.9 ms at C2): F2F is not the limiter
+#ifndef LCRW_SPMM_NZ_SMEM
+#define LCRW_SPMM_NZ_SMEM 1
 #endif
-// exact f32 -> f64 with integer ops for positive normal floats (exponent rebias 127 -> 1023,
-// mantissa shifted into place); zero, subnormals, negatives, inf and nan take cvt
-__device__ __forceinline__ double f2d_alu(float f) {
-  const uint32_t b = __float_as_uint(f);
-  if (b - 0x00800000u >= 0x7f000000u) return (double)f;
-  return __hiloint2double((int)((b >> 3) + (896u << 20)), (int)(b << 29));
+// Z holding distances (finite, >= 0, zero or normal: the pipeline's Z1) lets the f32 -> f64
+// widening run on the integer pipe: the f32 bits shifted into an f64 word are z * 2^-896
+// exactly (exponent field kept, not rebiased; 0 stays 0), and the weight carries the 2^896,
+// so fma(x * 2^896, z * 2^-896, acc) == fma(x, (double)z, acc) bit for bit, two shifts
+// instead of an F2F on the XU pipe (16 lanes/clk/SM, which ncu shows saturated here).
+__device__ __forceinline__ double dist_f64_scaled(float z) {
+  const uint32_t b = __float_as_uint(z);
+  return __hiloint2double((int)(b >> 3), (int)(b << 29));
 }
 constexpr int kSpmmUnroll = LCRW_SPMM_UNROLL;  // (#pragma unroll does not expand macros)
+template <bool kDist>
 __global__ void __launch_bounds__(kWarps * 32)
     spmm_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ cols, const float* __restrict__ vals,
                 int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int zs, int64_t z_block_rows,
                 int64_t z_block_stride, int64_t n_seg, float* __restrict__ out, int64_t ld_row, int64_t ld_panel) {
   const int lane = threadIdx.x & 31;
+#if LCRW_SPMM_NZ_SMEM
+  __shared__ longlong2 nz_s[kWarps][32];
+#endif
   const int64_t q0 = (int64_t)blockIdx.y * kSegPerBlock + lane * 4;
   const bool active = q0 < n_seg;
   const float* zq = Z + (q0 >> zs) * z_panel + (q0 & ((1 << zs) - 1));
@@ -54,25 +60,39 @@ __global__ void __launch_bounds__(kWarps * 32)
       // vocabulary-sliced Z (multi-GPU all-gather): row w lives in block w / z_block_rows
       const uint32_t blk = my_c / zbr;
       const int64_t my_off = (int64_t)blk * z_block_stride + ((int64_t)(my_c - blk * zbr) << zs);
+#if LCRW_SPMM_NZ_SMEM
+      // (offset, weight) of the 32 nonzeros staged per warp and read back as one broadcast
+      // LDS.128 each, instead of three SHFLs (a 64-bit offset + the weight) that share the
+      // L1TEX data pipe with the Z row loads
+      __syncwarp();
+      nz_s[threadIdx.x >> 5][lane] = make_longlong2(my_off, (long long)__float_as_int(my_x));
+      __syncwarp();
+#endif
 #pragma unroll kSpmmUnroll
       for (int t = 0; t < cnt; ++t) {
+#if LCRW_SPMM_NZ_SMEM
+        const longlong2 e = nz_s[threadIdx.x >> 5][t];
+        const int64_t zoff = e.x;
+        const float xf = __int_as_float((int)e.y);
+#else
         const int64_t zoff = __shfl_sync(0xffffffffu, my_off, t);
-        const double x = (double)__shfl_sync(0xffffffffu, my_x, t);
+        const float xf = __shfl_sync(0xffffffffu, my_x, t);
+#endif
+        const double x = (double)xf;
         if (active) {
           const float4 z = __ldg(reinterpret_cast<const float4*>(zq + zoff));
-#if LCRW_SPMM_ALU_CVT
-          // half of the f32 -> f64 conversions on the integer pipe: F2F runs on the XU pipe,
-          // which ncu shows saturated here (profiles/r01_spmm_full.ncu-rep)
-          a0 = fma(x, (double)z.x, a0);
-          a1 = fma(x, (double)z.y, a1);
-          a2 = fma(x, f2d_alu(z.z), a2);
-          a3 = fma(x, f2d_alu(z.w), a3);
-#else
-          a0 = fma(x, (double)z.x, a0);
-          a1 = fma(x, (double)z.y, a1);
-          a2 = fma(x, (double)z.z, a2);
-          a3 = fma(x, (double)z.w, a3);
-#endif
+          if (kDist && fabsf(xf) < 0x1p126f) {  // (x * 2^896 stays finite; warp-uniform branch)
+            const double xs = x * 0x1p896;
+            a0 = fma(xs, dist_f64_scaled(z.x), a0);
+            a1 = fma(xs, dist_f64_scaled(z.y), a1);
+            a2 = fma(xs, dist_f64_scaled(z.z), a2);
+            a3 = fma(xs, dist_f64_scaled(z.w), a3);
+          } else {
+            a0 = fma(x, (double)z.x, a0);
+            a1 = fma(x, (double)z.y, a1);
+            a2 = fma(x, (double)z.z, a2);
+            a3 = fma(x, (double)z.w, a3);
+          }
         }
       }
     }
@@ -400,9 +420,9 @@ using namespace lcrw::p2;
 
 extern "C" {
 
-int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
-              int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
-              int64_t ld_row, int64_t ld_panel, void* stream) {
+static int spmm_launch(bool dist, const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows,
+                       const float* Z, int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride,
+                       int64_t n_seg, float* out, int64_t ld_row, int64_t ld_panel, void* stream) {
   LCRW_REQUIRE(n_rows >= 0 && n_seg >= 0, "lcrw_spmm: bad shape");
   if (n_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(offs && cols && vals && Z && out, "lcrw_spmm: null pointer");
@@ -416,10 +436,31 @@ int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64
   const int64_t cap = (int64_t)sm_count() * 64;
   if (gx > cap) gx = cap;
   ProfScope prof(as_stream(stream), "spmm");
-  spmm_kernel<<<dim3((unsigned)gx, (unsigned)gy), kWarps * 32, 0, as_stream(stream)>>>(
-      offs, cols, vals, n_rows, Z, z_panel, z_shift, z_block_rows, z_block_stride, n_seg, out, ld_row, ld_panel);
+  const dim3 grid((unsigned)gx, (unsigned)gy);
+  if (dist)
+    spmm_kernel<true><<<grid, kWarps * 32, 0, as_stream(stream)>>>(offs, cols, vals, n_rows, Z, z_panel, z_shift,
+                                                                  z_block_rows, z_block_stride, n_seg, out, ld_row,
+                                                                  ld_panel);
+  else
+    spmm_kernel<false><<<grid, kWarps * 32, 0, as_stream(stream)>>>(offs, cols, vals, n_rows, Z, z_panel, z_shift,
+                                                                   z_block_rows, z_block_stride, n_seg, out, ld_row,
+                                                                   ld_panel);
   LCRW_CHECK_LAUNCH("spmm_kernel");
   return LCRW_OK;
+}
+
+int lcrw_spmm(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
+              int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg, float* out,
+              int64_t ld_row, int64_t ld_panel, void* stream) {
+  return spmm_launch(false, offs, cols, vals, n_rows, Z, z_panel, z_shift, z_block_rows, z_block_stride, n_seg, out,
+                     ld_row, ld_panel, stream);
+}
+
+int lcrw_spmm_dist(const int64_t* offs, const int32_t* cols, const float* vals, int64_t n_rows, const float* Z,
+                   int64_t z_panel, int z_shift, int64_t z_block_rows, int64_t z_block_stride, int64_t n_seg,
+                   float* out, int64_t ld_row, int64_t ld_panel, void* stream) {
+  return spmm_launch(true, offs, cols, vals, n_rows, Z, z_panel, z_shift, z_block_rows, z_block_stride, n_seg, out,
+                     ld_row, ld_panel, stream);
 }
 
 

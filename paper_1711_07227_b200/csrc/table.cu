@@ -68,15 +68,25 @@ constexpr int kTileStride = kChunk + 1;  // smem tile row stride (conflict-free 
 #define LCRW_TBL_UNROLL 8
 #endif
 #ifndef LCRW_TBL_MINB
-#define LCRW_TBL_MINB 4  // 4 CTAs (1024 threads) per SM: <= 64 registers
+#define LCRW_TBL_MINB 5  // 5 CTAs (40 warps) per SM: <= 48 registers
 #endif
-constexpr int kUnroll = LCRW_TBL_UNROLL;  // (#pragma unroll does not expand macros)
+[[maybe_unused]] constexpr int kUnroll = LCRW_TBL_UNROLL;  // (#pragma unroll does not expand macros)
 #ifndef LCRW_TBL_PANELS
 #define LCRW_TBL_PANELS 1
 #endif
 #ifndef LCRW_TBL_DYN
 #define LCRW_TBL_DYN 0
 #endif
+#ifndef LCRW_TBL_IDS_SMEM
+#define LCRW_TBL_IDS_SMEM 1
+#endif
+#ifndef LCRW_TBL_TILE_ROT
+#define LCRW_TBL_TILE_ROT 0  // measured neutral-to-worse (331 vs 329 ms)
+#endif
+#ifndef LCRW_TBL_QUAD_UNROLL
+#define LCRW_TBL_QUAD_UNROLL 1
+#endif
+constexpr int kQuadUnroll = LCRW_TBL_QUAD_UNROLL;  // quads of rows per unrolled step (4 rows in flight x 40 warps)
 constexpr int kCtaPanels = LCRW_TBL_PANELS;        // 32-doc Z2 panels per CTA
 constexpr int kCtaDocs = kCtaPanels * kPanelDocs;  // docs per CTA
 
@@ -163,7 +173,12 @@ __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uin
                                                         const float* __restrict__ a_norms, RefineSink sink) {
   __shared__ float tile[kCtaDocs * kTileStride];
   __shared__ float wsq[kChunk];  // the chunk words' scaled squared norms (refine test)
-  __shared__ int next_doc;       // dynamic doc assignment: warps take the unit's docs one at a time
+#if LCRW_TBL_DYN
+  __shared__ int next_doc;  // dynamic doc assignment: warps take the unit's docs one at a time
+#endif
+#if LCRW_TBL_IDS_SMEM
+  __shared__ __align__(16) int ids_s[8][32];  // per-warp word ids of the current 32-word block
+#endif
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool active = lane < kTableGroups;
   const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
@@ -174,10 +189,20 @@ __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uin
     const int64_t unit = blockIdx.x;
     const int64_t c = unit / cta_units, u0 = unit - c * cta_units;
     const int64_t d0 = u0 * kCtaDocs;  // first doc of the unit
+#if LCRW_TBL_DYN
     if (threadIdx.x == 0) next_doc = 8;
+#endif
     if (sink.list && threadIdx.x < kChunk)
       wsq[threadIdx.x] = c * kChunk + threadIdx.x < a_rows ? __ldg(a_norms + c * kChunk + threadIdx.x) : 0.f;
     __syncthreads();
+    // the chunk's largest squared norm: an entry at or above tau * max|a| cannot be near, so the
+    // per-word norm is only read for the (rare) entries below it
+    float wsq_max = 0.f;
+    if (sink.list) {
+      for (int q = lane; q < kChunk; q += 32) wsq_max = fmaxf(wsq_max, wsq[q]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wsq_max = fmaxf(wsq_max, __shfl_xor_sync(0xffffffffu, wsq_max, o));
+    }
     // lanes 30, 31 repeat lane 29's 16 bytes (same sector: no extra traffic) so the loop has
     // no predication; their minima are discarded
     const uint4* Tc =
@@ -190,21 +215,59 @@ __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uin
         for (int64_t j0 = b; j0 < e; j0 += 32) {
           const int n = e - j0 < 32 ? (int)(e - j0) : 32;
           const int mine = lane < n ? ld_stream(cols + j0 + lane, stream) : 0;
+#if LCRW_TBL_IDS_SMEM
+          // word ids broadcast four at a time from a per-warp smem slot (one LDS.128 wavefront
+          // per 4 words instead of 4 SHFL wavefronts, which share the L1TEX data pipe with the
+          // table loads)
+          __syncwarp();
+          ids_s[warp][lane] = mine;
+          __syncwarp();
+          const int4* q4 = reinterpret_cast<const int4*>(ids_s[warp]);
+          int j = 0;
+#pragma unroll kQuadUnroll
+          for (; j + 4 <= n; j += 4) {
+            const int4 u4 = q4[j >> 2];
+            const uint4 r0 = ld_keep_u4(Tc + (int64_t)u4.x * (kTableRowBytes / 16), keep);
+            const uint4 r1 = ld_keep_u4(Tc + (int64_t)u4.y * (kTableRowBytes / 16), keep);
+            const uint4 r2 = ld_keep_u4(Tc + (int64_t)u4.z * (kTableRowBytes / 16), keep);
+            const uint4 r3 = ld_keep_u4(Tc + (int64_t)u4.w * (kTableRowBytes / 16), keep);
+            keys_min1(k, r0);
+            keys_min1(k, r1);
+            keys_min1(k, r2);
+            keys_min1(k, r3);
+          }
+          for (; j < n; ++j) keys_min1(k, ld_keep_u4(Tc + (int64_t)ids_s[warp][j] * (kTableRowBytes / 16), keep));
+#else
 #pragma unroll kUnroll
           for (int j = 0; j < n; ++j) {
             const int u = __shfl_sync(0xffffffffu, mine, j);
             keys_min1(k, ld_keep_u4(Tc + (int64_t)u * (kTableRowBytes / 16), keep));
           }
+#endif
         }
       }
       if (active) {
         float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
+#if LCRW_TBL_TILE_ROT
+        // lanes l and l + 16 map to the same bank (6 * 16 = 96 = 0 mod 32): the upper half
+        // writes its six values rotated by three, so every store is conflict-free
+        const float v[kTableKeysPerGroup] = {key21_dist(k.k0 >> 11) * inv_scale, key21_dist(k.k1 >> 11) * inv_scale,
+                                             key21_dist(k.k2 >> 11) * inv_scale, key21_dist(k.k3 >> 11) * inv_scale,
+                                             key21_dist(k.k4 >> 11) * inv_scale, key21_dist(k.k5 >> 11) * inv_scale};
+        const bool hi = lane >= 16;
+#pragma unroll
+        for (int t = 0; t < kTableKeysPerGroup; ++t) {
+          const int r = (t + 3) % kTableKeysPerGroup;
+          trow[hi ? r : t] = hi ? v[r] : v[t];
+        }
+#else
         trow[0] = key21_dist(k.k0 >> 11) * inv_scale;
         trow[1] = key21_dist(k.k1 >> 11) * inv_scale;
         trow[2] = key21_dist(k.k2 >> 11) * inv_scale;
         trow[3] = key21_dist(k.k3 >> 11) * inv_scale;
         trow[4] = key21_dist(k.k4 >> 11) * inv_scale;
         trow[5] = key21_dist(k.k5 >> 11) * inv_scale;
+#endif
       }
 #if LCRW_TBL_DYN
       int nd = 0;
@@ -232,7 +295,9 @@ __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uin
           if (v == -1.f) st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);  // experiment: stores skipped
 #endif
           // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
-          if (sink.list && doc_ok && refine_flag(v * s0, wsq[q], kRefineTau * kRefineTau))
+          const float ds = v * s0;
+          if (sink.list && doc_ok && ds * ds < kRefineTau * kRefineTau * wsq_max &&
+              refine_flag(ds, wsq[q], kRefineTau * kRefineTau))
             refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
         }
       }

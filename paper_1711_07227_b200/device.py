@@ -294,8 +294,9 @@ def refine_near(Z, z_panel, z_shift, a_rows, n_seg, seg_offsets, seg_ids, a_ids,
 
 
 def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel,
-         z_block_rows: int = 0, z_block_stride: int = 0, z_shift: int = 3) -> None:
-    _lib.call("lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, z_shift, z_block_rows,
+         z_block_rows: int = 0, z_block_stride: int = 0, z_shift: int = 3, dist: bool = False) -> None:
+    """lcrw_spmm, or lcrw_spmm_dist (bitwise the same) when Z holds Phase-1 distances."""
+    _lib.call("lcrw_spmm_dist" if dist else "lcrw_spmm", _p(x_offsets), _p(x_cols), _p(x_vals), n_rows, _p(Z), z_panel, z_shift, z_block_rows,
               z_block_stride, n_seg, _p(out), ld_row, ld_panel, _stream())
 
 
@@ -396,7 +397,7 @@ def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR,
         ld_row, ld_panel = 8, 8 * n_res
         if n_q % 8:  # the last panel's padding queries: defined values (lcrw_reverse_panels reads 8 at a time)
             out[(n_q // 8) * 8 * n_res:].zero_()
-    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel, z_shift=zs)
+    spmm(res.csr.offsets, res.cols_r, res.csr.vals, n_res, Z, zp, n_q, out, ld_row, ld_panel, z_shift=zs, dist=True)
     return out
 
 
@@ -753,7 +754,7 @@ def forward_rows_into(res: "Restricted", prep: PreparedEmbeddings, q: DeviceCSR,
         zs = spmm_z_shift(nq)
         Z, zp = nearest_distances(res, prep, seg, q.cols[lo:hi], nq, zs)
         out = D.view(-1)[q0:]  # D[i, q0 + c] = out[i * ld + c]
-        spmm(res.csr.offsets, res.cols_r, res.csr.vals, n, Z, zp, nq, out, ld, 8, z_shift=zs)
+        spmm(res.csr.offsets, res.cols_r, res.csr.vals, n, Z, zp, nq, out, ld, 8, z_shift=zs, dist=True)
         del Z
 
 

@@ -146,7 +146,7 @@ def d1_from_slices(dx1: DeviceCSR, zall: torch.Tensor, R: int, n_q: int) -> torc
     if n_q % 8:  # padding queries of the last panel (read 8 at a time by lcrw_reverse_panels)
         out[(n_q // 8) * 8 * max(n1, 1):].zero_()
     device.spmm(dx1.offsets, dx1.cols, dx1.vals, n1, zall, W * R, n_q, out, 8, 8 * n1,
-                z_block_rows=R, z_block_stride=panels * R * W, z_shift=zs)
+                z_block_rows=R, z_block_stride=panels * R * W, z_shift=zs, dist=True)
     return out
 
 

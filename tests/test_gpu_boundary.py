@@ -229,3 +229,49 @@ def test_fused_topk_equals_topk_of_materialised_d(monkeypatch, k, reverse):
         order = np.lexsort((np.arange(x1.n_rows), full[:, j]))[:k]
         assert np.array_equal(fi[j].cpu().numpy(), order + 5)
         assert np.array_equal(fd[j].cpu().numpy(), full[order, j])
+
+
+def test_spmm_dist_bitwise_equals_spmm():
+    """lcrw_spmm_dist (f32 -> f64 widening by exponent shift, weight pre-scaled by 2^896)
+    equals lcrw_spmm bit for bit on distance matrices: zeros, tiny and large normal
+    values, and weights that take the fallback (|x| >= 2^126)."""
+    import torch
+    from paper_1711_07227_b200 import device
+    rng = np.random.default_rng(21)
+    V, n, nq = 700, 300, 37
+    rows = []
+    for i in range(n):
+        ids = np.sort(rng.choice(V, int(rng.integers(1, 60)), replace=False)).astype(np.int32)
+        x = (rng.random(len(ids)) + 0.05).astype(np.float32)
+        if i % 50 == 0:
+            x[0] = np.float32(2.0 ** 126 * 1.5)  # fallback path
+        rows.append((ids, x))
+    offs = np.zeros(n + 1, np.int64)
+    offs[1:] = np.cumsum([len(r[0]) for r in rows])
+    cols = np.concatenate([r[0] for r in rows])
+    vals = np.concatenate([r[1] for r in rows])
+    z = (rng.random((V, nq)) * 30).astype(np.float32)
+    z[rng.random((V, nq)) < 0.05] = 0.0
+    z[rng.random((V, nq)) < 0.01] = np.float32(1e-20)
+    z[rng.random((V, nq)) < 0.01] = np.float32(3e30)
+    dev = torch.device("cuda")
+    zs = 3
+    w = 1 << zs
+    panels = (nq + w - 1) // w
+    Zp = np.zeros((panels, V, w), np.float32)
+    for p in range(panels):
+        c = z[:, p * w:(p + 1) * w]
+        Zp[p, :, :c.shape[1]] = c
+    Zd = torch.as_tensor(Zp.ravel(), device=dev)
+    o, c_, v_ = (torch.as_tensor(a, device=dev) for a in (offs, cols, vals))
+    out = {}
+    for dist in (False, True):
+        t = torch.empty(n * nq, dtype=torch.float32, device=dev)
+        device.spmm(o, c_, v_, n, Zd, w * V, nq, t, nq, 8, z_shift=zs, dist=dist)
+        out[dist] = t.cpu().numpy()
+    assert np.array_equal(out[False].view(np.uint32), out[True].view(np.uint32))
+    ref = np.array([(vals[offs[i]:offs[i + 1]].astype(np.float64)[:, None] * z[cols[offs[i]:offs[i + 1]]]
+                     .astype(np.float64)).sum(0) for i in range(n)], dtype=np.float64)
+    with np.errstate(over="ignore"):  # the 2^126 weights times 3e30 overflow f32, as in the kernel
+        ref = ref.astype(np.float32).ravel()
+    assert np.allclose(out[True], ref, rtol=1e-6)
