@@ -354,8 +354,9 @@ def run_ours(args, cfg):
     table_bytes = float(_dev.TABLE_ROW_BYTES) * n_chunks * x1s.nnz + 4.0 * v_e2 * x1s.n_rows
     table_entries = float(v_e2) * x1s.nnz
     spmm_bytes = 8.0 * (x1s.n_rows + 1) + 8.0 * x1s.nnz + 4.0 * x1s.nnz * n2
-    # reverse_panels streams every Z2 panel once (4 * v_e2 bytes per doc), reads D1 and writes D
-    rev_bytes = 4.0 * v_e2 * x1s.n_rows + 8.0 * n2 * x1s.n_rows
+    # reverse_panels streams every Z2 panel once (4 * v_e2 bytes per doc) and reads D1; with the
+    # fused top-k (k <= 32) D is not written
+    rev_bytes = 4.0 * v_e2 * x1s.n_rows + (4.0 if k <= 32 else 8.0) * n2 * x1s.n_rows
     work = {"phase1": fwd_flops, "phase1_rev": rev_flops, "table_build": table_flops, "spmm": spmm_bytes,
             "reverse_panels": rev_bytes, "table_min": table_bytes}
     peak_tf = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))

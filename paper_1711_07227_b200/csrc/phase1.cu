@@ -34,11 +34,6 @@
 
 #include "common.cuh"
 
-#ifndef LCRW_EPI_MODE
-#define LCRW_EPI_MODE 0  // experiment switch: 1 = skip segment minima, 2 = also skip TMEM loads,
-                         // 3 = also no B traffic, 5 = minima but no Z stores
-#endif
-
 namespace lcrw {
 namespace p1 {
 
@@ -285,7 +280,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t a_full_l = mapa_shared(smem_u32(a_full), 0);
       const uint32_t b_full_l = mapa_shared(smem_u32(b_full), 0);
       uint32_t stage = 0, phase = 0, a_phase = 0;
-      int64_t b_loads = 0;
       const uint32_t tx_bytes = 2 * B_STAGE_BYTES + (p.a_stream ? 2 * A_KB_BYTES : 0);  // both CTAs' halves
       for (int64_t u = pair; u < n_units; u += n_pairs) {
         Unit U;
@@ -326,11 +320,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_gather4_2sm(&tmB, b_full_l + stage * 8, st_ptr + b_in_stage + lane * 4 * BK * 2,
                               kb * BK, g0, g1, g2, g3, pol_b);
             } else if (lane == 0) {
-#if LCRW_EPI_MODE == 3
-              if (b_loads >= p.stages) {  // experiment: ring filled once, then no more B traffic
-                if (leader) mbar_arrive(b_full + stage);
-              } else
-#endif
               {
                 if (leader) mbar_expect_tx(b_full + stage, tx_bytes);
                 tma_load_2d_2sm(&tmB, b_full_l + stage * 8, st_ptr + b_in_stage, kb * BK,
@@ -338,7 +327,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
             __syncwarp();
-            ++b_loads;
             if (++stage == (uint32_t)p.stages) {
               stage = 0;
               phase ^= 1;
@@ -365,7 +353,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int i = 0; i < n_tiles; ++i) {
           int h, k;
           unit_tile(U, i, h, k);
-#if LCRW_EPI_MODE != 4
 #ifdef LCRW_P1_STATS
           const long long _t0 = clock64();
 #endif
@@ -375,7 +362,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             atomicAdd(&g_p1_stats[4], (unsigned long long)(clock64() - _t0));
             atomicAdd(&g_p1_stats[6], 1ull);
           }
-#endif
 #endif
           e_phase ^= 1u << h;
           tc_fence_after();
@@ -470,9 +456,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       auto emit = [&](float segmin) {
         float d;
         asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(fmaxf(segmin + nE, 0.f)));
-#if LCRW_EPI_MODE == 5
-        if (d < -1.f)  // experiment: never true -- the global store is skipped
-#endif
         if (p.z_mode == kZTable) {
           const uint32_t key = dist_key21(d);
           const uint32_t pk = __shfl_sync(0xffffffffu, key, t_src);
@@ -522,16 +505,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
           uint32_t mask = __shfl_sync(0xffffffffu, wmask, ch);
-#if LCRW_EPI_MODE == 1
-          run = fminf(run, fminf(v[0], v[31]));
-          if (mask) { emit(run); run = kInf; }
-          continue;
-#endif
-#if LCRW_EPI_MODE == 6
-          run = fmin3(run, RangeMin<0, 15>::run(v), RangeMin<16, 31>::run(v));
-          if (mask) { emit(run); run = kInf; }
-          continue;
-#endif
           if (mask == 0) {
             run = chunk_min(run, v);
           } else if ((mask & (mask - 1u)) == 0) {  // exactly one segment end in the chunk
