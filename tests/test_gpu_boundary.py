@@ -275,3 +275,41 @@ def test_spmm_dist_bitwise_equals_spmm():
     with np.errstate(over="ignore"):  # the 2^126 weights times 3e30 overflow f32, as in the kernel
         ref = ref.astype(np.float32).ravel()
     assert np.allclose(out[True], ref, rtol=1e-6)
+
+
+def test_refine_list_overflow_falls_back_to_scan():
+    """lcrw_refine_near with a producer list whose count exceeds its capacity scans the
+    whole Z instead (device-side decision), giving the same Z as the scan mode; a list
+    within capacity refines exactly its entries."""
+    import ctypes as C
+    import torch
+    from paper_1711_07227_b200 import _lib, device
+    rng = np.random.default_rng(31)
+    V, m = 2000, 64
+    c = rng.standard_normal((40, m)).astype(np.float32)
+    E = (c[rng.integers(0, 40, V)] + 0.05 * rng.standard_normal((V, m))).astype(np.float32)
+    from paper_1711_07227_b200 import synthetic as S
+    x2 = S.histograms(50, V, 30, seed=32)
+    prep = device.PreparedEmbeddings(E)
+    d2 = device.DeviceCSR.upload(x2)
+    res = device.Restricted.build(device.DeviceCSR.upload(S.histograms(300, V, 30, seed=33)), prep)
+    B, _ = device.gather_rows(prep, d2.cols, "B")
+    Z0, zp = device.phase1(res.A, res.a_norms, res.v_e, B, d2.nnz, d2.offsets, d2.n_rows, prep, z_shift=3)
+    rep, nxt = prep.representatives(d2.cols)
+    device.zero_identical(d2.offsets, d2.n_rows, rep, nxt, res.remap, Z0, zp, 3)
+    scan = Z0.clone()
+    device.refine_near(scan, zp, 3, res.v_e, d2.n_rows, d2.offsets, d2.cols, res.used, res.a_norms, prep)
+    assert not torch.equal(scan, Z0)  # clustered rows: some entries were near
+    lst = torch.zeros(16, dtype=torch.int64, device=Z0.device)
+    cnt = torch.tensor([1 << 20], dtype=torch.int32, device=Z0.device)  # > capacity 8
+    over = Z0.clone()
+    _lib.call("lcrw_refine_near", device._p(over), zp, 3, res.v_e, d2.n_rows, device._p(d2.offsets), 0,
+              device._p(d2.cols), device._p(prep.E32), device._p(res.used), device._p(prep.E32), prep.m,
+              device._p(res.a_norms), device._p(prep.scale), device._p(lst), device._p(cnt), 8, device._stream())
+    assert torch.equal(over, scan)
+    empty = Z0.clone()
+    cnt.zero_()
+    _lib.call("lcrw_refine_near", device._p(empty), zp, 3, res.v_e, d2.n_rows, device._p(d2.offsets), 0,
+              device._p(d2.cols), device._p(prep.E32), device._p(res.used), device._p(prep.E32), prep.m,
+              device._p(res.a_norms), device._p(prep.scale), device._p(lst), device._p(cnt), 8, device._stream())
+    assert torch.equal(empty, Z0)  # an empty list changes nothing

@@ -885,7 +885,7 @@ def test_cli_end_to_end_overlap_precision_determinism(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["uniform", "dup_rows", "long_docs", "m37"])
+@pytest.mark.parametrize("case", ["uniform", "dup_rows", "long_docs", "m37", "clustered"])
 def test_reverse_table_mode_bitwise_equals_gemm_mode(case, monkeypatch):
     """The distance-table reverse Phase 1 (csrc/table.cu) against the GEMM form: the
     symmetric matrix and the top-k are bitwise equal (same Phase-1 entries, exact
@@ -894,11 +894,14 @@ def test_reverse_table_mode_bitwise_equals_gemm_mode(case, monkeypatch):
     embedding rows (exact zeros); and within tolerance of the oracle."""
     import torch
     from paper_1711_07227_b200 import device
-    rng = np.random.default_rng(60 + ["uniform", "dup_rows", "long_docs", "m37"].index(case))
+    rng = np.random.default_rng(60 + ["uniform", "dup_rows", "long_docs", "m37", "clustered"].index(case))
     V, m = 3000, (37 if case == "m37" else 300)
     E = rng.standard_normal((V, m)).astype(np.float32)
     if case == "dup_rows":
         E[1500:1700] = E[:200]
+    if case == "clustered":  # many near pairs: the table form's refine list vs the GEMM form's scan
+        c = rng.standard_normal((60, m)).astype(np.float32)
+        E = (c[rng.integers(0, 60, V)] + 0.05 * E).astype(np.float32)
     hi = 150 if case == "long_docs" else 60
     x1 = _rand_set(rng, 1111, V, 1, hi)
     x2 = _rand_set(rng, 45, V, 1, 60)
