@@ -94,6 +94,16 @@ class DeviceCSR:
     host_offsets: np.ndarray
     host_cols: np.ndarray | None = None
     host_vals: np.ndarray | None = None
+    ready: "torch.cuda.Event | None" = None  # set when uploaded on a side stream
+
+    def wait(self) -> None:
+        """Make the current stream wait for a side-stream upload (no host sync)."""
+        if self.ready is not None:
+            cur = torch.cuda.current_stream()
+            cur.wait_event(self.ready)
+            for t in (self.offsets, self.cols, self.vals):
+                t.record_stream(cur)
+            self.ready = None
 
     @property
     def n_rows(self) -> int:
@@ -119,7 +129,9 @@ class DeviceCSR:
                          None if self.host_vals is None else self.host_vals[lo:hi])
 
     @classmethod
-    def upload(cls, x: HistogramSet, name: str = "x") -> "DeviceCSR":
+    def upload(cls, x: HistogramSet, name: str = "x", stream: "torch.cuda.Stream | None" = None) -> "DeviceCSR":
+        """Copy to HBM (async from pinned arrays).  With ``stream`` the copies run there and
+        the set's first device use (``wait``) orders the consuming stream after them."""
         offs = np.asarray(x.row_offsets, dtype=np.int64)
         if x.n_rows and np.any(np.diff(offs) <= 0):
             raise CorpusError(f"{name}: every row must hold at least one word")
@@ -127,8 +139,15 @@ class DeviceCSR:
             raise CorpusError(f"{name}: offset/array length mismatch")
         cols = np.asarray(x.column_ids, dtype=np.int32)
         vals = np.asarray(x.values, dtype=np.float32)
-        return cls(to_device(offs, torch.int64), to_device(cols, torch.int32), to_device(vals, torch.float32),
-                   int(x.n_cols), offs, cols, vals)
+        if stream is None:
+            return cls(to_device(offs, torch.int64), to_device(cols, torch.int32), to_device(vals, torch.float32),
+                       int(x.n_cols), offs, cols, vals)
+        require_cuda()
+        with torch.cuda.stream(stream):
+            d = (to_device(offs, torch.int64), to_device(cols, torch.int32), to_device(vals, torch.float32))
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return cls(*d, int(x.n_cols), offs, cols, vals, ready=ev)
 
 
 class PreparedEmbeddings:
@@ -598,14 +617,19 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
     dev = x1.cols.device
     st = _stream()
     d1_ready = None  # (a side-stream forward pass measured slower: persistent kernels contend for SMs)
+    # the query side's device work first (restriction, distance table: only X2 and E), so an
+    # X1 still being copied in on another stream (DeviceCSR.upload(..., stream=)) overlaps it;
+    # then the forward pass; the host-side plan of the reverse pass is built while the
+    # forward kernels run
+    res2 = Restricted.build(x2, prep, host_plan=True)
+    mode = reverse_mode(prep.V, res2.v_e, x1.nnz)
+    table = distance_table(res2, prep) if mode == "table" else None
+    x1.wait()
     if d1 is None:
         res1 = Restricted.build(x1, prep)
         d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
         del res1
-    res2 = Restricted.build(x2, prep, host_plan=True)
     e_blk, e_tile = query_entries(x2, res2.host_rank, res2.v_e)
-    mode = reverse_mode(prep.V, res2.v_e, x1.nnz)
-    table = distance_table(res2, prep) if mode == "table" else None
     if table is not None and z2_budget_bytes == REVERSE_Z2_BYTES:
         total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
         live = torch.cuda.memory_allocated()  # host-side counter (mem_get_info would stall the stream)

@@ -173,9 +173,21 @@ def lcrwmd_all_pairs_topk(x: HistogramSet, embeddings: np.ndarray, k: int, batch
 
 def lcrwmd_topk_arrays(x1, x2, embeddings, k: int, prep=None):
     """(n2, min(k, n1)) distances and int64 ids; accepts host sets or DeviceCSRs."""
+    # the resident set (the big copy) goes over a side stream while E and the query side are
+    # prepared; device.symmetric waits for it only where X1 is first read
+    dx1 = x1 if isinstance(x1, device.DeviceCSR) else device.DeviceCSR.upload(x1, "x1", stream=_copy_stream())
     if prep is None:
         prep = device.PreparedEmbeddings(embeddings)
-    dx1 = x1 if isinstance(x1, device.DeviceCSR) else device.DeviceCSR.upload(x1, "x1")
     dx2 = x2 if isinstance(x2, device.DeviceCSR) else device.DeviceCSR.upload(x2, "x2")
     d, i = device.symmetric(dx1, dx2, prep, k)
     return d.cpu().numpy(), i.cpu().numpy()
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream():
+    dev = device.require_cuda()
+    if dev.index not in _COPY_STREAMS:
+        _COPY_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[dev.index]
