@@ -89,28 +89,66 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(Args g) {
       return;
     }
   }
-  // scan: warp w tests the 32 consecutive entries [32 w, 32 w + 32) of the panel-major Z
+  // scan: panels in order; inside a panel the warps take 128-entry steps, four consecutive
+  // entries per lane as one float4 (entry i = 128 c + 4 lane + j: row (i >> zs), segment
+  // p * zw + (i & (zw - 1))); no division, coalesced 512-byte warp loads, the flagged
+  // entries (rare) fixed one at a time by the whole warp
   const float s0 = __ldg(g.scale);
   const float tau2 = kRefineTau * kRefineTau;
   const int64_t zw = 1ll << g.z_shift;
-  const int64_t per_panel = g.a_rows << g.z_shift;
+  const int64_t per_panel = g.a_rows << g.z_shift;  // a multiple of 4 (z_shift >= 2)
+  const int64_t cpp = (per_panel + 127) >> 7;       // 128-entry steps per panel
   const int64_t n_panels = (g.n_seg + zw - 1) >> g.z_shift;
-  const int64_t total = n_panels * per_panel;
-  for (int64_t base = warp0 * 32; base < total; base += n_warps * 32) {
-    const int64_t i = base + lane;
-    bool flag = false;
-    int64_t row = 0, s = 0;
-    if (i < total) {
-      const int64_t p = i / per_panel, r = i - p * per_panel;
-      row = r >> g.z_shift;
-      s = p * zw + (r & (zw - 1));
-      if (s < g.n_seg) flag = refine_flag(g.Z[p * g.z_panel + r] * s0, __ldg(g.a_norms + row), tau2);
-    }
-    uint32_t ballot = __ballot_sync(0xffffffffu, flag);
-    while (ballot) {
-      const int src = __ffs(ballot) - 1;
-      ballot &= ballot - 1u;
-      fix(g, __shfl_sync(0xffffffffu, row, src), __shfl_sync(0xffffffffu, s, src), lane);
+  constexpr int kSteps = 4;  // 128-entry steps in flight per warp (independent loads)
+  for (int64_t p = 0; p < n_panels; ++p) {
+    const float* zp = g.Z + p * g.z_panel;
+    const int64_t seg_left = g.n_seg - p * zw;  // < zw only in a ragged last panel
+    for (int64_t c0 = warp0; c0 < cpp; c0 += kSteps * n_warps) {
+      float4 z4[kSteps];
+#pragma unroll
+      for (int u = 0; u < kSteps; ++u) {
+        const int64_t i0 = ((c0 + u * n_warps) << 7) + 4 * lane;
+        z4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i0 < per_panel) {
+          const int64_t sl = i0 & (zw - 1);  // segment of the lane's first entry inside the panel
+          if (sl + 4 <= seg_left) {
+            z4[u] = __ldg(reinterpret_cast<const float4*>(zp + i0));
+          } else {  // entries past the last segment hold no values: not read
+            if (sl + 0 < seg_left) z4[u].x = __ldg(zp + i0);
+            if (sl + 1 < seg_left) z4[u].y = __ldg(zp + i0 + 1);
+            if (sl + 2 < seg_left) z4[u].z = __ldg(zp + i0 + 2);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kSteps; ++u) {
+        const int64_t c = c0 + u * n_warps;
+        const int64_t i0 = (c << 7) + 4 * lane;
+        uint32_t flags = 0;
+        if (i0 < per_panel) {
+          // the lane's four entries share one row (z_shift >= 2): one norm, one bound
+          const float zv[4] = {z4[u].x, z4[u].y, z4[u].z, z4[u].w};
+          if (zv[0] > 0.f || zv[1] > 0.f || zv[2] > 0.f || zv[3] > 0.f) {
+            const float a_sq = __ldg(g.a_norms + (i0 >> g.z_shift));
+            const int64_t s_base = p * zw + (i0 & (zw - 1));
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (s_base + j < g.n_seg && refine_flag(zv[j] * s0, a_sq, tau2)) flags |= 1u << j;
+          }
+        }
+        if (__any_sync(0xffffffffu, flags != 0)) {  // rare: fix the warp's flagged entries one by one
+#pragma unroll 1
+          for (int j = 0; j < 4; ++j) {
+            uint32_t ballot = __ballot_sync(0xffffffffu, (flags >> j) & 1u);
+            while (ballot) {
+              const int src = __ffs(ballot) - 1;
+              ballot &= ballot - 1u;
+              const int64_t i = (c << 7) + 4 * src + j;
+              fix(g, i >> g.z_shift, p * zw + (i & (zw - 1)), lane);
+            }
+          }
+        }
+      }
     }
   }
 }
@@ -132,13 +170,15 @@ int lcrw_refine_near(float* Z, int64_t z_panel, int z_shift, int64_t a_rows, int
   if (a_rows == 0 || n_seg == 0) return LCRW_OK;
   LCRW_REQUIRE(Z && seg_offsets && seg_ids && A32 && a_ids && B32 && a_norms && scale,
                "lcrw_refine_near: null pointer");
-  LCRW_REQUIRE(z_shift >= 0 && z_shift <= 10 && z_panel >= (a_rows << z_shift), "lcrw_refine_near: bad Z layout");
+  LCRW_REQUIRE(z_shift >= 2 && z_shift <= 10 && z_panel >= (a_rows << z_shift) && z_panel % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(Z) & 15) == 0,
+               "lcrw_refine_near: bad Z layout (z_shift in [2, 10], z_panel % 4 == 0, Z 16-byte aligned)");
   LCRW_REQUIRE(!list || (count && cap >= 0), "lcrw_refine_near: a list needs its count and capacity");
   refine::Args g{Z, z_panel, z_shift, a_rows, n_seg, seg_offsets, seg_base, seg_ids, A32, a_ids, B32, m, a_norms,
                  scale, static_cast<const uint2*>(list), count, cap};
   const int64_t entries = ((n_seg + (1ll << z_shift) - 1) >> z_shift) * (a_rows << z_shift);
   const int64_t want = ceil_div(entries, (int64_t)refine::kThreads);
-  const int64_t cap_blocks = (int64_t)sm_count() * 8;
+  const int64_t cap_blocks = (int64_t)sm_count() * 16;
   const int blocks = (int)(want < cap_blocks ? (want > 0 ? want : 1) : cap_blocks);
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "refine");

@@ -519,7 +519,7 @@ TABLE_ROW_BYTES = 480             # per vocabulary word per 180-word chunk: 180 
 def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | None = None) -> str:
     """"table" when the reverse Phase 1 is cheaper as a distance table + per-doc gathers
     (table.cu): the vocabulary is small next to nnz(X1) (each (w, u) distance is then
-    needed ~nnz/V times), a 128-word chunk of it fits in L2, and the table fits in HBM;
+    needed ~nnz/V times), a 180-word chunk of it fits in L2, and the table fits in HBM;
     else "gemm".  LCRW_REVERSE=gemm|table overrides (tests, A/B runs)."""
     env = os.environ.get("LCRW_REVERSE", "")
     if env in ("gemm", "table"):

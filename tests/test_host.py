@@ -290,3 +290,24 @@ def test_reverse_mode_choice(monkeypatch):
     assert device.reverse_mode(100_000, 39_300, 50_000_000, hbm) == "gemm"
     monkeypatch.setenv("LCRW_REVERSE", "table")
     assert device.reverse_mode(3_000_000, 146_000, 75_000_000, hbm) == "table"
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the driver's reference arm: the pinned CPU oracle on the
+    host cores, bounded samples extrapolated part by part) prints one JSON line with the
+    contract keys and the same config object as our arm."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "1", "--warmup", "3", "--ref-docs", "64", "--ref-rows", "256"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "impl", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["config"]["n_docs"] == 2000 and line["config"]["n_queries"] == 64
