@@ -21,12 +21,6 @@ constexpr int kSegPerBlock = 128;   // spmm: 32 lanes x 4 segments
 // segments of one word row are one contiguous 512-byte run (four 128-byte
 // lines per nonzero), with zs = 3 they are 16 separate 32-byte sectors.
 // ---------------------------------------------------------------------------
-#ifndef LCRW_SPMM_UNROLL
-#define LCRW_SPMM_UNROLL 1
-#endif
-#ifndef LCRW_SPMM_NZ_SMEM
-#define LCRW_SPMM_NZ_SMEM 1
-#endif
 // Z holding distances (finite, >= 0, zero or normal: the pipeline's Z1) lets the f32 -> f64
 // widening run on the integer pipe: the f32 bits shifted into an f64 word are z * 2^-896
 // exactly (exponent field kept, not rebiased; 0 stays 0), and the weight carries the 2^896,
@@ -36,16 +30,16 @@ __device__ __forceinline__ double dist_f64_scaled(float z) {
   const uint32_t b = __float_as_uint(z);
   return __hiloint2double((int)(b >> 3), (int)(b << 29));
 }
-constexpr int kSpmmUnroll = LCRW_SPMM_UNROLL;  // (#pragma unroll does not expand macros)
+#ifndef LCRW_SPMM_MINB
+#define LCRW_SPMM_MINB 1
+#endif
 template <bool kDist>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, LCRW_SPMM_MINB)
     spmm_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ cols, const float* __restrict__ vals,
                 int64_t n_rows, const float* __restrict__ Z, int64_t z_panel, int zs, int64_t z_block_rows,
                 int64_t z_block_stride, int64_t n_seg, float* __restrict__ out, int64_t ld_row, int64_t ld_panel) {
   const int lane = threadIdx.x & 31;
-#if LCRW_SPMM_NZ_SMEM
   __shared__ longlong2 nz_s[kWarps][32];
-#endif
   const int64_t q0 = (int64_t)blockIdx.y * kSegPerBlock + lane * 4;
   const bool active = q0 < n_seg;
   const float* zq = Z + (q0 >> zs) * z_panel + (q0 & ((1 << zs) - 1));
@@ -60,24 +54,16 @@ __global__ void __launch_bounds__(kWarps * 32)
       // vocabulary-sliced Z (multi-GPU all-gather): row w lives in block w / z_block_rows
       const uint32_t blk = my_c / zbr;
       const int64_t my_off = (int64_t)blk * z_block_stride + ((int64_t)(my_c - blk * zbr) << zs);
-#if LCRW_SPMM_NZ_SMEM
       // (offset, weight) of the 32 nonzeros staged per warp and read back as one broadcast
       // LDS.128 each, instead of three SHFLs (a 64-bit offset + the weight) that share the
       // L1TEX data pipe with the Z row loads
       __syncwarp();
       nz_s[threadIdx.x >> 5][lane] = make_longlong2(my_off, (long long)__float_as_int(my_x));
       __syncwarp();
-#endif
-#pragma unroll kSpmmUnroll
       for (int t = 0; t < cnt; ++t) {
-#if LCRW_SPMM_NZ_SMEM
         const longlong2 e = nz_s[threadIdx.x >> 5][t];
         const int64_t zoff = e.x;
         const float xf = __int_as_float((int)e.y);
-#else
-        const int64_t zoff = __shfl_sync(0xffffffffu, my_off, t);
-        const float xf = __shfl_sync(0xffffffffu, my_x, t);
-#endif
         const double x = (double)xf;
         if (active) {
           const float4 z = __ldg(reinterpret_cast<const float4*>(zq + zoff));
@@ -212,10 +198,7 @@ __global__ void __launch_bounds__((kRpWarps + 1) * 32, 1)
       const float* zp = Z2 + p * z_panel;
       const int64_t* tb = e_tile + g * n_tiles;
       // D1 lines of this item, needed by the consumers' combine at the end
-#ifndef LCRW_RP_D1PF
-#define LCRW_RP_D1PF 1
-#endif
-      if (LCRW_RP_D1PF) {
+      {
         const int64_t q0 = g * kRpGroup;
         const int nqp = (int)((min((int64_t)kRpGroup, n_q - q0) + 7) / 8);
         const int64_t j0 = doc_base + p * 32;

@@ -17,9 +17,6 @@
 namespace lcrw {
 namespace tbl {
 
-#ifndef LCRW_TBL_HINTS
-#define LCRW_TBL_HINTS 1
-#endif
 
 // L2 policies: the table chunk is re-read by every doc (evict_last); doc word ids
 // and Z2 stores stream through once (evict_first), so they do not push the chunk out
@@ -34,61 +31,27 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
   return p;
 }
 __device__ __forceinline__ uint4 ld_keep_u4(const uint4* ptr, uint64_t pol) {
-#if LCRW_TBL_HINTS
   uint4 v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
       : "l"(ptr), "l"(pol));
   return v;
-#else
-  return __ldg(ptr);
-#endif
 }
 __device__ __forceinline__ int ld_stream(const int32_t* ptr, uint64_t pol) {
-#if LCRW_TBL_HINTS
   int v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
   return v;
-#else
-  return __ldg(ptr);
-#endif
 }
 __device__ __forceinline__ void st_stream(float* ptr, float v, uint64_t pol) {
-#if LCRW_TBL_HINTS
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
-#else
-  *ptr = v;
-#endif
 }
 
 constexpr int kChunk = kTableChunk;  // query-vocabulary words per table chunk (480-byte packed rows)
 constexpr int kPanelDocs = 32;       // Z2 panel width (lcrw_reverse_panels layout)
 constexpr int kTileStride = kChunk + 1;  // smem tile row stride (conflict-free both ways)
-#ifndef LCRW_TBL_UNROLL
-#define LCRW_TBL_UNROLL 8
-#endif
 #ifndef LCRW_TBL_MINB
 #define LCRW_TBL_MINB 5  // 5 CTAs (40 warps) per SM: <= 48 registers
 #endif
-[[maybe_unused]] constexpr int kUnroll = LCRW_TBL_UNROLL;  // (#pragma unroll does not expand macros)
-#ifndef LCRW_TBL_PANELS
-#define LCRW_TBL_PANELS 1
-#endif
-#ifndef LCRW_TBL_DYN
-#define LCRW_TBL_DYN 0
-#endif
-#ifndef LCRW_TBL_IDS_SMEM
-#define LCRW_TBL_IDS_SMEM 1
-#endif
-#ifndef LCRW_TBL_TILE_ROT
-#define LCRW_TBL_TILE_ROT 0  // measured neutral-to-worse (331 vs 329 ms)
-#endif
-#ifndef LCRW_TBL_QUAD_UNROLL
-#define LCRW_TBL_QUAD_UNROLL 1
-#endif
-constexpr int kQuadUnroll = LCRW_TBL_QUAD_UNROLL;  // quads of rows per unrolled step (4 rows in flight x 40 warps)
-constexpr int kCtaPanels = LCRW_TBL_PANELS;        // 32-doc Z2 panels per CTA
-constexpr int kCtaDocs = kCtaPanels * kPanelDocs;  // docs per CTA
 
 // Sets word w's key in row u (atomics: the fields of one 32-bit word belong to
 // different words w).  Cross-check and exact-zero paths only; the build writes whole words.
@@ -154,153 +117,101 @@ __device__ __forceinline__ void keys_min1(Keys& k, const uint4 r) {
   k.k4 = min(k.k4, __funnelshift_l(r.y << 21, r.x, 21));
   k.k5 = min(k.k5, __funnelshift_l(r.w << 21, r.z, 21));
 }
-// Work unit = (chunk c, kCtaPanels consecutive 32-doc panels), panels fastest, so the
-// units in flight share one L2-resident chunk (v_rows x 480 B: 48 MB at V = 100k);
-// one CTA per unit (4 resident per SM).  Warp j takes docs j, j+8, ... (LCRW_TBL_DYN=1:
-// an smem counter hands out docs one at a time -- measured neutral); lane l < 30 owns
-// words 6l..6l+5: per doc word, one 16-byte load of their six 21-bit keys (the warp reads
-// the 480-byte row once: 180 distances, 2.67 bytes each).  Four keys sit in the top 21 bits of
-// the group's words, so their minima are plain integer minima of the words; the other two
-// are reassembled from the words' low 11 bits with one shift + one funnel shift each.
-// The 32 x 180 result per panel is decoded, unscaled, staged in smem (row stride 181:
-// conflict-free both ways) and written as 180 coalesced 128-byte Z2 rows:
-// Z2[p * z_panel + w * 32 + doc].
+// One CTA per work unit (chunk c, 32-doc panel p), panels fastest, so the CTAs in flight
+// share one L2-resident chunk (v_rows x 480 B: 48 MB at V = 100k); 5 CTAs per SM.  (A
+// persistent loop over units measured 2.6x slower: CTAs drift apart and the chunks in
+// flight no longer fit L2.)  Warp j takes docs j, j+8, j+16, j+24.  Per 32 doc words the
+// warp stages the word ids in its smem slot and broadcasts them four at a time (one
+// LDS.128 wavefront per 4 rows -- a SHFL per row shares the L1TEX data pipe with the
+// table loads and measured 10 % slower); lane l < 30 owns words 6l..6l+5 of the chunk:
+// per doc word, one 16-byte load of their six 21-bit keys (the warp reads the 480-byte
+// row once: 180 distances, 2.67 bytes each), 4 rows in flight.  Four keys sit in the top
+// 21 bits of the group's words, so their minima are plain integer minima of the words;
+// the other two are reassembled from the words' low 11 bits with one shift + one funnel
+// shift each.  The 32 x 180 result is decoded, unscaled, staged in smem (row stride 181:
+// conflict-free reads; the writes are 2-way, a rotated write order measured no better)
+// and written as 180 coalesced 128-byte Z2 rows: Z2[p * z_panel + w * 32 + doc].
 __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uint8_t* __restrict__ T, int64_t v_rows, int64_t a_rows,
                                                         const int64_t* __restrict__ doc_offsets, int64_t seg_base,
                                                         int64_t n_docs, const int32_t* __restrict__ cols,
                                                         const float* __restrict__ scale, float* __restrict__ Z2,
-                                                        int64_t z_panel, int64_t cta_units,
+                                                        int64_t z_panel, int64_t panels,
                                                         const float* __restrict__ a_norms, RefineSink sink) {
-  __shared__ float tile[kCtaDocs * kTileStride];
-  __shared__ float wsq[kChunk];  // the chunk words' scaled squared norms (refine test)
-#if LCRW_TBL_DYN
-  __shared__ int next_doc;  // dynamic doc assignment: warps take the unit's docs one at a time
-#endif
-#if LCRW_TBL_IDS_SMEM
+  __shared__ float tile[kPanelDocs * kTileStride];
+  __shared__ float wsq[kChunk];               // the chunk words' scaled squared norms (refine test)
   __shared__ __align__(16) int ids_s[8][32];  // per-warp word ids of the current 32-word block
-#endif
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool active = lane < kTableGroups;
   const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
   const float inv_scale = __ldg(scale + 1);
   const float s0 = __ldg(scale);
-  {  // one work unit per CTA (a persistent loop over units measured 2.6x slower: CTAs drift
-     // apart and the chunks in flight no longer fit L2)
-    const int64_t unit = blockIdx.x;
-    const int64_t c = unit / cta_units, u0 = unit - c * cta_units;
-    const int64_t d0 = u0 * kCtaDocs;  // first doc of the unit
-#if LCRW_TBL_DYN
-    if (threadIdx.x == 0) next_doc = 8;
-#endif
-    if (sink.list && threadIdx.x < kChunk)
-      wsq[threadIdx.x] = c * kChunk + threadIdx.x < a_rows ? __ldg(a_norms + c * kChunk + threadIdx.x) : 0.f;
-    __syncthreads();
-    // the chunk's largest squared norm: an entry at or above tau * max|a| cannot be near, so the
-    // per-word norm is only read for the (rare) entries below it
-    float wsq_max = 0.f;
-    if (sink.list) {
-      for (int q = lane; q < kChunk; q += 32) wsq_max = fmaxf(wsq_max, wsq[q]);
+  const int64_t c = blockIdx.x / panels, p = blockIdx.x - c * panels;
+  if (sink.list && threadIdx.x < kChunk)
+    wsq[threadIdx.x] = c * kChunk + threadIdx.x < a_rows ? __ldg(a_norms + c * kChunk + threadIdx.x) : 0.f;
+  __syncthreads();
+  // the chunk's largest squared norm: an entry at or above tau * max|a| cannot be near, so the
+  // per-word norm is only read for the (rare) entries below it
+  float wsq_max = 0.f;
+  if (sink.list) {
+    for (int q = lane; q < kChunk; q += 32) wsq_max = fmaxf(wsq_max, wsq[q]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) wsq_max = fmaxf(wsq_max, __shfl_xor_sync(0xffffffffu, wsq_max, o));
+    for (int o = 16; o > 0; o >>= 1) wsq_max = fmaxf(wsq_max, __shfl_xor_sync(0xffffffffu, wsq_max, o));
+  }
+  // lanes 30, 31 repeat lane 29's 16 bytes (same sector: no extra traffic) so the loop has
+  // no predication; their minima are discarded
+  const uint4* Tc =
+      reinterpret_cast<const uint4*>(T + c * v_rows * kTableRowBytes) + (active ? lane : kTableGroups - 1);
+  for (int dd = warp; dd < kPanelDocs; dd += 8) {
+    const int64_t d = p * kPanelDocs + dd;
+    Keys k{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (d < n_docs) {
+      const int64_t b = __ldg(doc_offsets + d) - seg_base, e = __ldg(doc_offsets + d + 1) - seg_base;
+      for (int64_t j0 = b; j0 < e; j0 += 32) {
+        const int n = e - j0 < 32 ? (int)(e - j0) : 32;
+        __syncwarp();
+        ids_s[warp][lane] = lane < n ? ld_stream(cols + j0 + lane, stream) : 0;
+        __syncwarp();
+        const int4* q4 = reinterpret_cast<const int4*>(ids_s[warp]);
+        int j = 0;
+#pragma unroll 1
+        for (; j + 4 <= n; j += 4) {
+          const int4 u4 = q4[j >> 2];
+          const uint4 r0 = ld_keep_u4(Tc + (int64_t)u4.x * (kTableRowBytes / 16), keep);
+          const uint4 r1 = ld_keep_u4(Tc + (int64_t)u4.y * (kTableRowBytes / 16), keep);
+          const uint4 r2 = ld_keep_u4(Tc + (int64_t)u4.z * (kTableRowBytes / 16), keep);
+          const uint4 r3 = ld_keep_u4(Tc + (int64_t)u4.w * (kTableRowBytes / 16), keep);
+          keys_min1(k, r0);
+          keys_min1(k, r1);
+          keys_min1(k, r2);
+          keys_min1(k, r3);
+        }
+        for (; j < n; ++j) keys_min1(k, ld_keep_u4(Tc + (int64_t)ids_s[warp][j] * (kTableRowBytes / 16), keep));
+      }
     }
-    // lanes 30, 31 repeat lane 29's 16 bytes (same sector: no extra traffic) so the loop has
-    // no predication; their minima are discarded
-    const uint4* Tc =
-        reinterpret_cast<const uint4*>(T + c * v_rows * kTableRowBytes) + (active ? lane : kTableGroups - 1);
-    for (int dd = warp; dd < kCtaDocs;) {
-      const int64_t d = d0 + dd;
-      Keys k{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-      if (d < n_docs) {
-        const int64_t b = __ldg(doc_offsets + d) - seg_base, e = __ldg(doc_offsets + d + 1) - seg_base;
-        for (int64_t j0 = b; j0 < e; j0 += 32) {
-          const int n = e - j0 < 32 ? (int)(e - j0) : 32;
-          const int mine = lane < n ? ld_stream(cols + j0 + lane, stream) : 0;
-#if LCRW_TBL_IDS_SMEM
-          // word ids broadcast four at a time from a per-warp smem slot (one LDS.128 wavefront
-          // per 4 words instead of 4 SHFL wavefronts, which share the L1TEX data pipe with the
-          // table loads)
-          __syncwarp();
-          ids_s[warp][lane] = mine;
-          __syncwarp();
-          const int4* q4 = reinterpret_cast<const int4*>(ids_s[warp]);
-          int j = 0;
-#pragma unroll kQuadUnroll
-          for (; j + 4 <= n; j += 4) {
-            const int4 u4 = q4[j >> 2];
-            const uint4 r0 = ld_keep_u4(Tc + (int64_t)u4.x * (kTableRowBytes / 16), keep);
-            const uint4 r1 = ld_keep_u4(Tc + (int64_t)u4.y * (kTableRowBytes / 16), keep);
-            const uint4 r2 = ld_keep_u4(Tc + (int64_t)u4.z * (kTableRowBytes / 16), keep);
-            const uint4 r3 = ld_keep_u4(Tc + (int64_t)u4.w * (kTableRowBytes / 16), keep);
-            keys_min1(k, r0);
-            keys_min1(k, r1);
-            keys_min1(k, r2);
-            keys_min1(k, r3);
-          }
-          for (; j < n; ++j) keys_min1(k, ld_keep_u4(Tc + (int64_t)ids_s[warp][j] * (kTableRowBytes / 16), keep));
-#else
-#pragma unroll kUnroll
-          for (int j = 0; j < n; ++j) {
-            const int u = __shfl_sync(0xffffffffu, mine, j);
-            keys_min1(k, ld_keep_u4(Tc + (int64_t)u * (kTableRowBytes / 16), keep));
-          }
-#endif
-        }
-      }
-      if (active) {
-        float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
-#if LCRW_TBL_TILE_ROT
-        // lanes l and l + 16 map to the same bank (6 * 16 = 96 = 0 mod 32): the upper half
-        // writes its six values rotated by three, so every store is conflict-free
-        const float v[kTableKeysPerGroup] = {key21_dist(k.k0 >> 11) * inv_scale, key21_dist(k.k1 >> 11) * inv_scale,
-                                             key21_dist(k.k2 >> 11) * inv_scale, key21_dist(k.k3 >> 11) * inv_scale,
-                                             key21_dist(k.k4 >> 11) * inv_scale, key21_dist(k.k5 >> 11) * inv_scale};
-        const bool hi = lane >= 16;
-#pragma unroll
-        for (int t = 0; t < kTableKeysPerGroup; ++t) {
-          const int r = (t + 3) % kTableKeysPerGroup;
-          trow[hi ? r : t] = hi ? v[r] : v[t];
-        }
-#else
-        trow[0] = key21_dist(k.k0 >> 11) * inv_scale;
-        trow[1] = key21_dist(k.k1 >> 11) * inv_scale;
-        trow[2] = key21_dist(k.k2 >> 11) * inv_scale;
-        trow[3] = key21_dist(k.k3 >> 11) * inv_scale;
-        trow[4] = key21_dist(k.k4 >> 11) * inv_scale;
-        trow[5] = key21_dist(k.k5 >> 11) * inv_scale;
-#endif
-      }
-#if LCRW_TBL_DYN
-      int nd = 0;
-      if (lane == 0) nd = atomicAdd(&next_doc, 1);
-      dd = __shfl_sync(0xffffffffu, nd, 0);
-#else
-      dd += 8;
-#endif
+    if (active) {
+      float* trow = tile + dd * kTileStride + kTableKeysPerGroup * lane;
+      trow[0] = key21_dist(k.k0 >> 11) * inv_scale;
+      trow[1] = key21_dist(k.k1 >> 11) * inv_scale;
+      trow[2] = key21_dist(k.k2 >> 11) * inv_scale;
+      trow[3] = key21_dist(k.k3 >> 11) * inv_scale;
+      trow[4] = key21_dist(k.k4 >> 11) * inv_scale;
+      trow[5] = key21_dist(k.k5 >> 11) * inv_scale;
     }
-    __syncthreads();
-    const int64_t w0 = c * kChunk;
-#pragma unroll
-    for (int pp = 0; pp < kCtaPanels; ++pp) {
-      const int64_t p = u0 * kCtaPanels + pp;
-      if (p * kPanelDocs >= n_docs) break;
-      float* zp = Z2 + p * z_panel;
-      const bool doc_ok = p * kPanelDocs + lane < n_docs;
-      const float* trow = tile + (pp * kPanelDocs + lane) * kTileStride;
-      for (int q = warp; q < kChunk; q += 8) {  // lane = doc; word q of the chunk
-        if (w0 + q < a_rows) {
-          const float v = trow[q];
-#ifndef LCRW_TBL_NOSTORE
-          st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);
-#else
-          if (v == -1.f) st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);  // experiment: stores skipped
-#endif
-          // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
-          const float ds = v * s0;
-          if (sink.list && doc_ok && ds * ds < kRefineTau * kRefineTau * wsq_max &&
-              refine_flag(ds, wsq[q], kRefineTau * kRefineTau))
-            refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
-        }
-      }
+  }
+  __syncthreads();
+  float* zp = Z2 + p * z_panel;
+  const int64_t w0 = c * kChunk;
+  const bool doc_ok = p * kPanelDocs + lane < n_docs;
+  const float* trow = tile + lane * kTileStride;
+  for (int q = warp; q < kChunk; q += 8) {  // lane = doc; word q of the chunk
+    if (w0 + q < a_rows) {
+      const float v = trow[q];
+      st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);
+      // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
+      const float ds = v * s0;
+      if (sink.list && doc_ok && ds * ds < kRefineTau * kRefineTau * wsq_max &&
+          refine_flag(ds, wsq[q], kRefineTau * kRefineTau))
+        refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
     }
   }
 }
@@ -379,14 +290,13 @@ int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t*
                "lcrw_table_min: a refine list needs a_norms, its count and capacity");
   LCRW_REQUIRE(z_panel == a_rows * tbl::kPanelDocs && (reinterpret_cast<uintptr_t>(T) & 15) == 0,
                "lcrw_table_min: Z2 must be in 32-doc panels (z_panel = 32 * a_rows), T 16-byte aligned");
-  const int64_t units = ceil_div(n_docs, tbl::kCtaDocs);
-  const int64_t n_units = ceil_div(a_rows, tbl::kChunk) * units;
-  const int64_t blocks = n_units;
+  const int64_t panels = ceil_div(n_docs, tbl::kPanelDocs);
+  const int64_t blocks = ceil_div(a_rows, tbl::kChunk) * panels;
   LCRW_REQUIRE(blocks < (1ll << 31), "lcrw_table_min: too many (chunk, panel) blocks for one launch");
   cudaStream_t st = as_stream(stream);
   ProfScope prof(st, "table_min");
   tbl::table_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(T), v_rows, a_rows, doc_offsets,
-                                                          seg_base, n_docs, doc_cols, scale, Z2, z_panel, units, a_norms,
+                                                          seg_base, n_docs, doc_cols, scale, Z2, z_panel, panels, a_norms,
       RefineSink{static_cast<uint2*>(refine_list), refine_count, refine_cap});
   LCRW_CHECK_LAUNCH("table_min_kernel");
   return LCRW_OK;

@@ -1,6 +1,6 @@
 #!/bin/bash
 # experiment builds of csrc/phase2.cu (A/B of spmm / reverse_panels shapes; not shipped):
-#   VARIANTS="u4:-DLCRW_SPMM_UNROLL=4 ..." variants/build_p2_variants.sh
+#   VARIANTS="name:-DFLAG=VALUE ..." variants/build_p2_variants.sh  (compile-time knobs of phase2.cu)
 set -e
 cd "$(dirname "$0")/.."
 for spec in $VARIANTS; do
