@@ -26,6 +26,10 @@
   row blocks (17.5 GB per rank) is not part of the timed region (one GPU here);
   the received blocks are stood in for by the rank's own rows.
 
+* ``scaling``: rank 0's share of BASELINE configs[2] (C2 over N = 1, 2, 4, 8 GPUs)
+  through the sharded code path, timed on one GPU; the collectives are estimated,
+  not executed (projection).
+
 Inputs are resident in HBM for the device-timed value (CUDA events); these rows
 are not part of bench.py's headline line.
 """
@@ -235,6 +239,61 @@ def row_allpairs_rank(args):
     print(json.dumps(line), flush=True)
 
 
+def row_scaling(args):
+    """Per-rank compute of BASELINE configs[2] (C2 sharded over N GPUs) on one B200: for N in
+    1, 2, 4, 8 the step rank 0 runs in parallel.sharded_topk -- its vocabulary slice of the
+    forward Phase 1 (Z1 rows [0, V/N)), the forward SpMM and the whole reverse direction on
+    its 1M/N docs (the distance table is built by every rank: replicated E and X2), the
+    max-combine and its per-query top-10.  The two collectives (the Z1 all-gather, 400 MB,
+    and the gather of the 1k x 10 lists) are not executed: one GPU.  They are reported as
+    bytes with an NVLink 5 estimate (all-gather of (N-1)/N x 400 MB at 600 GB/s per GPU).
+    Projection, clearly not a multi-GPU measurement."""
+    import torch
+    from paper_1711_07227_b200 import device, parallel, synthetic as S
+    V, m, n1, n2, h, k = 100_000, 300, 1_000_000, 1000, 50, 10
+    E = S.embeddings(V, m, seed=0)
+    x1 = S.histograms(n1, V, h, seed=1)
+    x2 = S.histograms(n2, V, h, seed=2)
+    Et = torch.from_numpy(E).cuda()
+    dx2 = device.DeviceCSR.upload(x2)
+    out = []
+    base_ms = None
+    for world in (1, 2, 4, 8):
+        lo, hi = parallel.shard_range(n1, 0, world)
+        dx1 = device.DeviceCSR.upload(x1.slice_rows(lo, hi))
+        prep0 = device.PreparedEmbeddings(Et)
+        # the other ranks' Z1 slices (the all-gather's result), computed outside the timed step
+        slices = [parallel.z1_slice(dx2, prep0, r, world)[0] for r in range(world)]
+        zall = torch.stack(slices).contiguous()
+        R = parallel.vocab_slice(V, 0, world)[2]
+        del slices
+
+        def step():
+            prep = device.PreparedEmbeddings(Et)
+            zl, _ = parallel.z1_slice(dx2, prep, 0, world)  # this rank's slice (the all-gather's input)
+            d1 = parallel.d1_from_slices(dx1, zall, R, n2)
+            return device.symmetric(dx1, dx2, prep, k, d1=d1, id_offset=lo)
+
+        ms, _ = timed(step, args.steps, args.warmup)
+        if base_ms is None:
+            base_ms = ms
+        ag_bytes = (world - 1) / world * 4.0 * V * n2 if world > 1 else 0.0
+        ag_ms = ag_bytes / 600e9 * 1e3
+        proj = ms + ag_ms
+        out.append({"n_gpus": world, "rank0_ms": ms, "allgather_bytes": ag_bytes, "allgather_ms_est": ag_ms,
+                    "projected_step_ms": proj, "projected_pairs_per_s": n1 * n2 / (proj * 1e-3),
+                    "projected_efficiency": base_ms / (world * proj)})
+        del dx1, zall
+    line = {"metric": "symmetric RWMD doc-pairs/sec, C2 sharded over N GPUs (per-rank compute on one B200)",
+            "value": out[-1]["projected_pairs_per_s"], "unit": "doc-pairs/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": "f16 operands, fp32 accumulate",
+            "config": {"workload": "rank 0's share of BASELINE configs[2] (1M docs x 1k queries, V=100k, m=300, "
+                                   "top-10) for N = 1, 2, 4, 8; collectives not executed (one GPU), all-gather "
+                                   "time estimated at 600 GB/s", "scaling": "strong"},
+            "per_n": out}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", default="wmd,wcd")
@@ -244,7 +303,8 @@ def main():
     ap.add_argument("--allpairs-n", type=int, default=50_000)
     args = ap.parse_args()
     for r in args.rows.split(","):
-        {"wmd": row_wmd, "wcd": row_wcd, "allpairs": row_allpairs, "allpairs_rank": row_allpairs_rank}[r](args)
+        {"wmd": row_wmd, "wcd": row_wcd, "allpairs": row_allpairs, "allpairs_rank": row_allpairs_rank,
+         "scaling": row_scaling}[r](args)
 
 
 if __name__ == "__main__":
