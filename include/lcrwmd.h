@@ -162,6 +162,15 @@ int lcrw_spmm_dist(const int64_t* offs, const int32_t* cols, const float* vals, 
  * holds a multiple of I = lcrw_reverse_panels_ilp() entries and each aligned
  * group of I entries names I distinct queries; padding entries of warp w's
  * list use query G + w (that warp's scratch row) with weight 0. */
+/* The plan above, built on the HOST (plain C++, no device memory): offsets[n_q+1] /
+ * cols / vals = the query CSR (E word ids), rank = word id -> query-vocabulary row,
+ * T, G, W, I = the lcrw_reverse_panels_* geometry.  Writes words (capacity
+ * words_cap >= lcrw_plan_reverse_words_bound(...)), tile_off[n_groups*n_tiles+1]
+ * and *n_words.  Output identical to device.plan_query_entries. */
+int64_t lcrw_plan_reverse_words_bound(int64_t n_q, int64_t nnz, int64_t a_rows, int T, int G, int W, int I);
+int lcrw_plan_reverse(const int64_t* offsets, int64_t n_q, const int32_t* cols, const float* vals,
+                      const int32_t* rank, int64_t a_rows, int T, int G, int W, int I, uint32_t* words,
+                      int64_t words_cap, int64_t* tile_off, int64_t* n_words);
 int lcrw_reverse_panels_tile_rows(void);
 int lcrw_reverse_panels_group(void);
 int lcrw_reverse_panels_warps(void);

@@ -67,6 +67,8 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_reverse_panels_ilp": (I32, []),
     "lcrw_reverse_panels": (I32, [P, I64, I64, I64, I64, P, P, I64, P, I64, P, I64, I64, P, P, I32, I64, P]),
     "lcrw_reverse_panels_top_slots": (I32, []),
+    "lcrw_plan_reverse_words_bound": (I64, [I64, I64, I64, I32, I32, I32, I32]),
+    "lcrw_plan_reverse": (I32, [P, I64, P, P, P, I64, I32, I32, I32, I32, P, I64, P, P]),
     "lcrw_topk_rows_workspace": (I32, [I64, I64, I32, P]),
     "lcrw_emd_problem_bytes": (SZ, [I32, I32]),
     "lcrw_emd_batch": (I32, [P, P, P, P, P, P, P, I64, I32, P, P, I64, I32, I32, P, P, P, P, P]),
@@ -90,7 +92,7 @@ _VALUE_FUNCS = {"lcrw_emd_problem_bytes", "lcrw_abi_version", "lcrw_status_strin
                 "lcrw_reverse_panels_tile_rows", "lcrw_reverse_panels_group", "lcrw_reverse_panels_warps",
                 "lcrw_reverse_panels_ilp", "lcrw_profile_count", "lcrw_table_chunk", "lcrw_table_bytes",
                 "lcrw_table_operand_rows", "lcrw_refine_tau",
-                "lcrw_reverse_panels_top_slots"}
+                "lcrw_reverse_panels_top_slots", "lcrw_plan_reverse_words_bound"}
 
 # kernels each entry point launches (CUB-backed ones counted from an ncu launch list,
 # profiles/); bench.py multiplies these by the per-step call counts for "gpu_launches".

@@ -424,10 +424,31 @@ REVERSE_Z2_BYTES = 4 << 30   # Z2 batch budget (docs per batch = budget / (4 * v
 
 
 def query_entries(x: DeviceCSR, rank: np.ndarray, a_rows: int):
-    """Device copy of plan_query_entries for x (host ids of a DeviceCSR): (e_blk, e_tile)."""
+    """The reverse pass's plan for x (host ids of a DeviceCSR) built natively on the host
+    (lcrw_plan_reverse, identical to plan_query_entries) and copied to the device:
+    (e_blk, e_tile)."""
     hc, hv = x.host_ids()
-    blk, tile = plan_query_entries(x.host_offsets, hc, hv, rank, a_rows, *reverse_panels_geometry())
+    blk, tile = plan_query_entries_native(x.host_offsets, hc, hv, rank, a_rows, *reverse_panels_geometry())
     return to_device(blk.view(np.int32), torch.int32), to_device(tile, torch.int64)
+
+
+def plan_query_entries_native(offsets, cols, vals, rank, a_rows: int, T: int, G: int, W: int, I: int):
+    """lcrw_plan_reverse (csrc/plan.cu, host code): same output as plan_query_entries."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float32)
+    rank = np.ascontiguousarray(rank, dtype=np.int32)
+    n_q = len(offsets) - 1
+    cap = int(_lib.value("lcrw_plan_reverse_words_bound", n_q, int(offsets[-1]) if n_q else 0, a_rows, T, G, W, I))
+    words = np.empty(max(cap, 1), dtype=np.uint32)
+    n_tiles = (a_rows + T - 1) // T
+    n_groups = (n_q + G - 1) // G
+    tile_off = np.empty(n_groups * n_tiles + 1, dtype=np.int64)
+    n_words = C.c_int64(0)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.call("lcrw_plan_reverse", ptr(offsets), n_q, ptr(cols), ptr(vals), ptr(rank), a_rows, T, G, W, I,
+              ptr(words), cap, ptr(tile_off), C.byref(n_words))
+    return words[: n_words.value], tile_off
 
 
 def reverse_panels_geometry() -> tuple[int, int, int, int]:

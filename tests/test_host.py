@@ -311,3 +311,18 @@ def test_bench_reference_arm_contract():
     assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["config"]["n_docs"] == 2000 and line["config"]["n_queries"] == 64
+
+
+@pytest.mark.parametrize("n_q,h,V", [(1000, 50, 100_000), (70, 300, 2000), (2100, 20, 5000), (3, 1, 10)])
+def test_native_plan_equals_numpy_plan(n_q, h, V):
+    """lcrw_plan_reverse (csrc/plan.cu, host code in the library) builds exactly the words
+    and block offsets of the numpy restatement plan_query_entries."""
+    from paper_1711_07227_b200.device import plan_query_entries, plan_query_entries_native
+    x = S.histograms(n_q, V, h, seed=9)
+    offs, cols, vals = np.asarray(x.row_offsets), np.asarray(x.column_ids), np.asarray(x.values)
+    used = np.unique(cols)
+    rank = np.full(V, -1, np.int32)
+    rank[used] = np.arange(len(used))
+    w1, t1 = plan_query_entries(offs, cols, vals, rank, len(used), 128, 1024, 16, 4)
+    w2, t2 = plan_query_entries_native(offs, cols, vals, rank, len(used), 128, 1024, 16, 4)
+    assert np.array_equal(w1, w2) and np.array_equal(t1, t2)
