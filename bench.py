@@ -425,7 +425,7 @@ def run_ours(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f16 operands, fp32 accumulate",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f16 operands, fp32 accumulate",
         "data": "synthetic (N(0,1) embeddings, uniform word ids; seeds 0/1/2)",
         "config": bench_config(cfg, world),
         "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
@@ -474,7 +474,7 @@ def run_reference(args, cfg):
                                  "numpy, pinned to the reference's outputs (tests/golden)"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "impl": "reference",
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (N(0,1) embeddings, uniform word ids; seeds 0/1/2)",
             "config": bench_config(cfg, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "extrapolated": True,

@@ -173,9 +173,16 @@ def lcrwmd_all_pairs_topk(x: HistogramSet, embeddings: np.ndarray, k: int, batch
 
 def lcrwmd_topk_arrays(x1, x2, embeddings, k: int, prep=None):
     """(n2, min(k, n1)) distances and int64 ids; accepts host sets or DeviceCSRs."""
-    # the resident set (the big copy) goes over a side stream while E and the query side are
-    # prepared; device.symmetric waits for it only where X1 is first read
-    dx1 = x1 if isinstance(x1, device.DeviceCSR) else device.DeviceCSR.upload(x1, "x1", stream=_copy_stream())
+    # E first (the query-side work needs only E and X2), then the resident set -- the big
+    # copy -- over a side stream while E and the query side are prepared; device.symmetric
+    # waits for X1 only where it is first read
+    if prep is None and not isinstance(embeddings, torch.Tensor):
+        embeddings = device.to_device(np.asarray(embeddings, dtype=np.float32), torch.float32)
+    if not isinstance(x1, device.DeviceCSR):
+        side = _copy_stream()
+        side.wait_stream(torch.cuda.current_stream())  # after E's copy: it is needed first
+        x1 = device.DeviceCSR.upload(x1, "x1", stream=side)
+    dx1 = x1
     if prep is None:
         prep = device.PreparedEmbeddings(embeddings)
     dx2 = x2 if isinstance(x2, device.DeviceCSR) else device.DeviceCSR.upload(x2, "x2")
