@@ -75,7 +75,10 @@ __device__ __forceinline__ void fix(const Args& g, int64_t row, int64_t s, int l
   if (lane == 0) *z_at(g, row, s) = d;
 }
 
-__global__ void __launch_bounds__(kThreads) refine_kernel(Args g) {
+#ifndef LCRW_REFINE_MINB
+#define LCRW_REFINE_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, LCRW_REFINE_MINB) refine_kernel(Args g) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)kThreads + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * kThreads) >> 5;
