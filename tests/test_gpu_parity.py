@@ -1016,3 +1016,32 @@ def test_solve_batch_csr_equals_solve_batch():
                         embeddings=Et, ids1=[x1.row(int(i)).word_ids for i in docs],
                         ids2=[x2.row(int(j)).word_ids for j in qs])
     assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_words", [30, 180, 360, 181])
+def test_table_chunk_boundaries(n_words, monkeypatch):
+    """Query vocabularies of exactly one warp block (30 words), one chunk (180), two chunks
+    (360: no partial chunk, the tail memset is skipped) and one word past a chunk (181):
+    the table form equals the GEMM form bitwise."""
+    import torch
+    from paper_1711_07227_b200 import device
+    from paper_1711_07227_b200.corpus import HistogramSet
+    rng = np.random.default_rng(90 + n_words)
+    V = 1000
+    E = rng.standard_normal((V, 300)).astype(np.float32)
+    words = np.sort(rng.choice(V, n_words, replace=False)).astype(np.int32)
+    rows = []
+    for j in range(0, n_words, 20):  # queries covering exactly these words
+        ids = words[j:j + 20]
+        u = rng.random(len(ids)) + 0.1
+        rows.append((ids, (u / u.sum()).astype(np.float32)))
+    x2 = HistogramSet.from_rows(rows, V)
+    x1 = _rand_set(rng, 900, V, 5, 60)
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    out = {}
+    for mode in ("gemm", "table"):
+        monkeypatch.setenv("LCRW_REVERSE", mode)
+        out[mode] = device.symmetric(d1, d2, prep, None)
+    assert torch.equal(out["gemm"], out["table"])
