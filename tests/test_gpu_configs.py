@@ -153,3 +153,30 @@ def test_wide_dynamic_range_embeddings():
     for j, t in enumerate(top):
         ok, err = rel_close(t.distances, ref[t.ids, j], RTOL, atol)
         assert ok, (j, err)
+
+
+def test_clustered_mid_size_refine_overflow(monkeypatch):
+    """Clustered embeddings at a size where ~40 % of the reverse Z2 entries are near
+    (d < 0.5 |a|): the table form's refine list (1M entries per batch) overflows and the
+    device falls back to the scan; D still equals the GEMM form bitwise and the oracle at
+    plain 1e-4 relative on sampled entries."""
+    import torch
+    from paper_1711_07227_b200 import device, synthetic as S
+    V, m = 20_000, 300
+    E = S.embeddings(V, m, seed=61, clustered=True, centers=100, spread=0.05)
+    x1 = S.histograms(100_000, V, 50, seed=62)
+    x2 = S.histograms(200, V, 50, seed=63)
+    prep = device.PreparedEmbeddings(E)
+    d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    out = {}
+    for mode in ("table", "gemm"):
+        monkeypatch.setenv("LCRW_REVERSE", mode)
+        out[mode] = device.symmetric(d1, d2, prep, None)
+    assert torch.equal(out["table"], out["gemm"])
+    rng = np.random.default_rng(64)
+    di = np.sort(rng.choice(100_000, 200, replace=False))
+    qj = np.sort(rng.choice(200, 20, replace=False))
+    got = out["table"][torch.as_tensor(di, device=out["table"].device)][:, torch.as_tensor(qj, device=out["table"].device)]
+    ref = O.lcrwmd_full(x1.take_rows(di), x2.take_rows(qj), E, threads=O.default_threads())
+    ok, err = rel_close(got.cpu().numpy(), ref, RTOL, ATOL)
+    assert ok, err
