@@ -220,7 +220,11 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
  * zeros are skipped; rep, next, remap, EhB may be NULL).  In GEMM mode Z2 is
  * rounded through the table's 21-bit key, so both modes give the same D.
  * E32 (v_rows x dim f32, unscaled) and a_ids (E id of each A row) feed the
- * exact re-evaluation of near Z2 entries (lcrw_refine_near, list mode). */
+ * exact re-evaluation of near Z2 entries (lcrw_refine_near).  Without near_ws: GEMM
+ * form fix-mode scan; table form: lcrw_table_min marks and lists them, finalize over
+ * the list.  With near_ws (an lcrw_near_pairs workspace of these a_rows / v_rows and
+ * capacity near_cap): the GEMM form marks them (mark scan), lcrw_near_scatter lowers
+ * the marked entries of either form, then the finalize mode. */
 int lcrw_reverse_workspace(int64_t a_rows, int kp, int64_t batch_docs, int64_t max_batch_words, size_t* bytes);
 int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                           int m, int kp,
@@ -229,7 +233,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
                           float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols,
-                          const void* table, const float* E32, int dim,
+                          const void* table, const void* near_ws, int64_t near_cap, const float* E32, int dim,
                           const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- distance-table reverse Phase 1 (table.cu) ---------------------------
@@ -254,8 +258,9 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
  * lcrw_table_min: Z2[p * z_panel + w * 32 + (d & 31)] = min over the words u of
  * doc d of T[w, u], decoded and unscaled (32-doc panels, z_panel = 32 * a_rows;
  * docs as lcrw_phase1's segments: doc_offsets[d] - seg_base .. into doc_cols,
- * E ids < v_rows); with refine_list != NULL it appends every near entry (w, d)
- * (lcrw_refine_near's test on the decoded value, a_norms of the A rows).  The GEMM form of the reverse pass rounds its Z2 through the
+ * E ids < v_rows); with refine_list != NULL every near entry (w, d) (lcrw_refine_near's
+ * test on the decoded value, a_norms of the A rows) is stored MARKED (all bits set) and
+ * appended to the list (*refine_count counts them all, past refine_cap too).  The GEMM form of the reverse pass rounds its Z2 through the
  * same key, so both forms give identical Z2. */
 int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
                         int m, int kp, const int64_t* seg_offsets, const uint32_t* endmask, const int32_t* range_seg,
@@ -268,7 +273,7 @@ int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const 
                          void* stream);
 int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
                    int64_t n_docs, const int32_t* doc_cols, const float* scale, float* Z2, int64_t z_panel,
-                   const float* a_norms, void* refine_list, uint32_t* refine_count, int64_t refine_cap,
+                   const float* a_norms, void* refine_list, uint64_t* refine_count, int64_t refine_cap,
                    void* stream);
 
 /* ---- exact re-evaluation of near entries (refine.cu) ---------
@@ -280,13 +285,58 @@ int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t*
  * panel layout (z_panel, z_shift) of a_rows x n_seg entries; segment s holds
  * B rows seg_ids[seg_offsets[s] - seg_base ..].  list == NULL: every entry is
  * tested (scan).  Otherwise list/count hold the (row, segment) uint32 pairs a
- * producer flagged (lcrw_table_min, the reverse pipeline's Phase 1) and only
- * those are recomputed -- unless *count > cap, in which case it scans. */
+ * producer flagged (lcrw_table_min) and only those are visited -- unless
+ * *count > cap, in which case it scans.  mode 0 (fix): flagged entries are
+ * recomputed.  mode 1 (mark; scan only): flagged entries are set to all bits
+ * (marked) and *count += their number.  mode 2 (finalize): marked entries (sign
+ * bit set) that lcrw_near_scatter lowered get the sign bit cleared, those still
+ * all bits are recomputed; nothing happens when *count == 0.  All three give the
+ * same Z bitwise. */
 float lcrw_refine_tau(void);
 int lcrw_refine_near(float* Z, int64_t z_panel, int z_shift, int64_t a_rows, int64_t n_seg,
                      const int64_t* seg_offsets, int64_t seg_base, const int32_t* seg_ids, const float* A32,
                      const int32_t* a_ids, const float* B32, int m, const float* a_norms, const float* scale,
-                     const void* list, const uint32_t* count, int64_t cap, void* stream);
+                     const void* list, uint64_t* count, int64_t cap, int mode, void* stream);
+
+/* ---- near word pairs (near.cu) ---------------------------------
+ * The fast form of the refinement when a distance table exists (replaces the
+ * per-entry recomputation of kernels.py:72-110 semantics for flagged entries).
+ * lcrw_near_pairs_build: from the table T of lcrw_distance_table (a_rows query-
+ * vocabulary rows with E ids a_ids and scaled squared norms a_norms; v_rows E rows
+ * with scaled squared norms v_norms, f32 rows E32 of width m), the word pairs with
+ * table distance < 0.75 max(|a|, |b|) (+ sqrt(m) 2^-22), their exact distances, and
+ * two CSRs of the pairs with exact distance < 0.6 |row word|: the reverse one keyed
+ * by E id (entries: query-vocabulary row), the forward one keyed by query-vocabulary
+ * row (entries: E id).  Enqueued without host sync; skipped (empty lists) when
+ * *gate == 0 (gate may be NULL); more than cap candidates leave the lists empty.
+ * The first 8 bytes of ws hold the candidate count (uint64).
+ * lcrw_near_scatter: for each segment s of Z (lcrw_refine_near's layout) and word t
+ * of it, the near pairs of key = seg_ids[t] (forward: key_map[seg_ids[t]], -1 =
+ * none) lower each MARKED entry (row, s) -- row = the pair's query-vocabulary row
+ * (reverse) or row_map[E id] (forward, -1 = none) -- to the exact distance with
+ * the sign bit set (atomicMin); unmarked entries never change.  Nothing happens when
+ * *gate == 0 (gate may be NULL).  Then lcrw_refine_near (finalize). */
+int lcrw_near_pairs_workspace(int64_t a_rows, int64_t v_rows, int64_t cap, size_t* bytes);
+/* lcrw_near_pairs_build = reset + candidates over the whole table + finish.  Without a
+ * whole table (the GEMM form: large vocabularies), the candidates come from tables of
+ * row slices: lcrw_near_pairs_candidates over a table T of t_rows query-vocabulary rows
+ * starting at row row_base (lcrw_distance_table of those rows; its exact zeros are not
+ * needed), appending to the list; lcrw_near_pairs_finish then computes the exact
+ * distances and the two CSRs. */
+int lcrw_near_pairs_reset(int64_t a_rows, int64_t v_rows, int64_t cap, void* ws, void* stream);
+int lcrw_near_pairs_candidates(const void* T, int64_t row_base, int64_t t_rows, int64_t a_rows, int64_t v_rows,
+                               const float* a_norms, const float* v_norms, int m, const uint64_t* gate, int64_t cap,
+                               void* ws, void* stream);
+int lcrw_near_pairs_finish(int64_t a_rows, int64_t v_rows, const int32_t* a_ids, const float* a_norms,
+                           const float* v_norms, const float* E32, int m, const float* scale, int64_t cap, void* ws,
+                           void* stream);
+int lcrw_near_pairs_build(const void* T, int64_t a_rows, int64_t v_rows, const int32_t* a_ids, const float* a_norms,
+                          const float* v_norms, const float* E32, int m, const float* scale, const uint64_t* gate,
+                          int64_t cap, void* ws, void* stream);
+int lcrw_near_scatter(const void* ws, int64_t a_rows, int64_t v_rows, int64_t cap, int direction, float* Z,
+                      int64_t z_panel, int z_shift, int64_t n_seg, const int64_t* seg_offsets, int64_t seg_base,
+                      const int32_t* seg_ids, const int32_t* key_map, const int32_t* row_map, const uint64_t* gate,
+                      void* stream);
 
 /* ---- top-k (kernels.py:210-232) ------------------------------------------
  * For each of n_seg segments of seg_len (distance, id) candidates, the k

@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "liblcrwmd.so"
-SOURCES = ["abi.cu", "prep.cu", "phase1.cu", "phase2.cu", "topk.cu", "pipeline.cu", "emd.cu", "table.cu", "prims.cu", "refine.cu", "plan.cu"]
+SOURCES = ["abi.cu", "prep.cu", "phase1.cu", "phase2.cu", "topk.cu", "pipeline.cu", "emd.cu", "table.cu", "prims.cu", "refine.cu", "plan.cu", "near.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          f"-I{ROOT / 'include'}"]

@@ -49,7 +49,7 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_spmm_dist": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
-                                    I64, P, P, I32, I64, I64, I32, P, P, I32, P, P, P, SZ, P]),
+                                    I64, P, P, I32, I64, I64, I32, P, P, I64, P, I32, P, P, P, SZ, P]),
     "lcrw_table_chunk": (I32, []),
     "lcrw_table_bytes": (I64, [I64, I64]),
     "lcrw_table_operand_rows": (I64, [I64]),
@@ -57,7 +57,13 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_distance_table": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P]),
     "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, P, I64, P, P, P, I64, P]),
     "lcrw_refine_tau": (C.c_float, []),
-    "lcrw_refine_near": (I32, [P, I64, I32, I64, I64, P, I64, P, P, P, P, I32, P, P, P, P, I64, P]),
+    "lcrw_refine_near": (I32, [P, I64, I32, I64, I64, P, I64, P, P, P, P, I32, P, P, P, P, I64, I32, P]),
+    "lcrw_near_pairs_workspace": (I32, [I64, I64, I64, P]),
+    "lcrw_near_pairs_build": (I32, [P, I64, I64, P, P, P, P, I32, P, P, I64, P, P]),
+    "lcrw_near_pairs_reset": (I32, [I64, I64, I64, P, P]),
+    "lcrw_near_pairs_candidates": (I32, [P, I64, I64, I64, I64, P, P, I32, P, I64, P, P]),
+    "lcrw_near_pairs_finish": (I32, [I64, I64, P, P, P, P, I32, P, I64, P, P]),
+    "lcrw_near_scatter": (I32, [P, I64, I64, I64, I32, P, I64, I32, I64, P, I64, P, P, P, P, P]),
     "lcrw_symmetrize_max": (I32, [P, I64, I64, P]),
     "lcrw_max_transposed": (I32, [P, I64, P, I64, I64, I64, P]),
     "lcrw_max_transposed_into": (I32, [P, I64, P, I64, P, I64, I64, I64, P]),
@@ -104,11 +110,13 @@ KERNELS_PER_CALL = {
     "lcrw_reverse_panels": 1, "lcrw_emd_batch": 1, "lcrw_symmetrize_max": 1, "lcrw_max_transposed": 1,
     "lcrw_max_transposed_into": 1, "lcrw_table_transpose": 1, "lcrw_table_min": 1,
     "lcrw_distance_table": 2, "lcrw_topk_sort_any": 7, "lcrw_squared_norms": 1, "lcrw_euclidean_f64": 1,
-    "lcrw_segmented_min": 1, "lcrw_refine_near": 1,
+    "lcrw_segmented_min": 1, "lcrw_refine_near": 1, "lcrw_near_pairs_build": 7, "lcrw_near_scatter": 1,
+    "lcrw_near_pairs_candidates": 1, "lcrw_near_pairs_finish": 6,
 }
 # lcrw_reverse_pipeline launches 7 kernels per doc batch (gather, 2 plan, phase1, zeros, refine,
-# reverse_panels) in GEMM mode, 3 (table_min, refine, reverse_panels) with a distance table; bench.py
-# adds those from the batch count (= its reverse_panels launches).
+# reverse_panels) in GEMM mode, 3 (table_min, refine, reverse_panels) with a distance table, plus the
+# near-pair scatter when near pairs are given; bench.py adds those from the batch count (= its
+# reverse_panels launches).
 REVERSE_KERNELS_PER_BATCH = 7
 REVERSE_KERNELS_PER_BATCH_TABLE = 3
 

@@ -339,17 +339,40 @@ constexpr float kRefineTau = 0.5f;
 __device__ __forceinline__ bool refine_flag(float d_scaled, float a_sq, float tau2) {
   return d_scaled > 0.f && d_scaled * d_scaled < tau2 * a_sq;
 }
-// where a reverse-pass producer appends the (row, segment) pairs it flags
+// where a reverse-pass producer appends the (row, segment) pairs it flags (64-bit count:
+// a heavily clustered batch can flag more than 2^32 entries)
 struct RefineSink {
   uint2* list;
-  uint32_t* count;
+  unsigned long long* count;
   int64_t cap;
 };
-// append (row, segment) to a refine list (reverse pass); entries past the capacity are
-// dropped and the count still grows, which sends lcrw_refine_near to its full scan
-__device__ __forceinline__ void refine_append(uint2* list, uint32_t* count, int64_t cap, uint32_t row, uint32_t seg) {
-  const uint32_t i = atomicAdd(count, 1u);
-  if ((int64_t)i < cap) list[i] = make_uint2(row, seg);
+// Marked entries (near pairs, near.cu): a producer that flags an entry stores kZMarked
+// (all bits set) instead of its value; lcrw_near_scatter lowers a marked entry with
+// atomicMin(kZMarkBit | bits(exact distance)) -- unmarked entries are non-negative floats,
+// below kZMarkBit, and never change -- and lcrw_refine_near's finalize mode clears the
+// mark bit, or recomputes an entry no near pair reached (still kZMarked).
+constexpr uint32_t kZMarkBit = 0x80000000u;
+constexpr uint32_t kZMarked = 0xFFFFFFFFu;
+// near pairs (near.cu): candidates are the word pairs whose table distance is below
+// kNearCandTau * max(|a|, |b|) (+ an absolute f16-subnormal term); kept as near pairs of a
+// direction when the exact distance is below kNearTau * |row word| -- a margin of 0.15 max
+// norm over the Gram error and of 0.1 |a| over the refine test
+constexpr float kNearTau = 0.6f;
+constexpr float kNearCandTau = 0.75f;
+// exact squared distance sum_k (a_k - b_k)^2 of two f32 rows, warp-cooperative (lanes
+// split the m dimensions, xor-reduction; every lane returns it).  The one formula of every
+// exact re-evaluation (refine.cu, near.cu): (a - b)^2 == (b - a)^2 bitwise, so a pair gives
+// the same value in either role.
+__device__ __forceinline__ float exact_sq(const float* __restrict__ a, const float* __restrict__ b, int m,
+                                          int lane) {
+  float acc = 0.f;
+  for (int k = lane; k < m; k += 32) {
+    const float diff = __ldg(a + k) - __ldg(b + k);
+    acc = fmaf(diff, diff, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
 }
 // Packed table rows: 180 query-vocabulary words per chunk; per vocabulary word u one
 // 480-byte row of 30 16-byte groups (one 16-byte load per lane of lanes 0..29 per

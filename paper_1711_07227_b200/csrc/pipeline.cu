@@ -13,7 +13,8 @@
 //   reverse  D[q, doc] = max(D1, spmm(Xq, Z2)), panel-streaming (query-major D)
 // or, with a distance table (table.cu; built once per query set), the first four
 // steps are one lcrw_table_min launch (exact zeros are already in the table; it
-// lists the near entries for the refine step instead of a scan).
+// marks and lists the near entries), followed by the near-pair scatter (near.cu)
+// and the refine step's finalize over the list instead of a scan.
 // The loop runs in C++ so a batch costs a handful of launch calls, not Python.
 #include <cstdlib>
 
@@ -35,7 +36,7 @@ int auto_range_cols(int64_t b_rows, int64_t a_rows) {
   return (int)want;
 }
 
-constexpr int64_t kRefineCap = 1 << 20;  // refine list entries per batch (overflow -> full scan)
+constexpr int64_t kRefineCap = 1 << 22;  // refine list entries per batch (overflow -> full scan)
 
 struct Layout {
   size_t T, tn, mask, rs, Z, rlist, rcount, total;
@@ -75,8 +76,9 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           int64_t n_docs, const int32_t* doc_cols, const int32_t* rep, const int32_t* next,
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
-                          float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols, const void* table, const float* E32,
-                          int dim, const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream) {
+                          float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols,
+                          const void* table, const void* near_ws, int64_t near_cap, const float* E32, int dim,
+                          const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
   LCRW_REQUIRE(doc_offsets_host && doc_offsets && doc_cols && (rep || table) && ws && (D || top_d) && E32 && a_ids &&
@@ -98,7 +100,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
   int32_t* rs = reinterpret_cast<int32_t*>(base + L.rs);
   float* Z2 = reinterpret_cast<float*>(base + L.Z);
   uint2* rlist = reinterpret_cast<uint2*>(base + L.rlist);
-  uint32_t* rcount = reinterpret_cast<uint32_t*>(base + L.rcount);
+  uint64_t* rcount = reinterpret_cast<uint64_t*>(base + L.rcount);
   const int64_t z_panel = a_rows << kZShift;
   cudaStream_t st = as_stream(stream);
   int status;
@@ -112,11 +114,16 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     const int64_t j1 = j0 + batch_docs < n_docs ? j0 + batch_docs : n_docs;
     const int64_t nd = j1 - j0;
     const int64_t lo = doc_offsets_host[j0], nw = doc_offsets_host[j1] - lo;
-    cudaError_t ce = cudaMemsetAsync(rcount, 0, sizeof(uint32_t), st);
+    cudaError_t ce = cudaMemsetAsync(rcount, 0, sizeof(uint64_t), st);
     if (ce != cudaSuccess) return cuda_status(ce, "cudaMemsetAsync (refine count)");
     if (table) {
+      // near entries are marked and listed; the near pairs (near.cu) lower them to their exact minima
       if ((status = lcrw_table_min(table, a_rows, v_rows, doc_offsets + j0, lo, nd, doc_cols + lo, scale, Z2,
                                    z_panel, a_norms, rlist, rcount, kRefineCap, stream)))
+        return status;
+      if (near_ws && (status = lcrw_near_scatter(near_ws, a_rows, v_rows, near_cap, 0, Z2, z_panel, kZShift, nd,
+                                                 doc_offsets + j0, lo, doc_cols + lo, nullptr, nullptr, rcount,
+                                                 stream)))
         return status;
     } else {
     if (!gather_b && (status = lcrw_gather_rows(EhB, nullptr, kp, doc_cols + lo, nw, T, nullptr, stream)))
@@ -130,11 +137,22 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;
+    if (near_ws) {  // mark the near entries for the near-pair scatter
+      if ((status = lcrw_refine_near(Z2, z_panel, kZShift, a_rows, nd, doc_offsets + j0, lo, doc_cols + lo, E32,
+                                     a_ids, E32, dim, a_norms, scale, nullptr, rcount, 0, 1, stream)))
+        return status;
+      if ((status = lcrw_near_scatter(near_ws, a_rows, v_rows, near_cap, 0, Z2, z_panel, kZShift, nd,
+                                      doc_offsets + j0, lo, doc_cols + lo, nullptr, nullptr, rcount, stream)))
+        return status;
     }
-    // table form: the entries table_min listed; GEMM form: a scan of the batch's Z2 (small next
-    // to the GEMM's work) -- the same test on the same stored values either way
+    }
+    // table form: finalize the entries table_min marked and listed (clear the marks the near
+    // pairs lowered, recompute the rest); GEMM form: a scan of the batch's Z2 (small next to
+    // the GEMM's work) fixing flagged entries -- the same test on the same stored values and
+    // bitwise the same results either way
     if ((status = lcrw_refine_near(Z2, z_panel, kZShift, a_rows, nd, doc_offsets + j0, lo, doc_cols + lo, E32, a_ids,
-                                   E32, dim, a_norms, scale, table ? rlist : nullptr, rcount, kRefineCap, stream)))
+                                   E32, dim, a_norms, scale, table ? rlist : nullptr, rcount, kRefineCap,
+                                   table || near_ws ? 2 : 0, stream)))
       return status;
     if (j0 == 0 && d1_ready) {  // D1 may still be in flight on another stream (forward direction)
       cudaError_t e = cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d1_ready), 0);

@@ -203,15 +203,46 @@ __global__ void __launch_bounds__(256, LCRW_TBL_MINB) table_min_kernel(const uin
   const int64_t w0 = c * kChunk;
   const bool doc_ok = p * kPanelDocs + lane < n_docs;
   const float* trow = tile + lane * kTileStride;
+  // near entries (lcrw_refine_near's scan test on the value) are stored marked (kZMarked);
+  // lcrw_near_scatter / lcrw_refine_near (finalize) replace them
+  auto is_near = [&](int q, float v) {
+    const float ds = v * s0;
+    return sink.list && doc_ok && ds * ds < kRefineTau * kRefineTau * wsq_max &&
+           refine_flag(ds, wsq[q], kRefineTau * kRefineTau);
+  };
+  uint32_t n_near = 0;
   for (int q = warp; q < kChunk; q += 8) {  // lane = doc; word q of the chunk
     if (w0 + q < a_rows) {
       const float v = trow[q];
-      st_stream(zp + (w0 + q) * kPanelDocs + lane, v, stream);
-      // near entries go to the refine list: lcrw_refine_near's scan test on the stored value
-      const float ds = v * s0;
-      if (sink.list && doc_ok && ds * ds < kRefineTau * kRefineTau * wsq_max &&
-          refine_flag(ds, wsq[q], kRefineTau * kRefineTau))
-        refine_append(sink.list, sink.count, sink.cap, (uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
+      const bool near = is_near(q, v);
+      st_stream(zp + (w0 + q) * kPanelDocs + lane, near ? __uint_as_float(kZMarked) : v, stream);
+      n_near += __popc(__ballot_sync(0xffffffffu, near));
+    }
+  }
+  if (!sink.list) return;
+  // the refine list: one global atomic per CTA (a per-entry counter serialises on clustered
+  // data), then the entries -- only while the list has room
+  __shared__ uint32_t warp_near[8];
+  __shared__ unsigned long long cta_base;
+  if (lane == 0) warp_near[warp] = n_near;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t total = 0;
+    for (int w = 0; w < 8; ++w) total += warp_near[w];
+    cta_base = total ? atomicAdd(sink.count, (unsigned long long)total) : ~0ull;
+  }
+  __syncthreads();
+  if (cta_base >= (unsigned long long)sink.cap) return;
+  unsigned long long pos = cta_base;
+  for (int w = 0; w < warp; ++w) pos += warp_near[w];
+  for (int q = warp; q < kChunk && n_near; q += 8) {
+    if (w0 + q < a_rows) {
+      const bool near = is_near(q, trow[q]);
+      const uint32_t ballot = __ballot_sync(0xffffffffu, near);
+      const unsigned long long mine = pos + __popc(ballot & ((1u << lane) - 1u));
+      if (near && mine < (unsigned long long)sink.cap)
+        sink.list[mine] = make_uint2((uint32_t)(w0 + q), (uint32_t)(p * kPanelDocs + lane));
+      pos += __popc(ballot);
     }
   }
 }
@@ -281,7 +312,7 @@ int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const 
 
 int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
                    int64_t n_docs, const int32_t* doc_cols, const float* scale, float* Z2, int64_t z_panel,
-                   const float* a_norms, void* refine_list, uint32_t* refine_count, int64_t refine_cap,
+                   const float* a_norms, void* refine_list, uint64_t* refine_count, int64_t refine_cap,
                    void* stream) {
   LCRW_REQUIRE(a_rows >= 0 && v_rows >= 0 && n_docs >= 0, "lcrw_table_min: bad shape");
   if (a_rows == 0 || n_docs == 0) return LCRW_OK;
@@ -297,7 +328,7 @@ int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t*
   ProfScope prof(st, "table_min");
   tbl::table_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(T), v_rows, a_rows, doc_offsets,
                                                           seg_base, n_docs, doc_cols, scale, Z2, z_panel, panels, a_norms,
-      RefineSink{static_cast<uint2*>(refine_list), refine_count, refine_cap});
+      RefineSink{static_cast<uint2*>(refine_list), reinterpret_cast<unsigned long long*>(refine_count), refine_cap});
   LCRW_CHECK_LAUNCH("table_min_kernel");
   return LCRW_OK;
 }

@@ -303,13 +303,106 @@ def zero_identical(seg_offsets, n_seg, rep, nxt, remap, Z, z_panel, z_shift: int
 
 
 def refine_near(Z, z_panel, z_shift, a_rows, n_seg, seg_offsets, seg_ids, a_ids, a_norms, prep: "PreparedEmbeddings",
-                B32: torch.Tensor | None = None) -> None:
+                B32: torch.Tensor | None = None, mode: int = 0, count: torch.Tensor | None = None) -> None:
     """Exact re-evaluation of the near entries of a Phase-1 Z (lcrw_refine_near, scan
     mode): entries with 0 < d < tau |a| become the exact segment minimum from the f32
-    rows (A rows E32[a_ids], segment rows B32[seg_ids], B32 = E32 by default)."""
+    rows (A rows E32[a_ids], segment rows B32[seg_ids], B32 = E32 by default).
+    mode 1 marks them instead (count += their number), mode 2 finalizes marked entries
+    (after lcrw_near_scatter); ``count`` is an int64 device scalar."""
     B = prep.E32 if B32 is None else B32
     _lib.call("lcrw_refine_near", _p(Z), z_panel, z_shift, a_rows, n_seg, _p(seg_offsets), 0, _p(seg_ids),
-              _p(prep.E32), _p(a_ids), _p(B), prep.m, _p(a_norms), _p(prep.scale), None, None, 0, _stream())
+              _p(prep.E32), _p(a_ids), _p(B), prep.m, _p(a_norms), _p(prep.scale), None, _p(count), 0, mode,
+              _stream())
+
+
+NEAR_CAP = 1 << 24  # near-pair candidates per query set (LCRW_NEAR_CAP overrides; LCRW_NEAR=0: no near pairs)
+NEAR_SLICE_BYTES = 4 << 30  # GEMM form: the candidates come from distance tables of query-vocabulary row slices
+
+
+class NearPairs:
+    """Near word pairs of a query set (near.cu, include/lcrwmd.h), lowering the marked near
+    entries of both directions to their exact minima (scatter) before refine_near
+    finalizes them.  With the query set's distance table they are built on the stream when
+    the forward direction marked near entries (device-side gate); in the GEMM form (no
+    table: large vocabularies) from tables of row slices, after a host read of the forward
+    direction's mark count (built only when it is non-zero).  An optimisation only:
+    without it (LCRW_NEAR=0, or a candidate overflow) the marked entries are recomputed in
+    full, bitwise the same."""
+
+    def __init__(self, table: torch.Tensor | None, res2: "Restricted", prep: PreparedEmbeddings):
+        self.cap = int(os.environ.get("LCRW_NEAR_CAP", NEAR_CAP))
+        self.a_rows, self.v_rows = res2.v_e, prep.V
+        dev = res2.A.device
+        self.gate = torch.zeros(1, dtype=torch.int64, device=dev)  # entries the forward direction marked
+        self.table, self.res2, self.prep = table, res2, prep
+        self.built = table is not None  # (GEMM form: decided after the forward direction's marks)
+        self.ws = self._workspace() if table is not None else None
+
+    def _workspace(self) -> torch.Tensor:
+        ws_bytes = C.c_size_t(0)
+        _lib.call("lcrw_near_pairs_workspace", self.a_rows, self.v_rows, self.cap, C.byref(ws_bytes))
+        return torch.empty(ws_bytes.value, dtype=torch.uint8, device=self.gate.device)
+
+    @staticmethod
+    def enabled() -> bool:
+        return os.environ.get("LCRW_NEAR", "1") != "0"
+
+    def _build(self) -> None:
+        p, r2 = self.prep, self.res2
+        if self.table is not None:
+            _lib.call("lcrw_near_pairs_build", _p(self.table), self.a_rows, self.v_rows, _p(r2.used),
+                      _p(r2.a_norms), _p(p.norms), _p(p.E32), p.m, _p(p.scale), _p(self.gate), self.cap,
+                      _p(self.ws), _stream())
+            return
+        self.built = int(self.gate.item()) > 0
+        if not self.built:
+            return
+        self.ws = self._workspace()
+        _lib.call("lcrw_near_pairs_reset", self.a_rows, self.v_rows, self.cap, _p(self.ws), _stream())
+        chunk = int(_lib.value("lcrw_table_chunk"))
+        rows = max(1, NEAR_SLICE_BYTES // (p.V * TABLE_ROW_BYTES)) * chunk
+        dev = r2.A.device
+        seg = torch.arange(p.V + 1, dtype=torch.int64, device=dev)
+        plan = segment_plan(seg, p.V, p.V, min(rows, self.a_rows))
+        no_rows = torch.full((p.V,), -1, dtype=torch.int32, device=dev)  # (exact zeros: not needed)
+        for r0 in range(0, self.a_rows, rows):
+            n = min(rows, self.a_rows - r0)
+            T = torch.empty(int(_lib.value("lcrw_table_bytes", n, p.V)), dtype=torch.uint8, device=dev)
+            Ap, anp = _table_operand(r2.used[r0:r0 + n], p)
+            _lib.call("lcrw_distance_table", _p(Ap), _p(anp), n, _p(p.EhB), p.V, p.k_eff, p.kp, _p(seg), _p(plan[0]),
+                      _p(plan[1]), plan[2], _p(p.scale), _p(p.canon), _p(p.next), _p(no_rows), _p(T), _stream())
+            _lib.call("lcrw_near_pairs_candidates", _p(T), r0, n, self.a_rows, p.V, _p(r2.a_norms), _p(p.norms), p.m,
+                      None, self.cap, _p(self.ws), _stream())
+            del T
+        _lib.call("lcrw_near_pairs_finish", self.a_rows, self.v_rows, _p(r2.used), _p(r2.a_norms), _p(p.norms),
+                  _p(p.E32), p.m, _p(p.scale), self.cap, _p(self.ws), _stream())
+
+    def forward(self, Z, zp, zs, res1: "Restricted", queries_offsets, query_cols, n_q) -> None:
+        """Forward Z1 (rows: res1's words, segments: the queries): mark, build the pairs
+        (skipped when nothing was marked), scatter, finalize."""
+        refine_near(Z, zp, zs, res1.v_e, n_q, queries_offsets, query_cols, res1.used, res1.a_norms, self.prep,
+                    mode=1, count=self.gate)
+        self._build()
+        if self.built:
+            _lib.call("lcrw_near_scatter", _p(self.ws), self.a_rows, self.v_rows, self.cap, 1, _p(Z), zp, zs, n_q,
+                      _p(queries_offsets), 0, _p(query_cols), _p(self.res2.remap), _p(res1.remap), _p(self.gate),
+                      _stream())
+        refine_near(Z, zp, zs, res1.v_e, n_q, queries_offsets, query_cols, res1.used, res1.a_norms, self.prep,
+                    mode=2, count=self.gate)
+
+    def n_candidates(self) -> int:
+        """Candidate pairs of the last build (reads the device header; tests)."""
+        return int(self.ws[:8].view(torch.int64).item()) if self.built else 0
+
+
+def _table_operand(ids: torch.Tensor, prep: PreparedEmbeddings):
+    """The distance-table build's padded A operand for query-vocabulary E ids ``ids``: 30
+    rows per 32 (include/lcrwmd.h); the two filler rows of each block repeat a real row."""
+    n = ids.numel()
+    a_pad = int(_lib.value("lcrw_table_operand_rows", n))
+    r = np.arange(a_pad, dtype=np.int64)
+    real = np.minimum((r // 32) * 30 + np.minimum(r % 32, 29), n - 1)
+    return gather_rows(prep, ids[to_device(real, torch.int64)], "A")
 
 
 def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel,
@@ -391,23 +484,28 @@ class Restricted:
 
 
 def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: torch.Tensor, word_ids: torch.Tensor,
-                      n_seg: int, z_shift: int = 3) -> tuple[torch.Tensor, int]:
-    """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros)."""
+                      n_seg: int, z_shift: int = 3, near: NearPairs | None = None) -> tuple[torch.Tensor, int]:
+    """Z over res's vocabulary for segments of E rows ``word_ids`` (with exact zeros);
+    ``near``: the segments are the query set of those near pairs (faster refinement)."""
     B, _ = gather_rows(prep, word_ids, "B")
     Z, zp = phase1(res.A, res.a_norms, res.v_e, B, word_ids.numel(), seg_offsets, n_seg, prep, z_shift=z_shift)
     rep, nxt = prep.representatives(word_ids)
     zero_identical(seg_offsets, n_seg, rep, nxt, res.remap, Z, zp, z_shift)
-    refine_near(Z, zp, z_shift, res.v_e, n_seg, seg_offsets, word_ids, res.used, res.a_norms, prep)
+    if near is None:
+        refine_near(Z, zp, z_shift, res.v_e, n_seg, seg_offsets, word_ids, res.used, res.a_norms, prep)
+    else:
+        near.forward(Z, zp, z_shift, res, seg_offsets, word_ids, n_seg)
     return Z, zp
 
 
-def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR, layout: str = "rows") -> torch.Tensor:
+def one_direction(res: Restricted, prep: PreparedEmbeddings, queries: DeviceCSR, layout: str = "rows",
+                  near: NearPairs | None = None) -> torch.Tensor:
     """distances.py:181-204 for all queries at once: (n_res, n_q) bounds.
 
     layout "rows" -> row-major (n_res, n_q); "panels" -> out[(q>>3)*8*n_res + i*8 + (q&7)]."""
     n_res, n_q = res.csr.n_rows, queries.n_rows
     zs = spmm_z_shift(n_q)
-    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q, zs)
+    Z, zp = nearest_distances(res, prep, queries.offsets, queries.cols, n_q, zs, near)
     if layout == "rows":
         out = torch.empty(n_res * max(n_q, 1), dtype=torch.float32, device=Z.device)
         ld_row, ld_panel = n_q, 8
@@ -571,12 +669,7 @@ def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: 
         _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(prep.scale), _p(T), _stream())
         return T
     endmask, range_seg, n_ranges = segment_plan(seg, V, V, res2.v_e)
-    # the build's A operand: 30 query-vocabulary rows per 32 (include/lcrwmd.h); the two
-    # filler rows of each block repeat a real row and are not stored
-    a_pad = int(_lib.value("lcrw_table_operand_rows", res2.v_e))
-    r = np.arange(a_pad, dtype=np.int64)
-    real = np.minimum((r // 32) * 30 + np.minimum(r % 32, 29), res2.v_e - 1)
-    Ap, anp = gather_rows(prep, res2.used[to_device(real, torch.int64)], "A")
+    Ap, anp = _table_operand(res2.used, prep)
     _lib.call("lcrw_distance_table", _p(Ap), _p(anp), res2.v_e, _p(prep.EhB), V, prep.k_eff, prep.kp,
               _p(seg), _p(endmask), _p(range_seg), n_ranges, _p(prep.scale), _p(prep.canon), _p(prep.next),
               _p(res2.remap), _p(T), _stream())
@@ -645,10 +738,14 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
     res2 = Restricted.build(x2, prep, host_plan=True)
     mode = reverse_mode(prep.V, res2.v_e, x1.nnz)
     table = distance_table(res2, prep) if mode == "table" else None
+    # near word pairs of the table (near.cu): built on the device only when the forward
+    # direction marks near entries; they replace the per-entry exact recomputation
+    # (not when a caller supplies D1: the gate is the forward direction's count)
+    near = NearPairs(table, res2, prep) if d1 is None and NearPairs.enabled() else None
     x1.wait()
     if d1 is None:
         res1 = Restricted.build(x1, prep)
-        d1 = one_direction(res1, prep, x2, layout="panels")  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
+        d1 = one_direction(res1, prep, x2, layout="panels", near=near)  # D1[(q>>3)*8*n1 + j*8 + (q&7)]
         del res1
     e_blk, e_tile = query_entries(x2, res2.host_rank, res2.v_e)
     if table is not None and z2_budget_bytes == REVERSE_Z2_BYTES:
@@ -681,9 +778,12 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
               prep.kp,
               _p(prep.scale), _p(x1.offsets), host_offs.ctypes.data_as(C.c_void_p), n1, _p(x1.cols), _p(rep),
               _p(nxt), _p(res2.remap), _p(e_blk), _p(e_tile), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
-              _p(top_d), _p(top_i), k if fused else 0, id_offset, batch, 0, _p(table), _p(prep.E32), prep.m, _p(res2.used),
+              _p(top_d), _p(top_i), k if fused else 0, id_offset, batch, 0, _p(table),
+              _p(near.ws) if near is not None and near.built else None, near.cap if near is not None else 0,
+              _p(prep.E32), prep.m,
+              _p(res2.used),
               C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value, st)
-    del ws, table
+    del ws, table, near
     if k is None:
         return D.view(n1, n2)
     kk = min(k, n1)

@@ -301,15 +301,27 @@ def test_refine_list_overflow_falls_back_to_scan():
     device.refine_near(scan, zp, 3, res.v_e, d2.n_rows, d2.offsets, d2.cols, res.used, res.a_norms, prep)
     assert not torch.equal(scan, Z0)  # clustered rows: some entries were near
     lst = torch.zeros(16, dtype=torch.int64, device=Z0.device)
-    cnt = torch.tensor([1 << 20], dtype=torch.int32, device=Z0.device)  # > capacity 8
+    cnt = torch.tensor([1 << 20], dtype=torch.int64, device=Z0.device)  # > capacity 8
     over = Z0.clone()
     _lib.call("lcrw_refine_near", device._p(over), zp, 3, res.v_e, d2.n_rows, device._p(d2.offsets), 0,
               device._p(d2.cols), device._p(prep.E32), device._p(res.used), device._p(prep.E32), prep.m,
-              device._p(res.a_norms), device._p(prep.scale), device._p(lst), device._p(cnt), 8, device._stream())
+              device._p(res.a_norms), device._p(prep.scale), device._p(lst), device._p(cnt), 8, 0, device._stream())
     assert torch.equal(over, scan)
     empty = Z0.clone()
     cnt.zero_()
     _lib.call("lcrw_refine_near", device._p(empty), zp, 3, res.v_e, d2.n_rows, device._p(d2.offsets), 0,
               device._p(d2.cols), device._p(prep.E32), device._p(res.used), device._p(prep.E32), prep.m,
-              device._p(res.a_norms), device._p(prep.scale), device._p(lst), device._p(cnt), 8, device._stream())
+              device._p(res.a_norms), device._p(prep.scale), device._p(lst), device._p(cnt), 8, 0, device._stream())
     assert torch.equal(empty, Z0)  # an empty list changes nothing
+    # mark (flagged -> all bits, counted) then finalize without any near pairs: every marked
+    # entry is recomputed -- the fix scan's Z, bitwise
+    marked = Z0.clone()
+    cnt.zero_()
+    device.refine_near(marked, zp, 3, res.v_e, d2.n_rows, d2.offsets, d2.cols, res.used, res.a_norms, prep,
+                       mode=1, count=cnt)
+    n_marked = int(cnt.item())
+    assert n_marked > 0 and n_marked == int((marked.view(torch.int32) == -1).sum())
+    assert torch.equal(marked.view(torch.int32) == -1, marked != Z0)  # only the marks changed
+    device.refine_near(marked, zp, 3, res.v_e, d2.n_rows, d2.offsets, d2.cols, res.used, res.a_norms, prep,
+                       mode=2, count=cnt)
+    assert torch.equal(marked, scan)

@@ -157,9 +157,11 @@ def test_wide_dynamic_range_embeddings():
 
 def test_clustered_mid_size_refine_overflow(monkeypatch):
     """Clustered embeddings at a size where ~40 % of the reverse Z2 entries are near
-    (d < 0.5 |a|): the table form's refine list (1M entries per batch) overflows and the
-    device falls back to the scan; D still equals the GEMM form bitwise and the oracle at
-    plain 1e-4 relative on sampled entries."""
+    (d < 0.5 |a|): the table form's refine list (4M entries per batch) overflows and its
+    finalize step scans.  The near word pairs (near.cu) lower the marked entries to their
+    exact minima; without them (LCRW_NEAR=0), with a candidate list that overflows
+    (LCRW_NEAR_CAP), and in the GEMM form (per-entry recomputation) D is bitwise the same,
+    and equals the oracle at plain 1e-4 relative on sampled entries."""
     import torch
     from paper_1711_07227_b200 import device, synthetic as S
     V, m = 20_000, 300
@@ -168,11 +170,27 @@ def test_clustered_mid_size_refine_overflow(monkeypatch):
     x2 = S.histograms(200, V, 50, seed=63)
     prep = device.PreparedEmbeddings(E)
     d1, d2 = device.DeviceCSR.upload(x1), device.DeviceCSR.upload(x2)
+    built = []
+    orig_forward = device.NearPairs.forward
+
+    def forward(self, *a, **kw):
+        orig_forward(self, *a, **kw)
+        built.append(self.n_candidates())
+    monkeypatch.setattr(device.NearPairs, "forward", forward)
     out = {}
-    for mode in ("table", "gemm"):
-        monkeypatch.setenv("LCRW_REVERSE", mode)
-        out[mode] = device.symmetric(d1, d2, prep, None)
-    assert torch.equal(out["table"], out["gemm"])
+    for name, env in (("table", {}), ("table_no_near", {"LCRW_NEAR": "0"}),
+                      ("table_near_overflow", {"LCRW_NEAR_CAP": "64"}), ("gemm", {"LCRW_REVERSE": "gemm"})):
+        for key in ("LCRW_NEAR", "LCRW_NEAR_CAP"):
+            monkeypatch.delenv(key, raising=False)
+        monkeypatch.setenv("LCRW_REVERSE", "table")
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        out[name] = device.symmetric(d1, d2, prep, None)
+    # the near pairs were built: from the table, then overflowing, then from the GEMM form's
+    # slice tables (which also list the identical-word pairs: no exact-zero pass there)
+    assert len(built) == 3 and built[0] > 0 and built[1] > 64 and built[2] >= built[0], built
+    for name in ("table_no_near", "table_near_overflow", "gemm"):
+        assert torch.equal(out["table"], out[name]), name
     rng = np.random.default_rng(64)
     di = np.sort(rng.choice(100_000, 200, replace=False))
     qj = np.sort(rng.choice(200, 20, replace=False))
