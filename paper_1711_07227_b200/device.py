@@ -336,7 +336,10 @@ class NearPairs:
         self.gate = torch.zeros(1, dtype=torch.int64, device=dev)  # entries the forward direction marked
         self.table, self.res2, self.prep = table, res2, prep
         self.built = table is not None  # (GEMM form: decided after the forward direction's marks)
-        self.ws = self._workspace() if table is not None else None
+        self.ws = None
+        if table is not None:  # an empty header until built (a rank with no forward rows never builds)
+            self.ws = self._workspace()
+            _lib.call("lcrw_near_pairs_reset", self.a_rows, self.v_rows, self.cap, _p(self.ws), _stream())
 
     def _workspace(self) -> torch.Tensor:
         ws_bytes = C.c_size_t(0)
@@ -377,17 +380,18 @@ class NearPairs:
         _lib.call("lcrw_near_pairs_finish", self.a_rows, self.v_rows, _p(r2.used), _p(r2.a_norms), _p(p.norms),
                   _p(p.E32), p.m, _p(p.scale), self.cap, _p(self.ws), _stream())
 
-    def forward(self, Z, zp, zs, res1: "Restricted", queries_offsets, query_cols, n_q) -> None:
-        """Forward Z1 (rows: res1's words, segments: the queries): mark, build the pairs
-        (skipped when nothing was marked), scatter, finalize."""
-        refine_near(Z, zp, zs, res1.v_e, n_q, queries_offsets, query_cols, res1.used, res1.a_norms, self.prep,
+    def forward(self, Z, zp, zs, a_rows: int, a_ids, a_norms, row_map, queries_offsets, query_cols, n_q) -> None:
+        """Forward Z1 over this query set (rows: E ids a_ids with scaled squared norms
+        a_norms, row_map = E id -> Z1 row or -1; segments: the queries): mark, build the
+        pairs (skipped when nothing was marked), scatter, finalize."""
+        refine_near(Z, zp, zs, a_rows, n_q, queries_offsets, query_cols, a_ids, a_norms, self.prep,
                     mode=1, count=self.gate)
         self._build()
         if self.built:
             _lib.call("lcrw_near_scatter", _p(self.ws), self.a_rows, self.v_rows, self.cap, 1, _p(Z), zp, zs, n_q,
-                      _p(queries_offsets), 0, _p(query_cols), _p(self.res2.remap), _p(res1.remap), _p(self.gate),
+                      _p(queries_offsets), 0, _p(query_cols), _p(self.res2.remap), _p(row_map), _p(self.gate),
                       _stream())
-        refine_near(Z, zp, zs, res1.v_e, n_q, queries_offsets, query_cols, res1.used, res1.a_norms, self.prep,
+        refine_near(Z, zp, zs, a_rows, n_q, queries_offsets, query_cols, a_ids, a_norms, self.prep,
                     mode=2, count=self.gate)
 
     def n_candidates(self) -> int:
@@ -494,7 +498,7 @@ def nearest_distances(res: Restricted, prep: PreparedEmbeddings, seg_offsets: to
     if near is None:
         refine_near(Z, zp, z_shift, res.v_e, n_seg, seg_offsets, word_ids, res.used, res.a_norms, prep)
     else:
-        near.forward(Z, zp, z_shift, res, seg_offsets, word_ids, n_seg)
+        near.forward(Z, zp, z_shift, res.v_e, res.used, res.a_norms, res.remap, seg_offsets, word_ids, n_seg)
     return Z, zp
 
 
@@ -688,14 +692,15 @@ QUERY_SLICE = 16384  # queries per pass of the symmetric pipeline (bounds D, D1,
 
 def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
               z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0,
-              query_slice: int = QUERY_SLICE):
+              query_slice: int = QUERY_SLICE, prepared: "QuerySide | None" = None):
     """lcrwmd_full (k=None -> (n1, n2) matrix) or its per-query top-k ((n2, min(k, n1))
     dists, ids).  Query sets of any size: queries are processed in slices of
     ``query_slice`` (a multiple of 8), each slice a full pass (restriction, table, both
     directions) -- query batching never changes a result (distances.py:198-203).
 
     ``d1`` (8-query panels) may be supplied by a caller that computed the
-    forward direction itself (parallel.py); ``id_offset`` shifts returned doc ids."""
+    forward direction itself (parallel.py), with the query side it prepared for it
+    (``prepared``, a single-pass query set only); ``id_offset`` shifts returned doc ids."""
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
     if n1 == 0 or n2 == 0:
@@ -705,7 +710,7 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
                 torch.empty((n2, 0), dtype=torch.int64, device=dev))
     qs = max(8, query_slice // 8 * 8)
     if n2 <= qs:
-        return _symmetric_pass(x1, x2, prep, k, z2_budget_bytes, d1, id_offset)
+        return _symmetric_pass(x1, x2, prep, k, z2_budget_bytes, d1, id_offset, prepared)
     if k is None:
         D = torch.empty((n1, n2), dtype=torch.float32, device=dev)
     else:
@@ -724,8 +729,26 @@ def symmetric(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | N
     return D if k is None else (out_d, out_i)
 
 
+@dataclass
+class QuerySide:
+    """A query set's device-side preparation for one pass: its restriction, the reverse
+    distance table (None: GEMM form) and the near word pairs (None: disabled)."""
+
+    res2: "Restricted"
+    table: torch.Tensor | None
+    near: NearPairs | None
+
+    @classmethod
+    def build(cls, x2: DeviceCSR, prep: PreparedEmbeddings, nnz_docs: int) -> "QuerySide":
+        res2 = Restricted.build(x2, prep, host_plan=True)
+        mode = reverse_mode(prep.V, res2.v_e, nnz_docs)
+        table = distance_table(res2, prep) if mode == "table" else None
+        return cls(res2, table, NearPairs(table, res2, prep) if NearPairs.enabled() else None)
+
+
 def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: int | None,
-                    z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0):
+                    z2_budget_bytes: int = REVERSE_Z2_BYTES, d1: torch.Tensor | None = None, id_offset: int = 0,
+                    prepared: QuerySide | None = None):
     """One pass of ``symmetric`` over all of x2's queries."""
     n1, n2 = x1.n_rows, x2.n_rows
     dev = x1.cols.device
@@ -735,13 +758,14 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
     # X1 still being copied in on another stream (DeviceCSR.upload(..., stream=)) overlaps it;
     # then the forward pass; the host-side plan of the reverse pass is built while the
     # forward kernels run
-    res2 = Restricted.build(x2, prep, host_plan=True)
-    mode = reverse_mode(prep.V, res2.v_e, x1.nnz)
-    table = distance_table(res2, prep) if mode == "table" else None
-    # near word pairs of the table (near.cu): built on the device only when the forward
-    # direction marks near entries; they replace the per-entry exact recomputation
-    # (not when a caller supplies D1: the gate is the forward direction's count)
-    near = NearPairs(table, res2, prep) if d1 is None and NearPairs.enabled() else None
+    # near word pairs (near.cu): built only when the forward direction marks near entries;
+    # they replace the per-entry exact recomputation (a caller that supplies D1 passes the
+    # query side its forward direction used, or goes without them)
+    if prepared is None:
+        prepared = QuerySide.build(x2, prep, x1.nnz)
+        if d1 is not None:
+            prepared.near = None
+    res2, table, near = prepared.res2, prepared.table, prepared.near
     x1.wait()
     if d1 is None:
         res1 = Restricted.build(x1, prep)

@@ -111,9 +111,12 @@ def gather_candidates(d: torch.Tensor, i: torch.Tensor, group=None):
 # CUDA pipeline
 # ---------------------------------------------------------------------------
 
-def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) -> tuple[torch.Tensor, int]:
+def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int,
+             near: "device.NearPairs | None" = None) -> tuple[torch.Tensor, int]:
     """This rank's forward Phase-1 slice: Z1 rows [v0, v1) as (panels, R, W), zero padded,
-    W = 1 << device.spmm_z_shift(n_q) segments per panel."""
+    W = 1 << device.spmm_z_shift(n_q) segments per panel.  ``near``: the near word pairs
+    of dx2's query side (device.QuerySide), refining the slice's near entries (and built
+    by it when it marks any)."""
     n_q = dx2.n_rows
     v0, v1, R = vocab_slice(prep.V, rank, world)
     rows = v1 - v0
@@ -130,8 +133,11 @@ def z1_slice(dx2: DeviceCSR, prep: PreparedEmbeddings, rank: int, world: int) ->
         remap[v0:v1] = torch.arange(rows, dtype=torch.int32, device=dev)
         rep, nxt = prep.representatives(dx2.cols)
         device.zero_identical(dx2.offsets, n_q, rep, nxt, remap, Z, zp, zs)
-        device.refine_near(Z, zp, zs, rows, n_q, dx2.offsets, dx2.cols,
-                           torch.arange(v0, v1, dtype=torch.int32, device=dev), prep.norms[v0:v1], prep)
+        a_ids = torch.arange(v0, v1, dtype=torch.int32, device=dev)
+        if near is None:
+            device.refine_near(Z, zp, zs, rows, n_q, dx2.offsets, dx2.cols, a_ids, prep.norms[v0:v1], prep)
+        else:
+            near.forward(Z, zp, zs, rows, a_ids, prep.norms[v0:v1], remap, dx2.offsets, dx2.cols, n_q)
         zl[:, :rows, :] = Z.view(panels, rows, W)
     return zl, R
 
@@ -150,10 +156,11 @@ def d1_from_slices(dx1: DeviceCSR, zall: torch.Tensor, R: int, n_q: int) -> torc
     return out
 
 
-def forward_d1(dx1: DeviceCSR, dx2: DeviceCSR, prep: PreparedEmbeddings, group=None) -> torch.Tensor:
+def forward_d1(dx1: DeviceCSR, dx2: DeviceCSR, prep: PreparedEmbeddings, group=None,
+               near: "device.NearPairs | None" = None) -> torch.Tensor:
     """D1 (panels, local docs) with Phase 1 split by vocabulary slice + Z1 all-gather."""
     rank, world = _world()
-    zl, R = z1_slice(dx2, prep, rank, world)
+    zl, R = z1_slice(dx2, prep, rank, world, near)
     zall = allgather_slices(zl, group)  # [world][panels][R][W]
     return d1_from_slices(dx1, zall, R, dx2.n_rows)
 
@@ -162,8 +169,10 @@ def sharded_topk(dx1: DeviceCSR, doc_base: int, n1_total: int, dx2: DeviceCSR, p
                  group=None):
     """Per-query top-k over all ranks' docs; (n_q, k) on rank 0, None elsewhere."""
     rank, world = _world()
-    d1 = forward_d1(dx1, dx2, prep, group)
-    ld, li = device.symmetric(dx1, dx2, prep, k, d1=d1, id_offset=doc_base)
+    # the query side first: its near word pairs serve this rank's forward slice and reverse pass
+    qside = device.QuerySide.build(dx2, prep, dx1.nnz) if dx2.n_rows <= device.QUERY_SLICE else None
+    d1 = forward_d1(dx1, dx2, prep, group, qside.near if qside is not None else None)
+    ld, li = device.symmetric(dx1, dx2, prep, k, d1=d1, id_offset=doc_base, prepared=qside)
     if ld.shape[1] < k:  # shard smaller than k: pad with sentinels so gather shapes agree
         pd = torch.full((ld.shape[0], k), float("inf"), dtype=ld.dtype, device=ld.device)
         pi = torch.full((li.shape[0], k), torch.iinfo(torch.int64).max, dtype=li.dtype, device=li.device)

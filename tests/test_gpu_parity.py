@@ -257,6 +257,41 @@ def test_sharded_pipeline_emulated_ranks():
         assert torch.equal(gd, want_d) and torch.equal(gi, want_i), W
 
 
+@pytest.mark.parametrize("mode", ["table", "gemm"])
+def test_sharded_pipeline_emulated_ranks_near_pairs(monkeypatch, mode):
+    """The same decomposition on clustered embeddings with each rank's query side
+    (device.QuerySide: restriction, table, near word pairs) shared by its forward slice and
+    its reverse pass, as parallel.sharded_topk does: the near pairs are built per rank from
+    its own slice's marks, and the merged top-k equals the single-GPU result bitwise."""
+    import torch
+    from paper_1711_07227_b200 import device, parallel, synthetic as S
+    monkeypatch.setenv("LCRW_REVERSE", mode)
+    V, k, W = 4000, 10, 3
+    E = S.embeddings(V, 300, seed=41, clustered=True, centers=40, spread=0.1)
+    x1 = S.histograms(3000, V, 40, seed=42)
+    x2 = S.histograms(29, V, 40, seed=43)
+    prep = device.PreparedEmbeddings(E)
+    dx2 = device.DeviceCSR.upload(x2)
+    want_d, want_i = device.symmetric(device.DeviceCSR.upload(x1), dx2, prep, k)
+    shards = [parallel.shard_range(x1.n_rows, r, W) for r in range(W)]
+    dx1s = [device.DeviceCSR.upload(x1.slice_rows(lo, hi)) for lo, hi in shards]
+    qsides = [device.QuerySide.build(dx2, prep, dx1s[r].nnz) for r in range(W)]
+    slices = [parallel.z1_slice(dx2, prep, r, W, qsides[r].near) for r in range(W)]
+    assert all(q.near is not None and q.near.n_candidates() > 0 for q in qsides)
+    R = slices[0][1]
+    zall = torch.stack([z for z, _ in slices])
+    parts_d, parts_i = [], []
+    for r, (lo, hi) in enumerate(shards):
+        d1 = parallel.d1_from_slices(dx1s[r], zall, R, x2.n_rows)
+        ld, li = device.symmetric(dx1s[r], dx2, prep, k, d1=d1, id_offset=lo, prepared=qsides[r])
+        parts_d.append(ld)
+        parts_i.append(li)
+    cd = torch.cat(parts_d, 1).contiguous()
+    ci = torch.cat(parts_i, 1).contiguous()
+    gd, gi = device.topk_rows(cd, ci, x2.n_rows, cd.shape[1], k)
+    assert torch.equal(gd, want_d) and torch.equal(gi, want_i)
+
+
 @pytest.mark.slow
 def test_c2_full_size_sampled_parity():
     """BASELINE configs[1] at full size (1M docs x 1k queries, V=100k, m=300):
