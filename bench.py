@@ -346,8 +346,8 @@ def run_ours(args, cfg):
     rev_flops = 2.0 * v_e2 * x1s.nnz * cfg["dim"]
     fwd_flops = 2.0 * int(np.unique(x1s.column_ids).size) * x2.nnz * cfg["dim"]
     table_flops = 2.0 * v_e2 * cfg["vocab"] * cfg["dim"]
-    # table_min gathers, per doc word and 180-word table chunk, one 480-byte row of 21-bit keys
-    # (2.67 B per (query-vocabulary word, doc word) distance) and writes one 4-byte Z2 entry per
+    # table_min gathers, per doc word and 256-word table chunk, one 512-byte row of 16-bit keys
+    # (2 B per (query-vocabulary word, doc word) distance) and writes one 4-byte Z2 entry per
     # (query-vocabulary word, doc)
     from paper_1711_07227_b200 import _lib as _L, device as _dev
     n_chunks = -(-v_e2 // int(_L.value("lcrw_table_chunk")))
@@ -384,7 +384,7 @@ def run_ours(args, cfg):
                      "achieved": p1_work / (p1_ms * 1e-3) / 1e12 if p1_ms else None, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": p1_work / (p1_ms * 1e-3) / 1e12 / peak_tf if p1_ms else None,
                      "note": "algorithmic 2*rows*cols*m FLOP of the Phase-1 GEMMs launched per step; the table "
-                             "build is store-bound (10.5 GB of table at C2), the GEMM-path reverse Phase 1 "
+                             "build is store-bound (7.9 GB of table at C2), the GEMM-path reverse Phase 1 "
                              "(--reverse gemm) runs at 0.93-0.97 of the sustained peak"}
     if table_mode:  # dominant kernel: the distance-table gathers, bound by L2 bandwidth
         tm = ksum["table_min"]
@@ -392,8 +392,8 @@ def run_ours(args, cfg):
         l2path = ROOT / "profiles" / "l2_gather_peak.json"
         l2 = json.loads(l2path.read_text()) if l2path.exists() else {"gbs": float("nan"), "source": "missing"}
         tr = traffic_all.get("table_min_kernel")
-        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 480-B rows of 21-bit keys of "
-                              "an L2-resident 180-word distance-table chunk)",
+        roofline = {"kernel": "table_min_kernel (reverse Phase 1: per-doc min over 512-B rows of 16-bit keys of "
+                              "an L2-resident 256-word distance-table chunk)",
                     "bound": "l2", "achieved": achieved, "peak": l2["gbs"], "unit": "GB/s",
                     "frac": achieved / l2["gbs"],
                     "traffic": tr["dram_bytes_per_launch"] if tr else None,

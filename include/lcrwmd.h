@@ -218,7 +218,9 @@ int lcrw_max_transposed(float* D, int64_t ldd, const float* R, int64_t ldr, int6
  * lcrw_distance_table for these a_rows query-vocabulary rows and the v_rows E
  * rows; each batch's Z2 is then one lcrw_table_min (gather, plan, phase1 and
  * zeros are skipped; rep, next, remap, EhB may be NULL).  In GEMM mode Z2 is
- * rounded through the table's 21-bit key, so both modes give the same D.
+ * rounded through the table's 16-bit key when z2_keyed != 0, so both modes give the
+ * same D (z2_keyed = 0: plain f32 Z2 -- the split-operand precision of m <= 64, where
+ * the table form is not chosen).
  * E32 (v_rows x dim f32, unscaled) and a_ids (E id of each A row) feed the
  * exact re-evaluation of near Z2 entries (lcrw_refine_near).  Without near_ws: GEMM
  * form fix-mode scan; table form: lcrw_table_min marks and lists them, finalize over
@@ -233,33 +235,35 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
                           float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols,
-                          const void* table, const void* near_ws, int64_t near_cap, const float* E32, int dim,
-                          const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream);
+                          const void* table, const void* near_ws, int64_t near_cap, int z2_keyed, const float* E32,
+                          int dim, const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- distance-table reverse Phase 1 (table.cu) ---------------------------
  * When nnz(X1) >> V, every (w, u) distance of the reverse Phase 1 is needed
- * ~nnz/V times; the table holds each once, as a 21-bit order-preserving key of
- * the scaled distance (5 exponent + 16 mantissa bits, round to nearest:
- * relative error <= 2^-17; 0 stays 0 -- common.cuh dist_key21):
- *   chunk c = w / 180 of 180 query-vocabulary words, per E row u one 480-byte
- *   row at byte ((c * v_rows) + u) * 480: 30 16-byte groups of six keys
- *   (layout in common.cuh);  lcrw_table_bytes(a_rows, v_rows) bytes,
+ * ~nnz/V times; the table holds each once, as a 16-bit key of the scaled distance
+ * relative to its query word w (common.cuh dist_key16: 0 = exact zero, 1 = below
+ * 2^e (a near entry), 2..0xFFFE = 2 exponent + 14 mantissa bits over [2^e, 2^(e+4)),
+ * round to nearest: relative error <= 2^-15, 0xFFFF = saturated; 2^e <= |w| / 2 <
+ * 2^(e+1) from w's scaled squared norm a_norms[w]):
+ *   chunk c = w / 256 of 256 query-vocabulary words, per E row u one 512-byte
+ *   row at byte ((c * v_rows) + u) * 512 of little-endian uint16 keys, word w of
+ *   the chunk at byte 2 (w % 256);  lcrw_table_bytes(a_rows, v_rows) bytes,
  * with exact zeros for identical rows.
- * lcrw_distance_table builds it in one pass: lcrw_phase1 over the query-
- * vocabulary A rows and ALL v_rows E rows (EhB) as singleton segments
- * (seg_offsets = 0..v_rows and its lcrw_segment_plan), storing packed rows
- * directly (the same entries lcrw_phase1 computes in the GEMM form), then the
- * zeros (canon/next classes of lcrw_row_classes, remap = E id -> A row or -1).
- * A / a_norms are PADDED: lcrw_table_operand_rows(a_rows) rows, row
- * 32 * (r / 30) + r % 30 holding query-vocabulary row r (rows 30, 31 of each
- * 32 are ignored), so each warp of the epilogue stores whole 16-byte groups.
+ * lcrw_distance_table builds it in one pass: lcrw_phase1 over the a_rows query-
+ * vocabulary A rows (lcrw_table_operand_rows(a_rows) == a_rows: no padding) and
+ * ALL v_rows E rows (EhB) as singleton segments (seg_offsets = 0..v_rows and its
+ * lcrw_segment_plan), storing keys directly (the same entries lcrw_phase1 computes
+ * in the GEMM form), then the zeros (canon/next classes of lcrw_row_classes,
+ * remap = E id -> A row or -1).
  * lcrw_table_transpose builds the same table from lcrw_phase1's z_shift-7 f32
- * output Tp (unscaled; zeros already applied) and scale (cross-check path).
+ * output Tp (unscaled; zeros already applied), the A rows' a_norms and scale
+ * (cross-check path).
  * lcrw_table_min: Z2[p * z_panel + w * 32 + (d & 31)] = min over the words u of
  * doc d of T[w, u], decoded and unscaled (32-doc panels, z_panel = 32 * a_rows;
  * docs as lcrw_phase1's segments: doc_offsets[d] - seg_base .. into doc_cols,
  * E ids < v_rows); with refine_list != NULL every near entry (w, d) (lcrw_refine_near's
- * test on the decoded value, a_norms of the A rows) is stored MARKED (all bits set) and
+ * test on the decoded value, a_norms of the A rows) and every saturated one is stored
+ * MARKED (all bits set) and
  * appended to the list (*refine_count counts them all, past refine_cap too).  The GEMM form of the reverse pass rounds its Z2 through the
  * same key, so both forms give identical Z2. */
 int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows, const uint16_t* EhB, int64_t v_rows,
@@ -269,8 +273,8 @@ int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows,
 int lcrw_table_chunk(void);
 int64_t lcrw_table_bytes(int64_t a_rows, int64_t v_rows);
 int64_t lcrw_table_operand_rows(int64_t a_rows);
-int lcrw_table_transpose(const float* Tp, int64_t a_rows, int64_t v_rows, const float* scale, void* T,
-                         void* stream);
+int lcrw_table_transpose(const float* Tp, const float* a_norms, int64_t a_rows, int64_t v_rows, const float* scale,
+                         void* T, void* stream);
 int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t* doc_offsets, int64_t seg_base,
                    int64_t n_docs, const int32_t* doc_cols, const float* scale, float* Z2, int64_t z_panel,
                    const float* a_norms, void* refine_list, uint64_t* refine_count, int64_t refine_cap,
@@ -291,7 +295,9 @@ int lcrw_table_min(const void* T, int64_t a_rows, int64_t v_rows, const int64_t*
  * (marked) and *count += their number.  mode 2 (finalize): marked entries (sign
  * bit set) that lcrw_near_scatter lowered get the sign bit cleared, those still
  * all bits are recomputed; nothing happens when *count == 0.  All three give the
- * same Z bitwise. */
+ * same Z bitwise.  mode | 4 (keyed; fix and mark): Z holds values rounded through the
+ * reverse table's 16-bit key (a_norms = its rows' norms): entries at the key's
+ * saturation value are flagged too. */
 float lcrw_refine_tau(void);
 int lcrw_refine_near(float* Z, int64_t z_panel, int z_shift, int64_t a_rows, int64_t n_seg,
                      const int64_t* seg_offsets, int64_t seg_base, const int32_t* seg_ids, const float* A32,

@@ -49,11 +49,11 @@ SIGNATURES: dict[str, tuple] = {
     "lcrw_spmm_dist": (I32, [P, P, P, I64, P, I64, I32, I64, I64, I64, P, I64, I64, P]),
     "lcrw_reverse_workspace": (I32, [I64, I32, I64, I64, P]),
     "lcrw_reverse_pipeline": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P, I64, P, I64, P, I64,
-                                    I64, P, P, I32, I64, I64, I32, P, P, I64, P, I32, P, P, P, SZ, P]),
+                                    I64, P, P, I32, I64, I64, I32, P, P, I64, I32, P, I32, P, P, P, SZ, P]),
     "lcrw_table_chunk": (I32, []),
     "lcrw_table_bytes": (I64, [I64, I64]),
     "lcrw_table_operand_rows": (I64, [I64]),
-    "lcrw_table_transpose": (I32, [P, I64, I64, P, P, P]),
+    "lcrw_table_transpose": (I32, [P, P, I64, I64, P, P, P]),
     "lcrw_distance_table": (I32, [P, P, I64, P, I64, I32, I32, P, P, P, I64, P, P, P, P, P, P]),
     "lcrw_table_min": (I32, [P, I64, I64, P, I64, I64, P, P, P, I64, P, P, P, I64, P]),
     "lcrw_refine_tau": (C.c_float, []),

@@ -311,25 +311,37 @@ __device__ __forceinline__ float key_float(uint32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// 21-bit distance keys of the reverse direction (table.cu).
-// A distance d in the scaled operand space (0 <= d < 2^8: every scaled row has
-// |x'| < 2^7) is stored as an order-preserving 21-bit key: 5 exponent bits
-// relative to 2^-23 and 16 mantissa bits, rounded to nearest (relative error
-// <= 2^-17 ~ 7.6e-6); 0 -> 0 (exact zeros stay exact), 0 < d < 2^-22 -> 1.
-// Keys compare as integers, so min over keys == key of the min, and the table
-// form and the GEMM form of the reverse Phase 1 round identically.
+// 16-bit distance keys of the reverse direction (table.cu).
+// Reverse-direction distances are stored as 16-bit keys relative to their query-
+// vocabulary word w (the table's column; the A row of the Phase-1 GEMM): with |w|^2 the
+// A row's scaled squared norm and 2^e <= |w| / 2 < 2^(e+1) (key16_base),
+//   0          exact zero (identical rows);
+//   1          0 < d < 2^e (below the range: a near entry, d < |w| / 2, refined exactly;
+//              decodes to 2^(e-1));
+//   2..0xFFFE  d in [2^e, 2^(e+4)): 2 exponent bits (the binade above 2^e) and 14 mantissa
+//              bits, rounded to nearest (relative error <= 2^-15 ~ 3.1e-5);
+//   0xFFFF     saturated: d at or above the top of the range (> 4 |w|), refined exactly.
+// Codes of one word compare like its distances, so a doc's minimum over its words' rows
+// is an integer minimum, and the table form and the GEMM form of the reverse Phase 1
+// (which rounds its Z2 through the same key) give identical Z2.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kKeyExpBase = 104u;  // f32 biased exponent of 2^-23
-constexpr uint32_t kKeyMax = (1u << 21) - 1u;
-__device__ __forceinline__ uint32_t dist_key21(float d) {
+constexpr uint32_t kKey16Sat = 0xFFFFu;
+__device__ __forceinline__ uint32_t key16_base(float a_sq) {  // bits of 2^e (f32)
+  const int e2 = (int)(__float_as_uint(a_sq) >> 23) - 127;   // exponent of |w|^2
+  return (uint32_t)((e2 >> 1) - 1 + 127) << 23;               // 2^e <= |w| / 2 < 2^(e+1)
+}
+__device__ __forceinline__ uint32_t dist_key16(float d, uint32_t base) {
   const uint32_t b = __float_as_uint(d);
-  if (b < ((kKeyExpBase + 1u) << 23)) return b == 0u ? 0u : 1u;
-  const uint32_t k = (b - (kKeyExpBase << 23) + 64u) >> 7;
-  return k < kKeyMax ? k : kKeyMax;
+  if (b == 0u) return 0u;
+  if (b < base) return 1u;
+  const uint32_t c = (b - base + 256u) >> 9;
+  return c < 2u ? 1u : (c < kKey16Sat ? c : kKey16Sat);
 }
-__device__ __forceinline__ float key21_dist(uint32_t key) {
-  return key ? __uint_as_float((key << 7) + (kKeyExpBase << 23)) : 0.f;
+__device__ __forceinline__ float key16_dist(uint32_t c, uint32_t base) {
+  return c == 0u ? 0.f : __uint_as_float(c == 1u ? base - (1u << 23) : base + (c << 9));
 }
+// the decoded value of a saturated key: an entry at it is refined exactly
+__device__ __forceinline__ float key16_sat(uint32_t base) { return key16_dist(kKey16Sat, base); }
 // Near-entry refinement (refine.cu): a Z entry whose scaled distance d satisfies
 // 0 < d < kRefineTau * |a| (|a|^2 = the A row's scaled squared norm) is recomputed
 // exactly from the f32 rows.  The test always reads the stored (unscaled) Z value times
@@ -374,31 +386,15 @@ __device__ __forceinline__ float exact_sq(const float* __restrict__ a, const flo
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
-// Packed table rows: 180 query-vocabulary words per chunk; per vocabulary word u one
-// 480-byte row of 30 16-byte groups (one 16-byte load per lane of lanes 0..29 per
-// row in table_min: 2.67 bytes per distance).  Group g = four little-endian 32-bit
-// words q0..q3 holding words 6g .. 6g+5 of the chunk:
-//   q_i = key(6g + i) << 11 | piece_i      (i = 0..3)
-//   piece_0 = key(6g+4) >> 10,  piece_1 = (key(6g+4) & 0x3FF) << 1,
-//   piece_2 = key(6g+5) >> 10,  piece_3 = (key(6g+5) & 0x3FF) << 1
-// so the min of q_i over rows has key(6g + i) in its top 21 bits (no unpacking), and
-// key(6g+4) << 11 == funnelshift_l(q1 << 21, q0, 21) (likewise key(6g+5) from q2, q3).
-// The table build (phase1 epilogue, kZTable) runs on query-vocabulary rows padded to
-// 30 real rows per 32 (lcrw_table_rows): a warp's 30 rows are 5 whole groups, which it
-// assembles with one shuffle and stores as 80 contiguous bytes.
-constexpr int kTableChunk = 180;
-constexpr int kTableKeysPerGroup = 6;
-constexpr int kTableGroups = 30;
-#ifndef LCRW_TABLE_ROW_BYTES
-#define LCRW_TABLE_ROW_BYTES 480
-#endif
-constexpr int kTableRowBytes = LCRW_TABLE_ROW_BYTES;  // row stride (30 groups used; 512 = 128-B aligned rows)
-constexpr int kTableWarpRows = 30;  // real rows per 32-row warp block of the padded operand
-// word q_i of key p's group inside a row: byte offset of the group and the key's slot i
-__host__ __device__ __forceinline__ void table_key_slot(int p, int& group_byte, int& slot) {
-  group_byte = 16 * (p / kTableKeysPerGroup);
-  slot = p % kTableKeysPerGroup;
-}
+// Table rows: 256 query-vocabulary words per chunk; per vocabulary word u one 512-byte
+// row of 256 little-endian 16-bit keys (word w of the chunk at byte 2 w): 32 16-byte groups
+// of 8 keys, one per lane in table_min (2 bytes per distance; the minima are SIMD 16-bit
+// integer minima, VIMNMX.U16x2).  The table build (phase1 epilogue, kZTable) stores a
+// warp's 32 rows (= 32 consecutive words) of one column as 64 contiguous bytes.
+constexpr int kTableChunk = 256;
+constexpr int kTableKeysPerGroup = 8;
+constexpr int kTableGroups = 32;
+constexpr int kTableRowBytes = 512;
 
 namespace p1 {
 // the tcgen05 Phase-1 GEMM with fused segmented-min epilogue (phase1.cu)

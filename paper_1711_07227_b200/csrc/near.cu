@@ -29,7 +29,7 @@
 //
 // Build (lcrw_near_pairs_build, on the stream, no host sync; all kernels return at once
 // when the gate counter -- the forward direction's marked entries -- is 0):
-//   candidates  one thread per 16-byte table group (six keys), warp-aggregated appends
+//   candidates  one thread per 16-byte table group (eight keys), warp-aggregated appends
 //   exact       one warp per candidate: exact_sq, the two direction tests, per-key counts
 //   offsets     CUB inclusive sums of the counts -> two CSRs: reverse keyed by E id u
 //               (entries: query-vocabulary row, distance), forward keyed by query-
@@ -96,16 +96,16 @@ __global__ void __launch_bounds__(kThreads) candidates_kernel(const uint4* __res
       u = t / kTableGroups;
       w_base = w_chunk + kTableKeysPerGroup * (t - u * kTableGroups);
       const uint4 r = __ldg(Tc + t);
-      const uint32_t key[kTableKeysPerGroup] = {r.x >> 11, r.y >> 11, r.z >> 11, r.w >> 11,
-                                                __funnelshift_l(r.y << 21, r.x, 21) >> 11,
-                                                __funnelshift_l(r.w << 21, r.z, 21) >> 11};
+      const uint32_t kw[4] = {r.x, r.y, r.z, r.w};
       const float vs = __ldg(v_sq + u);
 #pragma unroll
       for (int j = 0; j < kTableKeysPerGroup; ++j) {
         const int64_t w = w_base + j;
-        if (w < a_rows && key[j] != 0u) {
-          const float thr = kNearCandTau * sqrtf(fmaxf(__ldg(a_sq + row_base + w), vs)) + delta;
-          if (key21_dist(key[j]) < thr) cm |= 1u << j;
+        const uint32_t key = (kw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+        if (w < a_rows && key != 0u) {
+          const float as = __ldg(a_sq + row_base + w);
+          const float thr = kNearCandTau * sqrtf(fmaxf(as, vs)) + delta;
+          if (key16_dist(key, key16_base(as)) < thr) cm |= 1u << j;
         }
       }
     }

@@ -67,8 +67,7 @@ enum ZMode : int {
   kZPanels = 0,     // f32 Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))] (segment panels)
   kZPanelsKey = 1,  // the same, values rounded through the 21-bit key (reverse direction, GEMM form)
   kZTable = 2,      // packed 21-bit distance table (kTableChunk-word chunks, kTableRowBytes per
-                    // segment = vocabulary word; z_panel = bytes per chunk); A rows padded to
-                    // 30 real rows per 32-row warp block (common.cuh)
+                    // segment = vocabulary word; z_panel = bytes per chunk; common.cuh)
 };
 
 struct Params {
@@ -429,24 +428,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float nE = valid ? __ldg(p.a_norms + row) : 0.f;
       // output cursor: segment s = U.sb(grp) + emitted so far, at
       //   Z[(s >> zs) * z_panel + (row << zs) + (s & (zw-1))]   (segment panels), or
-      //   packed table bytes: chunk (row / 192) of the padded rows, row s of 480 bytes,
-      //   group 5 (row % 192) / 32 + lane / 6, word lane % 6 (< 4) -- lanes 0..29 of a warp
-      //   hold 5 whole groups, so each segment's store is 80 contiguous bytes of the row
+      //   table bytes: chunk row / 256, row s of 512 bytes, key (row % 256) -- a warp's 32
+      //   rows are 64 contiguous bytes of the row
       const int64_t s_first = U.sb(grp);
       float* zq;
       int64_t step, wrap;
       uint32_t s_in = (uint32_t)s_first & (zw - 1);
       uint8_t* zb = nullptr;
-      const int t_slot = lane % kTableKeysPerGroup;
-      const int t_src = lane < kTableWarpRows ? lane - t_slot + 4 + (t_slot >> 1) : lane;  // its piece's key
-      const bool t_store = lane < kTableWarpRows && t_slot < 4 && valid;
+      const uint32_t kbase = key16_base(nE);  // the row word's 16-bit key range (reverse direction)
       if (p.z_mode == kZTable) {
         zq = nullptr;
         step = wrap = 0;
-        const int wb = (row % (kTableChunk / kTableWarpRows * 32)) >> 5;  // warp block inside the chunk
-        zb = reinterpret_cast<uint8_t*>(p.Z) + ((int64_t)row / (kTableChunk / kTableWarpRows * 32)) * p.z_panel +
-             s_first * kTableRowBytes + (wb * (kTableWarpRows / kTableKeysPerGroup) + lane / kTableKeysPerGroup) * 16 +
-             t_slot * 4;
+        zb = reinterpret_cast<uint8_t*>(p.Z) + ((int64_t)row / kTableChunk) * p.z_panel + s_first * kTableRowBytes +
+             (row % kTableChunk) * 2;
       } else {
         zq = p.Z + (s_first >> zs) * p.z_panel + ((int64_t)row << zs) + s_in;
         step = 1;
@@ -457,14 +451,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float d;
         asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(fmaxf(segmin + nE, 0.f)));
         if (p.z_mode == kZTable) {
-          const uint32_t key = dist_key21(d);
-          const uint32_t pk = __shfl_sync(0xffffffffu, key, t_src);
-          const uint32_t piece = (t_slot & 1) ? (pk & 0x3FFu) << 1 : pk >> 10;
-          if (t_store) *reinterpret_cast<uint32_t*>(zb) = key << 11 | piece;
+          if (valid) *reinterpret_cast<uint16_t*>(zb) = (uint16_t)dist_key16(d, kbase);
           zb += kTableRowBytes;
           return;
         }
-        if (p.z_mode == kZPanelsKey) d = key21_dist(dist_key21(d));
+        if (p.z_mode == kZPanelsKey) d = key16_dist(dist_key16(d, kbase), kbase);
         if (valid) *zq = d * inv_scale;
         zq += step;
         if (++s_in == zw) {

@@ -77,7 +77,8 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
                           const int32_t* remap, const uint32_t* e_blk, const int64_t* e_tile,
                           int64_t n_q, const float* D1, int64_t d1_ld_panel, float* D, int64_t ld_q, int64_t ld_doc,
                           float* top_d, int64_t* top_i, int k, int64_t id_base, int64_t batch_docs, int range_cols,
-                          const void* table, const void* near_ws, int64_t near_cap, const float* E32, int dim,
+                          const void* table, const void* near_ws, int64_t near_cap, int z2_keyed, const float* E32,
+                          int dim,
                           const int32_t* a_ids, void* d1_ready, void* ws, size_t ws_bytes, void* stream) {
   LCRW_REQUIRE(n_docs >= 0 && n_q >= 0 && a_rows >= 0, "lcrw_reverse_pipeline: bad shape");
   if (n_docs == 0 || n_q == 0) return LCRW_OK;
@@ -133,13 +134,14 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     if ((status = lcrw_segment_plan(doc_offsets + j0, lo, nd, nw, rc, mask, rs, n_ranges, stream))) return status;
     if ((status = p1::launch(A, a_norms, a_rows, gather_b ? EhB : T, nw, m, kp, doc_offsets + j0, lo, nd, mask, rs,
                              n_ranges, scale, Z2, z_panel, kZShift, st, "phase1_rev",
-                             gather_b ? doc_cols + lo : nullptr, v_table, 1 /* kZPanelsKey */)))
+                             gather_b ? doc_cols + lo : nullptr, v_table, z2_keyed ? 1 /* kZPanelsKey */ : 0)))
       return status;
     if ((status = lcrw_zero_identical(doc_offsets + j0, nd, rep, next, remap, Z2, z_panel, kZShift, stream)))
       return status;
     if (near_ws) {  // mark the near entries for the near-pair scatter
       if ((status = lcrw_refine_near(Z2, z_panel, kZShift, a_rows, nd, doc_offsets + j0, lo, doc_cols + lo, E32,
-                                     a_ids, E32, dim, a_norms, scale, nullptr, rcount, 0, 1, stream)))
+                                     a_ids, E32, dim, a_norms, scale, nullptr, rcount, 0, z2_keyed ? 1 | 4 : 1,
+                                     stream)))
         return status;
       if ((status = lcrw_near_scatter(near_ws, a_rows, v_rows, near_cap, 0, Z2, z_panel, kZShift, nd,
                                       doc_offsets + j0, lo, doc_cols + lo, nullptr, nullptr, rcount, stream)))
@@ -152,7 +154,7 @@ int lcrw_reverse_pipeline(const uint16_t* A, const float* a_norms, int64_t a_row
     // bitwise the same results either way
     if ((status = lcrw_refine_near(Z2, z_panel, kZShift, a_rows, nd, doc_offsets + j0, lo, doc_cols + lo, E32, a_ids,
                                    E32, dim, a_norms, scale, table ? rlist : nullptr, rcount, kRefineCap,
-                                   table || near_ws ? 2 : 0, stream)))
+                                   (table || near_ws) ? 2 : (z2_keyed ? 0 | 4 : 0), stream)))
       return status;
     if (j0 == 0 && d1_ready) {  // D1 may still be in flight on another stream (forward direction)
       cudaError_t e = cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d1_ready), 0);

@@ -42,7 +42,7 @@ __device__ __forceinline__ float exact_segment_min(const float* __restrict__ a, 
   return sqrtf(best);
 }
 
-enum Mode { kFix = 0, kMark = 1, kFinalize = 2 };
+enum Mode { kFix = 0, kMark = 1, kFinalize = 2, kKeyed = 4 };
 
 struct Args {
   float* Z;
@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(kThreads, LCRW_REFINE_MINB) refine_kernel(Args
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)kThreads + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * kThreads) >> 5;
-  const bool finalize = g.mode == kFinalize, mark = g.mode == kMark;
+  const bool finalize = (g.mode & 3) == kFinalize, mark = (g.mode & 3) == kMark;
+  const bool keyed = (g.mode & kKeyed) != 0;  // Z holds 16-bit key values: saturated ones are flagged too
   if (finalize && __ldg(g.count) == 0) return;  // nothing was marked
   if (g.list && !mark) {
     const unsigned long long n = __ldg(g.count);
@@ -166,10 +167,12 @@ __global__ void __launch_bounds__(kThreads, LCRW_REFINE_MINB) refine_kernel(Args
           } else if (zv[0] > 0.f || zv[1] > 0.f || zv[2] > 0.f || zv[3] > 0.f) {
             // the lane's four entries share one row (z_shift >= 2): one norm, one bound
             const float a_sq = __ldg(g.a_norms + (i0 >> g.z_shift));
+            const float sat = keyed ? key16_sat(key16_base(a_sq)) : __int_as_float(0x7f800000);
             const int64_t s_base = p * zw + (i0 & (zw - 1));
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              if (s_base + j < g.n_seg && refine_flag(zv[j] * s0, a_sq, tau2)) flags |= 1u << j;
+              if (s_base + j < g.n_seg && (refine_flag(zv[j] * s0, a_sq, tau2) || zv[j] * s0 >= sat))
+                flags |= 1u << j;
           }
         }
         if (mark || finalize) {
@@ -250,9 +253,10 @@ int lcrw_refine_near(float* Z, int64_t z_panel, int z_shift, int64_t a_rows, int
                "lcrw_refine_near: bad Z layout (z_shift in [2, 10], z_panel % 4 == 0, Z 16-byte aligned)");
   LCRW_REQUIRE(ceil_div(n_seg, 1ll << z_shift) < (1ll << 31) && ceil_div(a_rows << z_shift, 128) < (1ll << 31),
                "lcrw_refine_near: Z too large");
-  LCRW_REQUIRE(mode >= 0 && mode <= 2, "lcrw_refine_near: mode is 0 (fix), 1 (mark) or 2 (finalize)");
+  LCRW_REQUIRE((mode & ~4) >= 0 && (mode & ~4) <= 2,
+               "lcrw_refine_near: mode is 0 (fix), 1 (mark) or 2 (finalize), | 4 for keyed values");
   LCRW_REQUIRE(!list || (count && cap >= 0), "lcrw_refine_near: a list needs its count and capacity");
-  LCRW_REQUIRE(mode == 0 || count, "lcrw_refine_near: mark and finalize need the count");
+  LCRW_REQUIRE((mode & 3) == 0 || count, "lcrw_refine_near: mark and finalize need the count");
   refine::Args g{Z, z_panel, z_shift, a_rows, n_seg, seg_offsets, seg_base, seg_ids, A32, a_ids, B32, m, a_norms,
                  scale, static_cast<const uint2*>(list), reinterpret_cast<unsigned long long*>(count), cap, mode};
   // one warp per 128-entry step (scan) or list entry, at most one resident wave of CTAs

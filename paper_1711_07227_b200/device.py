@@ -400,13 +400,8 @@ class NearPairs:
 
 
 def _table_operand(ids: torch.Tensor, prep: PreparedEmbeddings):
-    """The distance-table build's padded A operand for query-vocabulary E ids ``ids``: 30
-    rows per 32 (include/lcrwmd.h); the two filler rows of each block repeat a real row."""
-    n = ids.numel()
-    a_pad = int(_lib.value("lcrw_table_operand_rows", n))
-    r = np.arange(a_pad, dtype=np.int64)
-    real = np.minimum((r // 32) * 30 + np.minimum(r % 32, 29), n - 1)
-    return gather_rows(prep, ids[to_device(real, torch.int64)], "A")
+    """The distance-table build's A operand: the query-vocabulary rows E[ids] and their norms."""
+    return gather_rows(prep, ids, "A")
 
 
 def spmm(x_offsets, x_cols, x_vals, n_rows, Z, z_panel, n_seg, out, ld_row, ld_panel,
@@ -635,20 +630,21 @@ def plan_query_entries(offsets: np.ndarray, cols: np.ndarray, vals: np.ndarray, 
 REVERSE_TABLE_Z2_FRACTION = 3  # table mode: Z2 batches up to 1/3 of HBM -- each batch re-streams the table
                                # once and larger batches keep one chunk L2-resident for longer (C2 on
                                # B200: 16 GB 502 ms, 32 GB 490 ms, 64 GB 485 ms per step)
-TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 480 B) must stay L2-resident
-TABLE_ROW_BYTES = 480             # per vocabulary word per 180-word chunk: 180 21-bit keys in 30 16-byte groups
+TABLE_CHUNK_L2_BYTES = 80 << 20   # a table chunk (v_rows x 512 B) must stay L2-resident
+TABLE_ROW_BYTES = 512             # per vocabulary word per 256-word chunk: 256 16-bit keys
 
 
-def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | None = None) -> str:
+def reverse_mode(v_rows: int, a_rows: int, nnz_docs: int, total_memory: int | None = None,
+                 split: bool = False) -> str:
     """"table" when the reverse Phase 1 is cheaper as a distance table + per-doc gathers
     (table.cu): the vocabulary is small next to nnz(X1) (each (w, u) distance is then
-    needed ~nnz/V times), a 180-word chunk of it fits in L2, and the table fits in HBM;
+    needed ~nnz/V times), a 256-word chunk of it fits in L2, and the table fits in HBM;
     else "gemm".  LCRW_REVERSE=gemm|table overrides (tests, A/B runs)."""
     env = os.environ.get("LCRW_REVERSE", "")
     if env in ("gemm", "table"):
         return env
-    if v_rows * TABLE_ROW_BYTES > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
-        return "gemm"
+    if split or v_rows * TABLE_ROW_BYTES > TABLE_CHUNK_L2_BYTES or 2 * v_rows > nnz_docs:
+        return "gemm"  # (split operands, m <= 64: the GEMM form keeps Z2 in f32 instead of 16-bit keys)
     table_bytes = int(_lib.value("lcrw_table_bytes", a_rows, v_rows))
     if total_memory is None:  # (mem_get_info would stall the stream)
         total_memory = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
@@ -670,7 +666,7 @@ def distance_table(res2: "Restricted", prep: PreparedEmbeddings, via_transpose: 
         zs = 7  # lcrw_table_transpose reads 128-segment panels
         Tp, zp = phase1(res2.A, res2.a_norms, res2.v_e, prep.EhB, V, seg, V, prep, z_shift=zs)
         zero_identical(seg, V, prep.canon, prep.next, res2.remap, Tp, zp, zs)
-        _lib.call("lcrw_table_transpose", _p(Tp), res2.v_e, V, _p(prep.scale), _p(T), _stream())
+        _lib.call("lcrw_table_transpose", _p(Tp), _p(res2.a_norms), res2.v_e, V, _p(prep.scale), _p(T), _stream())
         return T
     endmask, range_seg, n_ranges = segment_plan(seg, V, V, res2.v_e)
     Ap, anp = _table_operand(res2.used, prep)
@@ -741,7 +737,7 @@ class QuerySide:
     @classmethod
     def build(cls, x2: DeviceCSR, prep: PreparedEmbeddings, nnz_docs: int) -> "QuerySide":
         res2 = Restricted.build(x2, prep, host_plan=True)
-        mode = reverse_mode(prep.V, res2.v_e, nnz_docs)
+        mode = reverse_mode(prep.V, res2.v_e, nnz_docs, split=prep.split)
         table = distance_table(res2, prep) if mode == "table" else None
         return cls(res2, table, NearPairs(table, res2, prep) if NearPairs.enabled() else None)
 
@@ -804,7 +800,7 @@ def _symmetric_pass(x1: DeviceCSR, x2: DeviceCSR, prep: PreparedEmbeddings, k: i
               _p(nxt), _p(res2.remap), _p(e_blk), _p(e_tile), n2, _p(d1), 8 * n1, _p(D), ld_q, ld_doc,
               _p(top_d), _p(top_i), k if fused else 0, id_offset, batch, 0, _p(table),
               _p(near.ws) if near is not None and near.built else None, near.cap if near is not None else 0,
-              _p(prep.E32), prep.m,
+              0 if prep.split else 1, _p(prep.E32), prep.m,
               _p(res2.used),
               C.c_void_p(d1_ready.cuda_event) if d1_ready is not None else None, _p(ws), ws_bytes.value, st)
     del ws, table, near

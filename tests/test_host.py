@@ -285,7 +285,7 @@ def test_reverse_mode_choice(monkeypatch):
     assert device.reverse_mode(3_000_000, 146_000, 75_000_000, hbm) == "gemm"    # C4: chunk >> L2
     assert device.reverse_mode(400_000, 190_000, 1_250_000, hbm) == "gemm"      # C5 shard
     assert device.reverse_mode(20_000, 2_400, 30_000, hbm) == "gemm"            # few docs: 2V > nnz
-    assert device.reverse_mode(100_000, 39_300, 50_000_000, 32 << 30) == "gemm"  # table > HBM / 4
+    assert device.reverse_mode(100_000, 39_300, 50_000_000, 24 << 30) == "gemm"  # table > HBM / 4
     monkeypatch.setenv("LCRW_REVERSE", "gemm")
     assert device.reverse_mode(100_000, 39_300, 50_000_000, hbm) == "gemm"
     monkeypatch.setenv("LCRW_REVERSE", "table")

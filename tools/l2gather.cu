@@ -1,5 +1,5 @@
 // L2 gather ceiling probe (the "peak" of bench.py's table_min roofline, profiles/l2_gather_peak.json):
-// 480-byte (30 lanes x 16 B, the current table row) and 512-byte random row gathers + min
+// 512-byte (32 lanes x 16 B, the current table row) and 480-byte random row gathers + min
 // from an L2-resident ~50 MB table, the access pattern of csrc/table.cu without its Z2 stores.  nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/l2gather tools/l2gather.cu
 // Microbenchmark: random 512-B (or 1-KB) row gathers + min from an L2-resident table,
 // the access pattern of a distance-table formulation of the reverse Phase 1.
