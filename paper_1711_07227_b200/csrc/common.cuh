@@ -330,15 +330,16 @@ __device__ __forceinline__ uint32_t key16_base(float a_sq) {  // bits of 2^e (f3
   const int e2 = (int)(__float_as_uint(a_sq) >> 23) - 127;   // exponent of |w|^2
   return (uint32_t)((e2 >> 1) - 1 + 127) << 23;               // 2^e <= |w| / 2 < 2^(e+1)
 }
+// (branch-free: selects, so an epilogue's independent encodes interleave)
 __device__ __forceinline__ uint32_t dist_key16(float d, uint32_t base) {
   const uint32_t b = __float_as_uint(d);
-  if (b == 0u) return 0u;
-  if (b < base) return 1u;
-  const uint32_t c = (b - base + 256u) >> 9;
-  return c < 2u ? 1u : (c < kKey16Sat ? c : kKey16Sat);
+  uint32_t c = min(max((b - base + 256u) >> 9, 1u), kKey16Sat);
+  c = b < base ? 1u : c;
+  return b == 0u ? 0u : c;
 }
 __device__ __forceinline__ float key16_dist(uint32_t c, uint32_t base) {
-  return c == 0u ? 0.f : __uint_as_float(c == 1u ? base - (1u << 23) : base + (c << 9));
+  const uint32_t bits = c == 1u ? base - (1u << 23) : base + (c << 9);
+  return c == 0u ? 0.f : __uint_as_float(bits);
 }
 // the decoded value of a saturated key: an entry at it is refined exactly
 __device__ __forceinline__ float key16_sat(uint32_t base) { return key16_dist(kKey16Sat, base); }

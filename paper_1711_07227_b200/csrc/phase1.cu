@@ -451,7 +451,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float d;
         asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(fmaxf(segmin + nE, 0.f)));
         if (p.z_mode == kZTable) {
-          if (valid) *reinterpret_cast<uint16_t*>(zb) = (uint16_t)dist_key16(d, kbase);
+          // every lane stores (no branch per emit, so the encodes interleave): rows past a_rows
+          // are the last chunk's unused words, inside the table and never read as values
+          *reinterpret_cast<uint16_t*>(zb) = (uint16_t)dist_key16(d, kbase);
           zb += kTableRowBytes;
           return;
         }

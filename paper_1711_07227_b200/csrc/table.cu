@@ -268,13 +268,7 @@ int lcrw_distance_table(const uint16_t* A, const float* a_norms, int64_t a_rows,
   if (a_rows == 0 || v_rows == 0) return LCRW_OK;
   LCRW_REQUIRE(canon && next && remap && T, "lcrw_distance_table: null pointer");
   cudaStream_t st = as_stream(stream);
-  // a partial last chunk has keys no row writes: zero it (the gathers read them)
-  if (a_rows % kTableChunk) {
-    const int64_t last = ceil_div(a_rows, tbl::kChunk) - 1;
-    cudaError_t e = cudaMemsetAsync(static_cast<uint8_t*>(T) + last * v_rows * kTableRowBytes, 0,
-                                    (size_t)v_rows * kTableRowBytes, st);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync (table tail)");
-  }
+  // (the build writes every key of the last chunk: rows past a_rows hold unused values)
   int status = p1::launch(A, a_norms, a_rows, EhB, v_rows, m, kp, seg_offsets, 0, v_rows, endmask, range_seg,
                           n_ranges, scale, static_cast<float*>(T), v_rows * kTableRowBytes, 7, st, "table_build",
                           nullptr, 0, 2 /* kZTable */);
