@@ -313,6 +313,7 @@ def test_c2_full_size_sampled_parity():
     ref = O.lcrwmd_full(x1.take_rows(di), x2.take_rows(qj), E, threads=O.default_threads())
     ok, err = rel_close(got, ref, RTOL, ATOL)
     assert ok, err
+    print(f"C2 sampled parity: max rel err {float(np.max(np.abs(got - ref) / np.abs(ref))):.2e}")
     td, ti = device.symmetric(d1, d2, prep, 10)
     fd, fi = device.topk_rows(full.t().contiguous(),
                               torch.arange(1_000_000, device=full.device).repeat(1000, 1).contiguous(),
