@@ -31,10 +31,11 @@ __device__ __forceinline__ double dist_f64_scaled(float z) {
   return __hiloint2double((int)(b >> 3), (int)(b << 29));
 }
 #ifndef LCRW_SPMM_MINB
-#define LCRW_SPMM_MINB 6  // 6 CTAs (48 warps) per SM, <= 40 registers: 21 ms at C2 vs 27 ms at 54 registers
+#define LCRW_SPMM_MINB 4  // 4 CTAs (32 warps) per SM, <= 64 registers: 8 row loads in flight per warp
+                          // (C2: 16.6 ms; 5 CTAs / 48 registers 17.3 ms, unroll 16 at 80 registers 19.6 ms)
 #endif
 #ifndef LCRW_SPMM_UNROLL
-#define LCRW_SPMM_UNROLL 4
+#define LCRW_SPMM_UNROLL 8
 #endif
 constexpr int kSpmmUnroll = LCRW_SPMM_UNROLL;  // (#pragma unroll does not expand macros)
 template <bool kDist>
@@ -64,8 +65,36 @@ __global__ void __launch_bounds__(kWarps * 32, LCRW_SPMM_MINB)
       __syncwarp();
       nz_s[threadIdx.x >> 5][lane] = make_longlong2(my_off, (long long)__float_as_int(my_x));
       __syncwarp();
-#pragma unroll kSpmmUnroll
-      for (int t = 0; t < cnt; ++t) {
+      int t0 = 0;
+      // Distance Z with every weight of the block below 2^126 (always, for histogram
+      // weights): a branch-free loop whose kSpmmUnroll row loads are all issued before
+      // the first FMA (inactive lanes read segments 0-3 of the row, results unused),
+      // so each warp keeps kSpmmUnroll 512-byte runs in flight instead of one; the FMAs
+      // run in the same ascending order, so the sums are bitwise those of the loop below.
+      if (kDist && __all_sync(0xffffffffu, fabsf(my_x) < 0x1p126f)) {
+        const float* zl = active ? zq : Z;
+        // (the block's last cnt % kSpmmUnroll nonzeros go through the loop below: a whole
+        // last batch with weight-0 padding slots or predicated loads measured slower, and so
+        // did loading the next block's ids ahead)
+        for (; t0 + kSpmmUnroll <= cnt; t0 += kSpmmUnroll) {
+          float4 z[kSpmmUnroll];
+          double xs[kSpmmUnroll];
+#pragma unroll
+          for (int u = 0; u < kSpmmUnroll; ++u) {
+            const longlong2 e = nz_s[threadIdx.x >> 5][t0 + u];
+            z[u] = __ldg(reinterpret_cast<const float4*>(zl + e.x));
+            xs[u] = (double)__int_as_float((int)e.y) * 0x1p896;
+          }
+#pragma unroll
+          for (int u = 0; u < kSpmmUnroll; ++u) {
+            a0 = fma(xs[u], dist_f64_scaled(z[u].x), a0);
+            a1 = fma(xs[u], dist_f64_scaled(z[u].y), a1);
+            a2 = fma(xs[u], dist_f64_scaled(z[u].z), a2);
+            a3 = fma(xs[u], dist_f64_scaled(z[u].w), a3);
+          }
+        }
+      }
+      for (int t = t0; t < cnt; ++t) {
         const longlong2 e = nz_s[threadIdx.x >> 5][t];
         const int64_t zoff = e.x;
         const float xf = __int_as_float((int)e.y);

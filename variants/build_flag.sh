@@ -3,7 +3,7 @@
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p variants/$NAME
-for f in abi prep phase1 phase2 topk pipeline emd table; do
+for f in $(python -c 'from paper_1711_07227_b200._build import SOURCES; print(" ".join(s[:-3] for s in SOURCES))'); do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -Iinclude $FLAG -c paper_1711_07227_b200/csrc/$f.cu -o variants/$NAME/$f.o &
 done
 wait
