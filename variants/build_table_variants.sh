@@ -1,6 +1,6 @@
 #!/bin/bash
 # experiment builds of csrc/table.cu (A/B of table_min shapes; not shipped):
-#   VARIANTS="m4:-DLCRW_TBL_MINB=4 r512:-DLCRW_TABLE_ROW_BYTES=512 ..." variants/build_table_variants.sh
+#   VARIANTS="m4:-DLCRW_TBL_MINB=4 m6:-DLCRW_TBL_MINB=6 ..." variants/build_table_variants.sh
 # (the round-2 A/B knobs that lost were removed from table.cu; profiles/r02_summary.md lists them)
 # each variant links the shipped objects of paper_1711_07227_b200/build with its own table.o
 set -e
