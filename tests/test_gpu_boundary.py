@@ -231,19 +231,23 @@ def test_fused_topk_equals_topk_of_materialised_d(monkeypatch, k, reverse):
         assert np.array_equal(fd[j].cpu().numpy(), full[order, j])
 
 
-def test_spmm_dist_bitwise_equals_spmm():
-    """lcrw_spmm_dist (f32 -> f64 widening by exponent shift, weight pre-scaled by 2^896)
-    equals lcrw_spmm bit for bit on distance matrices: zeros, tiny and large normal
-    values, and weights that take the fallback (|x| >= 2^126)."""
+@pytest.mark.parametrize("zs,nq", [(3, 37), (7, 200)])
+def test_spmm_dist_bitwise_equals_spmm(zs, nq):
+    """lcrw_spmm_dist (f32 -> f64 widening by exponent shift, weight pre-scaled by 2^896,
+    8-row batches of loads + a serial tail) equals lcrw_spmm bit for bit on distance
+    matrices: zeros, tiny and large normal values, weights that take the fallback
+    (|x| >= 2^126), empty rows and rows of 1..99 nonzeros (1-4 staged blocks), lanes
+    past the last query (8- and 128-query panels)."""
     import torch
     from paper_1711_07227_b200 import device
-    rng = np.random.default_rng(21)
-    V, n, nq = 700, 300, 37
+    rng = np.random.default_rng(21 + zs)
+    V, n = 700, 300
     rows = []
     for i in range(n):
-        ids = np.sort(rng.choice(V, int(rng.integers(1, 60)), replace=False)).astype(np.int32)
+        ids = np.sort(rng.choice(V, int(rng.integers(0, 100)) if i % 7 else 32 * (i % 4) + i % 9,
+                                 replace=False)).astype(np.int32)
         x = (rng.random(len(ids)) + 0.05).astype(np.float32)
-        if i % 50 == 0:
+        if i % 50 == 0 and len(x):
             x[0] = np.float32(2.0 ** 126 * 1.5)  # fallback path
         rows.append((ids, x))
     offs = np.zeros(n + 1, np.int64)
@@ -255,7 +259,6 @@ def test_spmm_dist_bitwise_equals_spmm():
     z[rng.random((V, nq)) < 0.01] = np.float32(1e-20)
     z[rng.random((V, nq)) < 0.01] = np.float32(3e30)
     dev = torch.device("cuda")
-    zs = 3
     w = 1 << zs
     panels = (nq + w - 1) // w
     Zp = np.zeros((panels, V, w), np.float32)
