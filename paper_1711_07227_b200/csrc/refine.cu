@@ -134,13 +134,16 @@ __global__ void __launch_bounds__(kThreads, LCRW_REFINE_MINB) refine_kernel(Args
     }
     {
       float4 z4[kSteps];
+      float a_sq4[kSteps];  // the rows' norms, loaded with the entries (not after a test on them)
 #pragma unroll
       for (int u = 0; u < kSteps; ++u) {
         const int64_t i0 = ((int64_t)cu[u] << 7) + 4 * lane;
         const float* zp = g.Z + pu[u] * g.z_panel;
         const int64_t seg_left = g.n_seg - (int64_t)pu[u] * zw;  // < zw only in a ragged last panel
         z4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        a_sq4[u] = 0.f;
         if (pu[u] < n_panels && i0 < per_panel) {
+          if (!finalize) a_sq4[u] = __ldg(g.a_norms + (i0 >> g.z_shift));
           const int64_t sl = i0 & (zw - 1);  // segment of the lane's first entry inside the panel
           if (sl + 4 <= seg_left) {
             z4[u] = *reinterpret_cast<const float4*>(zp + i0);
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, LCRW_REFINE_MINB) refine_kernel(Args
               if (__float_as_uint(zv[j]) & kZMarkBit) flags |= 1u << j;
           } else if (zv[0] > 0.f || zv[1] > 0.f || zv[2] > 0.f || zv[3] > 0.f) {
             // the lane's four entries share one row (z_shift >= 2): one norm, one bound
-            const float a_sq = __ldg(g.a_norms + (i0 >> g.z_shift));
+            const float a_sq = a_sq4[u];
             const float sat = keyed ? key16_sat(key16_base(a_sq)) : __int_as_float(0x7f800000);
             const int64_t s_base = p * zw + (i0 & (zw - 1));
 #pragma unroll
