@@ -469,7 +469,9 @@ class Restricted:
         scatter each query's words over the Z2 tiles, which balances the
         per-(tile, warp) entry lists of that kernel."""
         if host_plan:
-            order = np.unique(x.host_ids()[0]).astype(np.int32)
+            seen = np.zeros(x.n_cols, dtype=bool)  # (a mask, not np.unique's sort: ~0.2 vs ~4 ms at C2,
+            seen[x.host_ids()[0]] = True            #  spent while the GPU waits for work)
+            order = np.flatnonzero(seen).astype(np.int32)
             rank = np.full(x.n_cols, -1, dtype=np.int32)
             rank[order] = np.arange(len(order), dtype=np.int32)
             used = to_device(order, torch.int32)

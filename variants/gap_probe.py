@@ -44,3 +44,7 @@ for g, a, b, t in sorted(gaps, reverse=True)[:20]:
            and c.time_range.elapsed_us() > 0.5 * g]
     names = sorted({c.name[:60] for c in cpu})[:8]
     print(f"gap {g/1e3:7.2f} ms after {a!r} before {b!r}; host: {names}")
+    inside = [c for c in prof.events() if c.device_type.name == "CPU" and t <= c.time_range.start <= t + g]
+    inside.sort(key=lambda c: -c.time_range.elapsed_us())
+    for c in inside[:12]:
+        print(f"    {c.time_range.elapsed_us()/1e3:6.2f} ms  {c.name[:70]}  {' <- '.join(str(x) for x in (c.stack or [])[:4])[:200]}")
