@@ -71,11 +71,11 @@ __global__ void __launch_bounds__(kWarps * 32, LCRW_SPMM_MINB)
           make_longlong2(my_off, __double_as_longlong(fast ? (double)my_x * 0x1p896 : (double)my_x));
       __syncwarp();
       int t0 = 0;
-      // Distance Z with every weight of the block below 2^126 (always, for histogram
-      // weights): a branch-free loop whose kSpmmUnroll row loads are all issued before
-      // the first FMA (inactive lanes read segments 0-3 of the row, results unused),
-      // so each warp keeps kSpmmUnroll 512-byte runs in flight instead of one; the FMAs
-      // run in the same ascending order, so the sums are bitwise those of the loop below.
+      // fast: a branch-free loop whose kSpmmUnroll row loads are all issued before the first
+      // FMA (inactive lanes read segments 0-3 of the row -- panel 0, always allocated --
+      // results unused), so each warp keeps kSpmmUnroll 512-byte runs in flight instead of
+      // one; the FMAs run in the same ascending order, so the sums are bitwise those of the
+      // loop below.
       if (fast) {
         const float* zl = active ? zq : Z;
         // (the block's last cnt % kSpmmUnroll nonzeros go through the loop below: a whole
